@@ -1,0 +1,211 @@
+/*
+ * salient_b200.h — C-ABI of the B200-native SALIENT batch-preparation library
+ * (libsalient_b200.so, built from paper_2110_08450_b200/csrc for sm_100a).
+ *
+ * The reference (`mfgprep`, /root/reference/pkg/src/mfgprep) has no native
+ * boundary of its own: its operator layer is a set of numba @njit functions
+ * over numpy arrays (`_kernels.py`).  Each entry point below replaces one of
+ * those operators, or one step of the Python driver that chains them; the
+ * reference symbol is cited on every declaration.  INTEGRATION.md shows the
+ * ctypes stub a maintainer adds to `mfgprep` to bind this library.
+ *
+ * Conventions
+ *   - every pointer argument named *_dev or typed as device data is a CUDA
+ *     device pointer; `stream` is a cudaStream_t (NULL = legacy default);
+ *   - calls only enqueue work (asynchronous); device faults surface at the
+ *     caller's next synchronisation;
+ *   - return value: 0 = SAL_OK, <0 = error; sal_last_error() returns a
+ *     thread-local message describing the last failure on this thread;
+ *   - node ids on device are int32 (graphs up to 2^31-1 nodes), the graph
+ *     row pointer is int64, MFG row pointers / source locals are int32;
+ *   - nothing here allocates device memory: callers pass workspaces sized by
+ *     the *_bytes / layout helpers.  No global mutable state apart from the
+ *     per-thread error message; reentrant across streams and threads.
+ */
+#ifndef SALIENT_B200_H
+#define SALIENT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAL_OK 0
+#define SAL_EINVAL (-1)
+#define SAL_ECUDA (-2)
+
+#define SAL_MAX_HOPS 8
+
+/* RNG policies of the sampler.  SPLITMIX reproduces the reference draw
+ * stream bit-exactly (rng.py:16-35, _kernels.py:30-39); PHILOX is the
+ * north-star counter-based policy keyed on (seed, batch, hop, dst). */
+#define SAL_RNG_SPLITMIX 0
+#define SAL_RNG_PHILOX 1
+
+/* element types (values 1/2 match graph.py:18-19 DTYPE_F16 / DTYPE_F32) */
+#define SAL_F16 1
+#define SAL_F32 2
+#define SAL_BF16 3
+
+/* CSR graph resident in HBM (graph.py:39-85 CsrGraph). */
+typedef struct {
+  int64_t num_nodes;
+  int64_t num_edges;
+  const int64_t* indptr;  /* device, int64[num_nodes + 1] */
+  const int32_t* indices; /* device, int32[num_edges]     */
+} sal_graph;
+
+/* Device-resident descriptor of one seed batch (prep.py:40-52 SeedBatch):
+ * seeds = seeds_base[seed_offset : seed_offset + n_seeds]. */
+typedef struct {
+  int64_t batch_id;
+  int64_t seed_offset;
+  int64_t n_seeds;
+} sal_batch_desc;
+
+/* Global->local map (sampler.py:106-171 IdMap, flat_probing variant).
+ * table: 64-bit slots, table_cap a power of two, reset to all-ones bytes. */
+typedef struct {
+  unsigned long long* table;
+  int64_t table_cap;
+  int32_t* globals; /* local -> global, capacity globals_cap */
+  int64_t globals_cap;
+} sal_idmap;
+
+/* Capacities of one multi-hop sample (sampler.py:321-346). */
+typedef struct {
+  int32_t num_hops;
+  int32_t fanout[SAL_MAX_HOPS];         /* expansion order: per_hop[L-1-h] */
+  int64_t max_seeds;
+  int64_t node_cap[SAL_MAX_HOPS + 1];   /* max id-map size after h hops   */
+  int64_t edge_cap[SAL_MAX_HOPS];       /* max edges emitted by hop h     */
+  int64_t table_cap;
+} sal_mfg_plan;
+
+/* Byte offsets of the arrays inside one batch workspace. */
+typedef struct {
+  int64_t table;                      /* u64[table_cap]                      */
+  int64_t globals;                    /* int32[node_cap[L]]                  */
+  int64_t sizes;                      /* int64[L+1]: id-map size after hop h */
+  int64_t etot;                       /* int64[L]:   edges of hop h          */
+  int64_t dst_indptr[SAL_MAX_HOPS];   /* int32[node_cap[h]+1] (hop h)        */
+  int64_t src_local[SAL_MAX_HOPS];    /* int32[edge_cap[h]]   (hop h)        */
+  int64_t src_glob;                   /* int32[max edge_cap] scratch         */
+  int64_t slot;                       /* int32[max edge_cap] scratch         */
+  int64_t rank;                       /* int32[max edge_cap] scratch         */
+  int64_t scan;                       /* look-back scan workspace            */
+  int64_t scan_bytes;
+  int64_t total;                      /* total workspace bytes               */
+} sal_mfg_layout;
+
+/* ---- library ------------------------------------------------------------ */
+int sal_version(void);
+const char* sal_last_error(void);
+
+/* HopStream.key_prefix (sampler.py:238-247) */
+uint64_t sal_hop_key_prefix(uint64_t global_seed, int64_t batch_id, int64_t hop);
+
+/* ---- batch-level driver: multihop_mfg (sampler.py:328-346) -------------- */
+/* per_hop is FanoutSpec.per_hop (outermost hop first, sampler.py:70-72). */
+int sal_mfg_plan_init(sal_mfg_plan* plan, int32_t num_hops, const int32_t* per_hop,
+                      int64_t max_seeds, int64_t num_nodes);
+int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* layout);
+/* Seeds -> L hops -> MFG, all on `stream`, no host synchronisation.
+ * Outputs land in the workspace at the layout's offsets; `sizes[h]` and
+ * `etot[h]` give the dynamic extents. */
+int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* layout,
+                   void* ws_dev, const int64_t* seeds_base_dev, const sal_batch_desc* desc_dev,
+                   uint64_t global_seed, int32_t rng_policy, void* stream);
+
+/* ---- hop-level operators (the _kernels.py operator layer) --------------- */
+size_t sal_scan_ws_bytes(int64_t max_items);
+/* reset every slot of the map to empty (IdMap.__init__, sampler.py:113-129) */
+int sal_idmap_reset(const sal_idmap* m, void* stream);
+/* rebuild the table from locals 0..n-1 after growth (sampler.py:131-145,
+ * rehash_flat _kernels.py:64-73) */
+int sal_idmap_rehash(const sal_idmap* m, int64_t n, void* stream);
+/* insert_keys (_kernels.py:216-222): get-or-insert keys in order.
+ * size_old_dev -> size_new_dev; local_out (nullable) receives each key's local. */
+int sal_idmap_insert(const sal_idmap* m, const int64_t* keys_dev, int64_t n,
+                     const int64_t* size_old_dev, int64_t* size_new_dev, int64_t* n_dev_scratch,
+                     int32_t* scratch_glob, int32_t* scratch_slot, int32_t* scratch_rank,
+                     int32_t* local_out, void* scan_ws, void* stream);
+/* hop_budget (_kernels.py:42-50) + the destination CSR of hop_kernel:
+ * dst_indptr[i] = sum_{j<i} min(deg(globals[j]), fanout); *e_total_dev = total. */
+int sal_hop_count(const sal_graph* g, const int32_t* globals_dev, const int64_t* n_dst_dev,
+                  int64_t max_dst, int32_t fanout, int32_t* dst_indptr_dev, int64_t* e_total_dev,
+                  void* scan_ws, void* stream);
+/* sampling half of hop_kernel (_kernels.py:161-183, _sample_positions 102-147):
+ * per destination take-all or rejection sampling; writes the sampled global
+ * ids and inserts them into the map.  inject_pos_dev (nullable, int64 per
+ * edge, same layout as hop_kernel's pos_all, _kernels.py:186-204) replaces
+ * the draws with externally supplied slot positions.  draws_out_dev
+ * (nullable, int32 per destination) receives the number of draws consumed
+ * (CounterRng.counter after sample_neighbors, rng.py:38-51). */
+int sal_hop_sample(const sal_graph* g, const sal_idmap* m, const int64_t* n_dst_dev,
+                   int64_t max_dst, int32_t fanout, uint64_t key_prefix, int32_t rng_policy,
+                   uint64_t global_seed, int64_t batch_id, int32_t hop,
+                   const int64_t* inject_pos_dev, const int32_t* dst_indptr_dev,
+                   int32_t* src_glob_dev, int32_t* slot_dev, int32_t* draws_out_dev,
+                   void* stream);
+/* relabel half of hop_kernel (_map_get_or_insert, _kernels.py:76-99). */
+int sal_hop_relabel(const sal_idmap* m, const int64_t* e_total_dev, int64_t max_edges,
+                    const int64_t* size_old_dev, int64_t* size_new_dev,
+                    const int32_t* src_glob_dev, const int32_t* slot_dev, int32_t* rank_dev,
+                    int32_t* src_local_dev, void* scan_ws, void* stream);
+
+/* ---- slicing (prep.py:153-182) ------------------------------------------ */
+/* gather_f16 / gather_f32 (_kernels.py:225-252): out[i,:] = X[ids[i],:]
+ * converted to out_dtype.  Row count = *n_dev if n_dev != NULL else n.
+ * ids are int32 (id_bytes 4) or int64 (id_bytes 8). */
+int sal_gather_rows(const void* x_dev, int64_t x_rows, int32_t cols, int64_t x_stride,
+                    int32_t in_dtype, const void* ids_dev, int32_t id_bytes,
+                    const int64_t* n_dev, int64_t n, void* out_dev, int64_t out_stride,
+                    int32_t out_dtype, void* stream);
+/* gather_labels (_kernels.py:255-258): out[j] = y[seeds[j]] */
+int sal_gather_labels(const int64_t* y_dev, const int64_t* seeds_base_dev,
+                      const sal_batch_desc* desc_dev, int64_t max_n, int64_t* out_dev,
+                      void* stream);
+
+/* ---- mean aggregation (mpnn.py:57-65 _mean_neighbors) -------------------- */
+/* out[d,:] = mean_{e in row d} h[src[e],:]  (0 when the row is empty),
+ * fp32 accumulation in edge order; rows [n_dst, n_pad) are zero-filled.
+ * n_dst = *n_dst_dev if non-NULL else n_pad. */
+int sal_segment_mean_fwd(const int32_t* indptr_dev, const int32_t* src_dev,
+                         const int64_t* n_dst_dev, int64_t n_pad, const void* h_dev,
+                         int32_t h_dtype, int64_t h_stride, int32_t f, void* out_dev,
+                         int32_t out_dtype, int64_t out_stride, void* stream);
+/* gradient of the above w.r.t. h: g_h[src[e],:] += g_out[d,:] / deg(d).
+ * g_h (fp32, n_src rows) must be zeroed by the caller. */
+int sal_segment_mean_bwd(const int32_t* indptr_dev, const int32_t* src_dev,
+                         const int64_t* n_dst_dev, int64_t n_pad, const void* g_out_dev,
+                         int32_t g_dtype, int64_t g_stride, int32_t f, float* g_h_dev,
+                         int64_t gh_stride, void* stream);
+/* Fused layer-0 aggregation straight from the global feature table (no
+ * materialised gather): out[d,:] = mean_e X[globals[src[e]],:]. */
+int sal_segment_mean_fwd_global(const int32_t* indptr_dev, const int32_t* src_dev,
+                                const int32_t* globals_dev, const int64_t* n_dst_dev,
+                                int64_t n_pad, const void* x_dev, int32_t x_dtype,
+                                int64_t x_stride, int32_t f, void* out_dev, int32_t out_dtype,
+                                int64_t out_stride, void* stream);
+
+/* ---- on-device synthetic data (graph.py:252-298 laws) ---- */
+/* owner[s] = v for every slot s in [indptr[v], indptr[v+1]) */
+int sal_gen_owner(const int64_t* indptr_dev, int64_t n, int32_t* owner_dev, void* stream);
+/* configuration-model pairing: indices[s] = owner[partner(s)], partner a
+ * seeded pseudo-random perfect matching of the n_stubs (even) slots */
+int sal_gen_pairing(const int32_t* owner_dev, int64_t n_stubs, uint64_t seed,
+                    int32_t* indices_dev, void* stream);
+/* uniform [-1,1) features rounded to fp16, row stride `stride` elements */
+int sal_gen_features_uniform(int64_t n, int32_t f, int64_t stride, uint64_t seed, void* out_dev,
+                             void* stream);
+/* i.i.d. uniform class labels (graph.py:295-298 law) */
+int sal_gen_labels_uniform(int64_t n, int32_t num_classes, uint64_t seed, int64_t* out_dev,
+                           void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SALIENT_B200_H */

@@ -1,0 +1,366 @@
+// extern "C" boundary of libsalient_b200.so (declared in include/salient_b200.h).
+//
+// Argument validation happens here, before any launch, and reports through a
+// thread-local message (the reference raises ValueError in Python before its
+// kernels run: sampler.py:99-100, 311-317; prep.py:160-164).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "salient_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SAL_OK;
+  return fail(SAL_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+sal::GraphDev to_dev(const sal_graph* g) {
+  sal::GraphDev d;
+  d.num_nodes = g->num_nodes;
+  d.num_edges = g->num_edges;
+  d.indptr = g->indptr;
+  d.indices = g->indices;
+  return d;
+}
+
+int idmap_dev(const sal_idmap* m, sal::IdMapDev* out) {
+  if (m == nullptr || m->table == nullptr || m->globals == nullptr)
+    return fail(SAL_EINVAL, "idmap: null table or globals");
+  const int l2 = sal::log2_exact(m->table_cap);
+  if (l2 < 4 || l2 > 31) return fail(SAL_EINVAL, "idmap: table_cap must be a power of two in [16, 2^31]");
+  out->table = m->table;
+  out->log2cap = l2;
+  out->globals = m->globals;
+  out->size_out = nullptr;
+  return SAL_OK;
+}
+
+int64_t pow2_at_least(int64_t n) {
+  int64_t p = 16;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" {
+
+int sal_version(void) { return 100; }
+
+const char* sal_last_error(void) { return g_err; }
+
+uint64_t sal_hop_key_prefix(uint64_t global_seed, int64_t batch_id, int64_t hop) {
+  return sal::hop_key_prefix(global_seed, (uint64_t)batch_id, (uint64_t)hop);
+}
+
+size_t sal_scan_ws_bytes(int64_t max_items) { return sal::scan_ws_bytes(max_items); }
+
+// ---------------------------------------------------------------------------
+// plan / layout (sampler.py:321-325 size_hint_for gives the same bound)
+// ---------------------------------------------------------------------------
+int sal_mfg_plan_init(sal_mfg_plan* plan, int32_t num_hops, const int32_t* per_hop,
+                      int64_t max_seeds, int64_t num_nodes) {
+  if (plan == nullptr || per_hop == nullptr) return fail(SAL_EINVAL, "plan: null argument");
+  if (num_hops < 1 || num_hops > SAL_MAX_HOPS)
+    return fail(SAL_EINVAL, "plan: need 1..%d hops, got %d", SAL_MAX_HOPS, num_hops);
+  if (max_seeds < 0 || num_nodes < 0) return fail(SAL_EINVAL, "plan: negative size");
+  if (num_nodes >= (1ll << 31)) return fail(SAL_EINVAL, "plan: graphs are limited to 2^31-1 nodes");
+  memset(plan, 0, sizeof(*plan));
+  plan->num_hops = num_hops;
+  plan->max_seeds = max_seeds;
+  int64_t nodes = max_seeds < num_nodes ? max_seeds : num_nodes;
+  plan->node_cap[0] = nodes;
+  for (int h = 0; h < num_hops; ++h) {
+    const int32_t f = per_hop[num_hops - 1 - h];  // expansion hop h uses per_hop[L-1-h]
+    if (f < 0) return fail(SAL_EINVAL, "plan: fanouts must be >= 0");
+    plan->fanout[h] = f;
+    plan->edge_cap[h] = nodes * (int64_t)f;
+    int64_t next = nodes + nodes * (int64_t)f;
+    if (next > num_nodes) next = num_nodes;
+    if (next < nodes) next = nodes;
+    nodes = next;
+    plan->node_cap[h + 1] = nodes;
+  }
+  if (nodes >= (1ll << 31) - 1) return fail(SAL_EINVAL, "plan: node capacity exceeds int32");
+  for (int h = 0; h < num_hops; ++h)
+    if (plan->edge_cap[h] >= (1ll << 31) - 1)
+      return fail(SAL_EINVAL, "plan: hop %d edge capacity exceeds int32", h);
+  plan->table_cap = pow2_at_least(2 * (nodes > 8 ? nodes : 8));
+  return SAL_OK;
+}
+
+int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* L) {
+  if (plan == nullptr || L == nullptr) return fail(SAL_EINVAL, "layout: null argument");
+  memset(L, 0, sizeof(*L));
+  const int nh = plan->num_hops;
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t o = off;
+    off = align_up(off + (bytes > 0 ? bytes : 0), 256);
+    return o;
+  };
+  int64_t max_e = 1, max_d = 1;
+  for (int h = 0; h < nh; ++h) {
+    if (plan->edge_cap[h] > max_e) max_e = plan->edge_cap[h];
+    if (plan->node_cap[h] > max_d) max_d = plan->node_cap[h];
+  }
+  L->table = take(plan->table_cap * 8);
+  L->globals = take(plan->node_cap[nh] * 4 + 4);
+  L->sizes = take((nh + 1) * 8);
+  L->etot = take(nh * 8);
+  for (int h = 0; h < nh; ++h) {
+    L->dst_indptr[h] = take((plan->node_cap[h] + 1) * 4);
+    L->src_local[h] = take(plan->edge_cap[h] * 4 + 4);
+  }
+  L->src_glob = take(max_e * 4 + 4);
+  L->slot = take(max_e * 4 + 4);
+  L->rank = take(max_e * 4 + 4);
+  const int64_t scan_items = max_e > max_d ? max_e : max_d;
+  L->scan_bytes = (int64_t)sal::scan_ws_bytes(scan_items);
+  L->scan = take(L->scan_bytes);
+  L->total = off;
+  return SAL_OK;
+}
+
+int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
+                   void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
+                   uint64_t global_seed, int32_t rng_policy, void* stream) {
+  if (g == nullptr || plan == nullptr || L == nullptr || ws == nullptr || seeds_base == nullptr ||
+      desc == nullptr)
+    return fail(SAL_EINVAL, "sample_mfg: null argument");
+  if (rng_policy != SAL_RNG_SPLITMIX && rng_policy != SAL_RNG_PHILOX)
+    return fail(SAL_EINVAL, "sample_mfg: unknown rng policy %d", rng_policy);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* base = (char*)ws;
+  sal::IdMapDev m;
+  m.table = (unsigned long long*)(base + L->table);
+  m.log2cap = sal::log2_exact(plan->table_cap);
+  m.globals = (int32_t*)(base + L->globals);
+  int64_t* sizes = (int64_t*)(base + L->sizes);
+  int64_t* etot = (int64_t*)(base + L->etot);
+  m.size_out = sizes;
+  const sal::GraphDev gd = to_dev(g);
+  int32_t* src_glob = (int32_t*)(base + L->src_glob);
+  int32_t* slot = (int32_t*)(base + L->slot);
+  int32_t* rank = (int32_t*)(base + L->rank);
+  void* scan = base + L->scan;
+
+  cudaError_t e = cudaMemsetAsync(m.table, 0xFF, plan->table_cap * 8, st);
+  if (e != cudaSuccess) return cuda_status(e, "sample_mfg: table reset");
+  e = sal::launch_seed_insert(seeds_base, desc, m, plan->max_seeds, st);
+  if (e != cudaSuccess) return cuda_status(e, "sample_mfg: seed insert");
+  for (int h = 0; h < plan->num_hops; ++h) {
+    int32_t* dst_indptr = (int32_t*)(base + L->dst_indptr[h]);
+    int32_t* src_local = (int32_t*)(base + L->src_local[h]);
+    e = sal::launch_hop_count(gd, m.globals, sizes + h, plan->node_cap[h], plan->fanout[h],
+                              dst_indptr, etot + h, scan, st);
+    if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop count");
+    sal::HopKey hk;
+    hk.prefix = 0;
+    hk.global_seed = global_seed;
+    hk.hop = (uint32_t)h;
+    hk.batch = 0;
+    hk.derive = 1;
+    e = sal::launch_hop_sample(gd, m, sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
+                               rng_policy, nullptr, dst_indptr, src_glob, slot, nullptr, st);
+    if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
+    e = sal::launch_hop_relabel(m, etot + h, plan->edge_cap[h], sizes + h, sizes + h + 1,
+                                src_glob, slot, rank, src_local, scan, st);
+    if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop relabel");
+  }
+  return SAL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// hop-level operators
+// ---------------------------------------------------------------------------
+int sal_idmap_reset(const sal_idmap* m, void* stream) {
+  sal::IdMapDev d;
+  const int rc = idmap_dev(m, &d);
+  if (rc) return rc;
+  return cuda_status(cudaMemsetAsync(m->table, 0xFF, m->table_cap * 8, (cudaStream_t)stream),
+                     "idmap_reset");
+}
+
+int sal_idmap_rehash(const sal_idmap* m, int64_t n, void* stream) {
+  sal::IdMapDev d;
+  const int rc = idmap_dev(m, &d);
+  if (rc) return rc;
+  if (n < 0 || n > m->globals_cap) return fail(SAL_EINVAL, "idmap_rehash: bad size %lld", (long long)n);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(m->table, 0xFF, m->table_cap * 8, st);
+  if (e != cudaSuccess) return cuda_status(e, "idmap_rehash: reset");
+  return cuda_status(sal::launch_rehash(d, n, st), "idmap_rehash");
+}
+
+int sal_idmap_insert(const sal_idmap* m, const int64_t* keys, int64_t n,
+                     const int64_t* size_old, int64_t* size_new, int64_t* n_dev_scratch,
+                     int32_t* scratch_glob, int32_t* scratch_slot, int32_t* scratch_rank,
+                     int32_t* local_out, void* scan_ws, void* stream) {
+  sal::IdMapDev d;
+  int rc = idmap_dev(m, &d);
+  if (rc) return rc;
+  if (n < 0) return fail(SAL_EINVAL, "idmap_insert: negative key count");
+  if (n > 0 && keys == nullptr) return fail(SAL_EINVAL, "idmap_insert: null keys");
+  if (size_old == nullptr || size_new == nullptr || n_dev_scratch == nullptr ||
+      scratch_glob == nullptr || scratch_slot == nullptr || scratch_rank == nullptr ||
+      scan_ws == nullptr)
+    return fail(SAL_EINVAL, "idmap_insert: null scratch argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = sal::launch_keys_insert(keys, n, d, scratch_glob, scratch_slot, n_dev_scratch, st);
+  if (e != cudaSuccess) return cuda_status(e, "idmap_insert");
+  e = sal::launch_hop_relabel(d, n_dev_scratch, n, size_old, size_new, scratch_glob, scratch_slot,
+                              scratch_rank, local_out, scan_ws, st);
+  return cuda_status(e, "idmap_insert: relabel");
+}
+
+int sal_hop_count(const sal_graph* g, const int32_t* globals, const int64_t* n_dst_dev,
+                  int64_t max_dst, int32_t fanout, int32_t* dst_indptr, int64_t* e_total,
+                  void* scan_ws, void* stream) {
+  if (g == nullptr || globals == nullptr || n_dst_dev == nullptr || dst_indptr == nullptr ||
+      e_total == nullptr || scan_ws == nullptr)
+    return fail(SAL_EINVAL, "hop_count: null argument");
+  if (fanout < 0) return fail(SAL_EINVAL, "hop_count: fanout must be >= 0");
+  return cuda_status(sal::launch_hop_count(to_dev(g), globals, n_dst_dev, max_dst, fanout,
+                                           dst_indptr, e_total, scan_ws, (cudaStream_t)stream),
+                     "hop_count");
+}
+
+int sal_hop_sample(const sal_graph* g, const sal_idmap* m, const int64_t* n_dst_dev,
+                   int64_t max_dst, int32_t fanout, uint64_t key_prefix, int32_t rng_policy,
+                   uint64_t global_seed, int64_t batch_id, int32_t hop,
+                   const int64_t* inject_pos, const int32_t* dst_indptr, int32_t* src_glob,
+                   int32_t* slot, int32_t* draws_out, void* stream) {
+  sal::IdMapDev d;
+  int rc = idmap_dev(m, &d);
+  if (rc) return rc;
+  if (g == nullptr || n_dst_dev == nullptr || dst_indptr == nullptr || src_glob == nullptr ||
+      slot == nullptr)
+    return fail(SAL_EINVAL, "hop_sample: null argument");
+  if (rng_policy != SAL_RNG_SPLITMIX && rng_policy != SAL_RNG_PHILOX)
+    return fail(SAL_EINVAL, "hop_sample: unknown rng policy %d", rng_policy);
+  sal::HopKey hk;
+  hk.prefix = key_prefix;
+  hk.global_seed = global_seed;
+  hk.hop = (uint32_t)hop;
+  hk.batch = (uint32_t)batch_id;
+  hk.derive = 0;
+  return cuda_status(sal::launch_hop_sample(to_dev(g), d, n_dst_dev, max_dst, fanout, hk, nullptr,
+                                            rng_policy, inject_pos, dst_indptr, src_glob, slot,
+                                            draws_out, (cudaStream_t)stream),
+                     "hop_sample");
+}
+
+int sal_hop_relabel(const sal_idmap* m, const int64_t* e_total, int64_t max_edges,
+                    const int64_t* size_old, int64_t* size_new, const int32_t* src_glob,
+                    const int32_t* slot, int32_t* rank, int32_t* src_local, void* scan_ws,
+                    void* stream) {
+  sal::IdMapDev d;
+  int rc = idmap_dev(m, &d);
+  if (rc) return rc;
+  if (e_total == nullptr || size_old == nullptr || size_new == nullptr || src_glob == nullptr ||
+      slot == nullptr || rank == nullptr || scan_ws == nullptr)
+    return fail(SAL_EINVAL, "hop_relabel: null argument");
+  return cuda_status(sal::launch_hop_relabel(d, e_total, max_edges, size_old, size_new, src_glob,
+                                             slot, rank, src_local, scan_ws,
+                                             (cudaStream_t)stream),
+                     "hop_relabel");
+}
+
+// ---------------------------------------------------------------------------
+// slicing
+// ---------------------------------------------------------------------------
+static bool valid_dtype(int32_t t) { return t == SAL_F16 || t == SAL_F32 || t == SAL_BF16; }
+
+int sal_gather_rows(const void* x, int64_t x_rows, int32_t cols, int64_t x_stride,
+                    int32_t in_dtype, const void* ids, int32_t id_bytes, const int64_t* n_dev,
+                    int64_t n, void* out, int64_t out_stride, int32_t out_dtype, void* stream) {
+  if (!valid_dtype(in_dtype) || !valid_dtype(out_dtype))
+    return fail(SAL_EINVAL, "gather_rows: unsupported dtype (%d -> %d)", in_dtype, out_dtype);
+  if (id_bytes != 4 && id_bytes != 8) return fail(SAL_EINVAL, "gather_rows: id_bytes must be 4 or 8");
+  if (cols < 0 || n < 0 || x_stride < cols || out_stride < cols)
+    return fail(SAL_EINVAL, "gather_rows: bad shape");
+  if (n == 0 && n_dev == nullptr) return SAL_OK;
+  if (cols == 0) return SAL_OK;
+  if (x == nullptr || ids == nullptr || out == nullptr)
+    return fail(SAL_EINVAL, "gather_rows: null argument");
+  return cuda_status(sal::launch_gather_rows(x, x_rows, cols, x_stride, in_dtype, ids, id_bytes,
+                                             n_dev, n, out, out_stride, out_dtype,
+                                             (cudaStream_t)stream),
+                     "gather_rows");
+}
+
+int sal_gather_labels(const int64_t* y, const int64_t* seeds_base, const sal_batch_desc* desc,
+                      int64_t max_n, int64_t* out, void* stream) {
+  if (y == nullptr || seeds_base == nullptr || desc == nullptr || out == nullptr)
+    return fail(SAL_EINVAL, "gather_labels: null argument");
+  return cuda_status(
+      sal::launch_gather_labels(y, seeds_base, desc, max_n, out, (cudaStream_t)stream),
+      "gather_labels");
+}
+
+// ---------------------------------------------------------------------------
+// aggregation
+// ---------------------------------------------------------------------------
+int sal_segment_mean_fwd(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
+                         int64_t n_pad, const void* h, int32_t h_dtype, int64_t h_stride,
+                         int32_t f, void* out, int32_t out_dtype, int64_t out_stride,
+                         void* stream) {
+  if (!valid_dtype(h_dtype) || !valid_dtype(out_dtype))
+    return fail(SAL_EINVAL, "segment_mean_fwd: unsupported dtype");
+  if (f < 0 || n_pad < 0) return fail(SAL_EINVAL, "segment_mean_fwd: bad shape");
+  if (n_pad == 0 || f == 0) return SAL_OK;
+  if (indptr == nullptr || src == nullptr || h == nullptr || out == nullptr)
+    return fail(SAL_EINVAL, "segment_mean_fwd: null argument");
+  return cuda_status(sal::launch_segment_mean_fwd(indptr, src, nullptr, n_dst_dev, n_pad, h,
+                                                  h_dtype, h_stride, f, out, out_dtype,
+                                                  out_stride, (cudaStream_t)stream),
+                     "segment_mean_fwd");
+}
+
+int sal_segment_mean_fwd_global(const int32_t* indptr, const int32_t* src,
+                                const int32_t* globals, const int64_t* n_dst_dev, int64_t n_pad,
+                                const void* x, int32_t x_dtype, int64_t x_stride, int32_t f,
+                                void* out, int32_t out_dtype, int64_t out_stride, void* stream) {
+  if (!valid_dtype(x_dtype) || !valid_dtype(out_dtype))
+    return fail(SAL_EINVAL, "segment_mean_fwd_global: unsupported dtype");
+  if (f < 0 || n_pad < 0) return fail(SAL_EINVAL, "segment_mean_fwd_global: bad shape");
+  if (n_pad == 0 || f == 0) return SAL_OK;
+  if (indptr == nullptr || src == nullptr || globals == nullptr || x == nullptr || out == nullptr)
+    return fail(SAL_EINVAL, "segment_mean_fwd_global: null argument");
+  return cuda_status(sal::launch_segment_mean_fwd(indptr, src, globals, n_dst_dev, n_pad, x,
+                                                  x_dtype, x_stride, f, out, out_dtype,
+                                                  out_stride, (cudaStream_t)stream),
+                     "segment_mean_fwd_global");
+}
+
+int sal_segment_mean_bwd(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
+                         int64_t n_pad, const void* g_out, int32_t g_dtype, int64_t g_stride,
+                         int32_t f, float* g_h, int64_t gh_stride, void* stream) {
+  if (!valid_dtype(g_dtype)) return fail(SAL_EINVAL, "segment_mean_bwd: unsupported dtype");
+  if (f < 0 || n_pad < 0) return fail(SAL_EINVAL, "segment_mean_bwd: bad shape");
+  if (n_pad == 0 || f == 0) return SAL_OK;
+  if (indptr == nullptr || src == nullptr || g_out == nullptr || g_h == nullptr)
+    return fail(SAL_EINVAL, "segment_mean_bwd: null argument");
+  return cuda_status(sal::launch_segment_mean_bwd(indptr, src, n_dst_dev, n_pad, g_out, g_dtype,
+                                                  g_stride, f, g_h, gh_stride,
+                                                  (cudaStream_t)stream),
+                     "segment_mean_bwd");
+}
+
+}  // extern "C"
