@@ -1,0 +1,397 @@
+"""Benchmark: papers100M-shape GraphSAGE epoch with all batch preparation on device.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--shape papers|products|arxiv|c1] [--fanouts 15,10,5]
+
+One step = one global training step: every rank prepares one 1024-seed batch
+on its GPU (sample 3 hops -> relabel -> gather features/labels), runs the
+GraphSAGE forward/backward, all-reduces gradients (NCCL, N > 1) and applies
+Adam.  Per-GPU work is fixed (weak scaling).  `value` is the epoch time in
+seconds: ms_per_step x steps_per_epoch(N), with steps_per_epoch =
+ceil(1172 / N) at papers shape (K < steps_per_epoch is extrapolated and says
+so in config).  Inputs (graph, features, labels) are generated directly in
+HBM and are far larger than L2 (36 GB vs 126 MB).
+
+`--impl reference` times the reference's CPU batch-preparation path (the C
+restatement in oracle/, pinned to the reference's golden vectors) on all
+host cores over a bounded sample of the same epoch, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+SHAPES = {
+    # name: (nodes, directed slots, feature dim, classes, train ids, test ids)
+    "papers": (111_059_956, 1_615_685_872, 128, 172, 1_207_179, 214_338),
+    "products": (2_449_029, 61_859_140, 100, 47, 196_615, 2_213_091),
+    "arxiv": (169_343, 1_166_243, 128, 40, 90_941, 48_603),
+    "c1": (100_000, 1_000_000, 128, 172, 100_000, 0),
+}
+WORKLOAD = {
+    "papers": "ogbn-papers100M-shaped synthetic (111M nodes, 1.6B slots, 128-d fp16), 3-layer "
+              "GraphSAGE hidden 256, batch 1024/GPU",
+    "products": "ogbn-products-shaped synthetic (2.4M nodes, 62M slots, 100-d fp16)",
+    "arxiv": "ogbn-arxiv-shaped synthetic (169K nodes, 1.17M slots, 128-d fp16)",
+    "c1": "synthetic power-law 100K nodes / 1M slots, 128-d fp16",
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=0, help="0 = one full epoch")
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--shape", choices=list(SHAPES), default="papers")
+    p.add_argument("--fanouts", default="15,10,5")
+    p.add_argument("--hidden", type=int, default=256)
+    p.add_argument("--depth", type=int, default=1)
+    p.add_argument("--gather-free", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--kernel-batches", type=int, default=20)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        torch.distributed.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        return json.loads((REPO / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def build_data(shape: str, seed: int = 1):
+    from paper_2110_08450_b200.graph import synth_graph_device
+    n, slots, f, c, ntrain, ntest = SHAPES[shape]
+    t0 = time.perf_counter()
+    dg = synth_graph_device(n, slots / n, 3.0, seed=seed, num_features=f, num_classes=c,
+                            feature_seed=seed, label_seed=seed)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed + 100)
+    perm = torch.randperm(n, device="cuda", generator=gen)
+    train = perm[:ntrain].sort().values.cpu().numpy()
+    test = perm[ntrain:ntrain + ntest].sort().values.cpu().numpy()
+    torch.cuda.synchronize()
+    return dg, train, test, time.perf_counter() - t0
+
+
+# ---------------------------------------------------------------------------
+def kernel_profile(trainer, nbatches: int):
+    """Prep-only pass: CUDA-event durations of the MFG build and the gather.
+
+    Returns sampled edges/s, gather GB/s and the per-launch gather figures
+    used for the roofline."""
+    from paper_2110_08450_b200.prep import gather_rows
+    slot = trainer.slots[0]
+    ws = slot.ws
+    L = trainer.nh
+    st = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t_mfg = t_gat = 0.0
+    edges = nodes = 0
+    x = trainer.x_table
+    f = x.shape[1]
+    for b in range(nbatches):
+        step = b % max(trainer.steps_per_epoch, 1)
+        ev[0].record(st)
+        ws.run(trainer.dg, trainer.seeds_all, trainer.desc_all[step], trainer.cfg.global_seed,
+               trainer.policy, st)
+        ev[1].record(st)
+        gather_rows(x, ws.globals, slot.feats[:, :f], n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
+                    stream=st)
+        ev[2].record(st)
+        sizes, etot = ws.read_extents()
+        if b == 0:
+            continue  # warm-up
+        t_mfg += ev[0].elapsed_time(ev[1]) / 1e3
+        t_gat += ev[1].elapsed_time(ev[2]) / 1e3
+        edges += sum(etot)
+        nodes += sizes[-1]
+    k = nbatches - 1
+    elem = x.element_size()
+    gat_bytes = nodes * f * (elem + elem) + 4 * nodes  # read rows + write rows + ids
+    return {
+        "sampled_edges_per_s": edges / t_mfg,
+        "mfg_ms_per_batch": 1e3 * t_mfg / k,
+        "edges_per_batch": edges / k,
+        "nodes_per_batch": nodes / k,
+        "gather_GBps": gat_bytes / t_gat / 1e9,
+        "gather_ms_per_launch": 1e3 * t_gat / k,
+        "gather_bytes_per_launch": gat_bytes / k,
+    }
+
+
+def cpu_baseline(dg, trainer, fanouts, target_s: float, global_seed: int):
+    """Reference CPU prep path (oracle port) on all host cores, bounded sample."""
+    sys.path.insert(0, str(REPO / "oracle"))
+    import oracle as O
+    t0 = time.perf_counter()
+    indptr = dg.indptr.cpu().numpy()
+    indices = dg.indices.cpu().numpy()
+    feats = dg.feature_view().cpu().numpy()
+    copy_s = time.perf_counter() - t0
+    cores = os.cpu_count() or 1
+    plan = trainer.plan
+    nb = len(plan)
+    order = [(b.batch_id, b.dst_ids) for b in plan.batches]
+    probe = order[:cores]
+    wall, stats, _ = O.epoch_prep(indptr, indices, dg.num_nodes, feats, None, probe,
+                                  fanouts.per_hop, global_seed, cores)
+    per_batch_wall = wall / len(probe)
+    want = int(min(nb, max(len(probe), target_s / max(per_batch_wall, 1e-6))))
+    sample = order[:want]
+    wall, stats, _ = O.epoch_prep(indptr, indices, dg.num_nodes, feats, None, sample,
+                                  fanouts.per_hop, global_seed, cores)
+    epoch_s = wall * nb / len(sample)
+    edges = int(stats[:, 1].sum())
+    samp_s = stats[:, 2].sum() / 1e9
+    slic_s = stats[:, 3].sum() / 1e9
+    nodes = int(stats[:, 0].sum())
+    f = feats.shape[1]
+    return {
+        "value": epoch_s, "unit": "s", "cores": cores, "kind": "port",
+        "sample": f"{len(sample)} of {nb} epoch batches (first in plan order), extrapolated "
+                  f"to the full epoch; {cores} threads, batch-level parallel like "
+                  f"prep.py:255-287; f16 features gathered to f32",
+        "wall_s": wall, "batches": len(sample),
+        "sampled_edges_per_s": edges / wall,
+        "sampled_edges_per_s_per_core": edges / samp_s if samp_s else None,
+        "gather_GBps_per_core": nodes * f * 6 / slic_s / 1e9 if slic_s else None,
+        "host_copy_s": copy_s,
+    }
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the reference CPU path on the host cores (rank 0 only)."""
+    rank, world, local = dist_setup(args)
+    if rank != 0:
+        barrier(world)
+        return
+    from paper_2110_08450_b200 import FanoutSpec
+    from paper_2110_08450_b200.train import TrainConfig, Trainer
+    fan = FanoutSpec(tuple(int(x) for x in args.fanouts.split(",")))
+    dg, train, _, _ = build_data(args.shape)
+    tr = Trainer(dg, train, TrainConfig(fanouts=fan, hidden=8))
+    spe_1 = tr.set_epoch(0)
+    cb = cpu_baseline(dg, tr, fan, args.cpu_seconds * 2, 1)
+    nb = len(tr.plan)
+    steps = math.ceil(nb / world)
+    line = {
+        "metric": "papers100M-shape epoch time (s) at 1/2/4/8 B200; sampled edges/s; gather GB/s",
+        "impl": "reference", "value": cb["value"], "unit": "s", "n_gpus": world,
+        "steps": args.steps or steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * cb["value"] / nb, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64/f32", "data": "synthetic (device-generated, copied "
+        "to host)", "config": {"workload": WORKLOAD[args.shape] + " — batch preparation only "
+                               "(the reference has no training step)",
+                               "fanouts": args.fanouts, "batch": 1024, "batches_per_epoch": nb},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": "s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "sampled_edges_per_s": cb["sampled_edges_per_s"],
+        "gather_GBps_per_core": cb["gather_GBps_per_core"],
+    }
+    print(json.dumps(line), flush=True)
+    barrier(world)
+
+
+def run_ours(args):
+    from paper_2110_08450_b200 import FanoutSpec, _lib
+    from paper_2110_08450_b200.train import TrainConfig, Trainer
+    rank, world, local = dist_setup(args)
+    fan = FanoutSpec(tuple(int(x) for x in args.fanouts.split(",")))
+    dg, train, test, gen_s = build_data(args.shape)
+    cfg = TrainConfig(fanouts=fan, hidden=args.hidden, depth=args.depth,
+                      gather_free=args.gather_free)
+    tr = Trainer(dg, train, cfg, rank=rank, world=world)
+    spe = tr.set_epoch(0)
+    K = args.steps if args.steps > 0 else spe
+    W = max(args.warmup, 3)
+    L = _lib.lib()
+
+    def timed(count, host_inputs=False):
+        start_step = 0
+        loss_out = torch.zeros(count, dtype=torch.float32).pin_memory() if host_inputs else None
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        torch.cuda.synchronize()
+        n0 = L.sal_launch_count()
+        ev0.record()
+        # epoch wraps: run in chunks of at most one epoch
+        done = 0
+        while done < count:
+            chunk = min(count - done, spe - start_step)
+            tr.train_steps(start_step, chunk, host_inputs=host_inputs,
+                           loss_out=None if loss_out is None else loss_out[done:done + chunk])
+            done += chunk
+            start_step = (start_step + chunk) % spe
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+        ms = ev0.elapsed_time(ev1)
+        return max_over_ranks(ms, world), L.sal_launch_count() - n0, loss_out
+
+    # warm-up (also JIT/cuBLAS heuristics)
+    tr.train_steps(0, min(W, spe))
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms, launches, _ = timed(K)
+    ms_step = ms / K
+    epoch_s = ms_step * spe / 1e3
+    e2e = None
+    if not args.no_e2e:
+        ms2, _, loss_host = timed(K, host_inputs=True)
+        e2e = {"value": ms2 / K * spe / 1e3, "unit": "s",
+               "h2d_bytes_per_step": 8 * (cfg.batch_size + 3),
+               "d2h_bytes_per_step": 4,
+               "ms_per_step": ms2 / K,
+               "path": "Trainer.train_steps(host_inputs=True): seeds + batch descriptor H2D "
+                       "from pinned memory each step, loss D2H each step"}
+    kp = kernel_profile(tr, args.kernel_batches) if rank == 0 else None
+    line = None
+    if rank == 0:
+        peaks = measured_peaks()
+        peak = peaks.get("hbm_gbs")
+        peak_src = "measured" if peak else "fallback"
+        peak = peak or 6650.0
+        ach = kp["gather_GBps"]
+        line = {
+            "metric": "papers100M-shape epoch time (s) at 1/2/4/8 B200; sampled edges/s; "
+                      "gather GB/s",
+            "value": round(epoch_s, 4), "unit": "s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": round(ms_step, 4), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (generated in HBM: synth_graph law, uniform fp16 features, "
+                    "uniform labels)",
+            "config": {"workload": WORKLOAD[args.shape], "fanouts": args.fanouts,
+                       "fanout_order": "reference FanoutSpec (outermost hop first)",
+                       "global_batch": cfg.batch_size * world, "batch_per_gpu": cfg.batch_size,
+                       "steps_per_epoch": spe, "epoch_extrapolated": K < spe,
+                       "parallelism": f"dp{world}", "hidden": args.hidden,
+                       "gather_free": args.gather_free, "prefetch_depth": args.depth,
+                       "l2": "inputs (36 GB graph+features) far larger than L2; no flush",
+                       "graph_gen_s": round(gen_s, 2)},
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "sampled_edges_per_s": kp["sampled_edges_per_s"],
+            "gather_GBps": kp["gather_GBps"],
+            "kernels": kp,
+            "roofline": {"kernel": "gather_rows_kernel (fp16 rows, 128-bit)", "bound": "hbm",
+                         "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4), "peak_source": peak_src,
+                         "traffic": None,
+                         "bytes_per_launch": kp["gather_bytes_per_launch"],
+                         "ms_per_launch": kp["gather_ms_per_launch"]},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_baseline(dg, tr, fan, args.cpu_seconds, cfg.global_seed)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
+                                                       "sample")}
+            line["cpu_baseline_detail"] = cb
+        print(json.dumps(line), flush=True)
+    barrier(world)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+    if torch.distributed.is_initialized():
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -103,6 +103,8 @@ typedef struct {
 /* ---- library ------------------------------------------------------------ */
 int sal_version(void);
 const char* sal_last_error(void);
+/* number of kernels this library has enqueued in this process (launch audit) */
+long long sal_launch_count(void);
 
 /* HopStream.key_prefix (sampler.py:238-247) */
 uint64_t sal_hop_key_prefix(uint64_t global_seed, int64_t batch_id, int64_t hop);
@@ -164,7 +166,8 @@ int sal_gather_rows(const void* x_dev, int64_t x_rows, int32_t cols, int64_t x_s
                     int32_t in_dtype, const void* ids_dev, int32_t id_bytes,
                     const int64_t* n_dev, int64_t n, void* out_dev, int64_t out_stride,
                     int32_t out_dtype, void* stream);
-/* gather_labels (_kernels.py:255-258): out[j] = y[seeds[j]] */
+/* gather_labels (_kernels.py:255-258): out[j] = y[seeds[j]] for j < n_seeds;
+ * rows [n_seeds, max_n) are set to -1 (ignore_index of a padded loss) */
 int sal_gather_labels(const int64_t* y_dev, const int64_t* seeds_base_dev,
                       const sal_batch_desc* desc_dev, int64_t max_n, int64_t* out_dev,
                       void* stream);

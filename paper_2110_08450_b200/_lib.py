@@ -59,6 +59,7 @@ P = ctypes.POINTER
 SIGNATURES = {
     "sal_version": (ctypes.c_int, []),
     "sal_last_error": (ctypes.c_char_p, []),
+    "sal_launch_count": (ctypes.c_longlong, []),
     "sal_hop_key_prefix": (u64, [u64, i64, i64]),
     "sal_mfg_plan_init": (ctypes.c_int, [P(SalMfgPlan), i32, P(i32), i64, i64]),
     "sal_mfg_layout_init": (ctypes.c_int, [P(SalMfgPlan), P(SalMfgLayout)]),

@@ -3,6 +3,7 @@
 // Argument validation happens here, before any launch, and reports through a
 // thread-local message (the reference raises ValueError in Python before its
 // kernels run: sampler.py:99-100, 311-317; prep.py:160-164).
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -13,6 +14,12 @@
 namespace {
 
 thread_local char g_err[512] = "";
+std::atomic<long long> g_launches{0};  // kernels enqueued by this library
+
+int counted(int rc, int kernels) {
+  if (rc == SAL_OK) g_launches.fetch_add(kernels, std::memory_order_relaxed);
+  return rc;
+}
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -63,6 +70,8 @@ extern "C" {
 int sal_version(void) { return 100; }
 
 const char* sal_last_error(void) { return g_err; }
+
+long long sal_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 uint64_t sal_hop_key_prefix(uint64_t global_seed, int64_t batch_id, int64_t hop) {
   return sal::hop_key_prefix(global_seed, (uint64_t)batch_id, (uint64_t)hop);
@@ -183,7 +192,7 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
                                 src_glob, slot, rank, src_local, scan, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop relabel");
   }
-  return SAL_OK;
+  return counted(SAL_OK, 1 + 4 * plan->num_hops);
 }
 
 // ---------------------------------------------------------------------------
@@ -205,7 +214,7 @@ int sal_idmap_rehash(const sal_idmap* m, int64_t n, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(m->table, 0xFF, m->table_cap * 8, st);
   if (e != cudaSuccess) return cuda_status(e, "idmap_rehash: reset");
-  return cuda_status(sal::launch_rehash(d, n, st), "idmap_rehash");
+  return counted(cuda_status(sal::launch_rehash(d, n, st), "idmap_rehash"), 1);
 }
 
 int sal_idmap_insert(const sal_idmap* m, const int64_t* keys, int64_t n,
@@ -226,7 +235,7 @@ int sal_idmap_insert(const sal_idmap* m, const int64_t* keys, int64_t n,
   if (e != cudaSuccess) return cuda_status(e, "idmap_insert");
   e = sal::launch_hop_relabel(d, n_dev_scratch, n, size_old, size_new, scratch_glob, scratch_slot,
                               scratch_rank, local_out, scan_ws, st);
-  return cuda_status(e, "idmap_insert: relabel");
+  return counted(cuda_status(e, "idmap_insert: relabel"), 3);
 }
 
 int sal_hop_count(const sal_graph* g, const int32_t* globals, const int64_t* n_dst_dev,
@@ -236,9 +245,9 @@ int sal_hop_count(const sal_graph* g, const int32_t* globals, const int64_t* n_d
       e_total == nullptr || scan_ws == nullptr)
     return fail(SAL_EINVAL, "hop_count: null argument");
   if (fanout < 0) return fail(SAL_EINVAL, "hop_count: fanout must be >= 0");
-  return cuda_status(sal::launch_hop_count(to_dev(g), globals, n_dst_dev, max_dst, fanout,
+  return counted(cuda_status(sal::launch_hop_count(to_dev(g), globals, n_dst_dev, max_dst, fanout,
                                            dst_indptr, e_total, scan_ws, (cudaStream_t)stream),
-                     "hop_count");
+                     "hop_count"), 1);
 }
 
 int sal_hop_sample(const sal_graph* g, const sal_idmap* m, const int64_t* n_dst_dev,
@@ -260,10 +269,10 @@ int sal_hop_sample(const sal_graph* g, const sal_idmap* m, const int64_t* n_dst_
   hk.hop = (uint32_t)hop;
   hk.batch = (uint32_t)batch_id;
   hk.derive = 0;
-  return cuda_status(sal::launch_hop_sample(to_dev(g), d, n_dst_dev, max_dst, fanout, hk, nullptr,
+  return counted(cuda_status(sal::launch_hop_sample(to_dev(g), d, n_dst_dev, max_dst, fanout, hk, nullptr,
                                             rng_policy, inject_pos, dst_indptr, src_glob, slot,
                                             draws_out, (cudaStream_t)stream),
-                     "hop_sample");
+                     "hop_sample"), 1);
 }
 
 int sal_hop_relabel(const sal_idmap* m, const int64_t* e_total, int64_t max_edges,
@@ -276,10 +285,10 @@ int sal_hop_relabel(const sal_idmap* m, const int64_t* e_total, int64_t max_edge
   if (e_total == nullptr || size_old == nullptr || size_new == nullptr || src_glob == nullptr ||
       slot == nullptr || rank == nullptr || scan_ws == nullptr)
     return fail(SAL_EINVAL, "hop_relabel: null argument");
-  return cuda_status(sal::launch_hop_relabel(d, e_total, max_edges, size_old, size_new, src_glob,
+  return counted(cuda_status(sal::launch_hop_relabel(d, e_total, max_edges, size_old, size_new, src_glob,
                                              slot, rank, src_local, scan_ws,
                                              (cudaStream_t)stream),
-                     "hop_relabel");
+                     "hop_relabel"), 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -299,19 +308,19 @@ int sal_gather_rows(const void* x, int64_t x_rows, int32_t cols, int64_t x_strid
   if (cols == 0) return SAL_OK;
   if (x == nullptr || ids == nullptr || out == nullptr)
     return fail(SAL_EINVAL, "gather_rows: null argument");
-  return cuda_status(sal::launch_gather_rows(x, x_rows, cols, x_stride, in_dtype, ids, id_bytes,
+  return counted(cuda_status(sal::launch_gather_rows(x, x_rows, cols, x_stride, in_dtype, ids, id_bytes,
                                              n_dev, n, out, out_stride, out_dtype,
                                              (cudaStream_t)stream),
-                     "gather_rows");
+                     "gather_rows"), 1);
 }
 
 int sal_gather_labels(const int64_t* y, const int64_t* seeds_base, const sal_batch_desc* desc,
                       int64_t max_n, int64_t* out, void* stream) {
   if (y == nullptr || seeds_base == nullptr || desc == nullptr || out == nullptr)
     return fail(SAL_EINVAL, "gather_labels: null argument");
-  return cuda_status(
+  return counted(cuda_status(
       sal::launch_gather_labels(y, seeds_base, desc, max_n, out, (cudaStream_t)stream),
-      "gather_labels");
+      "gather_labels"), 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -327,10 +336,10 @@ int sal_segment_mean_fwd(const int32_t* indptr, const int32_t* src, const int64_
   if (n_pad == 0 || f == 0) return SAL_OK;
   if (indptr == nullptr || src == nullptr || h == nullptr || out == nullptr)
     return fail(SAL_EINVAL, "segment_mean_fwd: null argument");
-  return cuda_status(sal::launch_segment_mean_fwd(indptr, src, nullptr, n_dst_dev, n_pad, h,
+  return counted(cuda_status(sal::launch_segment_mean_fwd(indptr, src, nullptr, n_dst_dev, n_pad, h,
                                                   h_dtype, h_stride, f, out, out_dtype,
                                                   out_stride, (cudaStream_t)stream),
-                     "segment_mean_fwd");
+                     "segment_mean_fwd"), 1);
 }
 
 int sal_segment_mean_fwd_global(const int32_t* indptr, const int32_t* src,
@@ -343,10 +352,10 @@ int sal_segment_mean_fwd_global(const int32_t* indptr, const int32_t* src,
   if (n_pad == 0 || f == 0) return SAL_OK;
   if (indptr == nullptr || src == nullptr || globals == nullptr || x == nullptr || out == nullptr)
     return fail(SAL_EINVAL, "segment_mean_fwd_global: null argument");
-  return cuda_status(sal::launch_segment_mean_fwd(indptr, src, globals, n_dst_dev, n_pad, x,
+  return counted(cuda_status(sal::launch_segment_mean_fwd(indptr, src, globals, n_dst_dev, n_pad, x,
                                                   x_dtype, x_stride, f, out, out_dtype,
                                                   out_stride, (cudaStream_t)stream),
-                     "segment_mean_fwd_global");
+                     "segment_mean_fwd_global"), 1);
 }
 
 int sal_segment_mean_bwd(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
@@ -357,10 +366,10 @@ int sal_segment_mean_bwd(const int32_t* indptr, const int32_t* src, const int64_
   if (n_pad == 0 || f == 0) return SAL_OK;
   if (indptr == nullptr || src == nullptr || g_out == nullptr || g_h == nullptr)
     return fail(SAL_EINVAL, "segment_mean_bwd: null argument");
-  return cuda_status(sal::launch_segment_mean_bwd(indptr, src, n_dst_dev, n_pad, g_out, g_dtype,
+  return counted(cuda_status(sal::launch_segment_mean_bwd(indptr, src, n_dst_dev, n_pad, g_out, g_dtype,
                                                   g_stride, f, g_h, gh_stride,
                                                   (cudaStream_t)stream),
-                     "segment_mean_bwd");
+                     "segment_mean_bwd"), 1);
 }
 
 }  // extern "C"

@@ -206,15 +206,16 @@ cudaError_t launch_gather_rows(const void* x, int64_t x_rows, int32_t cols, int6
                                                   out, out_stride, st);
 }
 
+// rows [n_seeds, max_n) receive -1 (an ignore_index for a padded loss)
 __global__ void gather_labels_kernel(const int64_t* __restrict__ y,
                                      const int64_t* __restrict__ seeds_base,
-                                     const BatchDesc* __restrict__ desc,
+                                     const BatchDesc* __restrict__ desc, int64_t max_n,
                                      int64_t* __restrict__ out) {
   const int64_t n = desc->n_seeds;
   const int64_t* seeds = seeds_base + desc->seed_offset;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < max_n;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = y[seeds[i]];
+    out[i] = i < n ? y[seeds[i]] : -1;
 }
 
 cudaError_t launch_gather_labels(const int64_t* y, const int64_t* seeds_base,
@@ -223,7 +224,7 @@ cudaError_t launch_gather_labels(const int64_t* y, const int64_t* seeds_base,
   int64_t grid = (max_n + 255) / 256;
   if (grid < 1) grid = 1;
   if (grid > 1024) grid = 1024;
-  gather_labels_kernel<<<(int)grid, 256, 0, st>>>(y, seeds_base, desc, out);
+  gather_labels_kernel<<<(int)grid, 256, 0, st>>>(y, seeds_base, desc, max_n, out);
   return cudaGetLastError();
 }
 

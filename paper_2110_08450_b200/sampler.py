@@ -156,7 +156,7 @@ class SeedBatch:
     dst_ids: np.ndarray
 
     def __post_init__(self):
-        ids = np.asarray(self.dst_ids, dtype=np.int64).reshape(-1)
+        ids = np.ascontiguousarray(np.asarray(self.dst_ids, dtype=np.int64).reshape(-1))
         object.__setattr__(self, "dst_ids", ids)
         if len(np.unique(ids)) != len(ids):
             raise ValueError("seed IDs must be distinct")
@@ -226,7 +226,8 @@ class IdMap:
 
     def insert(self, keys) -> None:
         """get-or-insert each key in order (insert_keys, _kernels.py:216-222)."""
-        k = torch.as_tensor(np.asarray(keys, dtype=np.int64).reshape(-1)).to(self.device)
+        k = torch.from_numpy(np.ascontiguousarray(np.asarray(keys, dtype=np.int64).reshape(-1)))
+        k = k.to(self.device)
         n = k.numel()
         if n == 0:
             return
