@@ -326,7 +326,7 @@ def synth_graph_device(n: int, avg_degree: float, exponent: float = 3.0, seed: i
         a = exponent - 1.0
         scale = avg_degree * (a - 1.0) / a
         u = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
-        degs = torch.rint(scale * (1.0 - u).pow(-1.0 / a)).clamp_(0, n - 1).to(torch.int64)
+        degs = torch.round(scale * (1.0 - u).pow(-1.0 / a)).clamp_(0, n - 1).to(torch.int64)
         del u
     else:
         degs = torch.full((n,), int(round(avg_degree)), dtype=torch.int64, device=dev)
