@@ -61,7 +61,7 @@ def parse():
     p.add_argument("--shape", choices=list(SHAPES), default="papers")
     p.add_argument("--fanouts", default="15,10,5")
     p.add_argument("--hidden", type=int, default=256)
-    p.add_argument("--depth", type=int, default=1)
+    p.add_argument("--no-graphs", action="store_true")
     p.add_argument("--gather-free", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -261,7 +261,7 @@ def run_reference(args):
     from paper_2110_08450_b200.train import TrainConfig, Trainer
     fan = FanoutSpec(tuple(int(x) for x in args.fanouts.split(",")))
     dg, train, _, _ = build_data(args.shape)
-    tr = Trainer(dg, train, TrainConfig(fanouts=fan, hidden=8))
+    tr = Trainer(dg, train, TrainConfig(fanouts=fan, hidden=8, graphs=False))
     spe_1 = tr.set_epoch(0)
     cb = cpu_baseline(dg, tr, fan, args.cpu_seconds * 2, 1)
     nb = len(tr.plan)
@@ -291,8 +291,8 @@ def run_ours(args):
     rank, world, local = dist_setup(args)
     fan = FanoutSpec(tuple(int(x) for x in args.fanouts.split(",")))
     dg, train, test, gen_s = build_data(args.shape)
-    cfg = TrainConfig(fanouts=fan, hidden=args.hidden, depth=args.depth,
-                      gather_free=args.gather_free)
+    cfg = TrainConfig(fanouts=fan, hidden=args.hidden, gather_free=args.gather_free,
+                      graphs=not args.no_graphs)
     tr = Trainer(dg, train, cfg, rank=rank, world=world)
     spe = tr.set_epoch(0)
     K = args.steps if args.steps > 0 else spe
@@ -300,30 +300,38 @@ def run_ours(args):
     L = _lib.lib()
 
     def timed(count, host_inputs=False):
-        start_step = 0
+        """Warm up (captures the CUDA graphs), then time `count` steps of a fresh epoch."""
+        tr.set_epoch(0)
+        tr.begin_epoch(host_inputs)
+        tr.run_steps(0, min(max(W, 4), spe), host_inputs=host_inputs)
+        torch.cuda.synchronize()
         loss_out = torch.zeros(count, dtype=torch.float32).pin_memory() if host_inputs else None
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        epoch = 1
+        tr.set_epoch(epoch)
+        tr.begin_epoch(host_inputs)
         barrier(world)
         torch.cuda.synchronize()
         n0 = L.sal_launch_count()
         ev0.record()
-        # epoch wraps: run in chunks of at most one epoch
-        done = 0
+        done, step = 0, 0
         while done < count:
-            chunk = min(count - done, spe - start_step)
-            tr.train_steps(start_step, chunk, host_inputs=host_inputs,
-                           loss_out=None if loss_out is None else loss_out[done:done + chunk])
+            chunk = min(count - done, spe - step)
+            tr.run_steps(step, chunk, host_inputs=host_inputs,
+                         loss_out=None if loss_out is None else loss_out[done:done + chunk])
             done += chunk
-            start_step = (start_step + chunk) % spe
+            step += chunk
+            if step == spe and done < count:  # next epoch (re-primes the pipeline)
+                epoch += 1
+                tr.set_epoch(epoch)
+                tr.begin_epoch(host_inputs)
+                step = 0
         ev1.record()
         torch.cuda.synchronize()
         barrier(world)
         ms = ev0.elapsed_time(ev1)
         return max_over_ranks(ms, world), L.sal_launch_count() - n0, loss_out
 
-    # warm-up (also JIT/cuBLAS heuristics)
-    tr.train_steps(0, min(W, spe))
-    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ms, launches, _ = timed(K)
     ms_step = ms / K
@@ -335,8 +343,9 @@ def run_ours(args):
                "h2d_bytes_per_step": 8 * (cfg.batch_size + 3),
                "d2h_bytes_per_step": 4,
                "ms_per_step": ms2 / K,
-               "path": "Trainer.train_steps(host_inputs=True): seeds + batch descriptor H2D "
-                       "from pinned memory each step, loss D2H each step"}
+               "final_loss": float(loss_host[-1]),
+               "path": "Trainer.run_steps(host_inputs=True): each step's seeds + batch "
+                       "descriptor H2D from pinned host memory, loss D2H to pinned memory"}
     kp = kernel_profile(tr, args.kernel_batches) if rank == 0 else None
     line = None
     if rank == 0:
@@ -358,7 +367,7 @@ def run_ours(args):
                        "global_batch": cfg.batch_size * world, "batch_per_gpu": cfg.batch_size,
                        "steps_per_epoch": spe, "epoch_extrapolated": K < spe,
                        "parallelism": f"dp{world}", "hidden": args.hidden,
-                       "gather_free": args.gather_free, "prefetch_depth": args.depth,
+                       "gather_free": args.gather_free, "cuda_graphs": not args.no_graphs,
                        "l2": "inputs (36 GB graph+features) far larger than L2; no flush",
                        "graph_gen_s": round(gen_s, 2)},
             "clocks": clk.summary(),

@@ -194,6 +194,25 @@ int sal_segment_mean_fwd_global(const int32_t* indptr_dev, const int32_t* src_de
                                 int64_t x_stride, int32_t f, void* out_dev, int32_t out_dtype,
                                 int64_t out_stride, void* stream);
 
+/* ---- training-step helpers (PAPER.md:2577-2585 GraphSAGE step) ---------- */
+/* device epoch cursor: *out = desc_all[*cursor] (or an empty batch past the
+ * end), then ++*cursor — one captured graph prepares a new batch per replay */
+int sal_plan_next(const int64_t* desc_all_dev, int64_t n_steps, int64_t* cursor_dev,
+                  sal_batch_desc* out_dev, void* stream);
+/* y = relu(x) * keep / (1-p), keep ~ Philox(seed, element, *salt_dev);
+ * mask gets one bit per element (x > 0 && keep).  n % 8 == 0. */
+int sal_relu_dropout_fwd(const void* x_dev, void* y_dev, uint8_t* mask_dev, int64_t n,
+                         int32_t dtype, float p, uint64_t seed, const int64_t* salt_dev,
+                         void* stream);
+/* dx = dy * bit / (1-p); dy fp32|bf16 -> dx bf16|fp32 (16-byte aligned) */
+int sal_relu_dropout_bwd(const void* dy_dev, int32_t dy_dtype, const uint8_t* mask_dev,
+                         void* dx_dev, int32_t dx_dtype, int64_t n, float p, void* stream);
+/* log_softmax + NLL (labels < 0 ignored, mean over valid rows) fused with its
+ * gradient: *loss += mean NLL (caller zeroes it); grad = (softmax-onehot)/count */
+int sal_lsm_nll(const void* logits_dev, int64_t ld, int64_t rows, int32_t num_classes,
+                int32_t dtype, const int64_t* labels_dev, float* loss_dev, void* grad_dev,
+                int64_t ldg, void* stream);
+
 /* ---- on-device synthetic data (graph.py:252-298 laws) ---- */
 /* owner[s] = v for every slot s in [indptr[v], indptr[v+1]) */
 int sal_gen_owner(const int64_t* indptr_dev, int64_t n, int32_t* owner_dev, void* stream);

@@ -14,7 +14,13 @@
 namespace {
 
 thread_local char g_err[512] = "";
+}  // namespace
+namespace sal {
 std::atomic<long long> g_launches{0};  // kernels enqueued by this library
+void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+}  // namespace sal
+namespace {
+using sal::g_launches;
 
 int counted(int rc, int kernels) {
   if (rc == SAL_OK) g_launches.fetch_add(kernels, std::memory_order_relaxed);

@@ -120,6 +120,66 @@ gather_rows_kernel(const TIn* __restrict__ x, int64_t x_stride, const TId* __res
   }
 }
 
+// Warp-row variant for rows of LPR x 16 B (LPR divides 32): a warp owns 32
+// consecutive output rows at a time — one coalesced load of their 32 ids
+// (prefetched one iteration ahead), then 32/LPR rows per instruction with
+// kRowUnroll instructions in flight before the stores.
+constexpr int kRowUnroll = 8;
+
+template <typename TIn, typename TOut, int LPR, typename TId>
+__global__ void __launch_bounds__(kGatherThreads)
+gather_rows_warp_kernel(const TIn* __restrict__ x, int64_t x_stride, const TId* __restrict__ ids,
+                        const int64_t* __restrict__ n_dev, int64_t n_host, TOut* __restrict__ out,
+                        int64_t out_stride) {
+  constexpr int EPV = 16 / (int)sizeof(TIn);
+  constexpr int VOUT = EPV * (int)sizeof(TOut);
+  constexpr int RPI = 32 / LPR;
+  constexpr int kPhase = RPI * kRowUnroll;  // rows per phase
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / LPR, sub = lane % LPR;
+  const int64_t n = n_dev ? *n_dev : n_host;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t r0 = warp * 32;
+  int64_t my = (r0 + lane < n) ? (int64_t)ids[r0 + lane] : 0;
+  for (; r0 < n; r0 += nwarps * 32) {
+    const int64_t rn = r0 + nwarps * 32;
+    const int64_t next = (rn + lane < n) ? (int64_t)ids[rn + lane] : 0;
+#pragma unroll
+    for (int ph = 0; ph < 32; ph += kPhase) {
+      uint4 buf[kRowUnroll];
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int r = ph + u * RPI + grp;
+        const int64_t s = __shfl_sync(0xffffffffu, my, r & 31);
+        if (r0 + r < n) {
+          const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(x + s * x_stride) + sub);
+          buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int r = ph + u * RPI + grp;
+        if (r0 + r < n) {
+          const TIn* v = reinterpret_cast<const TIn*>(&buf[u]);
+          TOut o[EPV];
+#pragma unroll
+          for (int j = 0; j < EPV; ++j) o[j] = convert<TIn, TOut>(v[j]);
+          TOut* dst = out + (r0 + r) * out_stride + (int64_t)sub * EPV;
+#pragma unroll
+          for (int q = 0; q < (VOUT + 15) / 16; ++q) {
+            if (VOUT >= 16)
+              store_vec<16>((char*)dst + 16 * q, (char*)o + 16 * q);
+            else
+              store_vec<(VOUT < 16 ? VOUT : 16)>(dst, o);
+          }
+        }
+      }
+    }
+    my = next;
+  }
+}
+
 template <typename TIn, typename TOut, typename TId>
 static cudaError_t gather_dispatch(const void* x, int32_t cols, int64_t x_stride, const void* ids,
                                    const int64_t* n_dev, int64_t n, void* out,
@@ -138,7 +198,29 @@ static cudaError_t gather_dispatch(const void* x, int32_t cols, int64_t x_stride
     vin >>= 1;
   }
   const int32_t cpr = (int32_t)(in_row_bytes / vin);
-  const int64_t max_items = (n_dev ? n : n) * (int64_t)cpr;
+  if (vin == 16 && cpr <= 32 && (32 % cpr) == 0 && (int)sizeof(TIn) <= 16) {
+    // whole rows per warp: the fast path for 16 B-aligned rows (f = 128 fp16 -> 16 lanes)
+    const int64_t warps = (n + 31) / 32;
+    int64_t wgrid = (warps + 7) / 8;
+    const int64_t wcap = (int64_t)num_sms() * 8;
+    if (wgrid > wcap) wgrid = wcap;
+    if (wgrid < 1) wgrid = 1;
+#define SAL_GW_CASE(L)                                                                       \
+  case L:                                                                                    \
+    gather_rows_warp_kernel<TIn, TOut, L, TId><<<(int)wgrid, kGatherThreads, 0, st>>>(        \
+        (const TIn*)x, x_stride, (const TId*)ids, n_dev, n, (TOut*)out, out_stride);         \
+    return cudaGetLastError();
+    switch (cpr) {
+      SAL_GW_CASE(1)
+      SAL_GW_CASE(2)
+      SAL_GW_CASE(4)
+      SAL_GW_CASE(8)
+      SAL_GW_CASE(16)
+      SAL_GW_CASE(32)
+    }
+#undef SAL_GW_CASE
+  }
+  const int64_t max_items = n * (int64_t)cpr;
   int64_t grid = (max_items + kGatherThreads * kUnroll - 1) / (kGatherThreads * kUnroll);
   const int64_t cap = (int64_t)num_sms() * 8;
   if (grid > cap) grid = cap;

@@ -36,6 +36,7 @@ struct HopKey {
 };
 
 int num_sms();
+void count_launch(int kernels);
 int log2_exact(int64_t cap);
 size_t scan_ws_bytes(int64_t max_items);
 

@@ -148,6 +148,75 @@ segment_mean_fwd_kernel(const int32_t* __restrict__ indptr, const int32_t* __res
   }
 }
 
+// Fast path for 16-bit rows of 16 B multiples: LPR lanes cover one row with
+// 16-byte vectors, so a warp loads 32/LPR source rows per instruction and
+// keeps kU such instructions in flight (all ~15 sampled edges of a typical
+// destination in one round).  The per-group partial sums are combined with
+// xor-shuffles at the end, so the summation order differs from the strict
+// edge order of segment_mean_fwd_kernel (used for fp32 parity).
+template <typename TIn, typename TOut, int LPR, bool kGlobal>
+__global__ void __launch_bounds__(kSegThreads)
+segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
+                         const int32_t* __restrict__ globals,
+                         const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
+                         const TIn* __restrict__ h, int64_t h_stride, TOut* __restrict__ out,
+                         int64_t out_stride) {
+  constexpr int RPI = 32 / LPR;
+  constexpr int kU = 8;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / LPR, sub = lane % LPR;
+  const int64_t n_dst = n_dst_dev ? *n_dst_dev : n_pad;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t d = warp; d < n_pad; d += nwarps) {
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    int32_t cnt = 0;
+    if (d < n_dst) {
+      const int32_t beg = indptr[d];
+      const int32_t end = indptr[d + 1];
+      cnt = end - beg;
+      for (int32_t e0 = beg; e0 < end; e0 += 32) {
+        const int m = min(32, end - e0);
+        int32_t my = 0;
+        if (lane < m) {
+          my = src[e0 + lane];
+          if (kGlobal) my = globals[my];
+        }
+        for (int k = 0; k < m; k += RPI * kU) {
+          uint4 buf[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int idx = k + u * RPI + grp;
+            const int64_t s = __shfl_sync(0xffffffffu, my, idx & 31);
+            if (idx < m)
+              buf[u] = __ldg(reinterpret_cast<const uint4*>(h + s * h_stride) + sub);
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            if (k + u * RPI + grp < m) {
+              const TIn* v = reinterpret_cast<const TIn*>(&buf[u]);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) acc[j] += Cvt<TIn>::in(v[j]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int off = LPR; off < 32; off <<= 1)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+      if (cnt > 0) {
+        const float fc = (float)cnt;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = __fdiv_rn(acc[j], fc);
+      }
+    }
+    if (grp == 0) store_row<TOut, 8>(out + d * out_stride + sub * 8, acc);
+  }
+}
+
 template <typename TG, int V>
 __global__ void __launch_bounds__(kSegThreads)
 segment_mean_bwd_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
@@ -210,10 +279,43 @@ static int seg_grid(int64_t rows) {
 }
 
 template <typename TIn, typename TOut, bool kGlobal>
+static bool fwd_rows(const int32_t* indptr, const int32_t* src, const int32_t* globals,
+                     const int64_t* n_dst_dev, int64_t n_pad, const void* h, int64_t h_stride,
+                     int32_t f, void* out, int64_t out_stride, cudaStream_t st) {
+  if (sizeof(TIn) != 2 || f % 8 != 0) return false;
+  const int lpr = f / 8;
+  if (lpr > 32 || (32 % lpr) != 0) return false;
+  if (h_stride % 8 != 0 || out_stride % 8 != 0 || ((uintptr_t)h % 16) != 0 ||
+      ((uintptr_t)out % 16) != 0)
+    return false;
+  const int grid = seg_grid(n_pad);
+  const TIn* hp = (const TIn*)h;
+  TOut* op = (TOut*)out;
+#define SAL_ROWS_CASE(L)                                                                     \
+  case L:                                                                                    \
+    segment_mean_rows_kernel<TIn, TOut, L, kGlobal><<<grid, kSegThreads, 0, st>>>(            \
+        indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);              \
+    return true;
+  switch (lpr) {
+    SAL_ROWS_CASE(1)
+    SAL_ROWS_CASE(2)
+    SAL_ROWS_CASE(4)
+    SAL_ROWS_CASE(8)
+    SAL_ROWS_CASE(16)
+    SAL_ROWS_CASE(32)
+  }
+#undef SAL_ROWS_CASE
+  return false;
+}
+
+template <typename TIn, typename TOut, bool kGlobal>
 static cudaError_t fwd_typed(const int32_t* indptr, const int32_t* src, const int32_t* globals,
                              const int64_t* n_dst_dev, int64_t n_pad, const void* h,
                              int64_t h_stride, int32_t f, void* out, int64_t out_stride,
                              cudaStream_t st) {
+  if (fwd_rows<TIn, TOut, kGlobal>(indptr, src, globals, n_dst_dev, n_pad, h, h_stride, f, out,
+                                    out_stride, st))
+    return cudaGetLastError();
   // vector width: 16 B of the narrower side, capped so one pass covers f
   const int max_v = 16 / (int)(sizeof(TIn) < sizeof(TOut) ? sizeof(TIn) : sizeof(TOut));
   int v = pick_vec(f, h_stride, out_stride, max_v);

@@ -134,3 +134,173 @@ class GraphSAGE(nn.Module):
                 if self.dropout and self.training:
                     h = F.dropout(h, p=self.dropout, training=True)
         return torch.log_softmax(h.float(), dim=-1)
+
+
+# ---------------------------------------------------------------------------
+# Explicit-backward GraphSAGE for the training hot path
+# ---------------------------------------------------------------------------
+class FusedSAGE:
+    """GraphSAGE with a hand-scheduled forward/backward (no autograd graph).
+
+    Parameters live in one flat fp32 buffer (Adam updates it with one fused
+    kernel); a bf16 shadow copy feeds the tensor-core GEMMs and is refreshed
+    with one cast after each optimizer step.  Weight gradients are written
+    straight into the flat fp32 gradient buffer by cuBLAS (bf16 x bf16 ->
+    fp32 output), so there is no gradient zeroing or accumulation pass, and
+    the flat buffer is what the data-parallel all-reduce sends.
+
+    Per layer i (consumption order):
+        mean_i = segment_mean(h_i)                         (library kernel)
+        z_i    = h_i[:n_pad_i] @ Ws_i^T + mean_i @ Wn_i^T  (2 cuBLAS GEMMs)
+        h_i+1  = relu_dropout(z_i)                         (library kernel)
+    loss = lsm_nll(z_L-1, labels)  (fused log_softmax + NLL + gradient)
+    """
+
+    def __init__(self, f_in: int, hidden: int, num_classes: int, num_layers: int = 3,
+                 dropout: float = 0.5, device=None, seed: int = 0,
+                 act_dtype: torch.dtype = torch.bfloat16):
+        dev = torch.device(device or "cuda")
+        self.dims = [f_in] + [hidden] * (num_layers - 1) + [num_classes]
+        self.L = num_layers
+        self.p = float(dropout)
+        self.act = act_dtype
+        shapes = []
+        for a, b in zip(self.dims[:-1], self.dims[1:]):
+            shapes += [(b, a), (b, a)]   # (w_neigh, w_self) per layer
+        total = sum(r * c for r, c in shapes)
+        self.flat = torch.empty(total, dtype=torch.float32, device=dev)
+        self.grad = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.shadow = torch.empty(total, dtype=act_dtype, device=dev)
+        g = torch.Generator(device="cpu")
+        g.manual_seed(seed)
+        off = 0
+        self.w, self.g, self.wb = [], [], []
+        for r, c in shapes:
+            bound = 1.0 / math.sqrt(c)
+            self.flat[off:off + r * c] = (torch.rand(r * c, generator=g) * 2 - 1).mul_(bound).to(dev)
+            self.w.append(self.flat[off:off + r * c].view(r, c))
+            self.g.append(self.grad[off:off + r * c].view(r, c))
+            self.wb.append(self.shadow[off:off + r * c].view(r, c))
+            off += r * c
+        self.param = torch.nn.Parameter(self.flat, requires_grad=False)
+        self.param.grad = self.grad
+        self.refresh_shadow()
+        self.training = True
+        self.seed = seed
+
+    def refresh_shadow(self):
+        self.shadow.copy_(self.flat)
+
+    def state_dict(self):
+        return {"flat": self.flat.detach().clone(), "dims": list(self.dims)}
+
+    def load_weights(self, layer_weights):
+        """layer_weights: list of (w_self, w_neigh) arrays/tensors (out, in)."""
+        for i, (ws, wn) in enumerate(layer_weights):
+            self.w[2 * i].copy_(torch.as_tensor(wn, dtype=torch.float32))
+            self.w[2 * i + 1].copy_(torch.as_tensor(ws, dtype=torch.float32))
+        self.refresh_shadow()
+
+    # ---------------------------------------------------------------- fwd
+    def forward(self, x: torch.Tensor, adjs, x_global=None, salt: torch.Tensor | None = None):
+        """Returns (logits, saved) — saved holds what backward needs."""
+        L = _lib.lib()
+        st = _lib.stream_ptr()
+        h = x
+        saved = []
+        for i in range(self.L):
+            indptr, src, n_pad, n_dev = adjs[i]
+            f = h.shape[1] if not (i == 0 and x_global is not None) else x_global[0].shape[1]
+            mean = torch.empty((n_pad, f), dtype=self.act, device=h.device)
+            if i == 0 and x_global is not None:
+                table, gl = x_global
+                _lib.check(L.sal_segment_mean_fwd_global(
+                    indptr.data_ptr(), src.data_ptr(), gl.data_ptr(), _lib.ptr(n_dev), n_pad,
+                    table.data_ptr(), _lib.dtype_code(table.dtype), table.stride(0), f,
+                    mean.data_ptr(), _lib.dtype_code(self.act), mean.stride(0), st),
+                    "segment_mean_fwd_global")
+            else:
+                _lib.check(L.sal_segment_mean_fwd(
+                    indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dev), n_pad, h.data_ptr(),
+                    _lib.dtype_code(h.dtype), h.stride(0), f, mean.data_ptr(),
+                    _lib.dtype_code(self.act), mean.stride(0), st), "segment_mean_fwd")
+            h_dst = h[:n_pad]
+            z = torch.mm(h_dst, self.wb[2 * i + 1].t())
+            z.addmm_(mean, self.wb[2 * i].t())
+            rec = dict(h=h, mean=mean, n_pad=n_pad, adj=adjs[i])
+            if i != self.L - 1:
+                y = torch.empty_like(z)
+                mask = torch.empty(z.numel() // 8, dtype=torch.uint8, device=z.device)
+                p = self.p if self.training else 0.0
+                _lib.check(L.sal_relu_dropout_fwd(
+                    z.data_ptr(), y.data_ptr(), mask.data_ptr(), z.numel(),
+                    _lib.dtype_code(z.dtype), p, (self.seed * 1000003 + i) & (2**64 - 1),
+                    _lib.ptr(salt), st), "relu_dropout_fwd")
+                rec["mask"] = mask
+                h = y
+            else:
+                h = z
+            saved.append(rec)
+        return h, saved
+
+    def loss(self, logits: torch.Tensor, labels: torch.Tensor):
+        """Fused log_softmax + NLL; returns (loss scalar fp32, dlogits)."""
+        L = _lib.lib()
+        loss = torch.zeros((), dtype=torch.float32, device=logits.device)
+        dlog = torch.empty_like(logits)
+        rows = min(logits.shape[0], labels.shape[0])
+        _lib.check(L.sal_lsm_nll(logits.data_ptr(), logits.stride(0), rows, logits.shape[1],
+                                 _lib.dtype_code(logits.dtype), labels.data_ptr(),
+                                 loss.data_ptr(), dlog.data_ptr(), dlog.stride(0),
+                                 _lib.stream_ptr()), "lsm_nll")
+        return loss, dlog
+
+    # ---------------------------------------------------------------- bwd
+    def backward(self, dlogits: torch.Tensor, saved) -> None:
+        """Writes every weight gradient into self.grad (overwrite semantics)."""
+        L = _lib.lib()
+        st = _lib.stream_ptr()
+        dz = dlogits
+        for i in reversed(range(self.L)):
+            rec = saved[i]
+            h, mean, n_pad = rec["h"], rec["mean"], rec["n_pad"]
+            dzt = dz.t()
+            _mm_f32(dzt, mean, self.g[2 * i])
+            _mm_f32(dzt, h[:n_pad], self.g[2 * i + 1])
+            if i == 0:
+                break
+            # input gradient of layer i: self term + scatter of the mean term
+            dh = torch.zeros((h.shape[0], h.shape[1]), dtype=torch.float32, device=h.device)
+            _mm_f32(dz, self.wb[2 * i + 1], dh[:n_pad])
+            dmean = torch.mm(dz, self.wb[2 * i])
+            indptr, src, _, n_dev = rec["adj"]
+            _lib.check(L.sal_segment_mean_bwd(
+                indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dev), n_pad, dmean.data_ptr(),
+                _lib.dtype_code(dmean.dtype), dmean.stride(0), dmean.shape[1], dh.data_ptr(),
+                dh.stride(0), st), "segment_mean_bwd")
+            # through relu+dropout of the previous layer's output
+            prev_mask = saved[i - 1]["mask"]
+            dzp = torch.empty((h.shape[0], h.shape[1]), dtype=self.act, device=h.device)
+            _lib.check(L.sal_relu_dropout_bwd(
+                dh.data_ptr(), _lib.SAL_F32, prev_mask.data_ptr(), dzp.data_ptr(),
+                _lib.dtype_code(self.act), dh.numel(), self.p if self.training else 0.0, st),
+                "relu_dropout_bwd")
+            dz = dzp
+
+    @torch.no_grad()
+    def predict(self, x, adjs, x_global=None):
+        was = self.training
+        self.training = False
+        try:
+            logits, _ = self.forward(x, adjs, x_global)
+        finally:
+            self.training = was
+        return logits
+
+
+def _mm_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:
+    """out (fp32) = a @ b; 16-bit operands accumulate and store in fp32 (cuBLAS)."""
+    if a.dtype == torch.float32:
+        torch.mm(a, b, out=out)
+    else:
+        torch.mm(a, b, out_dtype=torch.float32, out=out)

@@ -3,32 +3,34 @@
 The paper's training loop (PAPER.md:407-416 listing, 2562-2586 model) with
 SALIENT's pipeline moved onto the GPU:
 
-  prep stream   : sample MFG (sal_sample_mfg) -> gather features -> labels
-                  for batch i+1, into device slot (i+1) % S
-  compute stream: GraphSAGE fwd/bwd on slot i % S, gradient allreduce
-                  (NCCL over NVLink when world > 1), fused Adam
+  prep stream   : plan cursor -> sample MFG (sal_sample_mfg) -> gather features
+                  (fp16 table -> bf16 rows) -> labels, for batch i+1, into
+                  device slot (i+1) % 2
+  compute stream: GraphSAGE fwd/bwd on slot i % 2 (FusedSAGE), gradient
+                  all-reduce (NCCL over NVLink when world > 1), fused Adam
 
-Shapes are static: every layer is padded to the plan's worst-case
-destination count (node_cap) and kernels read the true counts from device
-memory, so a step needs no host synchronisation and can be captured in a
-CUDA graph (`graphs=True`).  Seed nodes are sharded across ranks: global
-step s of an epoch trains plan batch s*W + r on rank r (effective batch
-1024*W); a rank without a batch in the last step
-contributes a zero gradient.
+Shapes are static: each layer is padded to the plan's worst-case destination
+count (node_cap) and the kernels read the true counts from device memory, so
+a step has no host synchronisation.  With `graphs=True` the pair
+{prep(i+1) || train(i)} is captured once per slot parity and replayed; the
+device epoch cursor (sal_plan_next) makes every replay prepare the next batch
+of the plan.  Seed nodes are sharded across ranks: step s trains plan batch
+s*W + r on rank r (effective batch 1024*W); a rank
+without a batch in the last step contributes a zero gradient.
 """
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
-import torch.nn.functional as F
 
 from . import _lib
 from .graph import DeviceGraph
-from .model import GraphSAGE
+from .model import FusedSAGE
 from .prep import gather_rows, make_epoch_plan
 from .sampler import FanoutSpec, MfgWorkspace, RNG_POLICIES
 
@@ -43,23 +45,30 @@ class TrainConfig:
     act_dtype: torch.dtype = torch.bfloat16
     global_seed: int = 1
     shuffle_seed: int = 1
-    depth: int = 1                 # batches prepared ahead of the consumer
     gather_free: bool = False      # layer-0 mean straight from the feature table
     rng_policy: str = "splitmix"
-    graphs: bool = False           # capture prep+step in CUDA graphs
+    graphs: bool = True            # capture {prep || step} in CUDA graphs
+    model_seed: int = 0
 
 
 class _Slot:
     def __init__(self, dg: DeviceGraph, cfg: TrainConfig, device):
         self.ws = MfgWorkspace(dg.num_nodes, cfg.fanouts, cfg.batch_size, device=device)
         rows = self.ws.node_cap[-1] if not cfg.gather_free else self.ws.node_cap[-2]
-        f = dg.features.shape[1]
-        self.feats = torch.zeros((max(rows, 1), f), dtype=dg.features.dtype, device=device)
+        self.feats = torch.zeros((max(rows, 1), dg.num_features), dtype=cfg.act_dtype,
+                                 device=device)
         self.labels = torch.full((cfg.batch_size,), -1, dtype=torch.int64, device=device)
         self.desc = torch.zeros(3, dtype=torch.int64, device=device)
-        self.seeds = torch.zeros(cfg.batch_size, dtype=torch.int64, device=device)
-        self.done = torch.cuda.Event()
-        self.free = torch.cuda.Event()
+        self.seeds = torch.zeros(max(cfg.batch_size, 1), dtype=torch.int64, device=device)
+
+
+class _Staging:
+    """Pinned host inputs of one step for the end-to-end path."""
+
+    def __init__(self, batch_size: int):
+        self.desc = torch.zeros(3, dtype=torch.int64).pin_memory()
+        self.seeds = torch.zeros(max(batch_size, 1), dtype=torch.int64).pin_memory()
+        self.ev = torch.cuda.Event()
 
 
 class Trainer:
@@ -76,24 +85,27 @@ class Trainer:
         self.train_ids = np.asarray(train_ids, dtype=np.int64)
         self.num_classes = num_classes or dg.num_classes
         self.nh = len(cfg.fanouts)
-        torch.manual_seed(cfg.global_seed)
-        self.model = GraphSAGE(dg.num_features, cfg.hidden, self.num_classes, self.nh,
-                               cfg.dropout).to(self.device)
-        params = list(self.model.parameters())
-        total = sum(p.numel() for p in params)
-        self.flat_grad = torch.zeros(total, dtype=torch.float32, device=self.device)
-        off = 0
-        for p in params:
-            p.grad = self.flat_grad[off:off + p.numel()].view_as(p)
-            off += p.numel()
-        self.opt = torch.optim.Adam(params, lr=cfg.lr, fused=True)
-        self.slots = [_Slot(dg, cfg, self.device) for _ in range(cfg.depth + 1)]
+        self.model = FusedSAGE(dg.num_features, cfg.hidden, self.num_classes, self.nh,
+                               cfg.dropout, device=self.device, seed=cfg.model_seed,
+                               act_dtype=cfg.act_dtype)
+        if world > 1:  # identical initial weights on every rank
+            torch.distributed.broadcast(self.model.flat, src=0)
+            self.model.refresh_shadow()
+        self.opt = torch.optim.Adam([self.model.param], lr=cfg.lr, fused=True,
+                                    capturable=cfg.graphs)
+        self.slots = [_Slot(dg, cfg, self.device) for _ in range(2)]
+        self.staging = [_Staging(cfg.batch_size) for _ in range(4)]
         self.prep_stream = torch.cuda.Stream(device=self.device)
         self.policy = RNG_POLICIES[cfg.rng_policy]
         self.x_table = dg.feature_view()
-        self.loss_sum = torch.zeros((), dtype=torch.float32, device=self.device)
-        self.epoch = -1
+        self.cursor = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.step_ctr = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.losses = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.last_loss = torch.zeros((), dtype=torch.float32, device=self.device)
+        self.graphs = {}
         self.steps_per_epoch = 0
+        self.seeds_all = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.desc_all = torch.zeros((1, 3), dtype=torch.int64, device=self.device)
 
     # ---------------------------------------------------------------- plan
     def set_epoch(self, epoch: int) -> int:
@@ -102,8 +114,8 @@ class Trainer:
         nb = len(plan)
         W, r = self.world, self.rank
         self.steps_per_epoch = math.ceil(nb / W) if nb else 0
-        self.host_batches = []
         descs = []
+        self.host_batches = []
         for s in range(self.steps_per_epoch):
             b = s * W + r
             if b < nb:
@@ -114,108 +126,195 @@ class Trainer:
                 descs.append((-1, 0, 0))
                 self.host_batches.append(None)
         perm = np.concatenate([b.dst_ids for b in plan.batches]) if nb else np.zeros(1, np.int64)
-        self.seeds_all = torch.from_numpy(perm).to(self.device)
-        self.desc_all = torch.from_numpy(np.asarray(descs, dtype=np.int64).reshape(-1, 3)).to(
-            self.device)
-        self.seeds_pinned = torch.from_numpy(perm).pin_memory()
-        self.desc_pinned = torch.from_numpy(np.asarray(descs, dtype=np.int64).reshape(-1, 3)
-                                            ).pin_memory()
+        # copy into persistent buffers (captured graphs hold their addresses)
+        if self.seeds_all.numel() < len(perm):
+            self.seeds_all = torch.zeros(len(perm), dtype=torch.int64, device=self.device)
+            self.graphs.clear()
+        if self.desc_all.shape[0] < max(1, len(descs)):
+            self.desc_all = torch.zeros((max(1, len(descs)), 3), dtype=torch.int64,
+                                        device=self.device)
+            self.losses = torch.zeros(max(1, len(descs)), dtype=torch.float32,
+                                      device=self.device)
+            self.graphs.clear()
+        self.seeds_all[:len(perm)].copy_(torch.from_numpy(perm))
+        if descs:
+            self.desc_all[:len(descs)].copy_(torch.from_numpy(np.asarray(descs, np.int64)))
+        if getattr(self, "n_steps_dev", None) != len(descs):
+            self.graphs.clear()  # the step count is baked into the captured plan_next
+        self.n_steps_dev = len(descs)
+        self.desc_host = np.asarray(descs, dtype=np.int64).reshape(-1, 3)
+        self.perm_host = perm
         self.epoch = epoch
         self.plan = plan
+        self.cursor.zero_()
+        self.step_ctr.zero_()
         return self.steps_per_epoch
 
     # ---------------------------------------------------------------- prep
-    def _enqueue_prep(self, slot: _Slot, step: int, host_inputs: bool = False) -> None:
+    def _prep(self, slot: _Slot, stage: "_Staging | None") -> None:
+        """Enqueue one batch preparation on the current stream (capturable)."""
         ws = slot.ws
-        st = self.prep_stream
-        with torch.cuda.stream(st):
-            st.wait_event(slot.free)
-            if host_inputs:
-                # end-to-end mode: this step's seeds + descriptor come from pinned host memory
-                d = self.desc_pinned[step]
-                n = int(d[2])
-                slot.desc.copy_(d, non_blocking=True)
-                if n:
-                    off = int(d[1])
-                    slot.seeds[:n].copy_(self.seeds_pinned[off:off + n], non_blocking=True)
-                slot.desc[1:2].zero_()
-                seeds_base, desc = slot.seeds, slot.desc
-            else:
-                seeds_base, desc = self.seeds_all, self.desc_all[step]
-            ws.run(self.dg, seeds_base, desc, self.cfg.global_seed, self.policy, st)
-            L = self.nh
-            rows = ws.node_cap[L] if not self.cfg.gather_free else ws.node_cap[L - 1]
-            n_dev = ws.sizes[L:L + 1] if not self.cfg.gather_free else ws.sizes[L - 1:L]
-            gather_rows(self.x_table, ws.globals, slot.feats[:, :self.x_table.shape[1]],
-                        n=rows, n_dev=n_dev, stream=st)
-            _lib.check(_lib.lib().sal_gather_labels(
-                self.dg.labels.data_ptr(), seeds_base.data_ptr(), desc.data_ptr(),
-                self.cfg.batch_size, slot.labels.data_ptr(), _lib.stream_ptr(st)),
-                "gather_labels")
-            slot.done.record(st)
+        st = torch.cuda.current_stream()
+        L = _lib.lib()
+        if stage is not None:
+            slot.desc.copy_(stage.desc, non_blocking=True)
+            slot.seeds.copy_(stage.seeds, non_blocking=True)
+            seeds_base = slot.seeds
+        else:
+            _lib.check(L.sal_plan_next(self.desc_all.data_ptr(), self.n_steps_dev,
+                                       self.cursor.data_ptr(), slot.desc.data_ptr(),
+                                       _lib.stream_ptr(st)), "plan_next")
+            seeds_base = self.seeds_all
+        ws.run(self.dg, seeds_base, slot.desc, self.cfg.global_seed, self.policy, st)
+        nh = self.nh
+        rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
+        n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
+        gather_rows(self.x_table, ws.globals, slot.feats, n=rows, n_dev=n_dev, stream=st)
+        _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), seeds_base.data_ptr(),
+                                       slot.desc.data_ptr(), self.cfg.batch_size,
+                                       slot.labels.data_ptr(), _lib.stream_ptr(st)),
+                   "gather_labels")
 
-    # ---------------------------------------------------------------- step
     def _adjs(self, slot: _Slot):
         ws = slot.ws
-        L = self.nh
         out = []
-        for i in range(L):
-            h = L - 1 - i
+        for i in range(self.nh):
+            h = self.nh - 1 - i
             out.append((ws.dst_indptr[h], ws.src_local[h], ws.node_cap[h], ws.sizes[h:h + 1]))
         return out
 
-    def _step_compute(self, slot: _Slot) -> torch.Tensor:
-        cs = torch.cuda.current_stream()
-        cs.wait_event(slot.done)
-        self.flat_grad.zero_()
-        x_global = (self.x_table, slot.ws.globals) if self.cfg.gather_free else None
-        out = self.model(slot.feats, self._adjs(slot), self.cfg.act_dtype, x_global=x_global)
-        nll = F.nll_loss(out, slot.labels, ignore_index=-1, reduction="sum")
-        cnt = (slot.labels >= 0).sum().clamp_min(1).to(torch.float32)
-        loss = nll / cnt
-        loss.backward()
+    def _train(self, slot: _Slot) -> None:
+        """fwd + bwd + all-reduce + Adam on the current stream (capturable)."""
+        m = self.model
+        xg = (self.x_table, slot.ws.globals) if self.cfg.gather_free else None
+        logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg, salt=self.step_ctr)
+        loss, dlog = m.loss(logits, slot.labels)
+        m.backward(dlog, saved)
         if self.world > 1:
-            torch.distributed.all_reduce(self.flat_grad, op=torch.distributed.ReduceOp.AVG)
+            torch.distributed.all_reduce(m.grad, op=torch.distributed.ReduceOp.AVG)
         self.opt.step()
-        slot.free.record(cs)
-        return loss.detach()
+        m.refresh_shadow()
+        self.last_loss.copy_(loss)
+        self.losses.index_copy_(0, self.step_ctr.clamp(max=self.losses.numel() - 1),
+                                loss.view(1))
+        self.step_ctr.add_(1)
 
-    def train_steps(self, start: int, count: int, host_inputs: bool = False,
-                    loss_out: torch.Tensor | None = None) -> torch.Tensor:
-        """Run steps [start, start+count) of the current epoch; returns the
-        device tensor of per-step losses.  With host_inputs, seeds come from
-        pinned host memory each step and every loss is copied back to
-        `loss_out` (pinned) — the end-to-end path."""
-        self.model.train()
-        S = len(self.slots)
-        losses = torch.zeros(count, dtype=torch.float32, device=self.device)
-        depth = self.cfg.depth
-        for k in range(min(depth, count)):
-            self._enqueue_prep(self.slots[(start + k) % S], start + k, host_inputs)
-        for k in range(count):
-            step = start + k
-            if k + depth < count:
-                self._enqueue_prep(self.slots[(step + depth) % S], step + depth, host_inputs)
-            loss = self._step_compute(self.slots[step % S])
-            losses[k] = loss
+    def _pair(self, k: int, host_inputs: bool) -> None:
+        """{prep(slot k+1) on the prep stream || train(slot k)} on the current stream."""
+        cs = torch.cuda.current_stream()
+        ps = self.prep_stream
+        ps.wait_stream(cs)
+        with torch.cuda.stream(ps):
+            self._prep(self.slots[(k + 1) % 2],
+                       self.staging[(k + 1) % 4] if host_inputs else None)
+        self._train(self.slots[k % 2])
+        cs.wait_stream(ps)
+
+    # ---------------------------------------------------------------- driver
+    def _stage_host(self, stage: _Staging, step: int) -> None:
+        """End-to-end mode: one step's seeds + descriptor into pinned staging."""
+        if step < len(self.desc_host):
+            bid, off, n = (int(v) for v in self.desc_host[step])
+        else:
+            bid, off, n = -1, 0, 0
+        stage.desc[0], stage.desc[1], stage.desc[2] = bid, 0, n
+        if n:
+            stage.seeds[:n].copy_(torch.from_numpy(self.perm_host[off:off + n]))
+
+    def begin_epoch(self, host_inputs: bool = False) -> None:
+        """Prepare batch 0 into slot 0 (eager) before the first step."""
+        stage = None
+        if host_inputs:
+            stage = self.staging[0]
+            stage.ev.synchronize()
+            self._stage_host(stage, 0)
+        self._prep(self.slots[0], stage)
+        if stage is not None:
+            stage.ev.record()
+
+    def run_steps(self, start: int, count: int, host_inputs: bool = False,
+                  loss_out: torch.Tensor | None = None) -> None:
+        """Steps [start, start+count): step k trains slot k%2 and prepares k+1.
+
+        begin_epoch() must have prepared step `start` (the pipeline is primed
+        once per epoch).  With host_inputs each step stages its successor's
+        seeds in pinned host memory (4-deep ring, so the host runs ahead of
+        the GPU) and copies its loss back to `loss_out[k]` (pinned) — the
+        end-to-end path.
+        """
+        P = 4 if host_inputs else 2
+        for k in range(start, start + count):
+            stage = None
+            if host_inputs:
+                stage = self.staging[(k + 1) % 4]
+                stage.ev.synchronize()  # the replay that last read this staging buffer
+                self._stage_host(stage, k + 1)
+            if self.cfg.graphs:
+                key = (k % P, host_inputs)
+                g = self.graphs.get(key)
+                if g is None:
+                    g = self._capture(k % P, host_inputs)
+                g.replay()
+            else:
+                self._pair(k % P, host_inputs)
             if loss_out is not None:
-                loss_out[k].copy_(loss, non_blocking=True)
-        return losses
+                loss_out[k - start].copy_(self.last_loss, non_blocking=True)
+            if stage is not None:
+                stage.ev.record()
+
+    def _capture(self, parity: int, host_inputs: bool) -> torch.cuda.CUDAGraph:
+        """Capture {prep(next) || train(slot parity)} without disturbing state."""
+        torch.cuda.synchronize()
+        fresh_opt = len(self._opt_state()) == 0
+        saved = (self.cursor.clone(), self.step_ctr.clone(), self.model.flat.clone(),
+                 [s.clone() for s in self._opt_state()])
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up on a side stream (cuBLAS workspaces)
+            for _ in range(2):
+                self._pair(parity, host_inputs)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._pair(parity, host_inputs)
+        torch.cuda.synchronize()
+        # undo the warm-up's side effects
+        self.cursor.copy_(saved[0])
+        self.step_ctr.copy_(saved[1])
+        self.model.flat.copy_(saved[2])
+        if fresh_opt:
+            for a in self._opt_state():
+                a.zero_()
+        else:
+            for a, b in zip(self._opt_state(), saved[3]):
+                a.copy_(b)
+        self.model.refresh_shadow()
+        self.graphs[(parity, host_inputs)] = g
+        return g
+
+    def _opt_state(self):
+        out = []
+        for st in self.opt.state.values():
+            for v in st.values():
+                if torch.is_tensor(v):
+                    out.append(v)
+        return out
 
     def train_epoch(self, epoch: int) -> float:
         n = self.set_epoch(epoch)
-        losses = self.train_steps(0, n)
-        return float(losses.mean().item()) if n else 0.0
+        self.begin_epoch()
+        self.run_steps(0, n)
+        torch.cuda.synchronize()
+        return float(self.losses[:n].mean().item()) if n else 0.0
 
     # ---------------------------------------------------------------- eval
     @torch.no_grad()
     def evaluate(self, ids: np.ndarray, fanouts: FanoutSpec | None = None,
                  batch_size: int | None = None) -> tuple[int, int]:
         """Sampled inference over `ids` (this rank's shard); returns (correct, total)."""
-        from .prep import PrepConfig, run_epoch_prep
-        from .prep import EpochPlan
+        from .prep import EpochPlan, PrepConfig, run_epoch_prep
         from .sampler import SeedBatch
-        self.model.eval()
         fan = fanouts or self.cfg.fanouts
         bs = batch_size or self.cfg.batch_size
         ids = np.asarray(ids, dtype=np.int64)
@@ -224,12 +323,10 @@ class Trainer:
         correct = torch.zeros((), dtype=torch.int64, device=self.device)
         total = 0
         x = self.dg.feature_view()
-        cfg = PrepConfig(num_workers=2, fanouts=fan, feature_dtype="f16"
-                         if x.dtype == torch.float16 else "f32")
+        cfg = PrepConfig(num_workers=2, fanouts=fan, feature_dtype="bf16")
         for pb in run_epoch_prep(self.dg, x, self.dg.labels, plan, cfg, self.cfg.global_seed + 7):
             adjs = [(l.indptr, l.src_local, l.num_dst, None) for l in pb.mfg.layers]
-            out = self.model(pb.features, adjs, self.cfg.act_dtype)
-            correct += (out.argmax(dim=-1) == pb.labels).sum()
+            logits = self.model.predict(pb.features, adjs)
+            correct += (logits.argmax(dim=-1) == pb.labels).sum()
             total += len(pb.labels)
-        self.model.train()
         return int(correct.item()), total
