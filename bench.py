@@ -312,7 +312,7 @@ def run_ours(args):
         tr.begin_epoch(host_inputs)
         barrier(world)
         torch.cuda.synchronize()
-        n0 = L.sal_launch_count()
+        n0 = tr.kernel_launches
         ev0.record()
         done, step = 0, 0
         while done < count:
@@ -330,7 +330,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier(world)
         ms = ev0.elapsed_time(ev1)
-        return max_over_ranks(ms, world), L.sal_launch_count() - n0, loss_out
+        return max_over_ranks(ms, world), tr.kernel_launches - n0, loss_out
 
     with ClockSampler(local) as clk:
         ms, launches, _ = timed(K)

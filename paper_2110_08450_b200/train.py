@@ -103,6 +103,8 @@ class Trainer:
         self.losses = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.last_loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.graphs = {}
+        self.graph_kernels = {}
+        self.kernel_launches = 0   # library kernels executed by run_steps (launch audit)
         self.steps_per_epoch = 0
         self.seeds_all = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.desc_all = torch.zeros((1, 3), dtype=torch.int64, device=self.device)
@@ -255,8 +257,11 @@ class Trainer:
                 if g is None:
                     g = self._capture(k % P, host_inputs)
                 g.replay()
+                self.kernel_launches += self.graph_kernels[key]
             else:
+                n0 = _lib.lib().sal_launch_count()
                 self._pair(k % P, host_inputs)
+                self.kernel_launches += _lib.lib().sal_launch_count() - n0
             if loss_out is not None:
                 loss_out[k - start].copy_(self.last_loss, non_blocking=True)
             if stage is not None:
@@ -276,9 +281,12 @@ class Trainer:
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
+        n0 = _lib.lib().sal_launch_count()
         with torch.cuda.graph(g):
             self._pair(parity, host_inputs)
         torch.cuda.synchronize()
+        # library kernels per replay (the graph re-executes exactly these)
+        self.graph_kernels[(parity, host_inputs)] = _lib.lib().sal_launch_count() - n0
         # undo the warm-up's side effects
         self.cursor.copy_(saved[0])
         self.step_ctr.copy_(saved[1])

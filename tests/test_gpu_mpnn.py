@@ -42,7 +42,9 @@ def test_segment_mean_fp16_input_and_padding():
     got = segment_mean(torch.from_numpy(indptr.astype(np.int32)).cuda(),
                        torch.from_numpy(src.astype(np.int32)).cuda(),
                        torch.from_numpy(h).cuda(), n_dst, n_pad=256, n_dst_dev=nd)
-    assert np.array_equal(got[:n_dst].cpu().numpy(), want)
+    # 16-bit rows take the warp-row kernel: per-lane-group partial sums, so the
+    # fp32 summation order differs from strict edge order (tolerance, not bits)
+    assert np.allclose(got[:n_dst].cpu().numpy(), want, rtol=1e-6, atol=1e-6)
     assert not got[n_dst:].any()
 
 
