@@ -186,7 +186,7 @@ def kernel_profile(trainer, nbatches: int):
         ws.run(trainer.dg, trainer.seeds_all, trainer.desc_all[step], trainer.cfg.global_seed,
                trainer.policy, st)
         ev[1].record(st)
-        gather_rows(x, ws.globals, slot.feats[:, :f], n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
+        gather_rows(x, ws.globals, slot.feats[:, f:], n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
                     stream=st)
         ev[2].record(st)
         sizes, etot = ws.read_extents()

@@ -195,23 +195,51 @@ int sal_segment_mean_fwd_global(const int32_t* indptr_dev, const int32_t* src_de
                                 int64_t out_stride, void* stream);
 
 /* ---- training-step helpers (PAPER.md:2577-2585 GraphSAGE step) ---------- */
+/* Activations use a "cat" layout: layer i's input is [rows, 2f] with h in the
+ * right half and mean (first n_pad rows) in the left half, so a SAGEConv is
+ * one GEMM [mean | h_dst] @ [W_neigh | W_self]^T. */
 /* device epoch cursor: *out = desc_all[*cursor] (or an empty batch past the
  * end), then ++*cursor — one captured graph prepares a new batch per replay */
 int sal_plan_next(const int64_t* desc_all_dev, int64_t n_steps, int64_t* cursor_dev,
                   sal_batch_desc* out_dev, void* stream);
-/* y = relu(x) * keep / (1-p), keep ~ Philox(seed, element, *salt_dev);
- * mask gets one bit per element (x > 0 && keep).  n % 8 == 0. */
-int sal_relu_dropout_fwd(const void* x_dev, void* y_dev, uint8_t* mask_dev, int64_t n,
-                         int32_t dtype, float p, uint64_t seed, const int64_t* salt_dev,
-                         void* stream);
-/* dx = dy * bit / (1-p); dy fp32|bf16 -> dx bf16|fp32 (16-byte aligned) */
-int sal_relu_dropout_bwd(const void* dy_dev, int32_t dy_dtype, const uint8_t* mask_dev,
-                         void* dx_dev, int32_t dx_dtype, int64_t n, float p, void* stream);
+/* y = relu(x) * keep / (1-p), keep ~ Philox(seed, element, *salt_dev); mask
+ * gets one bit per element (x > 0 && keep), dense over [rows, cols].
+ * cols and both row strides (elements) multiples of 8. */
+int sal_relu_dropout_fwd(const void* x_dev, int64_t x_stride, void* y_dev, int64_t y_stride,
+                         int64_t rows, int32_t cols, int32_t dtype, uint8_t* mask_dev, float p,
+                         uint64_t seed, const int64_t* salt_dev, void* stream);
+/* dx = dy * bit / (1-p) */
+int sal_relu_dropout_bwd(const void* dy_dev, int64_t dy_stride, int32_t dy_dtype,
+                         const uint8_t* mask_dev, void* dx_dev, int64_t dx_stride,
+                         int32_t dx_dtype, int64_t rows, int32_t cols, float p, void* stream);
 /* log_softmax + NLL (labels < 0 ignored, mean over valid rows) fused with its
  * gradient: *loss += mean NLL (caller zeroes it); grad = (softmax-onehot)/count */
 int sal_lsm_nll(const void* logits_dev, int64_t ld, int64_t rows, int32_t num_classes,
                 int32_t dtype, const int64_t* labels_dev, float* loss_dev, void* grad_dev,
                 int64_t ldg, void* stream);
+/* reverse adjacency of an MFG layer: tindptr[n_src_rows+1], tdst[edges] lists
+ * for every source row the destinations that sampled it (order within a list
+ * is unspecified) */
+size_t sal_transpose_ws_bytes(int64_t n_src_rows);
+int sal_transpose_build(const int32_t* indptr_dev, const int32_t* src_dev,
+                        const int64_t* n_dst_dev, int64_t n_pad, int64_t n_src_rows,
+                        int64_t max_edges, int32_t* tindptr_dev, int32_t* tdst_dev, void* ws_dev,
+                        void* stream);
+/* input gradient of a SAGEConv layer, gathered per source row s < rows:
+ * dz[s] = mask(s) * (dA[s, f:2f] if s < n_pad) + sum_{d in T(s)} dA[d, 0:f]/deg(d),
+ * scaled by 1/(1-p) — relu/dropout backward fused, no atomics, no zero fill */
+int sal_mean_bwd_t(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
+                   const int32_t* indptr_dev, const int32_t* tindptr_dev, const int32_t* tdst_dev,
+                   int64_t rows, const uint8_t* mask_dev, float p, void* dz_dev, int64_t ldz,
+                   int32_t dz_dtype, void* stream);
+/* Adam (torch.optim.Adam, no weight decay) on flat fp32 params; step count
+ * t = *t_dev + 1; refreshes the optional bf16 shadow copy */
+int sal_adam_step(float* param_dev, const float* grad_dev, float* m_dev, float* v_dev,
+                  void* shadow_bf16_dev, int64_t n, float lr, float beta1, float beta2, float eps,
+                  const int64_t* t_dev, void* stream);
+/* per-step bookkeeping: *last = *loss; log[*step] = *loss; ++*step; ++*adam_t */
+int sal_step_tail(const float* loss_dev, float* last_dev, float* log_dev, int64_t log_len,
+                  int64_t* step_dev, int64_t* adam_t_dev, void* stream);
 
 /* ---- on-device synthetic data (graph.py:252-298 laws) ---- */
 /* owner[s] = v for every slot s in [indptr[v], indptr[v+1]) */

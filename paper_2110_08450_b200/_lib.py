@@ -83,9 +83,18 @@ SIGNATURES = {
     "sal_segment_mean_fwd_global": (ctypes.c_int, [vp, vp, vp, vp, i64, vp, i32, i64, i32, vp,
                                                    i32, i64, vp]),
     "sal_plan_next": (ctypes.c_int, [vp, i64, vp, vp, vp]),
-    "sal_relu_dropout_fwd": (ctypes.c_int, [vp, vp, vp, i64, i32, ctypes.c_float, u64, vp, vp]),
-    "sal_relu_dropout_bwd": (ctypes.c_int, [vp, i32, vp, vp, i32, i64, ctypes.c_float, vp]),
+    "sal_relu_dropout_fwd": (ctypes.c_int, [vp, i64, vp, i64, i64, i32, i32, vp, ctypes.c_float,
+                                            u64, vp, vp]),
+    "sal_relu_dropout_bwd": (ctypes.c_int, [vp, i64, i32, vp, vp, i64, i32, i64, i32,
+                                            ctypes.c_float, vp]),
     "sal_lsm_nll": (ctypes.c_int, [vp, i64, i64, i32, i32, vp, vp, vp, i64, vp]),
+    "sal_transpose_ws_bytes": (ctypes.c_size_t, [i64]),
+    "sal_transpose_build": (ctypes.c_int, [vp, vp, vp, i64, i64, i64, vp, vp, vp, vp]),
+    "sal_mean_bwd_t": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, i64, vp,
+                                      ctypes.c_float, vp, i64, i32, vp]),
+    "sal_adam_step": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, ctypes.c_float, ctypes.c_float,
+                                     ctypes.c_float, ctypes.c_float, vp, vp]),
+    "sal_step_tail": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
     "sal_gen_owner": (ctypes.c_int, [vp, i64, vp, vp]),
     "sal_gen_pairing": (ctypes.c_int, [vp, i64, u64, vp, vp]),
     "sal_gen_features_uniform": (ctypes.c_int, [i64, i32, i64, u64, vp, vp]),

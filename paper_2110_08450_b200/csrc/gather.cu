@@ -134,7 +134,8 @@ gather_rows_warp_kernel(const TIn* __restrict__ x, int64_t x_stride, const TId* 
   constexpr int EPV = 16 / (int)sizeof(TIn);
   constexpr int VOUT = EPV * (int)sizeof(TOut);
   constexpr int RPI = 32 / LPR;
-  constexpr int kPhase = RPI * kRowUnroll;  // rows per phase
+  constexpr int kU = (32 / RPI) < kRowUnroll ? (32 / RPI) : kRowUnroll;
+  constexpr int kPhase = RPI * kU;  // rows per phase (<= 32)
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPR, sub = lane % LPR;
   const int64_t n = n_dev ? *n_dev : n_host;
@@ -147,9 +148,9 @@ gather_rows_warp_kernel(const TIn* __restrict__ x, int64_t x_stride, const TId* 
     const int64_t next = (rn + lane < n) ? (int64_t)ids[rn + lane] : 0;
 #pragma unroll
     for (int ph = 0; ph < 32; ph += kPhase) {
-      uint4 buf[kRowUnroll];
+      uint4 buf[kU];
 #pragma unroll
-      for (int u = 0; u < kRowUnroll; ++u) {
+      for (int u = 0; u < kU; ++u) {
         const int r = ph + u * RPI + grp;
         const int64_t s = __shfl_sync(0xffffffffu, my, r & 31);
         if (r0 + r < n) {
@@ -158,7 +159,7 @@ gather_rows_warp_kernel(const TIn* __restrict__ x, int64_t x_stride, const TId* 
         }
       }
 #pragma unroll
-      for (int u = 0; u < kRowUnroll; ++u) {
+      for (int u = 0; u < kU; ++u) {
         const int r = ph + u * RPI + grp;
         if (r0 + r < n) {
           const TIn* v = reinterpret_cast<const TIn*>(&buf[u]);

@@ -1,10 +1,25 @@
-// Small fused kernels of the GraphSAGE training step:
-//   * plan_next      — device-side epoch cursor -> sal_batch_desc (lets one
-//                      captured CUDA graph prepare a different batch per replay)
-//   * relu_dropout   — y = relu(x) * keep / (1-p); one bit per element records
-//                      (x > 0 && keep) for the backward pass
-//   * lsm_nll        — log_softmax + NLL (ignore_index -1, mean over valid rows)
-//                      fused with its gradient (softmax - onehot) / count
+// Fused kernels of the GraphSAGE training step.
+//
+// Activation layout ("cat"): the input of layer i is a [rows, 2f] buffer whose
+// right half holds h_i and whose left half, for the first n_pad destination
+// rows, receives mean_i — so each SAGEConv is ONE GEMM  [mean | h_dst] @
+// [W_neigh | W_self]^T, and its backward is one weight-gradient GEMM plus
+// one input-gradient GEMM.
+//
+//   plan_next       device epoch cursor -> sal_batch_desc (one captured CUDA
+//                   graph prepares a new batch on every replay)
+//   relu_dropout    y = relu(x) * keep / (1-p) into the next cat buffer; one
+//                   bit per element records (x > 0 && keep)
+//   lsm_nll         log_softmax + NLL (labels < 0 ignored) fused with its
+//                   gradient (softmax - onehot) / count
+//   transpose_*     per-batch reverse adjacency of an MFG layer (src -> dsts),
+//                   built on the prep stream
+//   mean_bwd_t      input gradient of a layer, gathered per source row:
+//                   dz_prev[s] = mask(s) * scale * (dh_dst[s] + sum_{d: s in N(d)}
+//                   dmean[d] / deg(d)) — no atomics on the feature rows, no
+//                   zero-fill, relu/dropout backward fused
+//   adam            fused Adam over the flat fp32 parameters + bf16 shadow refresh
+//   step_tail       per-step bookkeeping (loss log, counters) in one launch
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -29,63 +44,92 @@ __global__ void plan_next_kernel(const int64_t* __restrict__ desc_all, int64_t n
 }
 
 // ---------------------------------------------------------------------------
+template <typename T> struct F;
+template <> struct F<float> {
+  static SAL_DEVINL float in(float v) { return v; }
+  static SAL_DEVINL float out(float v) { return v; }
+};
+template <> struct F<__nv_bfloat16> {
+  static SAL_DEVINL float in(__nv_bfloat16 v) { return __bfloat162float(v); }
+  static SAL_DEVINL __nv_bfloat16 out(float v) { return __float2bfloat16_rn(v); }
+};
+template <> struct F<__half> {
+  static SAL_DEVINL float in(__half v) { return __half2float(v); }
+  static SAL_DEVINL __half out(float v) { return __float2half_rn(v); }
+};
+
 template <typename T>
-SAL_DEVINL float to_f(T v);
-template <> SAL_DEVINL float to_f<float>(float v) { return v; }
-template <> SAL_DEVINL float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
-template <typename T>
-SAL_DEVINL T from_f(float v);
-template <> SAL_DEVINL float from_f<float>(float v) { return v; }
-template <> SAL_DEVINL __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
-  return __float2bfloat16_rn(v);
+SAL_DEVINL void ld8(const T* p, float* v) {
+  alignas(16) T t[8];
+#pragma unroll
+  for (int q = 0; q < (int)(8 * sizeof(T)) / 16; ++q)
+    reinterpret_cast<uint4*>(t)[q] = __ldg(reinterpret_cast<const uint4*>(p) + q);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = F<T>::in(t[j]);
 }
 
-// 8 elements per thread: one byte of the bit mask.
 template <typename T>
-__global__ void relu_dropout_fwd_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                        uint8_t* __restrict__ mask, int64_t n8, float p,
-                                        uint64_t seed, const int64_t* __restrict__ salt) {
+SAL_DEVINL void st8(T* p, const float* v) {
+  alignas(16) T t[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) t[j] = F<T>::out(v[j]);
+#pragma unroll
+  for (int q = 0; q < (int)(8 * sizeof(T)) / 16; ++q)
+    reinterpret_cast<uint4*>(p)[q] = reinterpret_cast<const uint4*>(t)[q];
+}
+
+// 8 consecutive columns of one row per thread (cols % 8 == 0); mask is dense
+// row-major over [rows, cols] bits.
+template <typename T>
+__global__ void relu_dropout_fwd_kernel(const T* __restrict__ x, int64_t sx, T* __restrict__ y,
+                                        int64_t sy, int64_t rows, int32_t cols,
+                                        uint8_t* __restrict__ mask, float p, uint64_t seed,
+                                        const int64_t* __restrict__ salt) {
   const uint32_t thresh = (uint32_t)(p * 65536.0f);
-  const float scale = p < 1.f ? 1.f / (1.f - p) : 0.f;
+  const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
   const uint32_t s = salt ? (uint32_t)*salt : 0u;
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const int c8 = cols / 8;
+  const int64_t n8 = rows * c8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 r = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), s, 0x5EEDu), key);
-    const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+    const int64_t r = i / c8;
+    const int c = (int)(i - r * c8) * 8;
+    float v[8];
+    ld8<T>(x + r * sx + c, v);
+    uint4 rnd = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (p > 0.f) rnd = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), s, 0x5EEDu), key);
+    const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
     uint8_t bits = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float v = to_f<T>(x[8 * i + j]);
       const uint32_t u16 = (rr[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
-      const bool keep = (p <= 0.f) || (u16 >= thresh);
-      const bool on = keep && v > 0.f;
+      const bool on = (u16 >= thresh) && v[j] > 0.f;
       bits |= (uint8_t)on << j;
-      y[8 * i + j] = from_f<T>(on ? v * (p > 0.f ? scale : 1.f) : 0.f);
+      v[j] = on ? v[j] * scale : 0.f;
     }
+    st8<T>(y + r * sy + c, v);
     mask[i] = bits;
   }
 }
 
 template <typename TDY, typename TDX>
-__global__ void relu_dropout_bwd_kernel(const TDY* __restrict__ dy,
+__global__ void relu_dropout_bwd_kernel(const TDY* __restrict__ dy, int64_t sdy,
                                         const uint8_t* __restrict__ mask, TDX* __restrict__ dx,
-                                        int64_t n8, float p) {
+                                        int64_t sdx, int64_t rows, int32_t cols, float p) {
   const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
+  const int c8 = cols / 8;
+  const int64_t n8 = rows * c8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
        i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / c8;
+    const int c = (int)(i - r * c8) * 8;
     const uint8_t bits = mask[i];
-    alignas(16) TDY in[8];
-    alignas(16) TDX out[8];
+    float v[8];
+    ld8<TDY>(dy + r * sdy + c, v);
 #pragma unroll
-    for (int q = 0; q < (int)(8 * sizeof(TDY)) / 16; ++q)
-      reinterpret_cast<uint4*>(in)[q] = reinterpret_cast<const uint4*>(dy + 8 * i)[q];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      out[j] = from_f<TDX>(((bits >> j) & 1) ? to_f<TDY>(in[j]) * scale : 0.f);
-#pragma unroll
-    for (int q = 0; q < (int)(8 * sizeof(TDX)) / 16; ++q)
-      reinterpret_cast<uint4*>(dx + 8 * i)[q] = reinterpret_cast<const uint4*>(out)[q];
+    for (int j = 0; j < 8; ++j) v[j] = ((bits >> j) & 1) ? v[j] * scale : 0.f;
+    st8<TDX>(dx + r * sdx + c, v);
   }
 }
 
@@ -116,22 +160,175 @@ __global__ void lsm_nll_kernel(const T* __restrict__ logits, int64_t ld, int64_t
   T* g = grad + row * ldg;
   const int64_t lab = labels[row];
   float m = -INFINITY;
-  for (int j = lane; j < C; j += 32) m = fmaxf(m, to_f<T>(x[j]));
+  for (int j = lane; j < C; j += 32) m = fmaxf(m, F<T>::in(x[j]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   float s = 0.f;
-  for (int j = lane; j < C; j += 32) s += __expf(to_f<T>(x[j]) - m);
+  for (int j = lane; j < C; j += 32) s += __expf(F<T>::in(x[j]) - m);
   s = warp_reduce_sum(s);
   const float lse = m + __logf(s);
   if (lab < 0) {
-    for (int j = lane; j < C; j += 32) g[j] = from_f<T>(0.f);
+    for (int j = lane; j < C; j += 32) g[j] = F<T>::out(0.f);
     return;
   }
   for (int j = lane; j < C; j += 32) {
-    const float pj = __expf(to_f<T>(x[j]) - lse);
-    g[j] = from_f<T>((pj - (j == lab ? 1.f : 0.f)) * inv);
+    const float pj = __expf(F<T>::in(x[j]) - lse);
+    g[j] = F<T>::out((pj - (j == lab ? 1.f : 0.f)) * inv);
   }
-  if (lane == 0) atomicAdd(loss, (lse - to_f<T>(x[lab])) * inv);
+  if (lane == 0) atomicAdd(loss, (lse - F<T>::in(x[lab])) * inv);
+}
+
+// ---------------------------------------------------------------------------
+// reverse adjacency of one MFG layer: for each source row s, the destinations
+// d with s in N(d).  count -> exclusive scan -> fill (warp per destination).
+__global__ void transpose_count_kernel(const int32_t* __restrict__ indptr,
+                                       const int32_t* __restrict__ src,
+                                       const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
+                                       int32_t* __restrict__ tcount) {
+  const int64_t n = n_dst_dev ? *n_dst_dev : n_pad;
+  const int64_t total = n > 0 ? indptr[n] : 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&tcount[src[e]], 1);
+}
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// exclusive scan of int32 counts over n items (n static), out[n] = total
+__global__ void __launch_bounds__(kScanThreads)
+scan_i32_kernel(const int32_t* __restrict__ in, int64_t n, int32_t* __restrict__ out, ScanWs ws) {
+  __shared__ uint64_t sh_scan[kScanThreads / kWarp + 1];
+  __shared__ uint64_t sh_prefix;
+  __shared__ int sh_tile;
+  const int64_t ntiles = n > 0 ? (n + kScanTile - 1) / kScanTile : 1;
+  const int tile = grab_tile(ws, &sh_tile);
+  if (tile >= ntiles) return;
+  const int64_t base = (int64_t)tile * kScanTile + threadIdx.x * kScanItems;
+  uint32_t c[kScanItems];
+  uint64_t local = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    c[k] = (base + k < n) ? (uint32_t)in[base + k] : 0u;
+    local += c[k];
+  }
+  uint64_t tile_total;
+  const uint64_t excl = block_exclusive_scan<uint64_t, kScanThreads>(local, sh_scan, &tile_total);
+  const uint64_t prefix = lookback_prefix(ws, tile, tile_total, &sh_prefix);
+  uint64_t run = prefix + excl;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < n) out[base + k] = (int32_t)run;
+    run += c[k];
+  }
+  if (tile == ntiles - 1 && threadIdx.x == kScanThreads - 1) out[n] = (int32_t)(prefix + tile_total);
+}
+
+__global__ void transpose_fill_kernel(const int32_t* __restrict__ indptr,
+                                      const int32_t* __restrict__ src,
+                                      const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
+                                      const int32_t* __restrict__ tindptr,
+                                      int32_t* __restrict__ tfill, int32_t* __restrict__ tdst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = n_dst_dev ? *n_dst_dev : n_pad;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t d = warp; d < n; d += nwarps) {
+    const int32_t beg = indptr[d], end = indptr[d + 1];
+    for (int32_t e = beg + lane; e < end; e += 32) {
+      const int32_t s = src[e];
+      tdst[tindptr[s] + atomicAdd(&tfill[s], 1)] = (int32_t)d;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dz_prev[s, :] = mask_prev(s) * scale * (dA[s, f:2f] (s < n_pad) +
+//                 sum_{d in T(s)} dA[d, 0:f] / deg(d));  warp per source row,
+// 8 columns per lane (f <= 256 per pass, looped for wider rows)
+template <typename TG, typename TO>
+__global__ void __launch_bounds__(256)
+mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_pad,
+                  const int32_t* __restrict__ indptr, const int32_t* __restrict__ tindptr,
+                  const int32_t* __restrict__ tdst, int64_t rows,
+                  const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz, int64_t ldz) {
+  const int lane = threadIdx.x & 31;
+  const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < rows; s += nwarps) {
+    const int32_t tb = tindptr[s], te = tindptr[s + 1];
+    for (int c0 = 0; c0 < f; c0 += 256) {
+      const int c = c0 + lane * 8;
+      const bool active = c < f;
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+      if (active && s < n_pad) ld8<TG>(dA + s * lda + f + c, acc);
+      for (int k0 = tb; k0 < te; k0 += 32) {
+        const int m = min(32, te - k0);
+        int32_t myd = 0;
+        float myw = 0.f;
+        if (lane < m) {
+          myd = tdst[k0 + lane];
+          myw = 1.f / (float)(indptr[myd + 1] - indptr[myd]);
+        }
+        for (int k = 0; k < m; ++k) {
+          const int64_t d = __shfl_sync(0xffffffffu, myd, k);
+          const float w = __shfl_sync(0xffffffffu, myw, k);
+          if (active) {
+            float v[8];
+            ld8<TG>(dA + d * lda + c, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += v[j] * w;
+          }
+        }
+      }
+      if (active) {
+        const uint8_t bits = mask[(s * f + c) >> 3];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = ((bits >> j) & 1) ? acc[j] * scale : 0.f;
+        st8<TO>(dz + s * ldz + c, acc);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Adam (torch.optim.Adam semantics, no weight decay) over flat fp32 params,
+// bias correction from the device step counter; refreshes the bf16 shadow.
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
+                            float* __restrict__ m, float* __restrict__ v,
+                            __nv_bfloat16* __restrict__ shadow, int64_t n, float lr, float b1,
+                            float b2, float eps, const int64_t* __restrict__ t_dev) {
+  const float t = (float)(*t_dev + 1);
+  const float bc1 = 1.f - __powf(b1, t);
+  const float bc2 = 1.f - __powf(b2, t);
+  const float step = lr / bc1;
+  const float rbc2 = rsqrtf(bc2);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float pi = p[i] - step * mi / (sqrtf(vi) * rbc2 + eps);
+    p[i] = pi;
+    if (shadow) shadow[i] = __float2bfloat16_rn(pi);
+  }
+}
+
+__global__ void step_tail_kernel(const float* __restrict__ loss, float* __restrict__ last,
+                                 float* __restrict__ log, int64_t log_len,
+                                 int64_t* __restrict__ step, int64_t* __restrict__ adam_t) {
+  const int64_t s = *step;
+  const float l = *loss;
+  *last = l;
+  if (s >= 0 && s < log_len) log[s] = l;
+  *step = s + 1;
+  if (adam_t) *adam_t += 1;
 }
 
 static int ew_grid(int64_t n) {
@@ -141,6 +338,19 @@ static int ew_grid(int64_t n) {
   return (int)(g < 1 ? 1 : g);
 }
 
+static int warp_grid(int64_t rows) {
+  int64_t g = (rows + 7) / 8;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+static int done(int kernels) {
+  if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
+  count_launch(kernels);
+  return SAL_OK;
+}
+
 }  // namespace sal
 
 extern "C" {
@@ -148,49 +358,44 @@ extern "C" {
 int sal_plan_next(const int64_t* desc_all, int64_t n_steps, int64_t* cursor, sal_batch_desc* out,
                   void* stream) {
   sal::plan_next_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(desc_all, n_steps, cursor, out);
-  if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
-  sal::count_launch(1);
-  return SAL_OK;
+  return sal::done(1);
 }
 
-int sal_relu_dropout_fwd(const void* x, void* y, uint8_t* mask, int64_t n, int32_t dtype, float p,
-                         uint64_t seed, const int64_t* salt_dev, void* stream) {
-  if (n % 8 != 0) return SAL_EINVAL;
-  const int64_t n8 = n / 8;
+int sal_relu_dropout_fwd(const void* x, int64_t sx, void* y, int64_t sy, int64_t rows,
+                         int32_t cols, int32_t dtype, uint8_t* mask, float p, uint64_t seed,
+                         const int64_t* salt_dev, void* stream) {
+  if (cols % 8 != 0 || sx % 8 != 0 || sy % 8 != 0) return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  const int g = sal::ew_grid(rows * (cols / 8));
   if (dtype == SAL_BF16)
-    sal::relu_dropout_fwd_kernel<__nv_bfloat16><<<sal::ew_grid(n8), 256, 0, st>>>(
-        (const __nv_bfloat16*)x, (__nv_bfloat16*)y, mask, n8, p, seed, salt_dev);
+    sal::relu_dropout_fwd_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(
+        (const __nv_bfloat16*)x, sx, (__nv_bfloat16*)y, sy, rows, cols, mask, p, seed, salt_dev);
   else if (dtype == SAL_F32)
-    sal::relu_dropout_fwd_kernel<float><<<sal::ew_grid(n8), 256, 0, st>>>(
-        (const float*)x, (float*)y, mask, n8, p, seed, salt_dev);
+    sal::relu_dropout_fwd_kernel<float><<<g, 256, 0, st>>>((const float*)x, sx, (float*)y, sy,
+                                                          rows, cols, mask, p, seed, salt_dev);
   else
     return SAL_EINVAL;
-  if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
-  sal::count_launch(1);
-  return SAL_OK;
+  return sal::done(1);
 }
 
-int sal_relu_dropout_bwd(const void* dy, int32_t dy_dtype, const uint8_t* mask, void* dx,
-                         int32_t dx_dtype, int64_t n, float p, void* stream) {
-  if (n % 8 != 0) return SAL_EINVAL;
-  const int64_t n8 = n / 8;
+int sal_relu_dropout_bwd(const void* dy, int64_t sdy, int32_t dy_dtype, const uint8_t* mask,
+                         void* dx, int64_t sdx, int32_t dx_dtype, int64_t rows, int32_t cols,
+                         float p, void* stream) {
+  if (cols % 8 != 0) return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  const int g = sal::ew_grid(n8);
+  const int g = sal::ew_grid(rows * (cols / 8));
   if (dy_dtype == SAL_F32 && dx_dtype == SAL_BF16)
     sal::relu_dropout_bwd_kernel<float, __nv_bfloat16><<<g, 256, 0, st>>>(
-        (const float*)dy, mask, (__nv_bfloat16*)dx, n8, p);
+        (const float*)dy, sdy, mask, (__nv_bfloat16*)dx, sdx, rows, cols, p);
   else if (dy_dtype == SAL_BF16 && dx_dtype == SAL_BF16)
     sal::relu_dropout_bwd_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(
-        (const __nv_bfloat16*)dy, mask, (__nv_bfloat16*)dx, n8, p);
+        (const __nv_bfloat16*)dy, sdy, mask, (__nv_bfloat16*)dx, sdx, rows, cols, p);
   else if (dy_dtype == SAL_F32 && dx_dtype == SAL_F32)
-    sal::relu_dropout_bwd_kernel<float, float><<<g, 256, 0, st>>>((const float*)dy, mask,
-                                                                 (float*)dx, n8, p);
+    sal::relu_dropout_bwd_kernel<float, float><<<g, 256, 0, st>>>((const float*)dy, sdy, mask,
+                                                                 (float*)dx, sdx, rows, cols, p);
   else
     return SAL_EINVAL;
-  if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
-  sal::count_launch(1);
-  return SAL_OK;
+  return sal::done(1);
 }
 
 int sal_lsm_nll(const void* logits, int64_t ld, int64_t rows, int32_t C, int32_t dtype,
@@ -207,9 +412,78 @@ int sal_lsm_nll(const void* logits, int64_t ld, int64_t rows, int32_t C, int32_t
                                                            labels, loss, (float*)grad, ldg);
   else
     return SAL_EINVAL;
-  if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
-  sal::count_launch(1);
-  return SAL_OK;
+  return sal::done(1);
+}
+
+size_t sal_transpose_ws_bytes(int64_t n_src_rows) {
+  // tcount + tfill (int32 each) + scan workspace
+  return (size_t)(8 * (n_src_rows + 1)) + sal::scan_ws_bytes(n_src_rows) + 64;
+}
+
+int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
+                        int64_t n_pad, int64_t n_src_rows, int64_t max_edges, int32_t* tindptr,
+                        int32_t* tdst, void* ws, void* stream) {
+  (void)max_edges;
+  if (indptr == nullptr || src == nullptr || tindptr == nullptr || tdst == nullptr || ws == nullptr)
+    return SAL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* tcount = (int32_t*)ws;
+  int32_t* tfill = tcount + (n_src_rows + 1);
+  char* scan = (char*)(tfill + (n_src_rows + 1));
+  scan = (char*)(((uintptr_t)scan + 15) & ~(uintptr_t)15);
+  const size_t zero_bytes = (size_t)(8 * (n_src_rows + 1));
+  if (cudaMemsetAsync(ws, 0, zero_bytes, st) != cudaSuccess) return SAL_ECUDA;
+  const size_t sb = sal::scan_ws_bytes(n_src_rows);
+  if (cudaMemsetAsync(scan, 0, sb, st) != cudaSuccess) return SAL_ECUDA;
+  sal::transpose_count_kernel<<<sal::ew_grid(n_pad * 16), 256, 0, st>>>(indptr, src, n_dst_dev,
+                                                                         n_pad, tcount);
+  sal::ScanWs sw;
+  const int64_t tiles = (n_src_rows + sal::kScanTile - 1) / sal::kScanTile + 1;
+  sw.status = (unsigned long long*)scan;
+  sw.tile_counter = (unsigned int*)(scan + tiles * 8);
+  const int sgrid = (int)((n_src_rows + sal::kScanTile - 1) / sal::kScanTile);
+  sal::scan_i32_kernel<<<sgrid > 0 ? sgrid : 1, sal::kScanThreads, 0, st>>>(tcount, n_src_rows,
+                                                                           tindptr, sw);
+  sal::transpose_fill_kernel<<<sal::warp_grid(n_pad), 256, 0, st>>>(indptr, src, n_dst_dev, n_pad,
+                                                                    tindptr, tfill, tdst);
+  return sal::done(3);
+}
+
+int sal_mean_bwd_t(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
+                   const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
+                   int64_t rows, const uint8_t* mask, float p, void* dz, int64_t ldz,
+                   int32_t dz_dtype, void* stream) {
+  if (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0) return SAL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = sal::warp_grid(rows);
+  if (dA_dtype == SAL_BF16 && dz_dtype == SAL_BF16)
+    sal::mean_bwd_t_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(
+        (const __nv_bfloat16*)dA, lda, f, n_pad, indptr, tindptr, tdst, rows, mask, p,
+        (__nv_bfloat16*)dz, ldz);
+  else if (dA_dtype == SAL_F32 && dz_dtype == SAL_F32)
+    sal::mean_bwd_t_kernel<float, float><<<g, 256, 0, st>>>((const float*)dA, lda, f, n_pad,
+                                                           indptr, tindptr, tdst, rows, mask, p,
+                                                           (float*)dz, ldz);
+  else
+    return SAL_EINVAL;
+  return sal::done(1);
+}
+
+int sal_adam_step(float* param, const float* grad, float* m, float* v, void* shadow_bf16,
+                  int64_t n, float lr, float beta1, float beta2, float eps,
+                  const int64_t* t_dev, void* stream) {
+  if (param == nullptr || grad == nullptr || m == nullptr || v == nullptr || t_dev == nullptr)
+    return SAL_EINVAL;
+  sal::adam_kernel<<<sal::ew_grid(n), 256, 0, (cudaStream_t)stream>>>(
+      param, grad, m, v, (__nv_bfloat16*)shadow_bf16, n, lr, beta1, beta2, eps, t_dev);
+  return sal::done(1);
+}
+
+int sal_step_tail(const float* loss, float* last, float* log, int64_t log_len, int64_t* step,
+                  int64_t* adam_t, void* stream) {
+  sal::step_tail_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(loss, last, log, log_len, step,
+                                                           adam_t);
+  return sal::done(1);
 }
 
 }  // extern "C"

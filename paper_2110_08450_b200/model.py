@@ -136,117 +136,152 @@ class GraphSAGE(nn.Module):
         return torch.log_softmax(h.float(), dim=-1)
 
 
+
 # ---------------------------------------------------------------------------
 # Explicit-backward GraphSAGE for the training hot path
 # ---------------------------------------------------------------------------
 class FusedSAGE:
     """GraphSAGE with a hand-scheduled forward/backward (no autograd graph).
 
-    Parameters live in one flat fp32 buffer (Adam updates it with one fused
-    kernel); a bf16 shadow copy feeds the tensor-core GEMMs and is refreshed
-    with one cast after each optimizer step.  Weight gradients are written
-    straight into the flat fp32 gradient buffer by cuBLAS (bf16 x bf16 ->
-    fp32 output), so there is no gradient zeroing or accumulation pass, and
-    the flat buffer is what the data-parallel all-reduce sends.
+    Activations use the library's "cat" layout: the input of layer i is a
+    [rows, 2f] buffer with h_i in the right half; segment_mean writes mean_i
+    into the left half of the first n_pad (destination) rows, so each
+    SAGEConv is ONE tensor-core GEMM  z = [mean | h_dst] @ [W_neigh | W_self]^T
+    and its backward is one weight-gradient GEMM (bf16 x bf16 -> fp32 straight
+    into the flat gradient buffer) plus, above layer 0, one input-gradient
+    GEMM dA = dz @ W_cat followed by sal_mean_bwd_t, which gathers the
+    mean-term gradient per source row over the reverse adjacency and applies
+    the ReLU/dropout backward in the same pass.
 
-    Per layer i (consumption order):
-        mean_i = segment_mean(h_i)                         (library kernel)
-        z_i    = h_i[:n_pad_i] @ Ws_i^T + mean_i @ Wn_i^T  (2 cuBLAS GEMMs)
-        h_i+1  = relu_dropout(z_i)                         (library kernel)
-    loss = lsm_nll(z_L-1, labels)  (fused log_softmax + NLL + gradient)
+    Parameters: one flat fp32 buffer (per layer [f_out, 2 f_in] = [W_n | W_s]),
+    updated by one fused Adam kernel that also refreshes the bf16 shadow the
+    GEMMs read.
     """
 
     def __init__(self, f_in: int, hidden: int, num_classes: int, num_layers: int = 3,
                  dropout: float = 0.5, device=None, seed: int = 0,
-                 act_dtype: torch.dtype = torch.bfloat16):
+                 act_dtype: torch.dtype = torch.bfloat16, lr: float = 0.003,
+                 betas=(0.9, 0.999), eps: float = 1e-8):
         dev = torch.device(device or "cuda")
+        self.device = dev
         self.dims = [f_in] + [hidden] * (num_layers - 1) + [num_classes]
         self.L = num_layers
         self.p = float(dropout)
         self.act = act_dtype
-        shapes = []
-        for a, b in zip(self.dims[:-1], self.dims[1:]):
-            shapes += [(b, a), (b, a)]   # (w_neigh, w_self) per layer
+        self.lr, self.betas, self.eps = lr, betas, eps
+        shapes = [(b, 2 * a) for a, b in zip(self.dims[:-1], self.dims[1:])]
         total = sum(r * c for r, c in shapes)
         self.flat = torch.empty(total, dtype=torch.float32, device=dev)
         self.grad = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.m = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.v = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.t = torch.zeros(1, dtype=torch.int64, device=dev)
         self.shadow = torch.empty(total, dtype=act_dtype, device=dev)
         g = torch.Generator(device="cpu")
         g.manual_seed(seed)
         off = 0
         self.w, self.g, self.wb = [], [], []
         for r, c in shapes:
-            bound = 1.0 / math.sqrt(c)
-            self.flat[off:off + r * c] = (torch.rand(r * c, generator=g) * 2 - 1).mul_(bound).to(dev)
+            bound = 1.0 / math.sqrt(c // 2)   # SAGEConv-style U(-1/sqrt(f_in), 1/sqrt(f_in))
+            self.flat[off:off + r * c] = ((torch.rand(r * c, generator=g) * 2 - 1) * bound).to(dev)
             self.w.append(self.flat[off:off + r * c].view(r, c))
             self.g.append(self.grad[off:off + r * c].view(r, c))
             self.wb.append(self.shadow[off:off + r * c].view(r, c))
             off += r * c
-        self.param = torch.nn.Parameter(self.flat, requires_grad=False)
-        self.param.grad = self.grad
         self.refresh_shadow()
         self.training = True
         self.seed = seed
 
+    # ------------------------------------------------------------- weights
     def refresh_shadow(self):
         self.shadow.copy_(self.flat)
 
-    def state_dict(self):
-        return {"flat": self.flat.detach().clone(), "dims": list(self.dims)}
+    def w_neigh(self, i):
+        return self.w[i][:, :self.dims[i]]
+
+    def w_self(self, i):
+        return self.w[i][:, self.dims[i]:]
 
     def load_weights(self, layer_weights):
         """layer_weights: list of (w_self, w_neigh) arrays/tensors (out, in)."""
         for i, (ws, wn) in enumerate(layer_weights):
-            self.w[2 * i].copy_(torch.as_tensor(wn, dtype=torch.float32))
-            self.w[2 * i + 1].copy_(torch.as_tensor(ws, dtype=torch.float32))
+            self.w_neigh(i).copy_(torch.as_tensor(wn, dtype=torch.float32))
+            self.w_self(i).copy_(torch.as_tensor(ws, dtype=torch.float32))
         self.refresh_shadow()
 
-    # ---------------------------------------------------------------- fwd
-    def forward(self, x: torch.Tensor, adjs, x_global=None, salt: torch.Tensor | None = None):
-        """Returns (logits, saved) — saved holds what backward needs."""
+    def adam_step(self):
+        L = _lib.lib()
+        _lib.check(L.sal_adam_step(self.flat.data_ptr(), self.grad.data_ptr(), self.m.data_ptr(),
+                                   self.v.data_ptr(),
+                                   self.shadow.data_ptr() if self.act == torch.bfloat16 else None,
+                                   self.flat.numel(), self.lr, self.betas[0], self.betas[1],
+                                   self.eps, self.t.data_ptr(), _lib.stream_ptr()), "adam_step")
+        if self.act != torch.bfloat16:
+            self.refresh_shadow()
+
+    def optimizer_tensors(self):
+        return [self.flat, self.m, self.v, self.t]
+
+    # ------------------------------------------------------------- buffers
+    def cat_input(self, x: torch.Tensor) -> torch.Tensor:
+        """Copy a plain [N, f] layer-0 input into a fresh cat buffer [N, 2f]."""
+        a = torch.zeros((x.shape[0], 2 * x.shape[1]), dtype=self.act, device=x.device)
+        a[:, x.shape[1]:] = x
+        return a
+
+    # ------------------------------------------------------------- fwd
+    def forward(self, a0: torch.Tensor, adjs, x_global=None, salt: torch.Tensor | None = None):
+        """a0: layer-0 cat buffer (right half = features in local order).
+
+        adjs[i] = (indptr, src, n_pad, n_dst_dev).  With x_global = (table,
+        globals) layer 0's mean is read straight from the feature table.
+        Returns (logits [n_pad_last, C], saved)."""
         L = _lib.lib()
         st = _lib.stream_ptr()
-        h = x
+        a = a0
         saved = []
         for i in range(self.L):
             indptr, src, n_pad, n_dev = adjs[i]
-            f = h.shape[1] if not (i == 0 and x_global is not None) else x_global[0].shape[1]
-            mean = torch.empty((n_pad, f), dtype=self.act, device=h.device)
+            f = self.dims[i]
+            h = a[:, f:]
+            mean = a[:n_pad, :f]
             if i == 0 and x_global is not None:
                 table, gl = x_global
                 _lib.check(L.sal_segment_mean_fwd_global(
                     indptr.data_ptr(), src.data_ptr(), gl.data_ptr(), _lib.ptr(n_dev), n_pad,
                     table.data_ptr(), _lib.dtype_code(table.dtype), table.stride(0), f,
-                    mean.data_ptr(), _lib.dtype_code(self.act), mean.stride(0), st),
+                    mean.data_ptr(), _lib.dtype_code(self.act), a.stride(0), st),
                     "segment_mean_fwd_global")
             else:
                 _lib.check(L.sal_segment_mean_fwd(
                     indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dev), n_pad, h.data_ptr(),
-                    _lib.dtype_code(h.dtype), h.stride(0), f, mean.data_ptr(),
-                    _lib.dtype_code(self.act), mean.stride(0), st), "segment_mean_fwd")
-            h_dst = h[:n_pad]
-            z = torch.mm(h_dst, self.wb[2 * i + 1].t())
-            z.addmm_(mean, self.wb[2 * i].t())
-            rec = dict(h=h, mean=mean, n_pad=n_pad, adj=adjs[i])
+                    _lib.dtype_code(h.dtype), a.stride(0), f, mean.data_ptr(),
+                    _lib.dtype_code(self.act), a.stride(0), st), "segment_mean_fwd")
+            z = torch.mm(a[:n_pad], self.wb[i].t())
+            rec = dict(a=a, n_pad=n_pad, adj=adjs[i])
             if i != self.L - 1:
-                y = torch.empty_like(z)
-                mask = torch.empty(z.numel() // 8, dtype=torch.uint8, device=z.device)
+                fo = self.dims[i + 1]
+                nxt = torch.empty((n_pad, 2 * fo), dtype=self.act, device=a.device)
+                mask = torch.empty(n_pad * fo // 8, dtype=torch.uint8, device=a.device)
                 p = self.p if self.training else 0.0
                 _lib.check(L.sal_relu_dropout_fwd(
-                    z.data_ptr(), y.data_ptr(), mask.data_ptr(), z.numel(),
-                    _lib.dtype_code(z.dtype), p, (self.seed * 1000003 + i) & (2**64 - 1),
-                    _lib.ptr(salt), st), "relu_dropout_fwd")
+                    z.data_ptr(), z.stride(0), nxt[:, fo:].data_ptr(), nxt.stride(0), n_pad, fo,
+                    _lib.dtype_code(self.act), mask.data_ptr(), p,
+                    (self.seed * 1000003 + i) & (2**64 - 1), _lib.ptr(salt), st),
+                    "relu_dropout_fwd")
                 rec["mask"] = mask
-                h = y
+                a = nxt
             else:
-                h = z
+                a = z
             saved.append(rec)
-        return h, saved
+        return a, saved
 
-    def loss(self, logits: torch.Tensor, labels: torch.Tensor):
+    def loss(self, logits: torch.Tensor, labels: torch.Tensor, out: torch.Tensor | None = None):
         """Fused log_softmax + NLL; returns (loss scalar fp32, dlogits)."""
         L = _lib.lib()
-        loss = torch.zeros((), dtype=torch.float32, device=logits.device)
+        loss = out if out is not None else torch.empty((), dtype=torch.float32,
+                                                       device=logits.device)
+        loss.zero_()
         dlog = torch.empty_like(logits)
         rows = min(logits.shape[0], labels.shape[0])
         _lib.check(L.sal_lsm_nll(logits.data_ptr(), logits.stride(0), rows, logits.shape[1],
@@ -255,47 +290,66 @@ class FusedSAGE:
                                  _lib.stream_ptr()), "lsm_nll")
         return loss, dlog
 
-    # ---------------------------------------------------------------- bwd
-    def backward(self, dlogits: torch.Tensor, saved) -> None:
-        """Writes every weight gradient into self.grad (overwrite semantics)."""
+    # ------------------------------------------------------------- bwd
+    def backward(self, dlogits: torch.Tensor, saved, transposes=None) -> None:
+        """Writes every weight gradient into self.grad (overwrite semantics).
+
+        transposes[i] = (tindptr, tdst) reverse adjacency of layer i (i >= 1);
+        built here when not supplied (the trainer builds them on the prep
+        stream)."""
         L = _lib.lib()
         st = _lib.stream_ptr()
         dz = dlogits
         for i in reversed(range(self.L)):
             rec = saved[i]
-            h, mean, n_pad = rec["h"], rec["mean"], rec["n_pad"]
-            dzt = dz.t()
-            _mm_f32(dzt, mean, self.g[2 * i])
-            _mm_f32(dzt, h[:n_pad], self.g[2 * i + 1])
+            a, n_pad = rec["a"], rec["n_pad"]
+            _mm_f32(dz.t(), a[:n_pad], self.g[i])
             if i == 0:
                 break
-            # input gradient of layer i: self term + scatter of the mean term
-            dh = torch.zeros((h.shape[0], h.shape[1]), dtype=torch.float32, device=h.device)
-            _mm_f32(dz, self.wb[2 * i + 1], dh[:n_pad])
-            dmean = torch.mm(dz, self.wb[2 * i])
+            f = self.dims[i]
+            dA = torch.mm(dz, self.wb[i])                 # [n_pad, 2f]: [dmean | dh_dst]
             indptr, src, _, n_dev = rec["adj"]
-            _lib.check(L.sal_segment_mean_bwd(
-                indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dev), n_pad, dmean.data_ptr(),
-                _lib.dtype_code(dmean.dtype), dmean.stride(0), dmean.shape[1], dh.data_ptr(),
-                dh.stride(0), st), "segment_mean_bwd")
-            # through relu+dropout of the previous layer's output
-            prev_mask = saved[i - 1]["mask"]
-            dzp = torch.empty((h.shape[0], h.shape[1]), dtype=self.act, device=h.device)
-            _lib.check(L.sal_relu_dropout_bwd(
-                dh.data_ptr(), _lib.SAL_F32, prev_mask.data_ptr(), dzp.data_ptr(),
-                _lib.dtype_code(self.act), dh.numel(), self.p if self.training else 0.0, st),
-                "relu_dropout_bwd")
+            rows = a.shape[0]
+            if transposes is not None and transposes[i] is not None:
+                tindptr, tdst = transposes[i]
+            else:
+                tindptr, tdst = build_transpose(indptr, src, n_dev, n_pad, rows)
+            dzp = torch.empty((rows, f), dtype=self.act, device=a.device)
+            _lib.check(L.sal_mean_bwd_t(
+                dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
+                indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), rows,
+                saved[i - 1]["mask"].data_ptr(), self.p if self.training else 0.0,
+                dzp.data_ptr(), dzp.stride(0), _lib.dtype_code(self.act), st), "mean_bwd_t")
             dz = dzp
 
     @torch.no_grad()
-    def predict(self, x, adjs, x_global=None):
+    def predict(self, x, adjs, x_global=None, cat: bool = False):
         was = self.training
         self.training = False
         try:
-            logits, _ = self.forward(x, adjs, x_global)
+            a0 = x if cat else self.cat_input(x)
+            logits, _ = self.forward(a0, adjs, x_global)
         finally:
             self.training = was
         return logits
+
+
+def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=None, ws=None):
+    """Reverse adjacency (tindptr [n_src_rows+1], tdst [edges]) of one MFG layer."""
+    L = _lib.lib()
+    dev = indptr.device
+    if out is None:
+        tindptr = torch.empty(n_src_rows + 1, dtype=torch.int32, device=dev)
+        tdst = torch.empty(max(src.numel(), 1), dtype=torch.int32, device=dev)
+    else:
+        tindptr, tdst = out
+    if ws is None:
+        ws = torch.empty(L.sal_transpose_ws_bytes(n_src_rows), dtype=torch.uint8, device=dev)
+    _lib.check(L.sal_transpose_build(indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dst_dev),
+                                     n_pad, n_src_rows, src.numel(), tindptr.data_ptr(),
+                                     tdst.data_ptr(), ws.data_ptr(), _lib.stream_ptr()),
+               "transpose_build")
+    return tindptr, tdst
 
 
 def _mm_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:

@@ -30,7 +30,7 @@ import torch
 
 from . import _lib
 from .graph import DeviceGraph
-from .model import FusedSAGE
+from .model import FusedSAGE, build_transpose
 from .prep import gather_rows, make_epoch_plan
 from .sampler import FanoutSpec, MfgWorkspace, RNG_POLICIES
 
@@ -54,12 +54,27 @@ class TrainConfig:
 class _Slot:
     def __init__(self, dg: DeviceGraph, cfg: TrainConfig, device):
         self.ws = MfgWorkspace(dg.num_nodes, cfg.fanouts, cfg.batch_size, device=device)
-        rows = self.ws.node_cap[-1] if not cfg.gather_free else self.ws.node_cap[-2]
-        self.feats = torch.zeros((max(rows, 1), dg.num_features), dtype=cfg.act_dtype,
-                                 device=device)
+        ws = self.ws
+        nh = ws.num_hops
+        rows = ws.node_cap[-1] if not cfg.gather_free else ws.node_cap[-2]
+        f = dg.num_features
+        # layer-0 "cat" buffer: right half = gathered features, left = mean
+        self.feats = torch.zeros((max(rows, 1), 2 * f), dtype=cfg.act_dtype, device=device)
         self.labels = torch.full((cfg.batch_size,), -1, dtype=torch.int64, device=device)
         self.desc = torch.zeros(3, dtype=torch.int64, device=device)
         self.seeds = torch.zeros(max(cfg.batch_size, 1), dtype=torch.int64, device=device)
+        # reverse adjacency of layers i >= 1 (hop h = L-1-i), built on the prep stream
+        L = _lib.lib()
+        self.transposes = [None]
+        self.t_ws = [None]
+        for i in range(1, nh):
+            h = nh - 1 - i
+            n_src = ws.node_cap[h + 1]
+            self.transposes.append((
+                torch.zeros(n_src + 1, dtype=torch.int32, device=device),
+                torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.int32, device=device)))
+            self.t_ws.append(torch.empty(L.sal_transpose_ws_bytes(n_src), dtype=torch.uint8,
+                                         device=device))
 
 
 class _Staging:
@@ -87,12 +102,11 @@ class Trainer:
         self.nh = len(cfg.fanouts)
         self.model = FusedSAGE(dg.num_features, cfg.hidden, self.num_classes, self.nh,
                                cfg.dropout, device=self.device, seed=cfg.model_seed,
-                               act_dtype=cfg.act_dtype)
+                               act_dtype=cfg.act_dtype, lr=cfg.lr)
         if world > 1:  # identical initial weights on every rank
             torch.distributed.broadcast(self.model.flat, src=0)
             self.model.refresh_shadow()
-        self.opt = torch.optim.Adam([self.model.param], lr=cfg.lr, fused=True,
-                                    capturable=cfg.graphs)
+        self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
         self.slots = [_Slot(dg, cfg, self.device) for _ in range(2)]
         self.staging = [_Staging(cfg.batch_size) for _ in range(4)]
         self.prep_stream = torch.cuda.Stream(device=self.device)
@@ -171,11 +185,16 @@ class Trainer:
         nh = self.nh
         rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
         n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
-        gather_rows(self.x_table, ws.globals, slot.feats, n=rows, n_dev=n_dev, stream=st)
+        f = self.x_table.shape[1]
+        gather_rows(self.x_table, ws.globals, slot.feats[:, f:], n=rows, n_dev=n_dev, stream=st)
         _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), seeds_base.data_ptr(),
                                        slot.desc.data_ptr(), self.cfg.batch_size,
                                        slot.labels.data_ptr(), _lib.stream_ptr(st)),
                    "gather_labels")
+        for i in range(1, nh):  # reverse adjacency for the backward pass
+            h = nh - 1 - i
+            build_transpose(ws.dst_indptr[h], ws.src_local[h], ws.sizes[h:h + 1], ws.node_cap[h],
+                            ws.node_cap[h + 1], out=slot.transposes[i], ws=slot.t_ws[i])
 
     def _adjs(self, slot: _Slot):
         ws = slot.ws
@@ -190,16 +209,15 @@ class Trainer:
         m = self.model
         xg = (self.x_table, slot.ws.globals) if self.cfg.gather_free else None
         logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg, salt=self.step_ctr)
-        loss, dlog = m.loss(logits, slot.labels)
-        m.backward(dlog, saved)
+        loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf)
+        m.backward(dlog, saved, slot.transposes)
         if self.world > 1:
             torch.distributed.all_reduce(m.grad, op=torch.distributed.ReduceOp.AVG)
-        self.opt.step()
-        m.refresh_shadow()
-        self.last_loss.copy_(loss)
-        self.losses.index_copy_(0, self.step_ctr.clamp(max=self.losses.numel() - 1),
-                                loss.view(1))
-        self.step_ctr.add_(1)
+        m.adam_step()
+        _lib.check(_lib.lib().sal_step_tail(loss.data_ptr(), self.last_loss.data_ptr(),
+                                            self.losses.data_ptr(), self.losses.numel(),
+                                            self.step_ctr.data_ptr(), m.t.data_ptr(),
+                                            _lib.stream_ptr()), "step_tail")
 
     def _pair(self, k: int, host_inputs: bool) -> None:
         """{prep(slot k+1) on the prep stream || train(slot k)} on the current stream."""
@@ -270,9 +288,8 @@ class Trainer:
     def _capture(self, parity: int, host_inputs: bool) -> torch.cuda.CUDAGraph:
         """Capture {prep(next) || train(slot parity)} without disturbing state."""
         torch.cuda.synchronize()
-        fresh_opt = len(self._opt_state()) == 0
-        saved = (self.cursor.clone(), self.step_ctr.clone(), self.model.flat.clone(),
-                 [s.clone() for s in self._opt_state()])
+        state = [self.cursor, self.step_ctr] + self.model.optimizer_tensors()
+        saved = [s.clone() for s in state]
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # warm-up on a side stream (cuBLAS workspaces)
@@ -287,27 +304,12 @@ class Trainer:
         torch.cuda.synchronize()
         # library kernels per replay (the graph re-executes exactly these)
         self.graph_kernels[(parity, host_inputs)] = _lib.lib().sal_launch_count() - n0
-        # undo the warm-up's side effects
-        self.cursor.copy_(saved[0])
-        self.step_ctr.copy_(saved[1])
-        self.model.flat.copy_(saved[2])
-        if fresh_opt:
-            for a in self._opt_state():
-                a.zero_()
-        else:
-            for a, b in zip(self._opt_state(), saved[3]):
-                a.copy_(b)
+        # undo the warm-up's side effects (cursor, counters, weights, Adam state)
+        for a, b in zip(state, saved):
+            a.copy_(b)
         self.model.refresh_shadow()
         self.graphs[(parity, host_inputs)] = g
         return g
-
-    def _opt_state(self):
-        out = []
-        for st in self.opt.state.values():
-            for v in st.values():
-                if torch.is_tensor(v):
-                    out.append(v)
-        return out
 
     def train_epoch(self, epoch: int) -> float:
         n = self.set_epoch(epoch)
