@@ -172,6 +172,8 @@ def kernel_profile(trainer, nbatches: int):
     used for the roofline."""
     from paper_2110_08450_b200.prep import gather_rows
     slot = trainer.slots[0]
+    out_buf = torch.empty((slot.ws.node_cap[-1], trainer.x_table.shape[1]), dtype=torch.float16,
+                          device=trainer.device)  # fp16 -> fp16 row gather (pure copy)
     ws = slot.ws
     L = trainer.nh
     st = torch.cuda.current_stream()
@@ -186,7 +188,7 @@ def kernel_profile(trainer, nbatches: int):
         ws.run(trainer.dg, trainer.seeds_all, trainer.desc_all[step], trainer.cfg.global_seed,
                trainer.policy, st)
         ev[1].record(st)
-        gather_rows(x, ws.globals, slot.feats[:, f:], n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
+        gather_rows(x, ws.globals, out_buf, n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
                     stream=st)
         ev[2].record(st)
         sizes, etot = ws.read_extents()

@@ -127,7 +127,7 @@ gather_rows_kernel(const TIn* __restrict__ x, int64_t x_stride, const TId* __res
 constexpr int kRowUnroll = 8;
 
 template <typename TIn, typename TOut, int LPR, typename TId>
-__global__ void __launch_bounds__(kGatherThreads)
+__global__ void __launch_bounds__(kGatherThreads, 4)
 gather_rows_warp_kernel(const TIn* __restrict__ x, int64_t x_stride, const TId* __restrict__ ids,
                         const int64_t* __restrict__ n_dev, int64_t n_host, TOut* __restrict__ out,
                         int64_t out_stride) {
@@ -146,7 +146,7 @@ gather_rows_warp_kernel(const TIn* __restrict__ x, int64_t x_stride, const TId* 
   for (; r0 < n; r0 += nwarps * 32) {
     const int64_t rn = r0 + nwarps * 32;
     const int64_t next = (rn + lane < n) ? (int64_t)ids[rn + lane] : 0;
-#pragma unroll
+#pragma unroll 1
     for (int ph = 0; ph < 32; ph += kPhase) {
       uint4 buf[kU];
 #pragma unroll

@@ -155,7 +155,7 @@ segment_mean_fwd_kernel(const int32_t* __restrict__ indptr, const int32_t* __res
 // xor-shuffles at the end, so the summation order differs from the strict
 // edge order of segment_mean_fwd_kernel (used for fp32 parity).
 template <typename TIn, typename TOut, int LPR, bool kGlobal>
-__global__ void __launch_bounds__(kSegThreads)
+__global__ void __launch_bounds__(kSegThreads, 4)
 segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
                          const int32_t* __restrict__ globals,
                          const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
