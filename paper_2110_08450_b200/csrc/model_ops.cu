@@ -87,8 +87,7 @@ __global__ void relu_dropout_fwd_kernel(const T* __restrict__ x, int64_t sx, T* 
                                         const int64_t* __restrict__ salt) {
   const uint32_t thresh = (uint32_t)(p * 65536.0f);
   const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
-  const uint32_t s = salt ? (uint32_t)*salt : 0u;
-  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint64_t key_base = mix64(seed ^ mix64((salt ? (uint64_t)*salt : 0ull) + 0x5EEDull));
   const int c8 = cols / 8;
   const int64_t n8 = rows * c8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
@@ -97,9 +96,15 @@ __global__ void relu_dropout_fwd_kernel(const T* __restrict__ x, int64_t sx, T* 
     const int c = (int)(i - r * c8) * 8;
     float v[8];
     ld8<T>(x + r * sx + c, v);
-    uint4 rnd = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    if (p > 0.f) rnd = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), s, 0x5EEDu), key);
-    const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+    // dropout stream: two splitmix64 draws per 8 elements, keyed on
+    // (seed, step salt, element group) — 16 bits of uniform per element
+    uint64_t r0 = ~0ull, r1 = ~0ull;
+    if (p > 0.f) {
+      const uint64_t k = key_base ^ ((uint64_t)i * 0xD1B54A32D192ED03ull);
+      r0 = mix64(k);
+      r1 = mix64(k + kGolden);
+    }
+    const uint32_t rr[4] = {(uint32_t)r0, (uint32_t)(r0 >> 32), (uint32_t)r1, (uint32_t)(r1 >> 32)};
     uint8_t bits = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {

@@ -234,7 +234,8 @@ class FusedSAGE:
         """a0: layer-0 cat buffer (right half = features in local order).
 
         adjs[i] = (indptr, src, n_pad, n_dst_dev).  With x_global = (table,
-        globals) layer 0's mean is read straight from the feature table.
+        edge_global_ids) layer 0's mean is read straight from the feature table
+        (the sampler's per-edge global ids of the last hop).
         Returns (logits [n_pad_last, C], saved)."""
         L = _lib.lib()
         st = _lib.stream_ptr()
@@ -246,12 +247,13 @@ class FusedSAGE:
             h = a[:, f:]
             mean = a[:n_pad, :f]
             if i == 0 and x_global is not None:
-                table, gl = x_global
-                _lib.check(L.sal_segment_mean_fwd_global(
-                    indptr.data_ptr(), src.data_ptr(), gl.data_ptr(), _lib.ptr(n_dev), n_pad,
+                # gather-free layer 0: edges carry global ids, rows come from the table
+                table, gsrc = x_global
+                _lib.check(L.sal_segment_mean_fwd(
+                    indptr.data_ptr(), gsrc.data_ptr(), _lib.ptr(n_dev), n_pad,
                     table.data_ptr(), _lib.dtype_code(table.dtype), table.stride(0), f,
                     mean.data_ptr(), _lib.dtype_code(self.act), a.stride(0), st),
-                    "segment_mean_fwd_global")
+                    "segment_mean_fwd(table)")
             else:
                 _lib.check(L.sal_segment_mean_fwd(
                     indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dev), n_pad, h.data_ptr(),

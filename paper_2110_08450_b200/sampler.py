@@ -374,6 +374,8 @@ class MfgWorkspace:
                            for h in range(self.num_hops)]
         self.src_local = [self._view(lay.src_local[h], self.edge_cap[h], torch.int32)
                           for h in range(self.num_hops)]
+        # after a sample: global source ids of the LAST hop's edges (layer 0)
+        self.src_glob = self._view(lay.src_glob, max(self.edge_cap + [1]), torch.int32)
         self.seeds = torch.empty(max(1, self.max_seeds), dtype=torch.int64, device=self.device)
         self.desc = torch.zeros(3, dtype=torch.int64, device=self.device)
 

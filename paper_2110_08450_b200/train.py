@@ -207,7 +207,7 @@ class Trainer:
     def _train(self, slot: _Slot) -> None:
         """fwd + bwd + all-reduce + Adam on the current stream (capturable)."""
         m = self.model
-        xg = (self.x_table, slot.ws.globals) if self.cfg.gather_free else None
+        xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free else None
         logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg, salt=self.step_ctr)
         loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf)
         m.backward(dlog, saved, slot.transposes)
