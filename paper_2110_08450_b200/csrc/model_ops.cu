@@ -88,19 +88,18 @@ __global__ void relu_dropout_fwd_kernel(const T* __restrict__ x, int64_t sx, T* 
   const uint32_t thresh = (uint32_t)(p * 65536.0f);
   const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
   const uint64_t key_base = mix64(seed ^ mix64((salt ? (uint64_t)*salt : 0ull) + 0x5EEDull));
-  const int c8 = cols / 8;
-  const int64_t n8 = rows * c8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / c8;
+  const uint32_t c8 = (uint32_t)cols / 8;
+  const uint32_t n8 = (uint32_t)(rows * c8);  // < 2^32 groups per activation
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+    const uint32_t r = i / c8;
     const int c = (int)(i - r * c8) * 8;
     float v[8];
-    ld8<T>(x + r * sx + c, v);
+    ld8<T>(x + (int64_t)r * sx + c, v);
     // dropout stream: two splitmix64 draws per 8 elements, keyed on
     // (seed, step salt, element group) — 16 bits of uniform per element
     uint64_t r0 = ~0ull, r1 = ~0ull;
     if (p > 0.f) {
-      const uint64_t k = key_base ^ ((uint64_t)i * 0xD1B54A32D192ED03ull);
+      const uint64_t k = key_base ^ ((uint64_t)i * 0xD1B54A32D192ED03ull);  // element group
       r0 = mix64(k);
       r1 = mix64(k + kGolden);
     }
@@ -113,7 +112,7 @@ __global__ void relu_dropout_fwd_kernel(const T* __restrict__ x, int64_t sx, T* 
       bits |= (uint8_t)on << j;
       v[j] = on ? v[j] * scale : 0.f;
     }
-    st8<T>(y + r * sy + c, v);
+    st8<T>(y + (int64_t)r * sy + c, v);
     mask[i] = bits;
   }
 }
@@ -123,18 +122,17 @@ __global__ void relu_dropout_bwd_kernel(const TDY* __restrict__ dy, int64_t sdy,
                                         const uint8_t* __restrict__ mask, TDX* __restrict__ dx,
                                         int64_t sdx, int64_t rows, int32_t cols, float p) {
   const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
-  const int c8 = cols / 8;
-  const int64_t n8 = rows * c8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / c8;
+  const uint32_t c8 = (uint32_t)cols / 8;
+  const uint32_t n8 = (uint32_t)(rows * c8);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+    const uint32_t r = i / c8;
     const int c = (int)(i - r * c8) * 8;
     const uint8_t bits = mask[i];
     float v[8];
-    ld8<TDY>(dy + r * sdy + c, v);
+    ld8<TDY>(dy + (int64_t)r * sdy + c, v);
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = ((bits >> j) & 1) ? v[j] * scale : 0.f;
-    st8<TDX>(dx + r * sdx + c, v);
+    st8<TDX>(dx + (int64_t)r * sdx + c, v);
   }
 }
 

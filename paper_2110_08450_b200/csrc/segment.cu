@@ -156,9 +156,9 @@ segment_mean_fwd_kernel(const int32_t* __restrict__ indptr, const int32_t* __res
 // edge order of segment_mean_fwd_kernel (used for fp32 parity).
 template <typename TIn, int LPR, int kU>
 SAL_DEVINL void accumulate_rows(const TIn* __restrict__ h, int64_t h_stride, int32_t my, int m,
-                                int grp, int sub, float* acc) {
+                                int grp, int sub, float* acc, int k0) {
   constexpr int RPI = 32 / LPR;
-  for (int k = 0; k < m; k += RPI * kU) {
+  for (int k = k0; k < m; k += RPI * kU) {
     uint4 buf[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -218,16 +218,34 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.f;
     const int32_t cnt = d < n_dst ? end - beg : 0;
-    if (cnt > 0) {
-      accumulate_rows<TIn, LPR, kU>(h, h_stride, my, min(32, cnt), grp, sub, acc);
-      for (int32_t e0 = beg + 32; e0 < end; e0 += 32) {  // rows with > 32 edges
-        const int m = min(32, end - e0);
-        const int32_t m2 = lane < m ? load_id<kGlobal>(src, globals, e0 + lane) : 0;
-        accumulate_rows<TIn, LPR, 1>(h, h_stride, m2, m, grp, sub, acc);
-      }
+    // first round: issue the rows, then the next destination's ids, then add
+    constexpr int RPI = 32 / LPR;
+    const int m0 = min(RPI * kU, cnt);
+    uint4 buf[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = u * RPI + grp;
+      const int64_t s = __shfl_sync(0xffffffffu, my, idx & 31);
+      if (idx < m0) buf[u] = __ldg(reinterpret_cast<const uint4*>(h + s * h_stride) + sub);
     }
     const int32_t nmy = (dn < n_dst && lane < nend - nbeg)
                             ? load_id<kGlobal>(src, globals, nbeg + lane) : 0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (u * RPI + grp < m0) {
+        const TIn* v = reinterpret_cast<const TIn*>(&buf[u]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += Cvt<TIn>::in(v[j]);
+      }
+    }
+    if (cnt > RPI * kU) {  // long rows: rest of the first 32 ids, then further chunks
+      accumulate_rows<TIn, LPR, 1>(h, h_stride, my, min(32, cnt), grp, sub, acc, RPI * kU);
+      for (int32_t e0 = beg + 32; e0 < end; e0 += 32) {
+        const int m = min(32, end - e0);
+        const int32_t m2 = lane < m ? load_id<kGlobal>(src, globals, e0 + lane) : 0;
+        accumulate_rows<TIn, LPR, 1>(h, h_stride, m2, m, grp, sub, acc, 0);
+      }
+    }
     if (cnt > 0) {
 #pragma unroll
       for (int off = LPR; off < 32; off <<= 1)
