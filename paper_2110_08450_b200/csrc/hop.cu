@@ -159,7 +159,13 @@ SAL_DEVINL uint32_t draw_position(uint64_t key, uint2 pkey, uint32_t ctr, uint32
   }
 }
 
-template <int kPolicy>
+// G lanes per destination (G = 32, 16 or 8; 32/G destinations per warp in
+// flight).  Rejection sampling runs G draws per round: lane l of the group
+// takes draw ctr + l; a draw is fresh if its position is not yet accepted and
+// no lower lane of the group drew the same position this round; fresh draws
+// are accepted in lane order until the fanout is reached — exactly the
+// sequential loop of _sample_positions (_kernels.py:119-146).
+template <int kPolicy, int G>
 __global__ void __launch_bounds__(256)
 sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                      const int32_t* __restrict__ globals, const int64_t* __restrict__ n_dst_ptr,
@@ -168,9 +174,12 @@ sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restri
                      unsigned long long* table, int log2cap, int32_t* src_glob,
                      int32_t* __restrict__ slot, int32_t* __restrict__ draws_out) {
   const int lane = threadIdx.x & 31;
+  const int grp = lane / G, gl = lane % G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+  const unsigned lt_mask = ((1u << lane) - 1u) & gmask;
   const int64_t n = *n_dst_ptr;
-  const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t group_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
   // key prefix: by value (hop API) or derived on device from the batch id
   uint64_t prefix = hk.prefix;
   uint32_t batch = hk.batch;
@@ -179,57 +188,57 @@ sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restri
     if (hk.derive) prefix = hop_key_prefix(hk.global_seed, (uint64_t)desc->batch_id, hk.hop);
   }
   const uint2 pkey = make_uint2((uint32_t)hk.global_seed, (uint32_t)(hk.global_seed >> 32));
-  const unsigned lt_mask = (1u << lane) - 1u;
   __shared__ int32_t sh_acc[8][32];
 
-  for (int64_t i = warp_id; i < n; i += nwarps) {
+  for (int64_t i = group_id; i < n; i += ngroups) {
     const int32_t v = globals[i];
     const int64_t lo = ld_i64(indptr + v);
     const int64_t deg = ld_i64(indptr + v + 1) - lo;
     const int64_t out = dst_indptr[i];
     if (deg <= fanout) {  // take-all, CSR order, no draws (_kernels.py:168-174)
-      if (draws_out != nullptr && lane == 0) draws_out[i] = 0;
-      for (int64_t p = lane; p < deg; p += 32)
+      if (draws_out != nullptr && gl == 0) draws_out[i] = 0;
+      for (int64_t p = gl; p < deg; p += G)
         emit_edge(indices, lo + p, out + p, table, log2cap, src_glob, slot);
       continue;
     }
     if (inject_pos != nullptr) {  // positions injected from the reference
-      for (int j = lane; j < fanout; j += 32)
+      for (int j = gl; j < fanout; j += G)
         emit_edge(indices, lo + inject_pos[out + j], out + j, table, log2cap, src_glob, slot);
       continue;
     }
     const uint64_t key = mix64(prefix ^ (uint64_t)i);  // _kernels.py:167
     const uint32_t udeg = (uint32_t)deg;
-    // accepted positions: per-warp shared memory for fanout <= 32, else staged
-    // in this destination's own output range (overwritten by the ids below)
-    int32_t* accepted = fanout <= 32 ? sh_acc[threadIdx.x >> 5] : src_glob + out;
+    // accepted positions: this group's slice of shared memory when the fanout
+    // fits, else staged in this destination's own output range
+    int32_t* accepted = fanout <= G ? &sh_acc[threadIdx.x >> 5][grp * G] : src_glob + out;
     int acc = 0;
     uint32_t ctr = 0;
     while (acc < fanout) {
-      const uint32_t pos = draw_position<kPolicy>(key, pkey, ctr + lane, (uint32_t)i, hk.hop,
+      const uint32_t pos = draw_position<kPolicy>(key, pkey, ctr + gl, (uint32_t)i, hk.hop,
                                                   batch, udeg);
       bool hit = false;
       for (int j = 0; j < acc; ++j) hit |= ((uint32_t)accepted[j] == pos);
-      const unsigned peers = __match_any_sync(0xffffffffu, pos);
+      const unsigned peers = __match_any_sync(gmask, pos) & gmask;
       const bool fresh = !hit && (peers & lt_mask) == 0;
-      const unsigned fresh_mask = __ballot_sync(0xffffffffu, fresh);
+      const unsigned fresh_mask = __ballot_sync(gmask, fresh) & gmask;
       const int rank = __popc(fresh_mask & lt_mask);
       if (fresh && acc + rank < fanout) accepted[acc + rank] = (int32_t)pos;
-      if (draws_out != nullptr && acc + __popc(fresh_mask) >= fanout && lane == 0) {
+      const int nfresh = __popc(fresh_mask);
+      if (draws_out != nullptr && acc + nfresh >= fanout && gl == 0) {
         // CounterRng.counter after the loop: index of the completing draw + 1
-        unsigned m = fresh_mask;
+        unsigned m = fresh_mask >> (grp * G);
         for (int t = 1; t < fanout - acc; ++t) m &= m - 1;
         draws_out[i] = (int32_t)(ctr + __ffs(m));
       }
-      acc += min(__popc(fresh_mask), fanout - acc);
-      ctr += 32;
-      __syncwarp();
+      acc += min(nfresh, fanout - acc);
+      ctr += G;
+      __syncwarp(gmask);
     }
-    for (int j = lane; j < fanout; j += 32) {
+    for (int j = gl; j < fanout; j += G) {
       const int64_t p = accepted[j];
       emit_edge(indices, lo + p, out + j, table, log2cap, src_glob, slot);
     }
-    __syncwarp();
+    __syncwarp(gmask);
   }
 }
 
@@ -396,14 +405,25 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
   int64_t grid = (warps_needed + 7) / 8;
   const int64_t cap = (int64_t)num_sms() * 8;  // 8 blocks x 8 warps per SM, grid-stride
   if (grid > cap) grid = cap;
-  if (policy == kRngSplitmix)
-    sample_insert_kernel<kRngSplitmix><<<(int)grid, 256, 0, st>>>(
-        g.indptr, g.indices, m.globals, n_dst, fanout, hk, desc, inject_pos, dst_indptr, m.table,
-        m.log2cap, src_glob, slot, draws_out);
-  else
-    sample_insert_kernel<kRngPhilox><<<(int)grid, 256, 0, st>>>(
-        g.indptr, g.indices, m.globals, n_dst, fanout, hk, desc, inject_pos, dst_indptr, m.table,
-        m.log2cap, src_glob, slot, draws_out);
+  // lanes per destination: the smallest group that holds the fanout
+  const int G = fanout <= 8 ? 8 : (fanout <= 16 ? 16 : 32);
+  grid = (warps_needed * G / 32 + 7) / 8;
+  if (grid < 1) grid = 1;
+  if (grid > cap) grid = cap;
+#define SAL_SAMPLE(P, GG)                                                                   \
+  sample_insert_kernel<P, GG><<<(int)grid, 256, 0, st>>>(                                   \
+      g.indptr, g.indices, m.globals, n_dst, fanout, hk, desc, inject_pos, dst_indptr, m.table, \
+      m.log2cap, src_glob, slot, draws_out)
+  if (policy == kRngSplitmix) {
+    if (G == 8) SAL_SAMPLE(kRngSplitmix, 8);
+    else if (G == 16) SAL_SAMPLE(kRngSplitmix, 16);
+    else SAL_SAMPLE(kRngSplitmix, 32);
+  } else {
+    if (G == 8) SAL_SAMPLE(kRngPhilox, 8);
+    else if (G == 16) SAL_SAMPLE(kRngPhilox, 16);
+    else SAL_SAMPLE(kRngPhilox, 32);
+  }
+#undef SAL_SAMPLE
   return cudaGetLastError();
 }
 
