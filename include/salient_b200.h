@@ -219,19 +219,19 @@ int sal_lsm_nll(const void* logits_dev, int64_t ld, int64_t rows, int32_t num_cl
                 int64_t ldg, void* stream);
 /* reverse adjacency of an MFG layer: tindptr[n_src_rows+1], tdst[edges] lists
  * for every source row the destinations that sampled it (order within a list
- * is unspecified) */
+ * is unspecified); tw (nullable) receives each entry's 1/deg(dst) */
 size_t sal_transpose_ws_bytes(int64_t n_src_rows);
 int sal_transpose_build(const int32_t* indptr_dev, const int32_t* src_dev,
                         const int64_t* n_dst_dev, int64_t n_pad, int64_t n_src_rows,
-                        int64_t max_edges, int32_t* tindptr_dev, int32_t* tdst_dev, void* ws_dev,
-                        void* stream);
+                        int64_t max_edges, int32_t* tindptr_dev, int32_t* tdst_dev,
+                        float* tw_dev, void* ws_dev, void* stream);
 /* input gradient of a SAGEConv layer, gathered per source row s < rows:
  * dz[s] = mask(s) * (dA[s, f:2f] if s < n_pad) + sum_{d in T(s)} dA[d, 0:f]/deg(d),
  * scaled by 1/(1-p) — relu/dropout backward fused, no atomics, no zero fill */
 int sal_mean_bwd_t(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
                    const int32_t* indptr_dev, const int32_t* tindptr_dev, const int32_t* tdst_dev,
-                   int64_t rows, const uint8_t* mask_dev, float p, void* dz_dev, int64_t ldz,
-                   int32_t dz_dtype, void* stream);
+                   const float* tw_dev, int64_t rows, const uint8_t* mask_dev, float p,
+                   void* dz_dev, int64_t ldz, int32_t dz_dtype, void* stream);
 /* Adam (torch.optim.Adam, no weight decay) on flat fp32 params; step count
  * t = *t_dev + 1; refreshes the optional bf16 shadow copy */
 int sal_adam_step(float* param_dev, const float* grad_dev, float* m_dev, float* v_dev,

@@ -232,16 +232,20 @@ __global__ void transpose_fill_kernel(const int32_t* __restrict__ indptr,
                                       const int32_t* __restrict__ src,
                                       const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
                                       const int32_t* __restrict__ tindptr,
-                                      int32_t* __restrict__ tfill, int32_t* __restrict__ tdst) {
+                                      int32_t* __restrict__ tfill, int32_t* __restrict__ tdst,
+                                      float* __restrict__ tw) {
   const int lane = threadIdx.x & 31;
   const int64_t n = n_dst_dev ? *n_dst_dev : n_pad;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t d = warp; d < n; d += nwarps) {
     const int32_t beg = indptr[d], end = indptr[d + 1];
+    const float w = 1.f / (float)(end - beg);
     for (int32_t e = beg + lane; e < end; e += 32) {
       const int32_t s = src[e];
-      tdst[tindptr[s] + atomicAdd(&tfill[s], 1)] = (int32_t)d;
+      const int32_t pos = tindptr[s] + atomicAdd(&tfill[s], 1);
+      tdst[pos] = (int32_t)d;
+      if (tw) tw[pos] = w;
     }
   }
 }
@@ -254,14 +258,24 @@ template <typename TG, typename TO>
 __global__ void __launch_bounds__(256)
 mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_pad,
                   const int32_t* __restrict__ indptr, const int32_t* __restrict__ tindptr,
-                  const int32_t* __restrict__ tdst, int64_t rows,
+                  const int32_t* __restrict__ tdst, const float* __restrict__ tw, int64_t rows,
                   const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz, int64_t ldz) {
   const int lane = threadIdx.x & 31;
   const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = warp; s < rows; s += nwarps) {
-    const int32_t tb = tindptr[s], te = tindptr[s + 1];
+  int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int32_t tb = 0, te = 0;
+  if (s < rows) {
+    tb = tindptr[s];
+    te = tindptr[s + 1];
+  }
+  while (s < rows) {
+    const int64_t sn = s + nwarps;
+    int32_t ntb = 0, nte = 0;
+    if (sn < rows) {  // prefetch the next row's reverse-adjacency bounds
+      ntb = tindptr[sn];
+      nte = tindptr[sn + 1];
+    }
     for (int c0 = 0; c0 < f; c0 += 256) {
       const int c = c0 + lane * 8;
       const bool active = c < f;
@@ -275,7 +289,7 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
         float myw = 0.f;
         if (lane < m) {
           myd = tdst[k0 + lane];
-          myw = 1.f / (float)(indptr[myd + 1] - indptr[myd]);
+          myw = tw ? tw[k0 + lane] : 1.f / (float)(indptr[myd + 1] - indptr[myd]);
         }
         for (int k = 0; k < m; ++k) {
           const int64_t d = __shfl_sync(0xffffffffu, myd, k);
@@ -295,6 +309,9 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
         st8<TO>(dz + s * ldz + c, acc);
       }
     }
+    s = sn;
+    tb = ntb;
+    te = nte;
   }
 }
 
@@ -425,7 +442,7 @@ size_t sal_transpose_ws_bytes(int64_t n_src_rows) {
 
 int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
                         int64_t n_pad, int64_t n_src_rows, int64_t max_edges, int32_t* tindptr,
-                        int32_t* tdst, void* ws, void* stream) {
+                        int32_t* tdst, float* tw, void* ws, void* stream) {
   (void)max_edges;
   if (indptr == nullptr || src == nullptr || tindptr == nullptr || tdst == nullptr || ws == nullptr)
     return SAL_EINVAL;
@@ -448,25 +465,25 @@ int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t
   sal::scan_i32_kernel<<<sgrid > 0 ? sgrid : 1, sal::kScanThreads, 0, st>>>(tcount, n_src_rows,
                                                                            tindptr, sw);
   sal::transpose_fill_kernel<<<sal::warp_grid(n_pad), 256, 0, st>>>(indptr, src, n_dst_dev, n_pad,
-                                                                    tindptr, tfill, tdst);
+                                                                    tindptr, tfill, tdst, tw);
   return sal::done(3);
 }
 
 int sal_mean_bwd_t(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
                    const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
-                   int64_t rows, const uint8_t* mask, float p, void* dz, int64_t ldz,
-                   int32_t dz_dtype, void* stream) {
+                   const float* tw, int64_t rows, const uint8_t* mask, float p, void* dz,
+                   int64_t ldz, int32_t dz_dtype, void* stream) {
   if (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0) return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const int g = sal::warp_grid(rows);
   if (dA_dtype == SAL_BF16 && dz_dtype == SAL_BF16)
     sal::mean_bwd_t_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(
-        (const __nv_bfloat16*)dA, lda, f, n_pad, indptr, tindptr, tdst, rows, mask, p,
+        (const __nv_bfloat16*)dA, lda, f, n_pad, indptr, tindptr, tdst, tw, rows, mask, p,
         (__nv_bfloat16*)dz, ldz);
   else if (dA_dtype == SAL_F32 && dz_dtype == SAL_F32)
     sal::mean_bwd_t_kernel<float, float><<<g, 256, 0, st>>>((const float*)dA, lda, f, n_pad,
-                                                           indptr, tindptr, tdst, rows, mask, p,
-                                                           (float*)dz, ldz);
+                                                           indptr, tindptr, tdst, tw, rows, mask,
+                                                           p, (float*)dz, ldz);
   else
     return SAL_EINVAL;
   return sal::done(1);

@@ -164,7 +164,10 @@ SAL_DEVINL void accumulate_rows(const TIn* __restrict__ h, int64_t h_stride, int
     for (int u = 0; u < kU; ++u) {
       const int idx = k + u * RPI + grp;
       const int64_t s = __shfl_sync(0xffffffffu, my, idx & 31);
-      if (idx < m) buf[u] = __ldg(reinterpret_cast<const uint4*>(h + s * h_stride) + sub);
+      if (idx < m) {
+        const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + s * h_stride) + sub);
+        buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
+      }
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -226,7 +229,10 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
     for (int u = 0; u < kU; ++u) {
       const int idx = u * RPI + grp;
       const int64_t s = __shfl_sync(0xffffffffu, my, idx & 31);
-      if (idx < m0) buf[u] = __ldg(reinterpret_cast<const uint4*>(h + s * h_stride) + sub);
+      if (idx < m0) {
+        const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + s * h_stride) + sub);
+        buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
+      }
     }
     const int32_t nmy = (dn < n_dst && lane < nend - nbeg)
                             ? load_id<kGlobal>(src, globals, nbeg + lane) : 0;

@@ -313,13 +313,13 @@ class FusedSAGE:
             indptr, src, _, n_dev = rec["adj"]
             rows = a.shape[0]
             if transposes is not None and transposes[i] is not None:
-                tindptr, tdst = transposes[i]
+                tindptr, tdst, tw = transposes[i]
             else:
-                tindptr, tdst = build_transpose(indptr, src, n_dev, n_pad, rows)
+                tindptr, tdst, tw = build_transpose(indptr, src, n_dev, n_pad, rows)
             dzp = torch.empty((rows, f), dtype=self.act, device=a.device)
             _lib.check(L.sal_mean_bwd_t(
                 dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
-                indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), rows,
+                indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows,
                 saved[i - 1]["mask"].data_ptr(), self.p if self.training else 0.0,
                 dzp.data_ptr(), dzp.stride(0), _lib.dtype_code(self.act), st), "mean_bwd_t")
             dz = dzp
@@ -337,21 +337,23 @@ class FusedSAGE:
 
 
 def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=None, ws=None):
-    """Reverse adjacency (tindptr [n_src_rows+1], tdst [edges]) of one MFG layer."""
+    """Reverse adjacency (tindptr [n_src_rows+1], tdst, tw [edges]) of one MFG layer."""
     L = _lib.lib()
     dev = indptr.device
     if out is None:
         tindptr = torch.empty(n_src_rows + 1, dtype=torch.int32, device=dev)
         tdst = torch.empty(max(src.numel(), 1), dtype=torch.int32, device=dev)
+        tw = torch.empty(max(src.numel(), 1), dtype=torch.float32, device=dev)
     else:
-        tindptr, tdst = out
+        tindptr, tdst, tw = out
     if ws is None:
         ws = torch.empty(L.sal_transpose_ws_bytes(n_src_rows), dtype=torch.uint8, device=dev)
     _lib.check(L.sal_transpose_build(indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dst_dev),
                                      n_pad, n_src_rows, src.numel(), tindptr.data_ptr(),
-                                     tdst.data_ptr(), ws.data_ptr(), _lib.stream_ptr()),
+                                     tdst.data_ptr(), tw.data_ptr(), ws.data_ptr(),
+                                     _lib.stream_ptr()),
                "transpose_build")
-    return tindptr, tdst
+    return tindptr, tdst, tw
 
 
 def _mm_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:

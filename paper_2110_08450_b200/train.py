@@ -72,7 +72,8 @@ class _Slot:
             n_src = ws.node_cap[h + 1]
             self.transposes.append((
                 torch.zeros(n_src + 1, dtype=torch.int32, device=device),
-                torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.int32, device=device)))
+                torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.int32, device=device),
+                torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.float32, device=device)))
             self.t_ws.append(torch.empty(L.sal_transpose_ws_bytes(n_src), dtype=torch.uint8,
                                          device=device))
 
