@@ -62,7 +62,9 @@ def parse():
     p.add_argument("--fanouts", default="15,10,5")
     p.add_argument("--hidden", type=int, default=256)
     p.add_argument("--no-graphs", action="store_true")
-    p.add_argument("--gather-free", action="store_true")
+    p.add_argument("--materialise", action="store_true",
+                   help="train on the materialised feature gather instead of the gather-free "
+                        "layer-0 path")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -166,20 +168,28 @@ def build_data(shape: str, seed: int = 1):
 
 # ---------------------------------------------------------------------------
 def kernel_profile(trainer, nbatches: int):
-    """Prep-only pass: CUDA-event durations of the MFG build and the gather.
+    """Prep-only pass timed with CUDA events on the launching stream.
 
-    Returns sampled edges/s, gather GB/s and the per-launch gather figures
-    used for the roofline."""
+    Per batch: the MFG build (sal_sample_mfg: count/sample/relabel x 3 hops),
+    the full row gather of all N sampled nodes (sal_gather_rows, fp16 -> fp16,
+    the drop-in slice_features kernel) and the layer-0 mean aggregation read
+    straight from the HBM feature table (sal_segment_mean_fwd over the last
+    hop's edges — the largest kernel of the training step)."""
+    from paper_2110_08450_b200 import _lib
     from paper_2110_08450_b200.prep import gather_rows
+    Lb = _lib.lib()
     slot = trainer.slots[0]
     out_buf = torch.empty((slot.ws.node_cap[-1], trainer.x_table.shape[1]), dtype=torch.float16,
                           device=trainer.device)  # fp16 -> fp16 row gather (pure copy)
     ws = slot.ws
     L = trainer.nh
+    h0 = L - 1  # expansion hop feeding layer 0
+    mean_buf = torch.empty((ws.node_cap[h0], trainer.x_table.shape[1]), dtype=torch.bfloat16,
+                           device=trainer.device)
     st = torch.cuda.current_stream()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    t_mfg = t_gat = 0.0
-    edges = nodes = 0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    t_mfg = t_gat = t_mean = 0.0
+    edges = nodes = e0 = d0 = 0
     x = trainer.x_table
     f = x.shape[1]
     for b in range(nbatches):
@@ -191,16 +201,26 @@ def kernel_profile(trainer, nbatches: int):
         gather_rows(x, ws.globals, out_buf, n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
                     stream=st)
         ev[2].record(st)
+        _lib.check(Lb.sal_segment_mean_fwd(
+            ws.dst_indptr[h0].data_ptr(), ws.src_glob.data_ptr(), ws.sizes[h0:h0 + 1].data_ptr(),
+            ws.node_cap[h0], x.data_ptr(), _lib.SAL_F16, x.stride(0), f, mean_buf.data_ptr(),
+            _lib.SAL_BF16, mean_buf.stride(0), _lib.stream_ptr(st)), "segment_mean_fwd")
+        ev[3].record(st)
         sizes, etot = ws.read_extents()
         if b == 0:
             continue  # warm-up
         t_mfg += ev[0].elapsed_time(ev[1]) / 1e3
         t_gat += ev[1].elapsed_time(ev[2]) / 1e3
+        t_mean += ev[2].elapsed_time(ev[3]) / 1e3
         edges += sum(etot)
         nodes += sizes[-1]
+        e0 += etot[h0]
+        d0 += sizes[h0]
     k = nbatches - 1
     elem = x.element_size()
     gat_bytes = nodes * f * (elem + elem) + 4 * nodes  # read rows + write rows + ids
+    # layer-0 mean: sampled rows read (fp16) + edge ids + row pointers + mean written (bf16)
+    mean_bytes = e0 * (f * elem + 4) + d0 * (4 + f * 2)
     return {
         "sampled_edges_per_s": edges / t_mfg,
         "mfg_ms_per_batch": 1e3 * t_mfg / k,
@@ -209,6 +229,10 @@ def kernel_profile(trainer, nbatches: int):
         "gather_GBps": gat_bytes / t_gat / 1e9,
         "gather_ms_per_launch": 1e3 * t_gat / k,
         "gather_bytes_per_launch": gat_bytes / k,
+        "l0_mean_GBps": mean_bytes / t_mean / 1e9,
+        "l0_mean_ms_per_launch": 1e3 * t_mean / k,
+        "l0_mean_bytes_per_launch": mean_bytes / k,
+        "l0_edges_per_batch": e0 / k,
     }
 
 
@@ -293,7 +317,7 @@ def run_ours(args):
     rank, world, local = dist_setup(args)
     fan = FanoutSpec(tuple(int(x) for x in args.fanouts.split(",")))
     dg, train, test, gen_s = build_data(args.shape)
-    cfg = TrainConfig(fanouts=fan, hidden=args.hidden, gather_free=args.gather_free,
+    cfg = TrainConfig(fanouts=fan, hidden=args.hidden, gather_free=not args.materialise,
                       graphs=not args.no_graphs)
     tr = Trainer(dg, train, cfg, rank=rank, world=world)
     spe = tr.set_epoch(0)
@@ -369,7 +393,7 @@ def run_ours(args):
                        "global_batch": cfg.batch_size * world, "batch_per_gpu": cfg.batch_size,
                        "steps_per_epoch": spe, "epoch_extrapolated": K < spe,
                        "parallelism": f"dp{world}", "hidden": args.hidden,
-                       "gather_free": args.gather_free, "cuda_graphs": not args.no_graphs,
+                       "gather_free": not args.materialise, "cuda_graphs": not args.no_graphs,
                        "l2": "inputs (36 GB graph+features) far larger than L2; no flush",
                        "graph_gen_s": round(gen_s, 2)},
             "clocks": clk.summary(),
@@ -378,12 +402,19 @@ def run_ours(args):
             "sampled_edges_per_s": kp["sampled_edges_per_s"],
             "gather_GBps": kp["gather_GBps"],
             "kernels": kp,
-            "roofline": {"kernel": "gather_rows_kernel (fp16 rows, 128-bit)", "bound": "hbm",
-                         "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(ach / peak, 4), "peak_source": peak_src,
-                         "traffic": None,
-                         "bytes_per_launch": kp["gather_bytes_per_launch"],
-                         "ms_per_launch": kp["gather_ms_per_launch"]},
+            "roofline": {"kernel": "segment_mean_rows_kernel (layer-0 mean over the sampled "
+                                   "edges, rows read from the HBM feature table)",
+                         "bound": "hbm", "achieved": round(kp["l0_mean_GBps"], 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(kp["l0_mean_GBps"] / peak, 4),
+                         "peak_source": peak_src, "traffic": None,
+                         "bytes_per_launch": kp["l0_mean_bytes_per_launch"],
+                         "ms_per_launch": kp["l0_mean_ms_per_launch"]},
+            "gather_roofline": {"kernel": "gather_rows_warp_kernel (fp16 rows, 128-bit)",
+                                "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                                "unit": "GB/s", "frac": round(ach / peak, 4),
+                                "peak_source": peak_src,
+                                "bytes_per_launch": kp["gather_bytes_per_launch"],
+                                "ms_per_launch": kp["gather_ms_per_launch"]},
         }
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(dg, tr, fan, args.cpu_seconds, cfg.global_seed)

@@ -51,6 +51,41 @@ class TrainConfig:
     model_seed: int = 0
 
 
+def shard_plan(plan, batch_size: int, rank: int, world: int):
+    """Seed-node sharding of one epoch: global step s trains plan
+    batch s*world + rank on this rank; ranks past the end of the plan get an
+    empty batch (batch_id -1) and contribute a zero gradient.
+
+    Returns (descs int64 [steps, 3] = (batch_id, seed_offset, n_seeds) into the
+    concatenated plan, host SeedBatch or None per step)."""
+    nb = len(plan)
+    steps = math.ceil(nb / world) if nb else 0
+    descs = np.zeros((steps, 3), dtype=np.int64)
+    host = []
+    for s in range(steps):
+        b = s * world + rank
+        if b < nb:
+            sb = plan.batches[b]
+            descs[s] = (sb.batch_id, b * batch_size, len(sb))
+            host.append(sb)
+        else:
+            descs[s] = (-1, 0, 0)
+            host.append(None)
+    return descs, host
+
+
+def allreduce_mean(t: torch.Tensor, world: int) -> None:
+    """In-place mean over ranks: NCCL AVG (NVLink/NVLS), SUM / world elsewhere."""
+    if world <= 1:
+        return
+    backend = torch.distributed.get_backend()
+    if backend == "nccl":
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.AVG)
+    else:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+        t.div_(world)
+
+
 class _Slot:
     def __init__(self, dg: DeviceGraph, cfg: TrainConfig, device):
         self.ws = MfgWorkspace(dg.num_nodes, cfg.fanouts, cfg.batch_size, device=device)
@@ -129,19 +164,9 @@ class Trainer:
         """Shuffle (make_epoch_plan with shuffle_seed + epoch), shard, upload."""
         plan = make_epoch_plan(self.train_ids, self.cfg.batch_size, self.cfg.shuffle_seed + epoch)
         nb = len(plan)
-        W, r = self.world, self.rank
-        self.steps_per_epoch = math.ceil(nb / W) if nb else 0
-        descs = []
-        self.host_batches = []
-        for s in range(self.steps_per_epoch):
-            b = s * W + r
-            if b < nb:
-                sb = plan.batches[b]
-                descs.append((sb.batch_id, b * self.cfg.batch_size, len(sb)))
-                self.host_batches.append(sb)
-            else:
-                descs.append((-1, 0, 0))
-                self.host_batches.append(None)
+        descs, self.host_batches = shard_plan(plan, self.cfg.batch_size, self.rank, self.world)
+        self.steps_per_epoch = len(descs)
+        descs = [tuple(d) for d in descs]
         perm = np.concatenate([b.dst_ids for b in plan.batches]) if nb else np.zeros(1, np.int64)
         # copy into persistent buffers (captured graphs hold their addresses)
         if self.seeds_all.numel() < len(perm):
@@ -213,7 +238,7 @@ class Trainer:
         loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf)
         m.backward(dlog, saved, slot.transposes)
         if self.world > 1:
-            torch.distributed.all_reduce(m.grad, op=torch.distributed.ReduceOp.AVG)
+            allreduce_mean(m.grad, self.world)
         m.adam_step()
         _lib.check(_lib.lib().sal_step_tail(loss.data_ptr(), self.last_loss.data_ptr(),
                                             self.losses.data_ptr(), self.losses.numel(),
