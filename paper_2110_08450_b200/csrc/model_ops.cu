@@ -254,64 +254,99 @@ __global__ void transpose_fill_kernel(const int32_t* __restrict__ indptr,
 // dz_prev[s, :] = mask_prev(s) * scale * (dA[s, f:2f] (s < n_pad) +
 //                 sum_{d in T(s)} dA[d, 0:f] / deg(d));  warp per source row,
 // 8 columns per lane (f <= 256 per pass, looped for wider rows)
+// A warp takes 32 consecutive source rows: lane j fetches row j's reverse-
+// adjacency bounds and its first in-edge (dst, 1/deg) in one coalesced pass;
+// then the rows are finished kRows at a time with their self-term and
+// first-edge rows loaded back to back (2 x kRows independent 16-byte loads
+// per lane in flight).  Rows with more in-edges take a short extra loop.
 template <typename TG, typename TO>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_pad,
                   const int32_t* __restrict__ indptr, const int32_t* __restrict__ tindptr,
                   const int32_t* __restrict__ tdst, const float* __restrict__ tw, int64_t rows,
                   const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz, int64_t ldz) {
+  constexpr int kRows = 4;
   const int lane = threadIdx.x & 31;
   const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int32_t tb = 0, te = 0;
-  if (s < rows) {
-    tb = tindptr[s];
-    te = tindptr[s + 1];
-  }
-  while (s < rows) {
-    const int64_t sn = s + nwarps;
-    int32_t ntb = 0, nte = 0;
-    if (sn < rows) {  // prefetch the next row's reverse-adjacency bounds
-      ntb = tindptr[sn];
-      nte = tindptr[sn + 1];
+  const int nrows = (int)rows, npad = (int)n_pad;
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  for (int base = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < nrows;
+       base += nwarps * 32) {
+    // lane-parallel row metadata
+    const int s_l = base + lane;
+    int tb = 0, te = 0, d0 = -1;
+    float w0 = 0.f;
+    if (s_l < nrows) {
+      tb = __ldg(tindptr + s_l);
+      te = __ldg(tindptr + s_l + 1);
+      if (te > tb) {
+        d0 = __ldg(tdst + tb);
+        w0 = tw ? __ldg(tw + tb) : 1.f / (float)(__ldg(indptr + d0 + 1) - __ldg(indptr + d0));
+      }
     }
+    const int nb = min(32, nrows - base);
     for (int c0 = 0; c0 < f; c0 += 256) {
       const int c = c0 + lane * 8;
       const bool active = c < f;
-      float acc[8];
+      for (int r0 = 0; r0 < nb; r0 += kRows) {
+        // raw 16-byte vectors in flight (converted after all loads are issued)
+        uint4 self_raw[kRows][sizeof(TG) / 2], nb_raw[kRows][sizeof(TG) / 2];
+        int dd[kRows];
+        float ww[kRows];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-      if (active && s < n_pad) ld8<TG>(dA + s * lda + f + c, acc);
-      for (int k0 = tb; k0 < te; k0 += 32) {
-        const int m = min(32, te - k0);
-        int32_t myd = 0;
-        float myw = 0.f;
-        if (lane < m) {
-          myd = tdst[k0 + lane];
-          myw = tw ? tw[k0 + lane] : 1.f / (float)(indptr[myd + 1] - indptr[myd]);
+        for (int k = 0; k < kRows; ++k) {
+          const int r = r0 + k;
+          dd[k] = __shfl_sync(0xffffffffu, d0, r & 31);
+          ww[k] = __shfl_sync(0xffffffffu, w0, r & 31);
+          const int s = base + r;
+#pragma unroll
+          for (int q = 0; q < (int)sizeof(TG) / 2; ++q) {
+            self_raw[k][q] = make_uint4(0, 0, 0, 0);
+            nb_raw[k][q] = make_uint4(0, 0, 0, 0);
+          }
+          if (active && r < nb && s < npad) {
+            const uint4* ps = reinterpret_cast<const uint4*>(dA + (int64_t)s * lda + f + c);
+#pragma unroll
+            for (int q = 0; q < (int)sizeof(TG) / 2; ++q) self_raw[k][q] = __ldg(ps + q);
+          }
+          if (active && r < nb && dd[k] >= 0) {
+            const uint4* pn = reinterpret_cast<const uint4*>(dA + (int64_t)dd[k] * lda + c);
+#pragma unroll
+            for (int q = 0; q < (int)sizeof(TG) / 2; ++q) nb_raw[k][q] = __ldg(pn + q);
+          }
         }
-        for (int k = 0; k < m; ++k) {
-          const int64_t d = __shfl_sync(0xffffffffu, myd, k);
-          const float w = __shfl_sync(0xffffffffu, myw, k);
-          if (active) {
-            float v[8];
-            ld8<TG>(dA + d * lda + c, v);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] += v[j] * w;
+        for (int k = 0; k < kRows; ++k) {
+          const int r = r0 + k;
+          if (r >= nb) break;
+          const int s = base + r;
+          const TG* sv = reinterpret_cast<const TG*>(self_raw[k]);
+          const TG* nv = reinterpret_cast<const TG*>(nb_raw[k]);
+          float acc[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = F<TG>::in(sv[j]) + F<TG>::in(nv[j]) * ww[k];
+          const int rtb = __shfl_sync(0xffffffffu, tb, r & 31);
+          const int rte = __shfl_sync(0xffffffffu, te, r & 31);
+          for (int q = rtb + 1; q < rte; ++q) {  // further in-edges (rare)
+            const int d = __ldg(tdst + q);
+            const float w = tw ? __ldg(tw + q)
+                               : 1.f / (float)(__ldg(indptr + d + 1) - __ldg(indptr + d));
+            if (active) {
+              float v[8];
+              ld8<TG>(dA + (int64_t)d * lda + c, v);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) acc[j] += v[j] * w;
+            }
+          }
+          if (active) {
+            const uint8_t bits = mask[((int64_t)s * f + c) >> 3];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = ((bits >> j) & 1) ? acc[j] * scale : 0.f;
+            st8<TO>(dz + (int64_t)s * ldz + c, acc);
           }
         }
       }
-      if (active) {
-        const uint8_t bits = mask[(s * f + c) >> 3];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = ((bits >> j) & 1) ? acc[j] * scale : 0.f;
-        st8<TO>(dz + s * ldz + c, acc);
-      }
     }
-    s = sn;
-    tb = ntb;
-    te = nte;
   }
 }
 
@@ -475,7 +510,7 @@ int sal_mean_bwd_t(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int
                    int64_t ldz, int32_t dz_dtype, void* stream) {
   if (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0) return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  const int g = sal::warp_grid(rows);
+  const int g = sal::warp_grid((rows + 31) / 32);
   if (dA_dtype == SAL_BF16 && dz_dtype == SAL_BF16)
     sal::mean_bwd_t_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(
         (const __nv_bfloat16*)dA, lda, f, n_pad, indptr, tindptr, tdst, tw, rows, mask, p,

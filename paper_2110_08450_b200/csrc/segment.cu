@@ -154,39 +154,21 @@ segment_mean_fwd_kernel(const int32_t* __restrict__ indptr, const int32_t* __res
 // destination in one round).  The per-group partial sums are combined with
 // xor-shuffles at the end, so the summation order differs from the strict
 // edge order of segment_mean_fwd_kernel (used for fp32 parity).
-template <typename TIn, int LPR, int kU>
-SAL_DEVINL void accumulate_rows(const TIn* __restrict__ h, int64_t h_stride, int32_t my, int m,
-                                int grp, int sub, float* acc, int k0) {
-  constexpr int RPI = 32 / LPR;
-  for (int k = k0; k < m; k += RPI * kU) {
-    uint4 buf[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int idx = k + u * RPI + grp;
-      const int64_t s = __shfl_sync(0xffffffffu, my, idx & 31);
-      if (idx < m) {
-        const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + s * h_stride) + sub);
-        buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      if (k + u * RPI + grp < m) {
-        const TIn* v = reinterpret_cast<const TIn*>(&buf[u]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += Cvt<TIn>::in(v[j]);
-      }
-    }
-  }
-}
-
 template <bool kGlobal>
 SAL_DEVINL int32_t load_id(const int32_t* __restrict__ src, const int32_t* __restrict__ globals,
                            int32_t e) {
-  const int32_t s = src[e];
-  return kGlobal ? globals[s] : s;
+  const int32_t s = __ldg(src + e);
+  return kGlobal ? __ldg(globals + s) : s;
 }
 
+// Warp per destination; LPR lanes cover a row with 16-byte vectors, so a warp
+// reads 32/LPR source rows per instruction and keeps kU instructions in
+// flight.  Each lane loads its own row id (the LPR lanes of a group hit the
+// same word: one transaction), so the hot loop has no shuffles and no
+// divergent collectives; the per-group partial sums are combined once per
+// destination.  The mean is acc * (1/cnt); with the group-split summation
+// this path is tolerance-equal (not bit-equal) to the strict edge-order
+// fp32 kernel above.
 template <typename TIn, typename TOut, int LPR, bool kGlobal>
 __global__ void __launch_bounds__(kSegThreads, 4)
 segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
@@ -194,78 +176,51 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
                          const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
                          const TIn* __restrict__ h, int64_t h_stride, TOut* __restrict__ out,
                          int64_t out_stride) {
-  // Software-pipelined over this warp's destinations: the row bounds and the
-  // first 32 source ids of destination d + nwarps are fetched while the rows
-  // of destination d are in flight, so each destination costs one dependent
-  // memory round trip (its rows) instead of three.
-  constexpr int kU = LPR >= 32 ? 4 : (LPR < 8 ? LPR : 8);  // rows in flight: 32/LPR * kU
+  constexpr int RPI = 32 / LPR;
+  constexpr int kU = LPR >= 32 ? 4 : (LPR < 8 ? LPR : 8);
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPR, sub = lane % LPR;
-  const int64_t n_dst = n_dst_dev ? *n_dst_dev : n_pad;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int64_t d = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int32_t beg = 0, end = 0, my = 0;
-  if (d < n_dst) {
-    beg = indptr[d];
-    end = indptr[d + 1];
-    if (lane < end - beg) my = load_id<kGlobal>(src, globals, beg + lane);
-  }
-  while (d < n_pad) {
-    const int64_t dn = d + nwarps;
-    int32_t nbeg = 0, nend = 0;
-    if (dn < n_dst) {
-      nbeg = indptr[dn];
-      nend = indptr[dn + 1];
-    }
+  const int n_dst = (int)(n_dst_dev ? *n_dst_dev : n_pad);
+  const int npad = (int)n_pad;
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  for (int d = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); d < npad; d += nwarps) {
     float acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-    const int32_t cnt = d < n_dst ? end - beg : 0;
-    // first round: issue the rows, then the next destination's ids, then add
-    constexpr int RPI = 32 / LPR;
-    const int m0 = min(RPI * kU, cnt);
-    uint4 buf[kU];
+    if (d < n_dst) {
+      const int beg = __ldg(indptr + d);
+      const int end = __ldg(indptr + d + 1);
+      for (int e0 = beg; e0 < end; e0 += RPI * kU) {
+        uint4 buf[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int idx = u * RPI + grp;
-      const int64_t s = __shfl_sync(0xffffffffu, my, idx & 31);
-      if (idx < m0) {
-        const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + s * h_stride) + sub);
-        buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
-      }
-    }
-    const int32_t nmy = (dn < n_dst && lane < nend - nbeg)
-                            ? load_id<kGlobal>(src, globals, nbeg + lane) : 0;
+        for (int u = 0; u < kU; ++u) {
+          const int e = e0 + u * RPI + grp;
+          if (e < end) {
+            const int64_t s = load_id<kGlobal>(src, globals, e);
+            const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + s * h_stride) + sub);
+            buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
+          }
+        }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      if (u * RPI + grp < m0) {
-        const TIn* v = reinterpret_cast<const TIn*>(&buf[u]);
+        for (int u = 0; u < kU; ++u) {
+          if (e0 + u * RPI + grp < end) {
+            const TIn* v = reinterpret_cast<const TIn*>(&buf[u]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += Cvt<TIn>::in(v[j]);
+            for (int j = 0; j < 8; ++j) acc[j] += Cvt<TIn>::in(v[j]);
+          }
+        }
       }
-    }
-    if (cnt > RPI * kU) {  // long rows: rest of the first 32 ids, then further chunks
-      accumulate_rows<TIn, LPR, 1>(h, h_stride, my, min(32, cnt), grp, sub, acc, RPI * kU);
-      for (int32_t e0 = beg + 32; e0 < end; e0 += 32) {
-        const int m = min(32, end - e0);
-        const int32_t m2 = lane < m ? load_id<kGlobal>(src, globals, e0 + lane) : 0;
-        accumulate_rows<TIn, LPR, 1>(h, h_stride, m2, m, grp, sub, acc, 0);
-      }
-    }
-    if (cnt > 0) {
 #pragma unroll
       for (int off = LPR; off < 32; off <<= 1)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
-      const float fc = (float)cnt;
+      if (end > beg) {
+        const float inv = 1.f / (float)(end - beg);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = __fdiv_rn(acc[j], fc);
+        for (int j = 0; j < 8; ++j) acc[j] *= inv;
+      }
     }
-    if (grp == 0) store_row<TOut, 8>(out + d * out_stride + sub * 8, acc);
-    d = dn;
-    beg = nbeg;
-    end = nend;
-    my = nmy;
+    if (grp == 0) store_row<TOut, 8>(out + (int64_t)d * out_stride + sub * 8, acc);
   }
 }
 
