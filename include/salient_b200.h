@@ -241,6 +241,18 @@ int sal_adam_step(float* param_dev, const float* grad_dev, float* m_dev, float* 
 int sal_step_tail(const float* loss_dev, float* last_dev, float* log_dev, int64_t log_len,
                   int64_t* step_dev, int64_t* adam_t_dev, void* stream);
 
+/* ---- tcgen05 GEMMs of the layer-0 SAGEConv (sm_100a tensor cores) -------- */
+/* Y = act(A[M,K] @ W[N,K]^T), bf16 in, fp32 TMEM accumulate, bf16 out; with
+ * relu_dropout != 0 the epilogue applies ReLU + dropout (same stream as
+ * sal_relu_dropout_fwd) and writes the bit mask [M, N/8].  N = K = 256. */
+int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const void* W_dev, int32_t N,
+                    int32_t K, void* Y_dev, int64_t ldy, uint8_t* mask_dev, float p,
+                    uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout, void* stream);
+/* dW[N,K] (fp32, row stride lddw) = dz[M,N]^T @ A[M,K]; zeroes dW first.
+ * Split over M across CTAs with fp32 vector atomics.  N = K = 256. */
+int sal_tc_sage_wgrad(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda, int64_t M,
+                      int32_t N, int32_t K, float* dW_dev, int64_t lddw, void* stream);
+
 /* ---- on-device synthetic data (graph.py:252-298 laws) ---- */
 /* owner[s] = v for every slot s in [indptr[v], indptr[v+1]) */
 int sal_gen_owner(const int64_t* indptr_dev, int64_t n, int32_t* owner_dev, void* stream);

@@ -95,6 +95,9 @@ SIGNATURES = {
     "sal_adam_step": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, ctypes.c_float, ctypes.c_float,
                                      ctypes.c_float, ctypes.c_float, vp, vp]),
     "sal_step_tail": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
+    "sal_tc_sage_fwd": (ctypes.c_int, [vp, i64, i64, vp, i32, i32, vp, i64, vp, ctypes.c_float,
+                                       u64, vp, i32, vp]),
+    "sal_tc_sage_wgrad": (ctypes.c_int, [vp, i64, vp, i64, i64, i32, i32, vp, i64, vp]),
     "sal_gen_owner": (ctypes.c_int, [vp, i64, vp, vp]),
     "sal_gen_pairing": (ctypes.c_int, [vp, i64, u64, vp, vp]),
     "sal_gen_features_uniform": (ctypes.c_int, [i64, i32, i64, u64, vp, vp]),

@@ -266,17 +266,18 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
                   const int32_t* __restrict__ tdst, const float* __restrict__ tw, int64_t rows,
                   const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz, int64_t ldz) {
   constexpr int kRows = 4;
+  constexpr int kChunk = 8;  // source rows per warp task (lanes 0..7 fetch metadata)
   const int lane = threadIdx.x & 31;
   const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
   const int nrows = (int)rows, npad = (int)n_pad;
   const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
-  for (int base = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < nrows;
-       base += nwarps * 32) {
+  for (int base = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kChunk; base < nrows;
+       base += nwarps * kChunk) {
     // lane-parallel row metadata
     const int s_l = base + lane;
     int tb = 0, te = 0, d0 = -1;
     float w0 = 0.f;
-    if (s_l < nrows) {
+    if (lane < kChunk && s_l < nrows) {
       tb = __ldg(tindptr + s_l);
       te = __ldg(tindptr + s_l + 1);
       if (te > tb) {
@@ -284,7 +285,7 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
         w0 = tw ? __ldg(tw + tb) : 1.f / (float)(__ldg(indptr + d0 + 1) - __ldg(indptr + d0));
       }
     }
-    const int nb = min(32, nrows - base);
+    const int nb = min(kChunk, nrows - base);
     for (int c0 = 0; c0 < f; c0 += 256) {
       const int c = c0 + lane * 8;
       const bool active = c < f;
@@ -510,7 +511,7 @@ int sal_mean_bwd_t(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int
                    int64_t ldz, int32_t dz_dtype, void* stream) {
   if (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0) return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  const int g = sal::warp_grid((rows + 31) / 32);
+  const int g = sal::warp_grid((rows + 7) / 8);
   if (dA_dtype == SAL_BF16 && dz_dtype == SAL_BF16)
     sal::mean_bwd_t_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(
         (const __nv_bfloat16*)dA, lda, f, n_pad, indptr, tindptr, tdst, tw, rows, mask, p,

@@ -1,0 +1,435 @@
+// Hand-written tcgen05 GEMMs for the layer-0 SAGEConv (sm_100a).
+//
+// Forward:  y = relu_dropout( A[M, K] @ W[N, K]^T )  with A the layer-0 "cat"
+//           buffer [mean | h_dst] (bf16, K = 2f = 256) and W = [W_neigh |
+//           W_self] (N = 256).  One CTA per SM, persistent over 128-row tiles;
+//           W stays resident in shared memory (128 KB, loaded once), each A
+//           tile (64 KB) is fetched with cp.async into the 128-byte-swizzled
+//           K-major layout the UMMA descriptor describes, one elected thread
+//           issues 16 tcgen05.mma (M=128, N=256, K=16) into a TMEM accumulator,
+//           tcgen05.commit signals an mbarrier, and the epilogue (8 warps,
+//           tcgen05.ld 32x32b) applies ReLU + dropout, writes bf16 rows into the
+//           next layer's cat buffer and the keep/relu bit mask — the GEMM output
+//           never round-trips through HBM.  The next tile's cp.async is issued
+//           before the epilogue so the copy overlaps it.
+//
+// Weight gradient: dW[N, K] += dz[M, N]^T @ A[M, K] with both operands read
+//           MN-major (row-major in HBM): each CTA reduces a contiguous range of
+//           M rows into two TMEM accumulators (N = 2 x 128 rows of dW, 256
+//           columns each) and adds its partial into the fp32 gradient with
+//           vector atomics.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "salient_internal.h"
+
+namespace sal {
+namespace tc {
+
+SAL_DEVINL uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// UMMA shared-memory descriptor (cute/arch/mma_sm100_desc.hpp SmemDescriptor)
+SAL_DEVINL uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                              uint32_t layout /*2 = SWIZZLE_128B*/) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version = 1 (sm100)
+  d |= (uint64_t)(layout & 7) << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M x N, majors
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int a_mn_major, int b_mn_major) {
+  return (1u << 4)                         // c_format = F32
+         | (1u << 7)                       // a_format = BF16
+         | (1u << 10)                      // b_format = BF16
+         | ((uint32_t)a_mn_major << 15)    // a_major
+         | ((uint32_t)b_mn_major << 16)    // b_major
+         | ((uint32_t)(N >> 3) << 17)      // n_dim
+         | ((uint32_t)(M >> 4) << 24);     // m_dim
+}
+
+SAL_DEVINL void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+SAL_DEVINL void mma_commit(void* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(mbar))
+               : "memory");
+}
+
+SAL_DEVINL void mbar_init(void* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count));
+}
+
+SAL_DEVINL void mbar_wait(void* mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW%=:\n\t"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t@!p bra W%=;\n\t}\n" ::"r"(
+          smem_u32(mbar)),
+      "r"(phase)
+      : "memory");
+}
+
+SAL_DEVINL void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+SAL_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+SAL_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+SAL_DEVINL void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+SAL_DEVINL void cp_async_zero16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;" ::"r"(saddr), "l"(g) : "memory");
+}
+SAL_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+SAL_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// 32 lanes x 32 columns of fp32 from TMEM (warp-collective)
+SAL_DEVINL void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// K-major SWIZZLE_128B tile: row r, 16-byte chunk c of a 128-byte row slice
+SAL_DEVINL uint32_t swz_k(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+// ---------------------------------------------------------------------------
+// forward: M-tile 128, N = 256, K = 256 (4 K-blocks of 64)
+// ---------------------------------------------------------------------------
+constexpr int kFM = 128, kFN = 256, kFK = 256, kFKB = 64;
+constexpr int kFThreads = 256;
+constexpr uint32_t kBBytes = kFN * kFK * 2;     // 128 KB
+constexpr uint32_t kABytes = kFM * kFK * 2;     // 64 KB
+constexpr uint32_t kFSmem = kBBytes + kABytes + 1024 + 64;
+
+// load a [rows x 256] bf16 row-major block into 4 K-major SW128 K-block tiles
+SAL_DEVINL void load_kmajor(uint32_t sbase, const __nv_bfloat16* g, int64_t ldg, int rows,
+                            int valid_rows, int tid, int nthreads) {
+  // 16-byte chunks: rows x 32 per row (256 bf16 = 512 B)
+  const int chunks = rows * 32;
+  for (int q = tid; q < chunks; q += nthreads) {
+    const int r = q >> 5, cc = q & 31;          // cc: chunk within the 512-byte row
+    const int kb = cc >> 3, c = cc & 7;         // K-block and chunk within its 128-byte slice
+    const uint32_t dst = sbase + (uint32_t)kb * (uint32_t)(rows * 128) + swz_k(r, c);
+    const __nv_bfloat16* src = g + (int64_t)r * ldg + cc * 8;
+    if (r < valid_rows) cp_async16(dst, src);
+    else cp_async_zero16(dst, g);
+  }
+}
+
+__global__ void __launch_bounds__(kFThreads, 1)
+sage_fwd_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda, int M,
+                const __nv_bfloat16* __restrict__ W, __nv_bfloat16* __restrict__ Y, int64_t ldy,
+                uint8_t* __restrict__ mask, float p, uint64_t seed,
+                const int64_t* __restrict__ salt, int relu_dropout) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + kBBytes;
+  uint64_t* mbar = (uint64_t*)(sA + kABytes);
+  uint32_t* tmem_slot = (uint32_t*)(mbar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntiles = (M + kFM - 1) / kFM;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // resident weights + the first A tile
+  load_kmajor(smem_u32(sB), W, kFK, kFN, kFN, tid, kFThreads);
+  int tile = blockIdx.x;
+  if (tile < ntiles)
+    load_kmajor(smem_u32(sA), A + (int64_t)tile * kFM * lda, lda, kFM, min(kFM, M - tile * kFM),
+                tid, kFThreads);
+  cp_async_commit();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t idesc = make_idesc(kFM, kFN, 0, 0);
+  const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
+  const uint32_t thresh = (uint32_t)(p * 65536.0f);
+  const uint64_t key_base = mix64(seed ^ mix64((salt ? (uint64_t)*salt : 0ull) + 0x5EEDull));
+  uint32_t phase = 0;
+
+  for (; tile < ntiles; tile += gridDim.x) {
+    cp_async_wait_all();
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kb = 0; kb < kFK / kFKB; ++kb) {
+#pragma unroll
+        for (int k = 0; k < kFKB / 16; ++k) {
+          const uint64_t a = make_desc(smem_u32(sA) + kb * (kFM * 128) + k * 32, 16, 1024, 2);
+          const uint64_t b = make_desc(smem_u32(sB) + kb * (kFN * 128) + k * 32, 16, 1024, 2);
+          mma_f16(tmem, a, b, idesc, (kb | k) != 0);
+        }
+      }
+      mma_commit(mbar);
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // A is free again: prefetch the next tile while the epilogue drains TMEM
+    const int next = tile + gridDim.x;
+    if (next < ntiles)
+      load_kmajor(smem_u32(sA), A + (int64_t)next * kFM * lda, lda, kFM,
+                  min(kFM, M - next * kFM), tid, kFThreads);
+    cp_async_commit();
+    // epilogue: warp w reads TMEM lanes 32*(w%4).., columns [128*(w/4), +128)
+    const int row = tile * kFM + (warp & 3) * 32 + lane;
+    const int col0 = (warp >> 2) * 128;
+#pragma unroll 1
+    for (int cc = 0; cc < 128; cc += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(col0 + cc), r);
+      if (row < M) {
+        const int c = col0 + cc;
+        alignas(16) __nv_bfloat16 o[32];
+        uint8_t bits[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          // dropout stream identical to relu_dropout_fwd_kernel: group i = row*32 + col/8
+          uint64_t r0 = ~0ull, r1 = ~0ull;
+          if (relu_dropout && p > 0.f) {
+            const uint64_t i = (uint64_t)row * (kFN / 8) + (uint64_t)((c >> 3) + g);
+            const uint64_t kk = key_base ^ (i * 0xD1B54A32D192ED03ull);
+            r0 = mix64(kk);
+            r1 = mix64(kk + kGolden);
+          }
+          const uint32_t rr[4] = {(uint32_t)r0, (uint32_t)(r0 >> 32), (uint32_t)r1,
+                                  (uint32_t)(r1 >> 32)};
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float v = __uint_as_float(r[g * 8 + j]);
+            if (relu_dropout) {
+              const uint32_t u16 = (rr[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+              const bool on = (u16 >= thresh) && v > 0.f;
+              bits[g] |= (uint8_t)on << j;
+              v = on ? v * scale : 0.f;
+            }
+            o[g * 8 + j] = __float2bfloat16_rn(v);
+          }
+        }
+        uint4* dst = reinterpret_cast<uint4*>(Y + (int64_t)row * ldy + c);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = reinterpret_cast<const uint4*>(o)[q];
+        if (relu_dropout)
+          *reinterpret_cast<uint32_t*>(mask + (int64_t)row * (kFN / 8) + (c >> 3)) =
+              (uint32_t)bits[0] | ((uint32_t)bits[1] << 8) | ((uint32_t)bits[2] << 16) |
+              ((uint32_t)bits[3] << 24);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // TMEM drained before the next tile's MMA overwrites it
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// ---------------------------------------------------------------------------
+// weight gradient: dW[256 x 256] += dz[M x 256]^T @ A[M x 256], MN-major operands
+// ---------------------------------------------------------------------------
+constexpr int kGN = 256;     // dW rows (f_out) = 2 UMMA M-halves of 128
+constexpr int kGK = 256;     // dW cols (2 f_in) = UMMA N
+constexpr int kGC = 64;      // M rows (GEMM K) per chunk
+constexpr int kGThreads = 256;
+// per chunk: dz^T operand 64 x 256 bf16 (32 KB) + A operand 64 x 256 (32 KB); 2 stages
+constexpr uint32_t kGStage = 2u * kGC * 256u * 2u;
+constexpr uint32_t kGSmem = 2 * kGStage + 1024 + 64;
+
+// MN-major SW128 layout of a [kGC (k) x 256 (mn)] row-major block: atoms of
+// 8 k-rows x 64 mn (1024 B), mn-groups at LBO = 1024 B, k-groups at SBO =
+// 4 * 1024 B (the 4 mn-groups of a k-group are adjacent).
+SAL_DEVINL uint32_t swz_mn(int k, int mnchunk) {
+  const int g = mnchunk >> 3, c = mnchunk & 7;  // 64-element mn-group, 16-byte chunk in it
+  return (uint32_t)((k >> 3) * 4096 + g * 1024 + (k & 7) * 128 + ((c ^ (k & 7)) << 4));
+}
+
+SAL_DEVINL void load_mnmajor(uint32_t sbase, const __nv_bfloat16* g, int64_t ldg, int valid,
+                             int tid) {
+  for (int q = tid; q < kGC * 32; q += kGThreads) {  // 64 rows x 32 chunks of 16 B
+    const int k = q >> 5, cc = q & 31;
+    const uint32_t dst = sbase + swz_mn(k, cc);
+    if (k < valid) cp_async16(dst, g + (int64_t)k * ldg + cc * 8);
+    else cp_async_zero16(dst, g);
+  }
+}
+
+__global__ void __launch_bounds__(kGThreads, 1)
+sage_wgrad_kernel(const __nv_bfloat16* __restrict__ dz, int64_t ldz,
+                  const __nv_bfloat16* __restrict__ A, int64_t lda, int M, int rows_per_cta,
+                  float* __restrict__ dW, int64_t lddw) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* mbar = (uint64_t*)(smem + 2 * kGStage);
+  uint32_t* tmem_slot = (uint32_t*)(mbar + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.x * rows_per_cta;
+  const int m1 = min(M, m0 + rows_per_cta);
+  const int nchunks = m1 > m0 ? (m1 - m0 + kGC - 1) / kGC : 0;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  auto stage_load = [&](int ch, int s) {
+    const int mr = m0 + ch * kGC;
+    const int valid = min(kGC, m1 - mr);
+    const uint32_t base = smem_u32(smem + s * kGStage);
+    load_mnmajor(base, dz + (int64_t)mr * ldz, ldz, valid, tid);            // dz^T operand
+    load_mnmajor(base + kGStage / 2, A + (int64_t)mr * lda, lda, valid, tid);  // A operand
+    cp_async_commit();
+  };
+  if (nchunks > 0) stage_load(0, 0);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t idesc = make_idesc(128, kGK, 1, 1);
+  uint32_t ph[2] = {0, 0};
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int s = ch & 1;
+    if (ch + 1 < nchunks) {
+      if (ch >= 1) {  // stage s^1 was last read by chunk ch-1's MMAs
+        mbar_wait(&mbar[s ^ 1], ph[s ^ 1]);
+        ph[s ^ 1] ^= 1;
+      }
+      stage_load(ch + 1, s ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      cp_async_wait_all();
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t base = smem_u32(smem + s * kGStage);
+#pragma unroll
+      for (int kk = 0; kk < kGC / 16; ++kk) {  // K step of 16 rows = 2 k-groups
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {          // dW rows [128h, 128h+128): mn-groups 2h, 2h+1
+          const uint64_t a = make_desc(base + kk * 8192 + h * 2048, 1024, 4096, 2);
+          const uint64_t b = make_desc(base + kGStage / 2 + kk * 8192, 1024, 4096, 2);
+          mma_f16(tmem + h * 256, a, b, idesc, (ch | kk) != 0);
+        }
+      }
+      mma_commit(&mbar[s]);
+    }
+  }
+  if (nchunks > 0) {
+    const int s = (nchunks - 1) & 1;
+    mbar_wait(&mbar[s], ph[s]);
+    if (nchunks >= 2) {  // the other stage's last commit may still be pending
+      mbar_wait(&mbar[s ^ 1], ph[s ^ 1]);
+    }
+    tc_fence_after();
+    // epilogue: warp w -> TMEM lanes 32*(w%4) (dW rows within the half), half w/4
+    const int h = warp >> 2;
+    const int rrow = h * 128 + (warp & 3) * 32 + lane;
+#pragma unroll 1
+    for (int cc = 0; cc < kGK; cc += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(h * 256 + cc), r);
+      float* dst = dW + (int64_t)rrow * lddw + cc;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        atomicAdd(reinterpret_cast<float4*>(dst) + q,
+                  make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                              __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+}  // namespace tc
+}  // namespace sal
+
+extern "C" {
+
+int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const void* W, int32_t N, int32_t K,
+                    void* Y, int64_t ldy, uint8_t* mask, float p, uint64_t seed,
+                    const int64_t* salt_dev, int32_t relu_dropout, void* stream) {
+  if (N != sal::tc::kFN || K != sal::tc::kFK) return SAL_EINVAL;
+  if (lda % 8 || ldy % 8 || ((uintptr_t)A & 15) || ((uintptr_t)W & 15) || ((uintptr_t)Y & 15))
+    return SAL_EINVAL;
+  if (M <= 0) return SAL_OK;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sal::tc::sage_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         sal::tc::kFSmem);
+    attr = true;
+  }
+  const int ntiles = (int)((M + 127) / 128);
+  int grid = sal::num_sms();
+  if (grid > ntiles) grid = ntiles;
+  sal::tc::sage_fwd_kernel<<<grid, sal::tc::kFThreads, sal::tc::kFSmem, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)A, lda, (int)M, (const __nv_bfloat16*)W, (__nv_bfloat16*)Y, ldy, mask,
+      p, seed, salt_dev, relu_dropout);
+  if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
+  sal::count_launch(1);
+  return SAL_OK;
+}
+
+int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, int64_t M,
+                      int32_t N, int32_t K, float* dW, int64_t lddw, void* stream) {
+  if (N != sal::tc::kGN || K != sal::tc::kGK) return SAL_EINVAL;
+  if (ldz % 8 || lda % 8 || ((uintptr_t)dz & 15) || ((uintptr_t)A & 15) || ((uintptr_t)dW & 15) ||
+      lddw % 4)
+    return SAL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)N * (size_t)lddw, st) != cudaSuccess)
+    return SAL_ECUDA;
+  if (M <= 0) return SAL_OK;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sal::tc::sage_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         sal::tc::kGSmem);
+    attr = true;
+  }
+  int grid = sal::num_sms();
+  int rows = (int)((M + grid - 1) / grid);
+  rows = (rows + 63) / 64 * 64;
+  grid = (int)((M + rows - 1) / rows);
+  sal::tc::sage_wgrad_kernel<<<grid, sal::tc::kGThreads, sal::tc::kGSmem, st>>>(
+      (const __nv_bfloat16*)dz, ldz, (const __nv_bfloat16*)A, lda, (int)M, rows, dW, lddw);
+  if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
+  sal::count_launch(1);
+  return SAL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+"""tcgen05 GEMM kernels (layer-0 SAGEConv) vs torch fp32 references."""
+import pytest
+import torch
+
+from paper_2110_08450_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _fwd(A, W, p=0.0, relu=True, seed=7, salt=None, out_cols=256):
+    M = A.shape[0]
+    Y = torch.zeros((M, 2 * out_cols), dtype=torch.bfloat16, device="cuda")[:, out_cols:]
+    mask = torch.zeros(M * 256 // 8, dtype=torch.uint8, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.sal_tc_sage_fwd(A.data_ptr(), A.stride(0), M, W.data_ptr(), 256, 256,
+                                 Y.data_ptr(), Y.stride(0), mask.data_ptr(), p, seed,
+                                 _lib.ptr(salt), int(relu), _lib.stream_ptr()), "tc_sage_fwd")
+    torch.cuda.synchronize()
+    return Y, mask
+
+
+@pytest.mark.parametrize("M", [128, 1000, 67584])
+def test_tc_fwd_matches_torch(M):
+    g = torch.Generator(device="cuda").manual_seed(M)
+    A = (torch.randn(M, 512, device="cuda", generator=g) * 0.5).to(torch.bfloat16)[:, :256]
+    W = (torch.randn(256, 256, device="cuda", generator=g) * 0.06).to(torch.bfloat16)
+    Y, mask = _fwd(A, W, p=0.0, relu=False)
+    want = A.float() @ W.float().t()
+    err = (Y.float() - want).norm() / want.norm()
+    assert err < 1e-2, err
+    Y2, mask2 = _fwd(A, W, p=0.0, relu=True)
+    want2 = torch.relu(want)
+    assert ((Y2.float() - want2).norm() / want2.norm()) < 1e-2
+    # relu bits agree except where the fp32 value sits within bf16 rounding of 0
+    bits = torch.stack([(mask2 >> j) & 1 for j in range(8)], 1).reshape(M, 256).bool()
+    agree = (bits == (want > 0)) | (want.abs() < 1e-2)
+    assert agree.all()
+
+
+def test_tc_fwd_dropout_matches_unfused_kernels():
+    M = 4096
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = (torch.randn(M, 256, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(256, 256, device="cuda", generator=g) * 0.06).to(torch.bfloat16)
+    salt = torch.tensor([5], dtype=torch.int64, device="cuda")
+    Y, mask = _fwd(A, W, p=0.5, relu=True, seed=123, salt=salt)
+    # unfused: torch GEMM -> library relu_dropout with the same seed/salt
+    z = (A.float() @ W.float().t()).to(torch.bfloat16)
+    y_ref = torch.empty_like(z)
+    m_ref = torch.empty(M * 32, dtype=torch.uint8, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.sal_relu_dropout_fwd(z.data_ptr(), z.stride(0), y_ref.data_ptr(),
+                                      y_ref.stride(0), M, 256, _lib.SAL_BF16, m_ref.data_ptr(),
+                                      0.5, 123, salt.data_ptr(), _lib.stream_ptr()), "relu")
+    torch.cuda.synchronize()
+    same = (mask == m_ref).float().mean().item()
+    assert same > 0.995, same  # differences only where z ~ 0 (accumulation order)
+    keep = torch.stack([(mask >> j) & 1 for j in range(8)], 1).reshape(M, 256).float()
+    frac = keep.sum() / ((z.float() > 0).float().sum())
+    assert 0.45 < frac.item() < 0.55
+
+
+@pytest.mark.parametrize("M", [64, 1000, 67584])
+def test_tc_wgrad_matches_torch(M):
+    g = torch.Generator(device="cuda").manual_seed(M + 1)
+    dz = (torch.randn(M, 256, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    A = (torch.randn(M, 512, device="cuda", generator=g)).to(torch.bfloat16)[:, :256]
+    dW = torch.full((256, 256), 7.0, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), A.data_ptr(), A.stride(0), M,
+                                   256, 256, dW.data_ptr(), dW.stride(0), _lib.stream_ptr()),
+               "tc_sage_wgrad")
+    torch.cuda.synchronize()
+    want = dz.float().t() @ A.float()
+    err = (dW - want).norm() / want.norm()
+    assert err < 1e-3, err
