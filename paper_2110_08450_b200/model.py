@@ -191,6 +191,7 @@ class FusedSAGE:
         self.refresh_shadow()
         self.training = True
         self.seed = seed
+        self.use_tc = True
 
     # ------------------------------------------------------------- weights
     def refresh_shadow(self):
@@ -221,6 +222,12 @@ class FusedSAGE:
 
     def optimizer_tensors(self):
         return [self.flat, self.m, self.v, self.t]
+
+    def _tc_layer(self, i: int) -> bool:
+        """Layers the hand-written tcgen05 kernels cover: bf16, K = 2 f_in = 256,
+        N = f_out = 256, with a hidden layer after it (the ReLU/dropout epilogue)."""
+        return (self.use_tc and self.act == torch.bfloat16 and i != self.L - 1
+                and 2 * self.dims[i] == 256 and self.dims[i + 1] == 256)
 
     # ------------------------------------------------------------- buffers
     def cat_input(self, x: torch.Tensor) -> torch.Tensor:
@@ -259,22 +266,29 @@ class FusedSAGE:
                     indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dev), n_pad, h.data_ptr(),
                     _lib.dtype_code(h.dtype), a.stride(0), f, mean.data_ptr(),
                     _lib.dtype_code(self.act), a.stride(0), st), "segment_mean_fwd")
-            z = torch.mm(a[:n_pad], self.wb[i].t())
             rec = dict(a=a, n_pad=n_pad, adj=adjs[i])
             if i != self.L - 1:
                 fo = self.dims[i + 1]
                 nxt = torch.empty((n_pad, 2 * fo), dtype=self.act, device=a.device)
                 mask = torch.empty(n_pad * fo // 8, dtype=torch.uint8, device=a.device)
                 p = self.p if self.training else 0.0
-                _lib.check(L.sal_relu_dropout_fwd(
-                    z.data_ptr(), z.stride(0), nxt[:, fo:].data_ptr(), nxt.stride(0), n_pad, fo,
-                    _lib.dtype_code(self.act), mask.data_ptr(), p,
-                    (self.seed * 1000003 + i) & (2**64 - 1), _lib.ptr(salt), st),
-                    "relu_dropout_fwd")
+                seed = (self.seed * 1000003 + i) & (2**64 - 1)
+                if self._tc_layer(i):
+                    # tcgen05 GEMM with the ReLU/dropout epilogue: z never reaches HBM
+                    _lib.check(L.sal_tc_sage_fwd(
+                        a.data_ptr(), a.stride(0), n_pad, self.wb[i].data_ptr(), fo, 2 * f,
+                        nxt[:, fo:].data_ptr(), nxt.stride(0), mask.data_ptr(), p, seed,
+                        _lib.ptr(salt), 1, st), "tc_sage_fwd")
+                else:
+                    z = torch.mm(a[:n_pad], self.wb[i].t())
+                    _lib.check(L.sal_relu_dropout_fwd(
+                        z.data_ptr(), z.stride(0), nxt[:, fo:].data_ptr(), nxt.stride(0), n_pad,
+                        fo, _lib.dtype_code(self.act), mask.data_ptr(), p, seed, _lib.ptr(salt),
+                        st), "relu_dropout_fwd")
                 rec["mask"] = mask
                 a = nxt
             else:
-                a = z
+                a = torch.mm(a[:n_pad], self.wb[i].t())
             saved.append(rec)
         return a, saved
 
@@ -305,7 +319,13 @@ class FusedSAGE:
         for i in reversed(range(self.L)):
             rec = saved[i]
             a, n_pad = rec["a"], rec["n_pad"]
-            _mm_f32(dz.t(), a[:n_pad], self.g[i])
+            if self._tc_layer(i):
+                _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), a.data_ptr(),
+                                               a.stride(0), n_pad, self.dims[i + 1],
+                                               2 * self.dims[i], self.g[i].data_ptr(),
+                                               self.g[i].stride(0), st), "tc_sage_wgrad")
+            else:
+                _mm_f32(dz.t(), a[:n_pad], self.g[i])
             if i == 0:
                 break
             f = self.dims[i]

@@ -36,17 +36,20 @@ def _torch_reference(weights, x, layers, labels):
     return h.detach(), loss.detach(), [p.grad for p in params]
 
 
-@pytest.mark.parametrize("act", [torch.float32, torch.bfloat16])
-def test_fused_sage_matches_autograd_reference(act):
+@pytest.mark.parametrize("act,fin,hid", [(torch.float32, 64, 32), (torch.bfloat16, 64, 32),
+                                         (torch.bfloat16, 128, 256)])
+def test_fused_sage_matches_autograd_reference(act, fin, hid):
+    """(bf16, 128, 256) runs layer 0 on the tcgen05 kernels (fwd + weight grad)."""
     torch.backends.cuda.matmul.allow_tf32 = False
     g = synth_graph(2000, 8, 3.0, seed=3)
-    fm = generate_features(2000, 64, "f32", seed=3)
+    fm = generate_features(2000, fin, "f32", seed=3)
     dg = DeviceGraph.from_host(g)
     seeds = SeedBatch(0, np.random.default_rng(1).choice(2000, 128, replace=False))
     mfg = multihop_mfg(dg, seeds, FanoutSpec((10, 5, 3)), 7)
     x = torch.from_numpy(fm.data).cuda()[mfg.id_map.global_ids.long()]
     labels = torch.from_numpy(np.random.default_rng(2).integers(0, 10, 128)).cuda()
-    m = FusedSAGE(64, 32, 10, 3, dropout=0.0, seed=5, act_dtype=act)
+    m = FusedSAGE(fin, hid, 10, 3, dropout=0.0, seed=5, act_dtype=act)
+    assert m._tc_layer(0) == (fin == 128 and act == torch.bfloat16)
     weights = [(m.w_neigh(i).clone(), m.w_self(i).clone()) for i in range(3)]
     adjs = [(l.indptr, l.src_local, l.num_dst, None) for l in mfg.layers]
     logits, saved = m.forward(m.cat_input(x.to(act)), adjs)
