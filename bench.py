@@ -144,6 +144,18 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def ncu_traffic(kernel_prefix: str):
+    """DRAM bytes (read + write) per launch from the committed ncu --set full capture."""
+    try:
+        d = json.loads((REPO / "profiles" / "ncu_traffic.json").read_text())
+    except Exception:
+        return None
+    for k, v in d.items():
+        if k.startswith(kernel_prefix):
+            return int(v["dram_read"]) + int(v["dram_write"])
+    return None
+
+
 def measured_peaks():
     try:
         return json.loads((REPO / "MEASURED_PEAKS.json").read_text())
@@ -406,7 +418,10 @@ def run_ours(args):
                                    "edges, rows read from the HBM feature table)",
                          "bound": "hbm", "achieved": round(kp["l0_mean_GBps"], 1), "peak": peak,
                          "unit": "GB/s", "frac": round(kp["l0_mean_GBps"] / peak, 4),
-                         "peak_source": peak_src, "traffic": None,
+                         "peak_source": peak_src,
+                         "traffic": ncu_traffic("segment_mean_rows_kernel<__half"),
+                         "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one "
+                                           "layer-0 launch)",
                          "bytes_per_launch": kp["l0_mean_bytes_per_launch"],
                          "ms_per_launch": kp["l0_mean_ms_per_launch"]},
             "gather_roofline": {"kernel": "gather_rows_warp_kernel (fp16 rows, 128-bit)",
