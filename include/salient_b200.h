@@ -252,6 +252,15 @@ int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const void* W_dev
  * Split over M across CTAs with fp32 vector atomics.  N = K = 256. */
 int sal_tc_sage_wgrad(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda, int64_t M,
                       int32_t N, int32_t K, float* dW_dev, int64_t lddw, void* stream);
+/* the same two GEMMs without TMA / warp specialisation (cp.async, one CTA
+ * role) — the reference implementation the TMA versions are checked against */
+int sal_tc_sage_fwd_simple(const void* A_dev, int64_t lda, int64_t M, const void* W_dev,
+                           int32_t N, int32_t K, void* Y_dev, int64_t ldy, uint8_t* mask_dev,
+                           float p, uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout,
+                           void* stream);
+int sal_tc_sage_wgrad_simple(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda,
+                             int64_t M, int32_t N, int32_t K, float* dW_dev, int64_t lddw,
+                             void* stream);
 
 /* ---- on-device synthetic data (graph.py:252-298 laws) ---- */
 /* owner[s] = v for every slot s in [indptr[v], indptr[v+1]) */

@@ -18,6 +18,8 @@
 //           M rows into two TMEM accumulators (N = 2 x 128 rows of dW, 256
 //           columns each) and adds its partial into the fp32 gradient with
 //           vector atomics.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -376,6 +378,326 @@ sage_wgrad_kernel(const __nv_bfloat16* __restrict__ dz, int64_t ldz,
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ===========================================================================
+// TMA + warp-specialised versions (the production path)
+// ===========================================================================
+SAL_DEVINL void mbar_expect_tx(void* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
+               "r"(bytes)
+               : "memory");
+}
+SAL_DEVINL void mbar_arrive(void* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
+}
+SAL_DEVINL void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, void* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(mbar))
+      : "memory");
+}
+SAL_DEVINL bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// forward: warp 0 = TMA producer, warp 1 = MMA issuer, warps 2..5 = epilogue
+constexpr int kPStages = 5;                      // A K-block ring (16 KB each)
+constexpr int kPThreads = 192;
+constexpr uint32_t kPABlk = kFM * kFKB * 2;      // 16 KB
+constexpr uint32_t kPSmem = kBBytes + kPStages * kPABlk + 1024 + 256;
+
+__global__ void __launch_bounds__(kPThreads, 1)
+sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
+                    const __grid_constant__ CUtensorMap mapW, int M,
+                    __nv_bfloat16* __restrict__ Y, int64_t ldy, uint8_t* __restrict__ mask,
+                    float p, uint64_t seed, const int64_t* __restrict__ salt, int relu_dropout) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + kBBytes;
+  uint64_t* bars = (uint64_t*)(sA + kPStages * kPABlk);
+  uint64_t* full = bars;                    // [kPStages]
+  uint64_t* empty = bars + kPStages;        // [kPStages]
+  uint64_t* bfull = bars + 2 * kPStages;    // W resident
+  uint64_t* tfull = bars + 2 * kPStages + 1;   // [2] accumulator ready
+  uint64_t* tempty = bars + 2 * kPStages + 3;  // [2] accumulator drained
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kPStages + 5);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (M + kFM - 1) / kFM;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < kPStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(bfull, 1);
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tfull[1], 1);
+    mbar_init(&tempty[0], 4);
+    mbar_init(&tempty[1], 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapW) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // resident weights: 4 K-blocks of [256 rows x 64]
+      mbar_expect_tx(bfull, kBBytes);
+#pragma unroll
+      for (int kb = 0; kb < kFK / kFKB; ++kb)
+        tma_load_2d(smem_u32(sB) + kb * (kFN * 128), &mapW, kb * kFKB, 0, bfull);
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kb = 0; kb < kFK / kFKB; ++kb) {
+          mbar_wait(&empty[stage], ph ^ 1);
+          mbar_expect_tx(&full[stage], kPABlk);
+          tma_load_2d(smem_u32(sA) + stage * kPABlk, &mapA, kb * kFKB, t * kFM, &full[stage]);
+          if (++stage == kPStages) { stage = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = make_idesc(kFM, kFN, 0, 0);
+    mbar_wait(bfull, 0);
+    int stage = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const uint32_t tph = (uint32_t)((it >> 1) & 1);
+      mbar_wait(&tempty[buf], tph ^ 1);  // epilogue drained this accumulator
+      tc_fence_after();
+      for (int kb = 0; kb < kFK / kFKB; ++kb) {
+        mbar_wait(&full[stage], ph);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < kFKB / 16; ++k) {
+            const uint64_t a = make_desc(smem_u32(sA) + stage * kPABlk + k * 32, 16, 1024, 2);
+            const uint64_t b = make_desc(smem_u32(sB) + kb * (kFN * 128) + k * 32, 16, 1024, 2);
+            mma_f16(tmem + buf * 256, a, b, idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (kb == kFK / kFKB - 1) mma_commit(&tfull[buf]);
+        }
+        __syncwarp();
+        if (++stage == kPStages) { stage = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane groups (warp % 4)
+    const int lg = warp & 3;
+    const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
+    const uint32_t thresh = (uint32_t)(p * 65536.0f);
+    const uint64_t key_base = mix64(seed ^ mix64((salt ? (uint64_t)*salt : 0ull) + 0x5EEDull));
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int buf = it & 1;
+      mbar_wait(&tfull[buf], (uint32_t)((it >> 1) & 1));
+      tc_fence_after();
+      const int row = t * kFM + lg * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < kFN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * 256 + c), r);
+        if (row < M) {
+          alignas(16) __nv_bfloat16 o[32];
+          uint8_t bits[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint64_t r0 = ~0ull, r1 = ~0ull;
+            if (relu_dropout && p > 0.f) {
+              const uint64_t i = (uint64_t)row * (kFN / 8) + (uint64_t)((c >> 3) + g);
+              const uint64_t kk = key_base ^ (i * 0xD1B54A32D192ED03ull);
+              r0 = mix64(kk);
+              r1 = mix64(kk + kGolden);
+            }
+            const uint32_t rr[4] = {(uint32_t)r0, (uint32_t)(r0 >> 32), (uint32_t)r1,
+                                    (uint32_t)(r1 >> 32)};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float v = __uint_as_float(r[g * 8 + j]);
+              if (relu_dropout) {
+                const uint32_t u16 = (rr[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+                const bool on = (u16 >= thresh) && v > 0.f;
+                bits[g] |= (uint8_t)on << j;
+                v = on ? v * scale : 0.f;
+              }
+              o[g * 8 + j] = __float2bfloat16_rn(v);
+            }
+          }
+          uint4* dst = reinterpret_cast<uint4*>(Y + (int64_t)row * ldy + c);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = reinterpret_cast<const uint4*>(o)[q];
+          if (relu_dropout)
+            *reinterpret_cast<uint32_t*>(mask + (int64_t)row * (kFN / 8) + (c >> 3)) =
+                (uint32_t)bits[0] | ((uint32_t)bits[1] << 8) | ((uint32_t)bits[2] << 16) |
+                ((uint32_t)bits[3] << 24);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// weight gradient with TMA: stage = dz chunk [64 rows x 256] + A chunk [64 x 256],
+// each loaded as 4 boxes of {64 mn, 64 k} (one per 64-wide mn-group).
+constexpr int kQStages = 3;
+constexpr int kQThreads = 192;
+constexpr uint32_t kQHalf = kGC * 256 * 2;   // 32 KB per operand per stage
+constexpr uint32_t kQStage = 2 * kQHalf;
+constexpr uint32_t kQSmem = kQStages * kQStage + 1024 + 256;
+
+__global__ void __launch_bounds__(kQThreads, 1)
+sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
+                      const __grid_constant__ CUtensorMap mapA, int M, int rows_per_cta,
+                      float* __restrict__ dW, int64_t lddw) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + kQStages * kQStage);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kQStages;
+  uint64_t* done = bars + 2 * kQStages;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kQStages + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * rows_per_cta;
+  const int m1 = min(M, m0 + rows_per_cta);
+  const int nchunks = m1 > m0 ? (m1 - m0 + kGC - 1) / kGC : 0;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < kQStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int mr = m0 + ch * kGC;
+        mbar_wait(&empty[stage], ph ^ 1);
+        mbar_expect_tx(&full[stage], kQStage);
+        const uint32_t base = smem_u32(smem + stage * kQStage);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          tma_load_2d(base + g * 8192, &mapDz, g * 64, mr, &full[stage]);
+          tma_load_2d(base + kQHalf + g * 8192, &mapA, g * 64, mr, &full[stage]);
+        }
+        if (++stage == kQStages) { stage = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = make_idesc(128, kGK, 1, 1);
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      mbar_wait(&full[stage], ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t base = smem_u32(smem + stage * kQStage);
+#pragma unroll
+        for (int kk = 0; kk < kGC / 16; ++kk) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            // mn-groups 2h, 2h+1 of dz (LBO 8 KB), k-groups 2kk, 2kk+1 (SBO 1 KB)
+            const uint64_t a = make_desc(base + h * 16384 + kk * 2048, 8192, 1024, 2);
+            const uint64_t b = make_desc(base + kQHalf + kk * 2048, 8192, 1024, 2);
+            mma_f16(tmem + h * 256, a, b, idesc, (ch | kk) != 0);
+          }
+        }
+        mma_commit(&empty[stage]);
+        if (ch == nchunks - 1) mma_commit(done);
+      }
+      __syncwarp();
+      if (++stage == kQStages) { stage = 0; ph ^= 1; }
+    }
+  } else if (nchunks > 0) {
+    // epilogue warps 2..5: TMEM lane group (warp % 4), both dW halves
+    const int lg = warp & 3;
+    mbar_wait(done, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int rrow = h * 128 + lg * 32 + lane;
+#pragma unroll 1
+      for (int cc = 0; cc < kGK; cc += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(h * 256 + cc), r);
+        float* dst = dW + (int64_t)rrow * lddw + cc;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          atomicAdd(reinterpret_cast<float4*>(dst) + q,
+                    make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// host: 2-D bf16 tensor map [rows x cols] (row stride in elements), SWIZZLE_128B
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                     uint64_t row_stride_elems, uint32_t box_cols, uint32_t box_rows) {
+  if (g_encode == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        fn == nullptr)
+      return false;
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {row_stride_elems * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace tc
 }  // namespace sal
 
@@ -384,6 +706,34 @@ extern "C" {
 int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const void* W, int32_t N, int32_t K,
                     void* Y, int64_t ldy, uint8_t* mask, float p, uint64_t seed,
                     const int64_t* salt_dev, int32_t relu_dropout, void* stream) {
+  if (N != sal::tc::kFN || K != sal::tc::kFK) return SAL_EINVAL;
+  if (lda % 8 || ldy % 8 || ((uintptr_t)A & 15) || ((uintptr_t)W & 15) || ((uintptr_t)Y & 15))
+    return SAL_EINVAL;
+  if (M <= 0) return SAL_OK;
+  CUtensorMap mA, mW;
+  if (!sal::tc::make_map(&mA, A, (uint64_t)M, 256, (uint64_t)lda, 64, 128) ||
+      !sal::tc::make_map(&mW, W, 256, 256, 256, 64, 256))
+    return SAL_ECUDA;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sal::tc::sage_fwd_tma_kernel,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sal::tc::kPSmem);
+    attr = true;
+  }
+  const int ntiles = (int)((M + 127) / 128);
+  int grid = sal::num_sms();
+  if (grid > ntiles) grid = ntiles;
+  sal::tc::sage_fwd_tma_kernel<<<grid, sal::tc::kPThreads, sal::tc::kPSmem,
+                                 (cudaStream_t)stream>>>(mA, mW, (int)M, (__nv_bfloat16*)Y, ldy,
+                                                         mask, p, seed, salt_dev, relu_dropout);
+  if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
+  sal::count_launch(1);
+  return SAL_OK;
+}
+
+int sal_tc_sage_fwd_simple(const void* A, int64_t lda, int64_t M, const void* W, int32_t N,
+                           int32_t K, void* Y, int64_t ldy, uint8_t* mask, float p, uint64_t seed,
+                           const int64_t* salt_dev, int32_t relu_dropout, void* stream) {
   if (N != sal::tc::kFN || K != sal::tc::kFK) return SAL_EINVAL;
   if (lda % 8 || ldy % 8 || ((uintptr_t)A & 15) || ((uintptr_t)W & 15) || ((uintptr_t)Y & 15))
     return SAL_EINVAL;
@@ -407,6 +757,37 @@ int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const void* W, int32_
 
 int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, int64_t M,
                       int32_t N, int32_t K, float* dW, int64_t lddw, void* stream) {
+  if (N != sal::tc::kGN || K != sal::tc::kGK) return SAL_EINVAL;
+  if (ldz % 8 || lda % 8 || ((uintptr_t)dz & 15) || ((uintptr_t)A & 15) || ((uintptr_t)dW & 15) ||
+      lddw % 4)
+    return SAL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)N * (size_t)lddw, st) != cudaSuccess)
+    return SAL_ECUDA;
+  if (M <= 0) return SAL_OK;
+  CUtensorMap mD, mA;
+  if (!sal::tc::make_map(&mD, dz, (uint64_t)M, 256, (uint64_t)ldz, 64, 64) ||
+      !sal::tc::make_map(&mA, A, (uint64_t)M, 256, (uint64_t)lda, 64, 64))
+    return SAL_ECUDA;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sal::tc::sage_wgrad_tma_kernel,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sal::tc::kQSmem);
+    attr = true;
+  }
+  int grid = sal::num_sms();
+  int rows = (int)((M + grid - 1) / grid);
+  rows = (rows + 63) / 64 * 64;
+  grid = (int)((M + rows - 1) / rows);
+  sal::tc::sage_wgrad_tma_kernel<<<grid, sal::tc::kQThreads, sal::tc::kQSmem, st>>>(
+      mD, mA, (int)M, rows, dW, lddw);
+  if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
+  sal::count_launch(1);
+  return SAL_OK;
+}
+
+int sal_tc_sage_wgrad_simple(const void* dz, int64_t ldz, const void* A, int64_t lda, int64_t M,
+                             int32_t N, int32_t K, float* dW, int64_t lddw, void* stream) {
   if (N != sal::tc::kGN || K != sal::tc::kGK) return SAL_EINVAL;
   if (ldz % 8 || lda % 8 || ((uintptr_t)dz & 15) || ((uintptr_t)A & 15) || ((uintptr_t)dW & 15) ||
       lddw % 4)
