@@ -404,9 +404,11 @@ SAL_DEVINL bool elect_one() {
   return pred != 0;
 }
 
-// forward: warp 0 = TMA producer, warp 1 = MMA issuer, warps 2..5 = epilogue
+// forward: warp 0 = TMA producer, warp 1 = MMA issuer, warps 2..9 = epilogue
+// (two warps per TMEM lane group, each draining half of the 256 columns)
 constexpr int kPStages = 5;                      // A K-block ring (16 KB each)
-constexpr int kPThreads = 192;
+constexpr int kPThreads = 320;
+constexpr int kPEpiWarps = 8;
 constexpr uint32_t kPABlk = kFM * kFKB * 2;      // 16 KB
 constexpr uint32_t kPSmem = kBBytes + kPStages * kPABlk + 1024 + 256;
 
@@ -437,8 +439,8 @@ sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
     mbar_init(bfull, 1);
     mbar_init(&tfull[0], 1);
     mbar_init(&tfull[1], 1);
-    mbar_init(&tempty[0], 4);
-    mbar_init(&tempty[1], 4);
+    mbar_init(&tempty[0], kPEpiWarps);
+    mbar_init(&tempty[1], kPEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapW) : "memory");
@@ -501,8 +503,9 @@ sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
       }
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane groups (warp % 4)
+    // epilogue warps 2..9 -> TMEM lane group (warp % 4), column half (warp - 2) / 4
     const int lg = warp & 3;
+    const int chalf = (warp - 2) >> 2;
     const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
     const uint32_t thresh = (uint32_t)(p * 65536.0f);
     const uint64_t key_base = mix64(seed ^ mix64((salt ? (uint64_t)*salt : 0ull) + 0x5EEDull));
@@ -513,7 +516,7 @@ sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
       tc_fence_after();
       const int row = t * kFM + lg * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < kFN; c += 32) {
+      for (int c = chalf * (kFN / 2); c < (chalf + 1) * (kFN / 2); c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * 256 + c), r);
         if (row < M) {
@@ -656,7 +659,9 @@ sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
     for (int h = 0; h < 2; ++h) {
       const int rrow = h * 128 + lg * 32 + lane;
 #pragma unroll 1
-      for (int cc = 0; cc < kGK; cc += 32) {
+      for (int c8 = 0; c8 < kGK / 32; ++c8) {
+        // CTAs start at different column blocks so their atomics spread over L2 slices
+        const int cc = ((c8 + blockIdx.x) % (kGK / 32)) * 32;
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(h * 256 + cc), r);
         float* dst = dW + (int64_t)rrow * lddw + cc;
