@@ -154,6 +154,7 @@ class Trainer:
         self.last_loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.graphs = {}
         self.graph_kernels = {}
+        self.graph_allreduce = True    # NCCL all-reduce captured inside the step graph
         self.kernel_launches = 0   # library kernels executed by run_steps (launch audit)
         self.steps_per_epoch = 0
         self.seeds_all = torch.zeros(1, dtype=torch.int64, device=self.device)
@@ -230,30 +231,42 @@ class Trainer:
             out.append((ws.dst_indptr[h], ws.src_local[h], ws.node_cap[h], ws.sizes[h:h + 1]))
         return out
 
-    def _train(self, slot: _Slot) -> None:
-        """fwd + bwd + all-reduce + Adam on the current stream (capturable)."""
-        m = self.model
-        xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free else None
-        logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg, salt=self.step_ctr)
-        loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf)
-        m.backward(dlog, saved, slot.transposes)
-        if self.world > 1:
-            allreduce_mean(m.grad, self.world)
-        m.adam_step()
-        _lib.check(_lib.lib().sal_step_tail(loss.data_ptr(), self.last_loss.data_ptr(),
-                                            self.losses.data_ptr(), self.losses.numel(),
-                                            self.step_ctr.data_ptr(), m.t.data_ptr(),
-                                            _lib.stream_ptr()), "step_tail")
+    def _train(self, slot: _Slot, part: str = "all") -> None:
+        """fwd + bwd [+ all-reduce] [+ Adam] on the current stream (capturable).
 
-    def _pair(self, k: int, host_inputs: bool) -> None:
+        part: "all" (one graph, the gradient all-reduce captured with it),
+        "pre" (fwd + bwd only) or "post" (Adam + bookkeeping) — the split used
+        when NCCL cannot be captured, with the all-reduce issued eagerly in
+        between."""
+        m = self.model
+        if part in ("all", "pre"):
+            xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free else None
+            logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg,
+                                      salt=self.step_ctr)
+            loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf)
+            m.backward(dlog, saved, slot.transposes)
+        if part == "all" and self.world > 1:
+            allreduce_mean(m.grad, self.world)
+        if part in ("all", "post"):
+            m.adam_step()
+            _lib.check(_lib.lib().sal_step_tail(self.loss_buf.data_ptr(),
+                                                self.last_loss.data_ptr(),
+                                                self.losses.data_ptr(), self.losses.numel(),
+                                                self.step_ctr.data_ptr(), m.t.data_ptr(),
+                                                _lib.stream_ptr()), "step_tail")
+
+    def _pair(self, k: int, host_inputs: bool, part: str = "all") -> None:
         """{prep(slot k+1) on the prep stream || train(slot k)} on the current stream."""
+        if part == "post":
+            self._train(self.slots[k % 2], "post")
+            return
         cs = torch.cuda.current_stream()
         ps = self.prep_stream
         ps.wait_stream(cs)
         with torch.cuda.stream(ps):
             self._prep(self.slots[(k + 1) % 2],
                        self.staging[(k + 1) % 4] if host_inputs else None)
-        self._train(self.slots[k % 2])
+        self._train(self.slots[k % 2], part)
         cs.wait_stream(ps)
 
     # ---------------------------------------------------------------- driver
@@ -296,12 +309,20 @@ class Trainer:
                 stage.ev.synchronize()  # the replay that last read this staging buffer
                 self._stage_host(stage, k + 1)
             if self.cfg.graphs:
-                key = (k % P, host_inputs)
-                g = self.graphs.get(key)
-                if g is None:
-                    g = self._capture(k % P, host_inputs)
-                g.replay()
-                self.kernel_launches += self.graph_kernels[key]
+                if self.graph_allreduce:
+                    key = (k % P, host_inputs, "all")
+                    g = self.graphs.get(key) or self._capture(k % P, host_inputs, "all")
+                    if g is not None:
+                        g.replay()
+                        self.kernel_launches += self.graph_kernels[key]
+                if not self.graph_allreduce:  # NCCL refused capture: two graphs per step
+                    for part in ("pre", "post"):
+                        key = (k % P, host_inputs, part)
+                        g = self.graphs.get(key) or self._capture(k % P, host_inputs, part)
+                        g.replay()
+                        self.kernel_launches += self.graph_kernels[key]
+                        if part == "pre":
+                            allreduce_mean(self.model.grad, self.world)
             else:
                 n0 = _lib.lib().sal_launch_count()
                 self._pair(k % P, host_inputs)
@@ -311,8 +332,11 @@ class Trainer:
             if stage is not None:
                 stage.ev.record()
 
-    def _capture(self, parity: int, host_inputs: bool) -> torch.cuda.CUDAGraph:
-        """Capture {prep(next) || train(slot parity)} without disturbing state."""
+    def _capture(self, parity: int, host_inputs: bool, part: str = "all"):
+        """Capture one step variant without disturbing the training state.
+
+        Returns None (and switches to the split "pre"/"post" graphs) when the
+        all-reduce cannot be captured."""
         torch.cuda.synchronize()
         state = [self.cursor, self.step_ctr] + self.model.optimizer_tensors()
         saved = [s.clone() for s in state]
@@ -320,21 +344,33 @@ class Trainer:
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # warm-up on a side stream (cuBLAS workspaces)
             for _ in range(2):
-                self._pair(parity, host_inputs)
+                self._pair(parity, host_inputs, part)
+                if part == "pre":
+                    allreduce_mean(self.model.grad, self.world)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = _lib.lib().sal_launch_count()
-        with torch.cuda.graph(g):
-            self._pair(parity, host_inputs)
+        try:
+            with torch.cuda.graph(g):
+                self._pair(parity, host_inputs, part)
+        except Exception:
+            if part != "all" or self.world == 1:
+                raise
+            torch.cuda.synchronize()
+            self.graph_allreduce = False
+            for a, b in zip(state, saved):
+                a.copy_(b)
+            self.model.refresh_shadow()
+            return None
         torch.cuda.synchronize()
         # library kernels per replay (the graph re-executes exactly these)
-        self.graph_kernels[(parity, host_inputs)] = _lib.lib().sal_launch_count() - n0
+        self.graph_kernels[(parity, host_inputs, part)] = _lib.lib().sal_launch_count() - n0
         # undo the warm-up's side effects (cursor, counters, weights, Adam state)
         for a, b in zip(state, saved):
             a.copy_(b)
         self.model.refresh_shadow()
-        self.graphs[(parity, host_inputs)] = g
+        self.graphs[(parity, host_inputs, part)] = g
         return g
 
     def train_epoch(self, epoch: int) -> float:

@@ -100,7 +100,9 @@ def _small_trainer(graphs, gather_free=False, seed=0):
 def test_graph_replay_matches_eager():
     tr_e, _ = _small_trainer(False)
     tr_g, _ = _small_trainer(True)
-    for tr in (tr_e, tr_g):
+    tr_s, _ = _small_trainer(True)
+    tr_s.graph_allreduce = False  # the split pre/post graphs used when NCCL can't be captured
+    for tr in (tr_e, tr_g, tr_s):
         tr.set_epoch(0)
         tr.begin_epoch()
         tr.run_steps(0, 6)
@@ -109,7 +111,9 @@ def test_graph_replay_matches_eager():
     lg = tr_g.losses[:6].cpu().numpy()
     # fp32 atomics in the mean backward make replays differ in the last bits
     assert np.allclose(le, lg, rtol=2e-2, atol=1e-3), (le, lg)
+    assert np.allclose(le, tr_s.losses[:6].cpu().numpy(), rtol=2e-2, atol=1e-3)
     assert int(tr_g.cursor.item()) == 7
+    assert ("pre" in {k[2] for k in tr_s.graphs}) and ("all" in {k[2] for k in tr_g.graphs})
 
 
 def test_gather_free_matches_materialised():
