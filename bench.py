@@ -62,6 +62,7 @@ def parse():
     p.add_argument("--fanouts", default="15,10,5")
     p.add_argument("--hidden", type=int, default=256)
     p.add_argument("--no-graphs", action="store_true")
+    p.add_argument("--prep-priority", type=int, default=-1)
     p.add_argument("--materialise", action="store_true",
                    help="train on the materialised feature gather instead of the gather-free "
                         "layer-0 path")
@@ -330,7 +331,7 @@ def run_ours(args):
     fan = FanoutSpec(tuple(int(x) for x in args.fanouts.split(",")))
     dg, train, test, gen_s = build_data(args.shape)
     cfg = TrainConfig(fanouts=fan, hidden=args.hidden, gather_free=not args.materialise,
-                      graphs=not args.no_graphs)
+                      graphs=not args.no_graphs, prep_priority=args.prep_priority)
     tr = Trainer(dg, train, cfg, rank=rank, world=world)
     spe = tr.set_epoch(0)
     K = args.steps if args.steps > 0 else spe

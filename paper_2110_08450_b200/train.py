@@ -49,6 +49,7 @@ class TrainConfig:
     rng_policy: str = "splitmix"
     graphs: bool = True            # capture {prep || step} in CUDA graphs
     model_seed: int = 0
+    prep_priority: int = -1        # CUDA stream priority of the prep stream (lower = higher)
 
 
 def shard_plan(plan, batch_size: int, rank: int, world: int):
@@ -145,7 +146,9 @@ class Trainer:
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
         self.slots = [_Slot(dg, cfg, self.device) for _ in range(2)]
         self.staging = [_Staging(cfg.batch_size) for _ in range(4)]
-        self.prep_stream = torch.cuda.Stream(device=self.device)
+        # high priority: the prep chain is latency-bound (many small dependent kernels), so
+        # it should take SMs first as the bandwidth-bound training kernels drain
+        self.prep_stream = torch.cuda.Stream(device=self.device, priority=cfg.prep_priority)
         self.policy = RNG_POLICIES[cfg.rng_policy]
         self.x_table = dg.feature_view()
         self.cursor = torch.zeros(1, dtype=torch.int64, device=self.device)
