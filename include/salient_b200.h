@@ -121,14 +121,6 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
                    void* ws_dev, const int64_t* seeds_base_dev, const sal_batch_desc* desc_dev,
                    uint64_t global_seed, int32_t rng_policy, void* stream);
 
-/* as sal_sample_mfg; tcount_per_hop (host array of L device pointers, entries
- * nullable) receives, per hop, the number of edges sourced at each local id
- * (the reverse-adjacency row sizes of that MFG layer) */
-int sal_sample_mfg_ex(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* layout,
-                      void* ws_dev, const int64_t* seeds_base_dev,
-                      const sal_batch_desc* desc_dev, uint64_t global_seed, int32_t rng_policy,
-                      int32_t* const* tcount_per_hop, void* stream);
-
 /* ---- hop-level operators (the _kernels.py operator layer) --------------- */
 size_t sal_scan_ws_bytes(int64_t max_items);
 /* reset every slot of the map to empty (IdMap.__init__, sampler.py:113-129) */
@@ -233,14 +225,6 @@ int sal_transpose_build(const int32_t* indptr_dev, const int32_t* src_dev,
                         const int64_t* n_dst_dev, int64_t n_pad, int64_t n_src_rows,
                         int64_t max_edges, int32_t* tindptr_dev, int32_t* tdst_dev,
                         float* tw_dev, void* ws_dev, void* stream);
-/* as above; counts_ready: tcount (at the start of ws) was already filled by
- * sal_sample_mfg_ex; first_d/first_w (nullable, [n_src_rows]) receive each
- * row's first in-edge (dst | sign bit "more follow", 1/deg) for sal_mean_bwd_t_ex */
-int sal_transpose_build_ex(const int32_t* indptr_dev, const int32_t* src_dev,
-                           const int64_t* n_dst_dev, int64_t n_pad, int64_t n_src_rows,
-                           int64_t max_edges, int32_t* tindptr_dev, int32_t* tdst_dev,
-                           float* tw_dev, int32_t* first_d_dev, float* first_w_dev,
-                           int32_t counts_ready, void* ws_dev, void* stream);
 /* input gradient of a SAGEConv layer, gathered per source row s < rows:
  * dz[s] = mask(s) * (dA[s, f:2f] if s < n_pad) + sum_{d in T(s)} dA[d, 0:f]/deg(d),
  * scaled by 1/(1-p) — relu/dropout backward fused, no atomics, no zero fill */
@@ -248,12 +232,6 @@ int sal_mean_bwd_t(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f,
                    const int32_t* indptr_dev, const int32_t* tindptr_dev, const int32_t* tdst_dev,
                    const float* tw_dev, int64_t rows, const uint8_t* mask_dev, float p,
                    void* dz_dev, int64_t ldz, int32_t dz_dtype, void* stream);
-/* same, reading each row's first in-edge from first_d/first_w */
-int sal_mean_bwd_t_ex(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
-                      const int32_t* indptr_dev, const int32_t* tindptr_dev,
-                      const int32_t* tdst_dev, const float* tw_dev, const int32_t* first_d_dev,
-                      const float* first_w_dev, int64_t rows, const uint8_t* mask_dev, float p,
-                      void* dz_dev, int64_t ldz, int32_t dz_dtype, void* stream);
 /* Adam (torch.optim.Adam, no weight decay) on flat fp32 params; step count
  * t = *t_dev + 1; refreshes the optional bf16 shadow copy */
 int sal_adam_step(float* param_dev, const float* grad_dev, float* m_dev, float* v_dev,

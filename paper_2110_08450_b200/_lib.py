@@ -65,8 +65,6 @@ SIGNATURES = {
     "sal_mfg_layout_init": (ctypes.c_int, [P(SalMfgPlan), P(SalMfgLayout)]),
     "sal_sample_mfg": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp, vp,
                                       u64, i32, vp]),
-    "sal_sample_mfg_ex": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp,
-                                         vp, u64, i32, vp, vp]),
     "sal_scan_ws_bytes": (ctypes.c_size_t, [i64]),
     "sal_idmap_reset": (ctypes.c_int, [P(SalIdMap), vp]),
     "sal_idmap_rehash": (ctypes.c_int, [P(SalIdMap), i64, vp]),
@@ -94,10 +92,6 @@ SIGNATURES = {
     "sal_transpose_build": (ctypes.c_int, [vp, vp, vp, i64, i64, i64, vp, vp, vp, vp, vp]),
     "sal_mean_bwd_t": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp,
                                       ctypes.c_float, vp, i64, i32, vp]),
-    "sal_mean_bwd_t_ex": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, vp, vp, i64,
-                                         vp, ctypes.c_float, vp, i64, i32, vp]),
-    "sal_transpose_build_ex": (ctypes.c_int, [vp, vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, i32,
-                                              vp, vp]),
     "sal_adam_step": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, ctypes.c_float, ctypes.c_float,
                                      ctypes.c_float, ctypes.c_float, vp, vp]),
     "sal_step_tail": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),

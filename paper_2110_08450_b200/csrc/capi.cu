@@ -152,10 +152,9 @@ int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* L) {
   return SAL_OK;
 }
 
-int sal_sample_mfg_ex(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
-                      void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
-                      uint64_t global_seed, int32_t rng_policy, int32_t* const* tcount_per_hop,
-                      void* stream) {
+int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
+                   void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
+                   uint64_t global_seed, int32_t rng_policy, void* stream) {
   if (g == nullptr || plan == nullptr || L == nullptr || ws == nullptr || seeds_base == nullptr ||
       desc == nullptr)
     return fail(SAL_EINVAL, "sample_mfg: null argument");
@@ -195,23 +194,11 @@ int sal_sample_mfg_ex(const sal_graph* g, const sal_mfg_plan* plan, const sal_mf
     e = sal::launch_hop_sample(gd, m, sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
                                rng_policy, nullptr, dst_indptr, src_glob, slot, nullptr, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
-    int32_t* tcount = tcount_per_hop ? tcount_per_hop[h] : nullptr;
-    if (tcount != nullptr) {
-      e = cudaMemsetAsync(tcount, 0, sizeof(int32_t) * (size_t)(plan->node_cap[h + 1] + 1), st);
-      if (e != cudaSuccess) return cuda_status(e, "sample_mfg: reverse-adjacency counters");
-    }
     e = sal::launch_hop_relabel(m, etot + h, plan->edge_cap[h], sizes + h, sizes + h + 1,
-                                src_glob, slot, rank, src_local, scan, st, tcount);
+                                src_glob, slot, rank, src_local, scan, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop relabel");
   }
   return counted(SAL_OK, 1 + 4 * plan->num_hops);
-}
-
-int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
-                   void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
-                   uint64_t global_seed, int32_t rng_policy, void* stream) {
-  return sal_sample_mfg_ex(g, plan, L, ws, seeds_base, desc, global_seed, rng_policy, nullptr,
-                           stream);
 }
 
 // ---------------------------------------------------------------------------

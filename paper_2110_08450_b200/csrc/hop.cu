@@ -310,7 +310,7 @@ __global__ void resolve_kernel(unsigned long long* table, const int32_t* __restr
                                const int64_t* __restrict__ e_total,
                                const int64_t* __restrict__ size_old_ptr,
                                const int32_t* __restrict__ rank_of,
-                               int32_t* __restrict__ src_local, int32_t* __restrict__ tcount) {
+                               int32_t* __restrict__ src_local) {
   const int64_t n = *e_total;
   const int64_t size_old = *size_old_ptr;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -327,7 +327,6 @@ __global__ void resolve_kernel(unsigned long long* table, const int32_t* __restr
       local = lo;
     }
     if (src_local != nullptr) src_local[e] = (int32_t)local;
-    if (tcount != nullptr) atomicAdd(&tcount[local], 1);  // reverse-adjacency row sizes
   }
 }
 
@@ -442,8 +441,7 @@ cudaError_t launch_keys_insert(const int64_t* keys, int64_t n, const IdMapDev& m
 cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_t max_edges,
                                const int64_t* size_old, int64_t* size_new,
                                const int32_t* src_glob, const int32_t* slot, int32_t* rank_of,
-                               int32_t* src_local, void* scan_ws, cudaStream_t st,
-                               int32_t* tcount) {
+                               int32_t* src_local, void* scan_ws, cudaStream_t st) {
   ScanWs ws = carve_scan_ws(scan_ws, max_edges);
   cudaError_t err = cudaMemsetAsync(scan_ws, 0, scan_ws_bytes(max_edges), st);
   if (err != cudaSuccess) return err;
@@ -454,8 +452,7 @@ cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_
   int64_t grid = (max_edges + 255) / 256;
   if (grid < 1) grid = 1;
   if (grid > num_sms() * 16) grid = num_sms() * 16;
-  resolve_kernel<<<(int)grid, 256, 0, st>>>(m.table, slot, e_total, size_old, rank_of, src_local,
-                                            tcount);
+  resolve_kernel<<<(int)grid, 256, 0, st>>>(m.table, slot, e_total, size_old, rank_of, src_local);
   return cudaGetLastError();
 }
 

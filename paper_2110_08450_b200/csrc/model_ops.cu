@@ -232,10 +232,8 @@ __global__ void transpose_fill_kernel(const int32_t* __restrict__ indptr,
                                       const int32_t* __restrict__ src,
                                       const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
                                       const int32_t* __restrict__ tindptr,
-                                      const int32_t* __restrict__ tcount,
                                       int32_t* __restrict__ tfill, int32_t* __restrict__ tdst,
-                                      float* __restrict__ tw, int32_t* __restrict__ first_d,
-                                      float* __restrict__ first_w) {
+                                      float* __restrict__ tw) {
   const int lane = threadIdx.x & 31;
   const int64_t n = n_dst_dev ? *n_dst_dev : n_pad;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -245,15 +243,9 @@ __global__ void transpose_fill_kernel(const int32_t* __restrict__ indptr,
     const float w = 1.f / (float)(end - beg);
     for (int32_t e = beg + lane; e < end; e += 32) {
       const int32_t s = src[e];
-      const int32_t off = atomicAdd(&tfill[s], 1);
-      const int32_t pos = tindptr[s] + off;
+      const int32_t pos = tindptr[s] + atomicAdd(&tfill[s], 1);
       tdst[pos] = (int32_t)d;
       if (tw) tw[pos] = w;
-      if (first_d != nullptr && off == 0) {
-        // first in-edge of row s, sign bit = "more entries follow in tdst"
-        first_d[s] = (int32_t)d | (tcount[s] > 1 ? (int32_t)0x80000000 : 0);
-        first_w[s] = w;
-      }
     }
   }
 }
@@ -271,10 +263,8 @@ template <typename TG, typename TO>
 __global__ void __launch_bounds__(256, 3)
 mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_pad,
                   const int32_t* __restrict__ indptr, const int32_t* __restrict__ tindptr,
-                  const int32_t* __restrict__ tdst, const float* __restrict__ tw,
-                  const int32_t* __restrict__ first_d, const float* __restrict__ first_w,
-                  int64_t rows, const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz,
-                  int64_t ldz) {
+                  const int32_t* __restrict__ tdst, const float* __restrict__ tw, int64_t rows,
+                  const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz, int64_t ldz) {
   constexpr int kRows = 4;
   constexpr int kChunk = 8;  // source rows per warp task (lanes 0..7 fetch metadata)
   const int lane = threadIdx.x & 31;
@@ -288,25 +278,11 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
     int tb = 0, te = 0, d0 = -1;
     float w0 = 0.f;
     if (lane < kChunk && s_l < nrows) {
-      if (first_d != nullptr) {
-        // first in-edge straight from the per-row arrays (one coalesced round trip);
-        // the sign bit says whether tdst holds more entries for this row
-        const int32_t fd = __ldg(first_d + s_l);
-        if (fd != -1) {
-          d0 = fd & 0x7FFFFFFF;
-          w0 = __ldg(first_w + s_l);
-          if (fd < 0) {
-            tb = __ldg(tindptr + s_l);
-            te = __ldg(tindptr + s_l + 1);
-          }
-        }
-      } else {
-        tb = __ldg(tindptr + s_l);
-        te = __ldg(tindptr + s_l + 1);
-        if (te > tb) {
-          d0 = __ldg(tdst + tb);
-          w0 = tw ? __ldg(tw + tb) : 1.f / (float)(__ldg(indptr + d0 + 1) - __ldg(indptr + d0));
-        }
+      tb = __ldg(tindptr + s_l);
+      te = __ldg(tindptr + s_l + 1);
+      if (te > tb) {
+        d0 = __ldg(tdst + tb);
+        w0 = tw ? __ldg(tw + tb) : 1.f / (float)(__ldg(indptr + d0 + 1) - __ldg(indptr + d0));
       }
     }
     const int nb = min(kChunk, nrows - base);
@@ -352,8 +328,7 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
           for (int j = 0; j < 8; ++j) acc[j] = F<TG>::in(sv[j]) + F<TG>::in(nv[j]) * ww[k];
           const int rtb = __shfl_sync(0xffffffffu, tb, r & 31);
           const int rte = __shfl_sync(0xffffffffu, te, r & 31);
-          // further in-edges (rare): the first one (offset 0) sits at tdst[tb]
-          for (int q = rtb + 1; q < rte; ++q) {
+          for (int q = rtb + 1; q < rte; ++q) {  // further in-edges (rare)
             const int d = __ldg(tdst + q);
             const float w = tw ? __ldg(tw + q)
                                : 1.f / (float)(__ldg(indptr + d + 1) - __ldg(indptr + d));
@@ -436,16 +411,6 @@ static int done(int kernels) {
 
 extern "C" {
 
-int sal_transpose_build_ex(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
-                           int64_t n_pad, int64_t n_src_rows, int64_t max_edges, int32_t* tindptr,
-                           int32_t* tdst, float* tw, int32_t* first_d, float* first_w,
-                           int32_t counts_ready, void* ws, void* stream);
-int sal_mean_bwd_t_ex(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
-                      const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
-                      const float* tw, const int32_t* first_d, const float* first_w,
-                      int64_t rows, const uint8_t* mask, float p, void* dz, int64_t ldz,
-                      int32_t dz_dtype, void* stream);
-
 int sal_plan_next(const int64_t* desc_all, int64_t n_steps, int64_t* cursor, sal_batch_desc* out,
                   void* stream) {
   sal::plan_next_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(desc_all, n_steps, cursor, out);
@@ -514,41 +479,20 @@ size_t sal_transpose_ws_bytes(int64_t n_src_rows) {
 int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
                         int64_t n_pad, int64_t n_src_rows, int64_t max_edges, int32_t* tindptr,
                         int32_t* tdst, float* tw, void* ws, void* stream) {
-  return sal_transpose_build_ex(indptr, src, n_dst_dev, n_pad, n_src_rows, max_edges, tindptr,
-                                tdst, tw, nullptr, nullptr, 0, ws, stream);
-}
-
-int sal_transpose_build_ex(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
-                           int64_t n_pad, int64_t n_src_rows, int64_t max_edges, int32_t* tindptr,
-                           int32_t* tdst, float* tw, int32_t* first_d, float* first_w,
-                           int32_t counts_ready, void* ws, void* stream) {
   (void)max_edges;
   if (indptr == nullptr || src == nullptr || tindptr == nullptr || tdst == nullptr || ws == nullptr)
     return SAL_EINVAL;
-  if ((first_d == nullptr) != (first_w == nullptr)) return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   int32_t* tcount = (int32_t*)ws;
   int32_t* tfill = tcount + (n_src_rows + 1);
   char* scan = (char*)(tfill + (n_src_rows + 1));
   scan = (char*)(((uintptr_t)scan + 15) & ~(uintptr_t)15);
-  // tcount is produced by the relabel pass (sal_sample_mfg_ex) when counts_ready
-  if (counts_ready) {
-    if (cudaMemsetAsync(tfill, 0, sizeof(int32_t) * (size_t)(n_src_rows + 1), st) != cudaSuccess)
-      return SAL_ECUDA;
-  } else if (cudaMemsetAsync(ws, 0, (size_t)(8 * (n_src_rows + 1)), st) != cudaSuccess) {
-    return SAL_ECUDA;
-  }
-  if (first_d != nullptr &&
-      cudaMemsetAsync(first_d, 0xFF, sizeof(int32_t) * (size_t)n_src_rows, st) != cudaSuccess)
-    return SAL_ECUDA;
+  const size_t zero_bytes = (size_t)(8 * (n_src_rows + 1));
+  if (cudaMemsetAsync(ws, 0, zero_bytes, st) != cudaSuccess) return SAL_ECUDA;
   const size_t sb = sal::scan_ws_bytes(n_src_rows);
   if (cudaMemsetAsync(scan, 0, sb, st) != cudaSuccess) return SAL_ECUDA;
-  int kernels = 2;
-  if (!counts_ready) {
-    sal::transpose_count_kernel<<<sal::ew_grid(n_pad * 16), 256, 0, st>>>(indptr, src, n_dst_dev,
-                                                                           n_pad, tcount);
-    kernels = 3;
-  }
+  sal::transpose_count_kernel<<<sal::ew_grid(n_pad * 16), 256, 0, st>>>(indptr, src, n_dst_dev,
+                                                                         n_pad, tcount);
   sal::ScanWs sw;
   const int64_t tiles = (n_src_rows + sal::kScanTile - 1) / sal::kScanTile + 1;
   sw.status = (unsigned long long*)scan;
@@ -556,36 +500,26 @@ int sal_transpose_build_ex(const int32_t* indptr, const int32_t* src, const int6
   const int sgrid = (int)((n_src_rows + sal::kScanTile - 1) / sal::kScanTile);
   sal::scan_i32_kernel<<<sgrid > 0 ? sgrid : 1, sal::kScanThreads, 0, st>>>(tcount, n_src_rows,
                                                                            tindptr, sw);
-  sal::transpose_fill_kernel<<<sal::warp_grid(n_pad), 256, 0, st>>>(
-      indptr, src, n_dst_dev, n_pad, tindptr, tcount, tfill, tdst, tw, first_d, first_w);
-  return sal::done(kernels);
+  sal::transpose_fill_kernel<<<sal::warp_grid(n_pad), 256, 0, st>>>(indptr, src, n_dst_dev, n_pad,
+                                                                    tindptr, tfill, tdst, tw);
+  return sal::done(3);
 }
 
 int sal_mean_bwd_t(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
                    const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
                    const float* tw, int64_t rows, const uint8_t* mask, float p, void* dz,
                    int64_t ldz, int32_t dz_dtype, void* stream) {
-  return sal_mean_bwd_t_ex(dA, lda, dA_dtype, f, n_pad, indptr, tindptr, tdst, tw, nullptr,
-                           nullptr, rows, mask, p, dz, ldz, dz_dtype, stream);
-}
-
-int sal_mean_bwd_t_ex(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
-                      const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
-                      const float* tw, const int32_t* first_d, const float* first_w,
-                      int64_t rows, const uint8_t* mask, float p, void* dz, int64_t ldz,
-                      int32_t dz_dtype, void* stream) {
   if (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0) return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const int g = sal::warp_grid((rows + 7) / 8);
   if (dA_dtype == SAL_BF16 && dz_dtype == SAL_BF16)
     sal::mean_bwd_t_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(
-        (const __nv_bfloat16*)dA, lda, f, n_pad, indptr, tindptr, tdst, tw, first_d, first_w, rows,
-        mask, p, (__nv_bfloat16*)dz, ldz);
+        (const __nv_bfloat16*)dA, lda, f, n_pad, indptr, tindptr, tdst, tw, rows, mask, p,
+        (__nv_bfloat16*)dz, ldz);
   else if (dA_dtype == SAL_F32 && dz_dtype == SAL_F32)
     sal::mean_bwd_t_kernel<float, float><<<g, 256, 0, st>>>((const float*)dA, lda, f, n_pad,
-                                                           indptr, tindptr, tdst, tw, first_d,
-                                                           first_w, rows, mask, p, (float*)dz,
-                                                           ldz);
+                                                           indptr, tindptr, tdst, tw, rows, mask,
+                                                           p, (float*)dz, ldz);
   else
     return SAL_EINVAL;
   return sal::done(1);

@@ -57,8 +57,7 @@ cudaError_t launch_keys_insert(const int64_t* keys, int64_t n, const IdMapDev& m
 cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_t max_edges,
                                const int64_t* size_old, int64_t* size_new,
                                const int32_t* src_glob, const int32_t* slot, int32_t* rank_of,
-                               int32_t* src_local, void* scan_ws, cudaStream_t st,
-                               int32_t* tcount = nullptr);
+                               int32_t* src_local, void* scan_ws, cudaStream_t st);
 
 cudaError_t launch_gather_rows(const void* x, int64_t x_rows, int32_t cols, int64_t x_stride,
                                int32_t in_dtype, const void* ids, int32_t id_bytes,

@@ -313,9 +313,9 @@ class FusedSAGE:
     def backward(self, dlogits: torch.Tensor, saved, transposes=None) -> None:
         """Writes every weight gradient into self.grad (overwrite semantics).
 
-        transposes[i] = (tindptr, tdst, tw[, first_d, first_w]) reverse adjacency of
-        layer i (i >= 1); built here when not supplied (the trainer builds them on
-        the prep stream)."""
+        transposes[i] = (tindptr, tdst) reverse adjacency of layer i (i >= 1);
+        built here when not supplied (the trainer builds them on the prep
+        stream)."""
         L = _lib.lib()
         st = _lib.stream_ptr()
         dz = dlogits
@@ -336,16 +336,13 @@ class FusedSAGE:
             indptr, src, _, n_dev = rec["adj"]
             rows = a.shape[0]
             if transposes is not None and transposes[i] is not None:
-                tr = transposes[i]
+                tindptr, tdst, tw = transposes[i]
             else:
-                tr = build_transpose(indptr, src, n_dev, n_pad, rows)
-            tindptr, tdst, tw = tr[:3]
-            first_d, first_w = tr[3:5] if len(tr) >= 5 else (None, None)
+                tindptr, tdst, tw = build_transpose(indptr, src, n_dev, n_pad, rows)
             dzp = torch.empty((rows, f), dtype=self.act, device=a.device)
-            _lib.check(L.sal_mean_bwd_t_ex(
+            _lib.check(L.sal_mean_bwd_t(
                 dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
-                indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(),
-                _lib.ptr(first_d), _lib.ptr(first_w), rows,
+                indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows,
                 saved[i - 1]["mask"].data_ptr(), self.p if self.training else 0.0,
                 dzp.data_ptr(), dzp.stride(0), _lib.dtype_code(self.act), st), "mean_bwd_t")
             dz = dzp
@@ -362,33 +359,24 @@ class FusedSAGE:
         return logits
 
 
-def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=None, ws=None,
-                    counts_ready: bool = False):
-    """Reverse adjacency of one MFG layer: (tindptr [n_src_rows+1], tdst, tw [edges],
-    first_d, first_w [n_src_rows]). counts_ready: the row sizes were already
-    written to the start of `ws` by the sampler (MfgWorkspace.run(tcounts=...))."""
+def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=None, ws=None):
+    """Reverse adjacency (tindptr [n_src_rows+1], tdst, tw [edges]) of one MFG layer."""
     L = _lib.lib()
     dev = indptr.device
     if out is None:
-        ne = max(src.numel(), 1)
-        out = (torch.empty(n_src_rows + 1, dtype=torch.int32, device=dev),
-               torch.empty(ne, dtype=torch.int32, device=dev),
-               torch.empty(ne, dtype=torch.float32, device=dev),
-               torch.empty(max(n_src_rows, 1), dtype=torch.int32, device=dev),
-               torch.empty(max(n_src_rows, 1), dtype=torch.float32, device=dev))
-    tindptr, tdst, tw = out[:3]
-    first_d, first_w = out[3:5] if len(out) >= 5 else (None, None)
+        tindptr = torch.empty(n_src_rows + 1, dtype=torch.int32, device=dev)
+        tdst = torch.empty(max(src.numel(), 1), dtype=torch.int32, device=dev)
+        tw = torch.empty(max(src.numel(), 1), dtype=torch.float32, device=dev)
+    else:
+        tindptr, tdst, tw = out
     if ws is None:
-        if counts_ready:
-            raise ValueError("counts_ready needs the workspace the sampler filled")
         ws = torch.empty(L.sal_transpose_ws_bytes(n_src_rows), dtype=torch.uint8, device=dev)
-    _lib.check(L.sal_transpose_build_ex(indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dst_dev),
-                                        n_pad, n_src_rows, src.numel(), tindptr.data_ptr(),
-                                        tdst.data_ptr(), tw.data_ptr(), _lib.ptr(first_d),
-                                        _lib.ptr(first_w), int(counts_ready), ws.data_ptr(),
-                                        _lib.stream_ptr()),
+    _lib.check(L.sal_transpose_build(indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dst_dev),
+                                     n_pad, n_src_rows, src.numel(), tindptr.data_ptr(),
+                                     tdst.data_ptr(), tw.data_ptr(), ws.data_ptr(),
+                                     _lib.stream_ptr()),
                "transpose_build")
-    return out
+    return tindptr, tdst, tw
 
 
 def _mm_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:

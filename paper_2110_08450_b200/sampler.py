@@ -384,22 +384,15 @@ class MfgWorkspace:
         return self.buf[off:off + nbytes].view(dt)
 
     def run(self, g: DeviceGraph, seeds_base: torch.Tensor, desc: torch.Tensor,
-            global_seed: int, rng_policy: int = _lib.SAL_RNG_SPLITMIX, stream=None,
-            tcounts=None) -> None:
-        """Enqueue the whole multi-hop sample on `stream` (no host sync).
-
-        tcounts: optional per-hop int32 device tensors (or None) that receive the
-        reverse-adjacency row sizes of each hop (see sal_sample_mfg_ex)."""
+            global_seed: int, rng_policy: int = _lib.SAL_RNG_SPLITMIX, stream=None) -> None:
+        """Enqueue the whole multi-hop sample on `stream` (no host sync)."""
         L = _lib.lib()
         gc = g.cstruct
-        tc = None
-        if tcounts is not None:
-            tc = (ctypes.c_void_p * self.num_hops)(*[_lib.ptr(t) for t in tcounts])
-        _lib.check(L.sal_sample_mfg_ex(ctypes.byref(gc), ctypes.byref(self.plan),
-                                       ctypes.byref(self.layout), self.buf.data_ptr(),
-                                       seeds_base.data_ptr(), desc.data_ptr(),
-                                       int(global_seed) & MASK64, int(rng_policy), tc,
-                                       _lib.stream_ptr(stream)), "sample_mfg")
+        _lib.check(L.sal_sample_mfg(ctypes.byref(gc), ctypes.byref(self.plan),
+                                    ctypes.byref(self.layout), self.buf.data_ptr(),
+                                    seeds_base.data_ptr(), desc.data_ptr(),
+                                    int(global_seed) & MASK64, int(rng_policy),
+                                    _lib.stream_ptr(stream)), "sample_mfg")
 
     def load_seeds(self, seeds: SeedBatch, stream=None) -> None:
         n = len(seeds)

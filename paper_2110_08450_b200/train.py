@@ -109,15 +109,9 @@ class _Slot:
             self.transposes.append((
                 torch.zeros(n_src + 1, dtype=torch.int32, device=device),
                 torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.int32, device=device),
-                torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.float32, device=device),
-                torch.zeros(max(n_src, 1), dtype=torch.int32, device=device),
-                torch.zeros(max(n_src, 1), dtype=torch.float32, device=device)))
+                torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.float32, device=device)))
             self.t_ws.append(torch.empty(L.sal_transpose_ws_bytes(n_src), dtype=torch.uint8,
                                          device=device))
-        # the relabel pass of hop h counts the reverse-adjacency rows into t_ws[L-1-h]
-        self.tcounts = [None] * nh
-        for i in range(1, nh):
-            self.tcounts[nh - 1 - i] = self.t_ws[i]
 
 
 class _Staging:
@@ -217,8 +211,7 @@ class Trainer:
                                        self.cursor.data_ptr(), slot.desc.data_ptr(),
                                        _lib.stream_ptr(st)), "plan_next")
             seeds_base = self.seeds_all
-        ws.run(self.dg, seeds_base, slot.desc, self.cfg.global_seed, self.policy, st,
-               tcounts=slot.tcounts)
+        ws.run(self.dg, seeds_base, slot.desc, self.cfg.global_seed, self.policy, st)
         nh = self.nh
         rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
         n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
@@ -231,8 +224,7 @@ class Trainer:
         for i in range(1, nh):  # reverse adjacency for the backward pass
             h = nh - 1 - i
             build_transpose(ws.dst_indptr[h], ws.src_local[h], ws.sizes[h:h + 1], ws.node_cap[h],
-                            ws.node_cap[h + 1], out=slot.transposes[i], ws=slot.t_ws[i],
-                            counts_ready=True)
+                            ws.node_cap[h + 1], out=slot.transposes[i], ws=slot.t_ws[i])
 
     def _adjs(self, slot: _Slot):
         ws = slot.ws

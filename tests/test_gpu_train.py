@@ -151,64 +151,3 @@ def test_training_learns_planted_labels():
     correct, total = tr.evaluate(test_ids)
     assert total == 4000
     assert correct / total > 0.5, correct / total
-
-
-def test_transpose_counts_from_sampler_and_first_edge_path():
-    """Reverse adjacency with row sizes counted by the relabel pass
-    (sal_sample_mfg_ex) equals the standalone count kernel's, and the
-    first-edge fast path of sal_mean_bwd_t_ex gives the same input gradient as
-    the plain CSR walk (sal_mean_bwd_t) on the same transpose."""
-    from paper_2110_08450_b200 import _lib
-    from paper_2110_08450_b200.model import build_transpose
-    from paper_2110_08450_b200.sampler import MfgWorkspace
-    L = _lib.lib()
-    g = synth_graph(3000, 8, 3.0, seed=4)
-    dg = DeviceGraph.from_host(g)
-    fan = FanoutSpec((15, 10, 5))
-    ws = MfgWorkspace(dg.num_nodes, fan, 256)
-    seeds = SeedBatch(3, np.random.default_rng(3).choice(3000, 256, replace=False))
-    ws.load_seeds(seeds)
-    nh = ws.num_hops
-    t_ws = [torch.empty(L.sal_transpose_ws_bytes(ws.node_cap[h + 1]), dtype=torch.uint8,
-                        device="cuda") for h in range(nh)]
-    ws.run(dg, ws.seeds, ws.desc, 11, tcounts=t_ws[:nh - 1] + [None])
-    torch.cuda.synchronize()
-    for h in range(nh - 1):
-        n_dst, n_src = ws.node_cap[h], ws.node_cap[h + 1]
-        a = build_transpose(ws.dst_indptr[h], ws.src_local[h], ws.sizes[h:h + 1], n_dst, n_src,
-                            ws=t_ws[h], counts_ready=True)
-        b = build_transpose(ws.dst_indptr[h], ws.src_local[h], ws.sizes[h:h + 1], n_dst, n_src)
-        torch.cuda.synchronize()
-        assert torch.equal(a[0], b[0])
-        ns = int(ws.sizes[h + 1])
-        ne = int(a[0][ns])
-        assert ne == int(ws.etot[h])
-        ip = a[0][:ns + 1].long().cpu()
-        for t in (a, b):  # same edge multiset per row, first edge at the row start
-            fd = t[3][:ns].cpu()
-            td = t[1][:ne].cpu()
-            more = (fd < 0) & (fd != -1)
-            assert torch.equal(fd[ip[:-1] < ip[1:]] & 0x7FFFFFFF, td[ip[:-1][ip[:-1] < ip[1:]]])
-            assert torch.equal(more, (ip[1:] - ip[:-1]) > 1)
-        sa = [sorted(a[1][ip[r]:ip[r + 1]].tolist()) for r in range(0, ns, max(1, ns // 200))]
-        sb = [sorted(b[1][ip[r]:ip[r + 1]].tolist()) for r in range(0, ns, max(1, ns // 200))]
-        assert sa == sb
-        f = 32
-        dA = torch.randn(n_dst, 2 * f, device="cuda")
-        mask = torch.full((n_src * f // 8 + 8,), 255, dtype=torch.uint8, device="cuda")
-        out = []
-        for fast in (False, True):
-            dz = torch.full((n_src, f), 7.0, device="cuda")
-            args = [dA.data_ptr(), dA.stride(0), _lib.SAL_F32, f, n_dst,
-                    ws.dst_indptr[h].data_ptr(), a[0].data_ptr(), a[1].data_ptr(),
-                    a[2].data_ptr()]
-            if fast:
-                _lib.check(L.sal_mean_bwd_t_ex(*args, a[3].data_ptr(), a[4].data_ptr(), n_src,
-                                               mask.data_ptr(), 0.0, dz.data_ptr(), dz.stride(0),
-                                               _lib.SAL_F32, _lib.stream_ptr()), "bwd_ex")
-            else:
-                _lib.check(L.sal_mean_bwd_t(*args, n_src, mask.data_ptr(), 0.0, dz.data_ptr(),
-                                            dz.stride(0), _lib.SAL_F32, _lib.stream_ptr()), "bwd")
-            out.append(dz)
-        torch.cuda.synchronize()
-        assert torch.equal(out[0], out[1])
