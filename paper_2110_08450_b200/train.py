@@ -264,7 +264,7 @@ class Trainer:
             self._train(self.slots[k % 2], "post")
             return
         cs = torch.cuda.current_stream()
-        ps = self.prep_stream
+        ps = self.prep_stream or cs  # None: prep serialised on the compute stream
         ps.wait_stream(cs)
         with torch.cuda.stream(ps):
             self._prep(self.slots[(k + 1) % 2],
