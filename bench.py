@@ -190,11 +190,13 @@ def kernel_profile(trainer, nbatches: int):
     hop's edges — the largest kernel of the training step)."""
     from paper_2110_08450_b200 import _lib
     from paper_2110_08450_b200.prep import gather_rows
+    from paper_2110_08450_b200.sampler import MfgWorkspace
     Lb = _lib.lib()
-    slot = trainer.slots[0]
-    out_buf = torch.empty((slot.ws.node_cap[-1], trainer.x_table.shape[1]), dtype=torch.float16,
+    # the full MFG (every hop relabelled: the drop-in multihop_mfg / prepare_batch work)
+    ws = MfgWorkspace(trainer.dg.num_nodes, trainer.cfg.fanouts, trainer.cfg.batch_size,
+                      device=trainer.device)
+    out_buf = torch.empty((ws.node_cap[-1], trainer.x_table.shape[1]), dtype=torch.float16,
                           device=trainer.device)  # fp16 -> fp16 row gather (pure copy)
-    ws = slot.ws
     L = trainer.nh
     h0 = L - 1  # expansion hop feeding layer 0
     mean_buf = torch.empty((ws.node_cap[h0], trainer.x_table.shape[1]), dtype=torch.bfloat16,

@@ -82,7 +82,16 @@ typedef struct {
   int64_t node_cap[SAL_MAX_HOPS + 1];   /* max id-map size after h hops   */
   int64_t edge_cap[SAL_MAX_HOPS];       /* max edges emitted by hop h     */
   int64_t table_cap;
+  int32_t flags;                        /* SAL_MFG_* plan flags            */
+  int32_t reserved;
 } sal_mfg_plan;
+
+/* Plan flag: the last hop emits its edges as global ids only (layout.src_glob);
+ * no id-map insertion, no relabel, sizes[L] = -1 and src_local[L-1] is not
+ * written.  For training with the layer-0 aggregation read straight from the
+ * feature table, where the last hop's local ids are never consumed; the id
+ * map then only holds hops 0..L-2 (table_cap sized for node_cap[L-1]). */
+#define SAL_MFG_LAST_HOP_EDGES 1
 
 /* Byte offsets of the arrays inside one batch workspace. */
 typedef struct {
@@ -113,6 +122,9 @@ uint64_t sal_hop_key_prefix(uint64_t global_seed, int64_t batch_id, int64_t hop)
 /* per_hop is FanoutSpec.per_hop (outermost hop first, sampler.py:70-72). */
 int sal_mfg_plan_init(sal_mfg_plan* plan, int32_t num_hops, const int32_t* per_hop,
                       int64_t max_seeds, int64_t num_nodes);
+/* as sal_mfg_plan_init with SAL_MFG_* flags */
+int sal_mfg_plan_init_ex(sal_mfg_plan* plan, int32_t num_hops, const int32_t* per_hop,
+                         int64_t max_seeds, int64_t num_nodes, int32_t flags);
 int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* layout);
 /* Seeds -> L hops -> MFG, all on `stream`, no host synchronisation.
  * Outputs land in the workspace at the layout's offsets; `sizes[h]` and

@@ -16,6 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libsalient_b200.so"
 SAL_MAX_HOPS = 8
 SAL_RNG_SPLITMIX = 0
 SAL_RNG_PHILOX = 1
+SAL_MFG_LAST_HOP_EDGES = 1
 SAL_F16 = 1
 SAL_F32 = 2
 SAL_BF16 = 3
@@ -43,7 +44,7 @@ class SalIdMap(ctypes.Structure):
 class SalMfgPlan(ctypes.Structure):
     _fields_ = [("num_hops", i32), ("fanout", i32 * SAL_MAX_HOPS), ("max_seeds", i64),
                 ("node_cap", i64 * (SAL_MAX_HOPS + 1)), ("edge_cap", i64 * SAL_MAX_HOPS),
-                ("table_cap", i64)]
+                ("table_cap", i64), ("flags", i32), ("reserved", i32)]
 
 
 class SalMfgLayout(ctypes.Structure):
@@ -62,6 +63,7 @@ SIGNATURES = {
     "sal_launch_count": (ctypes.c_longlong, []),
     "sal_hop_key_prefix": (u64, [u64, i64, i64]),
     "sal_mfg_plan_init": (ctypes.c_int, [P(SalMfgPlan), i32, P(i32), i64, i64]),
+    "sal_mfg_plan_init_ex": (ctypes.c_int, [P(SalMfgPlan), i32, P(i32), i64, i64, i32]),
     "sal_mfg_layout_init": (ctypes.c_int, [P(SalMfgPlan), P(SalMfgLayout)]),
     "sal_sample_mfg": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp, vp,
                                       u64, i32, vp]),

@@ -90,7 +90,13 @@ size_t sal_scan_ws_bytes(int64_t max_items) { return sal::scan_ws_bytes(max_item
 // ---------------------------------------------------------------------------
 int sal_mfg_plan_init(sal_mfg_plan* plan, int32_t num_hops, const int32_t* per_hop,
                       int64_t max_seeds, int64_t num_nodes) {
+  return sal_mfg_plan_init_ex(plan, num_hops, per_hop, max_seeds, num_nodes, 0);
+}
+
+int sal_mfg_plan_init_ex(sal_mfg_plan* plan, int32_t num_hops, const int32_t* per_hop,
+                         int64_t max_seeds, int64_t num_nodes, int32_t flags) {
   if (plan == nullptr || per_hop == nullptr) return fail(SAL_EINVAL, "plan: null argument");
+  if (flags & ~SAL_MFG_LAST_HOP_EDGES) return fail(SAL_EINVAL, "plan: unknown flags 0x%x", flags);
   if (num_hops < 1 || num_hops > SAL_MAX_HOPS)
     return fail(SAL_EINVAL, "plan: need 1..%d hops, got %d", SAL_MAX_HOPS, num_hops);
   if (max_seeds < 0 || num_nodes < 0) return fail(SAL_EINVAL, "plan: negative size");
@@ -115,7 +121,10 @@ int sal_mfg_plan_init(sal_mfg_plan* plan, int32_t num_hops, const int32_t* per_h
   for (int h = 0; h < num_hops; ++h)
     if (plan->edge_cap[h] >= (1ll << 31) - 1)
       return fail(SAL_EINVAL, "plan: hop %d edge capacity exceeds int32", h);
-  plan->table_cap = pow2_at_least(2 * (nodes > 8 ? nodes : 8));
+  plan->flags = flags;
+  // the id map holds every node, or (last hop edges-only) the nodes of hops 0..L-2
+  const int64_t mapped = (flags & SAL_MFG_LAST_HOP_EDGES) ? plan->node_cap[num_hops - 1] : nodes;
+  plan->table_cap = pow2_at_least(2 * (mapped > 8 ? mapped : 8));
   return SAL_OK;
 }
 
@@ -191,6 +200,17 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
     hk.hop = (uint32_t)h;
     hk.batch = 0;
     hk.derive = 1;
+    const bool edges_only = (plan->flags & SAL_MFG_LAST_HOP_EDGES) && h == plan->num_hops - 1;
+    if (edges_only) {  // global ids only; sizes[L] = -1 (written by the kernel)
+      sal::IdMapDev none = m;
+      none.table = nullptr;
+      none.size_out = sizes + h + 1;
+      e = sal::launch_hop_sample(gd, none, sizes + h, plan->node_cap[h], plan->fanout[h], hk,
+                                 desc, rng_policy, nullptr, dst_indptr, src_glob, nullptr,
+                                 nullptr, st);
+      if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
+      return counted(SAL_OK, 4 * plan->num_hops - 1);
+    }
     e = sal::launch_hop_sample(gd, m, sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
                                rng_policy, nullptr, dst_indptr, src_glob, slot, nullptr, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");

@@ -142,7 +142,8 @@ SAL_DEVINL void emit_edge(const int32_t* __restrict__ indices, int64_t slot_pos,
                           int32_t* __restrict__ slot) {
   const uint32_t key = (uint32_t)__ldg(indices + slot_pos);
   src_glob[e] = (int32_t)key;
-  slot[e] = (int32_t)table_insert_min(table, log2cap, key, (uint32_t)e);
+  if (table != nullptr)  // null: edges-only hop (SAL_MFG_LAST_HOP_EDGES)
+    slot[e] = (int32_t)table_insert_min(table, log2cap, key, (uint32_t)e);
 }
 
 // Draw -> position for the two RNG policies.
@@ -172,7 +173,8 @@ sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restri
                      int32_t fanout, HopKey hk, const BatchDesc* __restrict__ desc,
                      const int64_t* __restrict__ inject_pos, const int32_t* __restrict__ dst_indptr,
                      unsigned long long* table, int log2cap, int32_t* src_glob,
-                     int32_t* __restrict__ slot, int32_t* __restrict__ draws_out) {
+                     int32_t* __restrict__ slot, int32_t* __restrict__ draws_out,
+                     int64_t* __restrict__ size_unknown) {
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, gl = lane % G;
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
@@ -189,6 +191,7 @@ sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restri
   }
   const uint2 pkey = make_uint2((uint32_t)hk.global_seed, (uint32_t)(hk.global_seed >> 32));
   __shared__ int32_t sh_acc[8][32];
+  if (size_unknown != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *size_unknown = -1;
 
   for (int64_t i = group_id; i < n; i += ngroups) {
     const int32_t v = globals[i];
@@ -413,7 +416,7 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
 #define SAL_SAMPLE(P, GG)                                                                   \
   sample_insert_kernel<P, GG><<<(int)grid, 256, 0, st>>>(                                   \
       g.indptr, g.indices, m.globals, n_dst, fanout, hk, desc, inject_pos, dst_indptr, m.table, \
-      m.log2cap, src_glob, slot, draws_out)
+      m.log2cap, src_glob, slot, draws_out, m.table == nullptr ? m.size_out : nullptr)
   if (policy == kRngSplitmix) {
     if (G == 8) SAL_SAMPLE(kRngSplitmix, 8);
     else if (G == 16) SAL_SAMPLE(kRngSplitmix, 16);

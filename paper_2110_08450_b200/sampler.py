@@ -348,17 +348,24 @@ class MfgWorkspace:
     edge_cap[h] = node_cap[h]*f, so no hop ever needs a host round trip.
     """
 
-    def __init__(self, num_nodes: int, fanouts: FanoutSpec, max_seeds: int, device=None):
+    def __init__(self, num_nodes: int, fanouts: FanoutSpec, max_seeds: int, device=None,
+                 last_hop_edges: bool = False):
+        """last_hop_edges: SAL_MFG_LAST_HOP_EDGES — the last hop only emits global
+        source ids (src_glob); its relabel is skipped (training with the
+        layer-0 mean read straight from the feature table)."""
         _lib.require_cuda()
         L = _lib.lib()
         self.device = torch.device(device or "cuda")
         self.fanouts = fanouts
         self.num_hops = len(fanouts)
         self.max_seeds = int(max_seeds)
+        self.last_hop_edges = bool(last_hop_edges)
         self.plan = _lib.SalMfgPlan()
         per = (ctypes.c_int32 * self.num_hops)(*fanouts.per_hop)
-        _lib.check(L.sal_mfg_plan_init(ctypes.byref(self.plan), self.num_hops, per,
-                                       self.max_seeds, int(num_nodes)), "mfg_plan_init")
+        flags = _lib.SAL_MFG_LAST_HOP_EDGES if last_hop_edges else 0
+        _lib.check(L.sal_mfg_plan_init_ex(ctypes.byref(self.plan), self.num_hops, per,
+                                          self.max_seeds, int(num_nodes), flags),
+                   "mfg_plan_init")
         self.layout = _lib.SalMfgLayout()
         _lib.check(L.sal_mfg_layout_init(ctypes.byref(self.plan), ctypes.byref(self.layout)),
                    "mfg_layout_init")
@@ -410,6 +417,8 @@ class MfgWorkspace:
         return both[:self.num_hops + 1], both[self.num_hops + 1:]
 
     def to_mfg(self, seeds: SeedBatch, variant: SamplerVariant = SamplerVariant()) -> Mfg:
+        if self.last_hop_edges:
+            raise ValueError("to_mfg: the last hop of an edges-only workspace has no local ids")
         sizes, etot = self.read_extents()
         layers = []
         for h in range(self.num_hops):

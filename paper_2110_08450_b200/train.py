@@ -89,7 +89,9 @@ def allreduce_mean(t: torch.Tensor, world: int) -> None:
 
 class _Slot:
     def __init__(self, dg: DeviceGraph, cfg: TrainConfig, device):
-        self.ws = MfgWorkspace(dg.num_nodes, cfg.fanouts, cfg.batch_size, device=device)
+        # gather-free: layer 0 reads rows by global id, so the last hop needs no relabel
+        self.ws = MfgWorkspace(dg.num_nodes, cfg.fanouts, cfg.batch_size, device=device,
+                               last_hop_edges=cfg.gather_free)
         ws = self.ws
         nh = ws.num_hops
         rows = ws.node_cap[-1] if not cfg.gather_free else ws.node_cap[-2]

@@ -225,3 +225,36 @@ def test_philox_uniform_without_replacement():
     chi2 = float(((counts - expected) ** 2 / expected).sum())
     # chi-square(39) upper 1e-4 quantile ~ 83.3 (fpc makes the statistic smaller)
     assert chi2 < 83.3, (chi2, counts)
+
+
+@pytest.mark.parametrize("fan", [(15, 10, 5), (4, 3), (6,)])
+def test_last_hop_edges_only_matches_full_sample(fan):
+    """SAL_MFG_LAST_HOP_EDGES: hops 0..L-2 identical to the full sample, the last
+    hop's edges identical as global ids (against the reference-exact full MFG),
+    sizes[L] = -1."""
+    from paper_2110_08450_b200.sampler import MfgWorkspace
+    g = synth_graph(100_000, 10, 3.0, seed=1)
+    dg = DeviceGraph.from_host(g)
+    plan = make_epoch_plan(np.arange(100_000), 1024, 1)
+    spec = FanoutSpec(fan)
+    full = MfgWorkspace(dg.num_nodes, spec, 1024)
+    edg = MfgWorkspace(dg.num_nodes, spec, 1024, last_hop_edges=True)
+    assert edg.plan.table_cap <= full.plan.table_cap
+    L = len(fan)
+    for b in (plan.batches[0], plan.batches[-1]):
+        for ws in (full, edg):
+            ws.load_seeds(b)
+            ws.run(dg, ws.seeds, ws.desc, 1)
+        torch.cuda.synchronize()
+        sf, ef = full.read_extents()
+        se, ee = edg.read_extents()
+        assert se[:L] == sf[:L] and ee == ef and se[L] == -1
+        assert torch.equal(edg.globals[:sf[L - 1]], full.globals[:sf[L - 1]])
+        for h in range(L):
+            assert torch.equal(edg.dst_indptr[h][:sf[h] + 1], full.dst_indptr[h][:sf[h] + 1])
+        for h in range(L - 1):
+            assert torch.equal(edg.src_local[h][:ef[h]], full.src_local[h][:ef[h]])
+        want = full.globals[full.src_local[L - 1][:ef[L - 1]].long()]
+        assert torch.equal(edg.src_glob[:ef[L - 1]], want)
+        with pytest.raises(ValueError):
+            edg.to_mfg(b)
