@@ -169,9 +169,13 @@ class FusedSAGE:
         self.p = float(dropout)
         self.act = act_dtype
         self.lr, self.betas, self.eps = lr, betas, eps
-        shapes = [(b, 2 * a) for a, b in zip(self.dims[:-1], self.dims[1:])]
+        # the output layer's rows are padded to a multiple of 8 (zero weights, zero
+        # gradients) so every logits / dlogits row is 16-byte aligned for the GEMMs
+        self.c_pad = -(-num_classes // 8) * 8
+        rows_pad = self.dims[1:-1] + [self.c_pad]
+        shapes = [(r, 2 * a) for a, r in zip(self.dims[:-1], rows_pad)]
         total = sum(r * c for r, c in shapes)
-        self.flat = torch.empty(total, dtype=torch.float32, device=dev)
+        self.flat = torch.zeros(total, dtype=torch.float32, device=dev)
         self.grad = torch.zeros(total, dtype=torch.float32, device=dev)
         self.m = torch.zeros(total, dtype=torch.float32, device=dev)
         self.v = torch.zeros(total, dtype=torch.float32, device=dev)
@@ -180,14 +184,18 @@ class FusedSAGE:
         g = torch.Generator(device="cpu")
         g.manual_seed(seed)
         off = 0
-        self.w, self.g, self.wb = [], [], []
-        for r, c in shapes:
+        # w/g: logical [f_out, 2 f_in] views; wb/gp: the padded views the GEMMs use
+        self.w, self.g, self.wb, self.gp = [], [], [], []
+        for (r, c), fo in zip(shapes, self.dims[1:]):
             bound = 1.0 / math.sqrt(c // 2)   # SAGEConv-style U(-1/sqrt(f_in), 1/sqrt(f_in))
-            self.flat[off:off + r * c] = ((torch.rand(r * c, generator=g) * 2 - 1) * bound).to(dev)
-            self.w.append(self.flat[off:off + r * c].view(r, c))
-            self.g.append(self.grad[off:off + r * c].view(r, c))
+            self.flat[off:off + fo * c] = ((torch.rand(fo * c, generator=g) * 2 - 1)
+                                           * bound).to(dev)
+            self.w.append(self.flat[off:off + r * c].view(r, c)[:fo])
+            self.gp.append(self.grad[off:off + r * c].view(r, c))
+            self.g.append(self.gp[-1][:fo])
             self.wb.append(self.shadow[off:off + r * c].view(r, c))
             off += r * c
+        self._dlog = None
         self.refresh_shadow()
         self.training = True
         self.seed = seed
@@ -240,12 +248,14 @@ class FusedSAGE:
         return a
 
     # ------------------------------------------------------------- fwd
-    def forward(self, a0: torch.Tensor, adjs, x_global=None, salt: torch.Tensor | None = None):
+    def forward(self, a0: torch.Tensor, adjs, x_global=None, salt: torch.Tensor | None = None,
+                mean0_ready: bool = False):
         """a0: layer-0 cat buffer (right half = features in local order).
 
         adjs[i] = (indptr, src, n_pad, n_dst_dev).  With x_global = (table,
         edge_global_ids) layer 0's mean is read straight from the feature table
-        (the sampler's per-edge global ids of the last hop).
+        (the sampler's per-edge global ids of the last hop).  mean0_ready: the
+        left half of a0 already holds layer 0's mean (computed by the prep stream).
         Returns (logits [n_pad_last, C], saved)."""
         L = _lib.lib()
         st = _lib.stream_ptr()
@@ -256,7 +266,9 @@ class FusedSAGE:
             f = self.dims[i]
             h = a[:, f:]
             mean = a[:n_pad, :f]
-            if i == 0 and x_global is not None:
+            if i == 0 and mean0_ready:
+                pass
+            elif i == 0 and x_global is not None:
                 # gather-free layer 0: edges carry global ids, rows come from the table
                 table, gsrc = x_global
                 _lib.check(L.sal_segment_mean_fwd(
@@ -291,17 +303,22 @@ class FusedSAGE:
                 rec["mask"] = mask
                 a = nxt
             else:
-                a = torch.mm(a[:n_pad], self.wb[i].t())
+                a = torch.mm(a[:n_pad], self.wb[i].t())[:, :self.dims[-1]]
             saved.append(rec)
         return a, saved
 
     def loss(self, logits: torch.Tensor, labels: torch.Tensor, out: torch.Tensor | None = None):
-        """Fused log_softmax + NLL; returns (loss scalar fp32, dlogits)."""
+        """Fused log_softmax + NLL; returns (loss scalar fp32, dlogits [rows, c_pad]).
+
+        dlogits lives in a persistent buffer whose padded columns stay zero."""
         L = _lib.lib()
         loss = out if out is not None else torch.empty((), dtype=torch.float32,
                                                        device=logits.device)
         loss.zero_()
-        dlog = torch.empty_like(logits)
+        n = logits.shape[0]
+        if self._dlog is None or self._dlog.shape[0] != n or self._dlog.dtype != logits.dtype:
+            self._dlog = torch.zeros((n, self.c_pad), dtype=logits.dtype, device=logits.device)
+        dlog = self._dlog
         rows = min(logits.shape[0], labels.shape[0])
         _lib.check(L.sal_lsm_nll(logits.data_ptr(), logits.stride(0), rows, logits.shape[1],
                                  _lib.dtype_code(logits.dtype), labels.data_ptr(),
@@ -328,7 +345,7 @@ class FusedSAGE:
                                                2 * self.dims[i], self.g[i].data_ptr(),
                                                self.g[i].stride(0), st), "tc_sage_wgrad")
             else:
-                _mm_f32(dz.t(), a[:n_pad], self.g[i])
+                _mm_f32(dz.t(), a[:n_pad], self.gp[i])
             if i == 0:
                 break
             f = self.dims[i]

@@ -50,6 +50,7 @@ class TrainConfig:
     graphs: bool = True            # capture {prep || step} in CUDA graphs
     model_seed: int = 0
     prep_priority: int = -1        # CUDA stream priority of the prep stream (lower = higher)
+    prep_mean0: bool = False       # gather-free: layer-0 mean on the prep stream (measured slower)
 
 
 def shard_plan(plan, batch_size: int, rank: int, world: int):
@@ -219,6 +220,17 @@ class Trainer:
         n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
         f = self.x_table.shape[1]
         gather_rows(self.x_table, ws.globals, slot.feats[:, f:], n=rows, n_dev=n_dev, stream=st)
+        if self.cfg.gather_free and self.cfg.prep_mean0:
+            # layer-0 mean over the last hop's edges, rows read by global id from the
+            # table, written into the left half of the layer-0 cat buffer
+            h0 = nh - 1
+            a0 = slot.feats
+            _lib.check(L.sal_segment_mean_fwd(
+                ws.dst_indptr[h0].data_ptr(), ws.src_glob.data_ptr(),
+                ws.sizes[h0:h0 + 1].data_ptr(), ws.node_cap[h0], self.x_table.data_ptr(),
+                _lib.dtype_code(self.x_table.dtype), self.x_table.stride(0), f, a0.data_ptr(),
+                _lib.dtype_code(a0.dtype), a0.stride(0), _lib.stream_ptr(st)),
+                "segment_mean_fwd(table)")
         _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), seeds_base.data_ptr(),
                                        slot.desc.data_ptr(), self.cfg.batch_size,
                                        slot.labels.data_ptr(), _lib.stream_ptr(st)),
@@ -245,9 +257,10 @@ class Trainer:
         between."""
         m = self.model
         if part in ("all", "pre"):
-            xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free else None
+            ready = self.cfg.gather_free and self.cfg.prep_mean0
+            xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free and not ready else None
             logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg,
-                                      salt=self.step_ctr)
+                                      salt=self.step_ctr, mean0_ready=ready)
             loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf)
             m.backward(dlog, saved, slot.transposes)
         if part == "all" and self.world > 1:
