@@ -261,7 +261,8 @@ int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const void* W_dev
                     int32_t K, void* Y_dev, int64_t ldy, uint8_t* mask_dev, float p,
                     uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout, void* stream);
 /* dW[N,K] (fp32, row stride lddw) = dz[M,N]^T @ A[M,K]; zeroes dW first.
- * Split over M across CTAs with fp32 vector atomics.  N = K = 256. */
+ * 128 x 128 output tiles x split-K over M (about one CTA per SM), partials
+ * added with fp32 vector atomics.  N, K multiples of 128. */
 int sal_tc_sage_wgrad(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda, int64_t M,
                       int32_t N, int32_t K, float* dW_dev, int64_t lddw, void* stream);
 /* the same two GEMMs without TMA / warp specialisation (cp.async, one CTA

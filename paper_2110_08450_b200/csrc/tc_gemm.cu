@@ -565,18 +565,23 @@ sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-// weight gradient with TMA: stage = dz chunk [64 rows x 256] + A chunk [64 x 256],
-// each loaded as 4 boxes of {64 mn, 64 k} (one per 64-wide mn-group).
-constexpr int kQStages = 3;
+// weight gradient with TMA, tiled split-K: CTA (tile, split) accumulates one
+// 128 x 128 tile of dW (rows n0.., cols k0..) over a contiguous range of GEMM-K
+// rows (= M rows of dz / A).  Splitting the output into tiles cuts the fp32
+// partials the epilogue adds atomically (S x N x K instead of 148 x N x K);
+// the CTAs of one split read the same dz/A rows at the same time, so the
+// second read of each chunk hits L2.  Stage = dz chunk [64 rows x 128] + A
+// chunk [64 x 128], each two TMA boxes of {64 mn, 64 k}.
+constexpr int kQStages = 6;
 constexpr int kQThreads = 192;
-constexpr uint32_t kQHalf = kGC * 256 * 2;   // 32 KB per operand per stage
+constexpr uint32_t kQHalf = kGC * 128 * 2;   // 16 KB per operand per stage
 constexpr uint32_t kQStage = 2 * kQHalf;
 constexpr uint32_t kQSmem = kQStages * kQStage + 1024 + 256;
 
 __global__ void __launch_bounds__(kQThreads, 1)
 sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
-                      const __grid_constant__ CUtensorMap mapA, int M, int rows_per_cta,
-                      float* __restrict__ dW, int64_t lddw) {
+                      const __grid_constant__ CUtensorMap mapA, int M, int rows_per_split,
+                      int tiles_k, float* __restrict__ dW, int64_t lddw) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + kQStages * kQStage);
@@ -585,8 +590,10 @@ sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
   uint64_t* done = bars + 2 * kQStages;
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kQStages + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * rows_per_cta;
-  const int m1 = min(M, m0 + rows_per_cta);
+  const int tile = blockIdx.x, split = blockIdx.y;
+  const int n0 = (tile / tiles_k) * 128, k0 = (tile % tiles_k) * 128;
+  const int m0 = split * rows_per_split;
+  const int m1 = min(M, m0 + rows_per_split);
   const int nchunks = m1 > m0 ? (m1 - m0 + kGC - 1) / kGC : 0;
 
   if (warp == 0 && lane == 0) {
@@ -600,7 +607,7 @@ sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(512));
+                 "r"(128));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -618,15 +625,15 @@ sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
         mbar_expect_tx(&full[stage], kQStage);
         const uint32_t base = smem_u32(smem + stage * kQStage);
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          tma_load_2d(base + g * 8192, &mapDz, g * 64, mr, &full[stage]);
-          tma_load_2d(base + kQHalf + g * 8192, &mapA, g * 64, mr, &full[stage]);
+        for (int g = 0; g < 2; ++g) {
+          tma_load_2d(base + g * 8192, &mapDz, n0 + g * 64, mr, &full[stage]);
+          tma_load_2d(base + kQHalf + g * 8192, &mapA, k0 + g * 64, mr, &full[stage]);
         }
         if (++stage == kQStages) { stage = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = make_idesc(128, kGK, 1, 1);
+    const uint32_t idesc = make_idesc(128, 128, 1, 1);
     int stage = 0;
     uint32_t ph = 0;
     for (int ch = 0; ch < nchunks; ++ch) {
@@ -636,13 +643,10 @@ sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
         const uint32_t base = smem_u32(smem + stage * kQStage);
 #pragma unroll
         for (int kk = 0; kk < kGC / 16; ++kk) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            // mn-groups 2h, 2h+1 of dz (LBO 8 KB), k-groups 2kk, 2kk+1 (SBO 1 KB)
-            const uint64_t a = make_desc(base + h * 16384 + kk * 2048, 8192, 1024, 2);
-            const uint64_t b = make_desc(base + kQHalf + kk * 2048, 8192, 1024, 2);
-            mma_f16(tmem + h * 256, a, b, idesc, (ch | kk) != 0);
-          }
+          // mn-groups of 64 at LBO 8 KB, 8-row k-groups at SBO 1 KB
+          const uint64_t a = make_desc(base + kk * 2048, 8192, 1024, 2);
+          const uint64_t b = make_desc(base + kQHalf + kk * 2048, 8192, 1024, 2);
+          mma_f16(tmem, a, b, idesc, (ch | kk) != 0);
         }
         mma_commit(&empty[stage]);
         if (ch == nchunks - 1) mma_commit(done);
@@ -651,32 +655,29 @@ sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
       if (++stage == kQStages) { stage = 0; ph ^= 1; }
     }
   } else if (nchunks > 0) {
-    // epilogue warps 2..5: TMEM lane group (warp % 4), both dW halves
+    // epilogue warps 2..5: TMEM lane group warp % 4 -> dW rows n0 + 32 (warp % 4) + lane
     const int lg = warp & 3;
     mbar_wait(done, 0);
     tc_fence_after();
+    const int rrow = n0 + lg * 32 + lane;
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      const int rrow = h * 128 + lg * 32 + lane;
-#pragma unroll 1
-      for (int c8 = 0; c8 < kGK / 32; ++c8) {
-        // CTAs start at different column blocks so their atomics spread over L2 slices
-        const int cc = ((c8 + blockIdx.x) % (kGK / 32)) * 32;
-        uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(h * 256 + cc), r);
-        float* dst = dW + (int64_t)rrow * lddw + cc;
+    for (int c4 = 0; c4 < 4; ++c4) {
+      // splits start at different column blocks so their atomics spread over L2 slices
+      const int cc = ((c4 + split) & 3) * 32;
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)cc, r);
+      float* dst = dW + (int64_t)rrow * lddw + k0 + cc;
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          atomicAdd(reinterpret_cast<float4*>(dst) + q,
-                    make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
-      }
+      for (int q = 0; q < 8; ++q)
+        atomicAdd(reinterpret_cast<float4*>(dst) + q,
+                  make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                              __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
 }
 
 // host: 2-D bf16 tensor map [rows x cols] (row stride in elements), SWIZZLE_128B
@@ -762,17 +763,17 @@ int sal_tc_sage_fwd_simple(const void* A, int64_t lda, int64_t M, const void* W,
 
 int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, int64_t M,
                       int32_t N, int32_t K, float* dW, int64_t lddw, void* stream) {
-  if (N != sal::tc::kGN || K != sal::tc::kGK) return SAL_EINVAL;
+  if (N <= 0 || K <= 0 || N % 128 || K % 128) return SAL_EINVAL;
   if (ldz % 8 || lda % 8 || ((uintptr_t)dz & 15) || ((uintptr_t)A & 15) || ((uintptr_t)dW & 15) ||
-      lddw % 4)
+      lddw % 4 || lddw < K)
     return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)N * (size_t)lddw, st) != cudaSuccess)
     return SAL_ECUDA;
   if (M <= 0) return SAL_OK;
   CUtensorMap mD, mA;
-  if (!sal::tc::make_map(&mD, dz, (uint64_t)M, 256, (uint64_t)ldz, 64, 64) ||
-      !sal::tc::make_map(&mA, A, (uint64_t)M, 256, (uint64_t)lda, 64, 64))
+  if (!sal::tc::make_map(&mD, dz, (uint64_t)M, (uint64_t)N, (uint64_t)ldz, 64, 64) ||
+      !sal::tc::make_map(&mA, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, 64, 64))
     return SAL_ECUDA;
   static bool attr = false;
   if (!attr) {
@@ -780,12 +781,16 @@ int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, i
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sal::tc::kQSmem);
     attr = true;
   }
-  int grid = sal::num_sms();
-  int rows = (int)((M + grid - 1) / grid);
+  // one CTA per SM: tiles x splits ~ #SMs, splits of whole 64-row chunks
+  const int tiles_k = K / 128;
+  const int tiles = (N / 128) * tiles_k;
+  int splits = sal::num_sms() / tiles;
+  if (splits < 1) splits = 1;
+  int rows = (int)((M + splits - 1) / splits);
   rows = (rows + 63) / 64 * 64;
-  grid = (int)((M + rows - 1) / rows);
-  sal::tc::sage_wgrad_tma_kernel<<<grid, sal::tc::kQThreads, sal::tc::kQSmem, st>>>(
-      mD, mA, (int)M, rows, dW, lddw);
+  splits = (int)((M + rows - 1) / rows);
+  sal::tc::sage_wgrad_tma_kernel<<<dim3(tiles, splits), sal::tc::kQThreads, sal::tc::kQSmem, st>>>(
+      mD, mA, (int)M, rows, tiles_k, dW, lddw);
   if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
   sal::count_launch(1);
   return SAL_OK;

@@ -200,9 +200,9 @@ class FusedSAGE:
         self.training = True
         self.seed = seed
         self.use_tc = True
-        # the split-M tcgen05 weight gradient measures 29 us vs cuBLAS 25 us at the
-        # papers shape (tools/tc_bench.py), so cuBLAS stays the default for dW
-        self.tc_wgrad = False
+        # tcgen05 weight gradients (tiled split-K, sal_tc_sage_wgrad) where the
+        # shapes allow; cuBLAS for the rest
+        self.tc_wgrad = True
 
     # ------------------------------------------------------------- weights
     def refresh_shadow(self):
@@ -239,6 +239,11 @@ class FusedSAGE:
         N = f_out = 256, with a hidden layer after it (the ReLU/dropout epilogue)."""
         return (self.use_tc and self.act == torch.bfloat16 and i != self.L - 1
                 and 2 * self.dims[i] == 256 and self.dims[i + 1] == 256)
+
+    def _tc_wgrad_layer(self, i: int) -> bool:
+        """dW_i on sal_tc_sage_wgrad: bf16 operands, dW rows and cols multiples of 128."""
+        return (self.tc_wgrad and self.act == torch.bfloat16
+                and self.gp[i].shape[0] % 128 == 0 and self.gp[i].shape[1] % 128 == 0)
 
     # ------------------------------------------------------------- buffers
     def cat_input(self, x: torch.Tensor) -> torch.Tensor:
@@ -339,11 +344,11 @@ class FusedSAGE:
         for i in reversed(range(self.L)):
             rec = saved[i]
             a, n_pad = rec["a"], rec["n_pad"]
-            if self._tc_layer(i) and self.tc_wgrad:
+            if self._tc_wgrad_layer(i):
+                gi = self.gp[i]
                 _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), a.data_ptr(),
-                                               a.stride(0), n_pad, self.dims[i + 1],
-                                               2 * self.dims[i], self.g[i].data_ptr(),
-                                               self.g[i].stride(0), st), "tc_sage_wgrad")
+                                               a.stride(0), n_pad, gi.shape[0], gi.shape[1],
+                                               gi.data_ptr(), gi.stride(0), st), "tc_sage_wgrad")
             else:
                 _mm_f32(dz.t(), a[:n_pad], self.gp[i])
             if i == 0:

@@ -50,6 +50,8 @@ class TrainConfig:
     graphs: bool = True            # capture {prep || step} in CUDA graphs
     model_seed: int = 0
     prep_priority: int = -1        # CUDA stream priority of the prep stream (lower = higher)
+    tc_wgrad: bool = True          # tcgen05 weight gradients where the shapes allow
+    late_prep: bool = True         # labels + reverse adjacency built beside the forward pass
     prep_mean0: bool = False       # gather-free: layer-0 mean on the prep stream (measured slower)
 
 
@@ -143,6 +145,7 @@ class Trainer:
         self.model = FusedSAGE(dg.num_features, cfg.hidden, self.num_classes, self.nh,
                                cfg.dropout, device=self.device, seed=cfg.model_seed,
                                act_dtype=cfg.act_dtype, lr=cfg.lr)
+        self.model.tc_wgrad = cfg.tc_wgrad
         if world > 1:  # identical initial weights on every rank
             torch.distributed.broadcast(self.model.flat, src=0)
             self.model.refresh_shadow()
@@ -152,6 +155,9 @@ class Trainer:
         # high priority: the prep chain is latency-bound (many small dependent kernels), so
         # it should take SMs first as the bandwidth-bound training kernels drain
         self.prep_stream = torch.cuda.Stream(device=self.device, priority=cfg.prep_priority)
+        # the backward-only inputs of the step being trained (labels, reverse adjacency)
+        # are built on a third stream while its forward pass runs
+        self.late_stream = torch.cuda.Stream(device=self.device, priority=cfg.prep_priority)
         self.policy = RNG_POLICIES[cfg.rng_policy]
         self.x_table = dg.feature_view()
         self.cursor = torch.zeros(1, dtype=torch.int64, device=self.device)
@@ -200,8 +206,9 @@ class Trainer:
         return self.steps_per_epoch
 
     # ---------------------------------------------------------------- prep
-    def _prep(self, slot: _Slot, stage: "_Staging | None") -> None:
-        """Enqueue one batch preparation on the current stream (capturable)."""
+    def _prep(self, slot: _Slot, stage: "_Staging | None", late: bool = False) -> None:
+        """Enqueue one batch preparation on the current stream (capturable): seeds ->
+        MFG -> layer-0 feature rows, plus (late=True) what _prep_late builds."""
         ws = slot.ws
         st = torch.cuda.current_stream()
         L = _lib.lib()
@@ -231,6 +238,17 @@ class Trainer:
                 _lib.dtype_code(self.x_table.dtype), self.x_table.stride(0), f, a0.data_ptr(),
                 _lib.dtype_code(a0.dtype), a0.stride(0), _lib.stream_ptr(st)),
                 "segment_mean_fwd(table)")
+        if late:
+            self._prep_late(slot, stage is not None)
+
+    def _prep_late(self, slot: _Slot, host_inputs: bool) -> None:
+        """The inputs only the loss / backward read: labels and the reverse adjacency
+        of layers >= 1 (capturable, current stream)."""
+        ws = slot.ws
+        st = torch.cuda.current_stream()
+        L = _lib.lib()
+        nh = self.nh
+        seeds_base = slot.seeds if host_inputs else self.seeds_all
         _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), seeds_base.data_ptr(),
                                        slot.desc.data_ptr(), self.cfg.batch_size,
                                        slot.labels.data_ptr(), _lib.stream_ptr(st)),
@@ -248,19 +266,22 @@ class Trainer:
             out.append((ws.dst_indptr[h], ws.src_local[h], ws.node_cap[h], ws.sizes[h:h + 1]))
         return out
 
-    def _train(self, slot: _Slot, part: str = "all") -> None:
+    def _train(self, slot: _Slot, part: str = "all", late=None) -> None:
         """fwd + bwd [+ all-reduce] [+ Adam] on the current stream (capturable).
 
         part: "all" (one graph, the gradient all-reduce captured with it),
         "pre" (fwd + bwd only) or "post" (Adam + bookkeeping) — the split used
         when NCCL cannot be captured, with the all-reduce issued eagerly in
-        between."""
+        between.  late: the stream building this slot's labels / reverse adjacency,
+        joined after the forward pass."""
         m = self.model
         if part in ("all", "pre"):
             ready = self.cfg.gather_free and self.cfg.prep_mean0
             xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free and not ready else None
             logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg,
                                       salt=self.step_ctr, mean0_ready=ready)
+            if late is not None:
+                torch.cuda.current_stream().wait_stream(late)
             loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf)
             m.backward(dlog, saved, slot.transposes)
         if part == "all" and self.world > 1:
@@ -280,11 +301,18 @@ class Trainer:
             return
         cs = torch.cuda.current_stream()
         ps = self.prep_stream or cs  # None: prep serialised on the compute stream
+        split = self.cfg.late_prep and self.prep_stream is not None
         ps.wait_stream(cs)
+        ls = None
+        if split:
+            ls = self.late_stream
+            ls.wait_stream(cs)
+            with torch.cuda.stream(ls):
+                self._prep_late(self.slots[k % 2], host_inputs)
         with torch.cuda.stream(ps):
             self._prep(self.slots[(k + 1) % 2],
-                       self.staging[(k + 1) % 4] if host_inputs else None)
-        self._train(self.slots[k % 2], part)
+                       self.staging[(k + 1) % 4] if host_inputs else None, late=not split)
+        self._train(self.slots[k % 2], part, late=ls)
         cs.wait_stream(ps)
 
     # ---------------------------------------------------------------- driver
@@ -305,7 +333,9 @@ class Trainer:
             stage = self.staging[0]
             stage.ev.synchronize()
             self._stage_host(stage, 0)
-        self._prep(self.slots[0], stage)
+        # with the late split, pair 0 builds slot 0's labels / reverse adjacency
+        self._prep(self.slots[0], stage,
+                   late=not (self.cfg.late_prep and self.prep_stream is not None))
         if stage is not None:
             stage.ev.record()
 

@@ -60,15 +60,16 @@ def test_tc_fwd_dropout_matches_unfused_kernels():
     assert 0.45 < frac.item() < 0.55
 
 
-@pytest.mark.parametrize("M", [64, 1000, 67584])
-def test_tc_wgrad_matches_torch(M):
+@pytest.mark.parametrize("M,N,K", [(64, 256, 256), (1000, 256, 256), (67584, 256, 256),
+                                   (6144, 256, 512), (777, 128, 384)])
+def test_tc_wgrad_matches_torch(M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M + 1)
-    dz = (torch.randn(M, 256, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
-    A = (torch.randn(M, 512, device="cuda", generator=g)).to(torch.bfloat16)[:, :256]
-    dW = torch.full((256, 256), 7.0, device="cuda")
+    dz = (torch.randn(M, N, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    A = (torch.randn(M, 2 * K, device="cuda", generator=g)).to(torch.bfloat16)[:, :K]
+    dW = torch.full((N, K), 7.0, device="cuda")
     L = _lib.lib()
     _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), A.data_ptr(), A.stride(0), M,
-                                   256, 256, dW.data_ptr(), dW.stride(0), _lib.stream_ptr()),
+                                   N, K, dW.data_ptr(), dW.stride(0), _lib.stream_ptr()),
                "tc_sage_wgrad")
     torch.cuda.synchronize()
     want = dz.float().t() @ A.float()

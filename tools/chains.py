@@ -50,7 +50,7 @@ def main():
     tr.run_steps(0, 8)
     torch.cuda.synchronize()
     s0, s1 = tr.slots
-    print(f"prep alone   {graph_time(lambda: tr._prep(s1, None)):7.1f} us")
+    print(f"prep alone   {graph_time(lambda: tr._prep(s1, None, late=True)):7.1f} us")
     print(f"train alone  {graph_time(lambda: tr._train(s0)):7.1f} us")
     print(f"pair         {graph_time(lambda: tr._pair(0, False)):7.1f} us")
 
