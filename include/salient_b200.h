@@ -229,6 +229,13 @@ int sal_relu_dropout_bwd(const void* dy_dev, int64_t dy_stride, int32_t dy_dtype
 int sal_lsm_nll(const void* logits_dev, int64_t ld, int64_t rows, int32_t num_classes,
                 int32_t dtype, const int64_t* labels_dev, float* loss_dev, void* grad_dev,
                 int64_t ldg, void* stream);
+/* sampled-inference scoring (PAPER.md:1428-1439 evaluation): pred[r] =
+ * argmax of logits row r (first maximum, NaN as maximum — torch.argmax);
+ * counts_dev[0] += #(pred == label), counts_dev[1] += #(label >= 0) over the
+ * rows with label >= 0.  pred_dev is nullable.  counts are int64. */
+int sal_argmax_correct(const void* logits_dev, int64_t ld, int64_t rows, int32_t num_classes,
+                       int32_t dtype, const int64_t* labels_dev, int64_t* counts_dev,
+                       int64_t* pred_dev, void* stream);
 /* reverse adjacency of an MFG layer: tindptr[n_src_rows+1], tdst[edges] lists
  * for every source row the destinations that sampled it (order within a list
  * is unspecified); tw (nullable) receives each entry's 1/deg(dst) */

@@ -90,6 +90,7 @@ SIGNATURES = {
     "sal_relu_dropout_bwd": (ctypes.c_int, [vp, i64, i32, vp, vp, i64, i32, i64, i32,
                                             ctypes.c_float, vp]),
     "sal_lsm_nll": (ctypes.c_int, [vp, i64, i64, i32, i32, vp, vp, vp, i64, vp]),
+    "sal_argmax_correct": (ctypes.c_int, [vp, i64, i64, i32, i32, vp, vp, vp, vp]),
     "sal_transpose_ws_bytes": (ctypes.c_size_t, [i64]),
     "sal_transpose_build": (ctypes.c_int, [vp, vp, vp, i64, i64, i64, vp, vp, vp, vp, vp]),
     "sal_mean_bwd_t": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp,

@@ -182,6 +182,55 @@ __global__ void lsm_nll_kernel(const T* __restrict__ logits, int64_t ld, int64_t
 }
 
 // ---------------------------------------------------------------------------
+// sampled-inference scoring: pred = argmax (first maximum, torch.argmax rule)
+// of each logits row; counts[0] += #(pred == label), counts[1] += #(label >= 0).
+// One warp per row, one pair of atomics per block.
+template <typename T>
+__global__ void argmax_correct_kernel(const T* __restrict__ logits, int64_t ld, int64_t rows,
+                                      int32_t C, const int64_t* __restrict__ labels,
+                                      unsigned long long* __restrict__ counts,
+                                      int64_t* __restrict__ pred) {
+  __shared__ int sh_ok, sh_tot;
+  if (threadIdx.x == 0) sh_ok = sh_tot = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
+  if (row < rows) {
+    const T* x = logits + row * ld;
+    float m = -INFINITY;
+    int arg = C;
+    for (int j = lane; j < C; j += 32) {
+      const float v = F<T>::in(x[j]);
+      if (v > m || (v != v && m == m)) { m = v; arg = j; }  // NaN counts as the maximum
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      const bool onan = om != om, mnan = m != m;
+      if ((onan && !mnan) || (onan == mnan && (om > m || (om == m && oa < arg))) ||
+          (onan && mnan && oa < arg)) {
+        m = om;
+        arg = oa;
+      }
+    }
+    if (lane == 0) {
+      if (pred) pred[row] = arg;
+      const int64_t lab = labels[row];
+      if (lab >= 0) {
+        atomicAdd(&sh_tot, 1);
+        if (lab == arg) atomicAdd(&sh_ok, 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && sh_tot) {
+    atomicAdd(&counts[0], (unsigned long long)sh_ok);
+    atomicAdd(&counts[1], (unsigned long long)sh_tot);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // reverse adjacency of one MFG layer: for each source row s, the destinations
 // d with s in N(d).  count -> exclusive scan -> fill (warp per destination).
 __global__ void transpose_count_kernel(const int32_t* __restrict__ indptr,
@@ -466,6 +515,25 @@ int sal_lsm_nll(const void* logits, int64_t ld, int64_t rows, int32_t C, int32_t
   else if (dtype == SAL_F32)
     sal::lsm_nll_kernel<float><<<grid, 32 * warps, 0, st>>>((const float*)logits, ld, rows, C,
                                                            labels, loss, (float*)grad, ldg);
+  else
+    return SAL_EINVAL;
+  return sal::done(1);
+}
+
+int sal_argmax_correct(const void* logits, int64_t ld, int64_t rows, int32_t C, int32_t dtype,
+                       const int64_t* labels, int64_t* counts, int64_t* pred, void* stream) {
+  if (rows < 0 || C <= 0 || !counts || !labels) return SAL_EINVAL;
+  if (rows == 0) return SAL_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int warps = 8;
+  const int grid = (int)((rows + warps - 1) / warps);
+  unsigned long long* c = (unsigned long long*)counts;
+  if (dtype == SAL_BF16)
+    sal::argmax_correct_kernel<__nv_bfloat16><<<grid, 32 * warps, 0, st>>>(
+        (const __nv_bfloat16*)logits, ld, rows, C, labels, c, pred);
+  else if (dtype == SAL_F32)
+    sal::argmax_correct_kernel<float><<<grid, 32 * warps, 0, st>>>((const float*)logits, ld,
+                                                                  rows, C, labels, c, pred);
   else
     return SAL_EINVAL;
   return sal::done(1);

@@ -91,7 +91,7 @@ def allreduce_mean(t: torch.Tensor, world: int) -> None:
 
 
 class _Slot:
-    def __init__(self, dg: DeviceGraph, cfg: TrainConfig, device):
+    def __init__(self, dg: DeviceGraph, cfg: TrainConfig, device, backward: bool = True):
         # gather-free: layer 0 reads rows by global id, so the last hop needs no relabel
         self.ws = MfgWorkspace(dg.num_nodes, cfg.fanouts, cfg.batch_size, device=device,
                                last_hop_edges=cfg.gather_free)
@@ -108,7 +108,7 @@ class _Slot:
         L = _lib.lib()
         self.transposes = [None]
         self.t_ws = [None]
-        for i in range(1, nh):
+        for i in range(1, nh if backward else 1):
             h = nh - 1 - i
             n_src = ws.node_cap[h + 1]
             self.transposes.append((
@@ -429,10 +429,29 @@ class Trainer:
         return float(self.losses[:n].mean().item()) if n else 0.0
 
     # ---------------------------------------------------------------- eval
-    @torch.no_grad()
     def evaluate(self, ids: np.ndarray, fanouts: FanoutSpec | None = None,
                  batch_size: int | None = None) -> tuple[int, int]:
-        """Sampled inference over `ids` (this rank's shard); returns (correct, total)."""
+        """Sampled inference over `ids` on the device pipeline (Evaluator);
+        returns (correct, total) summed over ranks when world > 1."""
+        fan = fanouts or self.cfg.fanouts
+        bs = batch_size or self.cfg.batch_size
+        key = (tuple(fan.per_hop), bs)
+        ev = self._evaluators.get(key) if hasattr(self, "_evaluators") else None
+        if ev is None:
+            self._evaluators = getattr(self, "_evaluators", {})
+            ev = Evaluator(self.dg, self.model, fan, bs, self.cfg.global_seed + 7,
+                           rank=self.rank, world=self.world, rng_policy=self.cfg.rng_policy,
+                           graphs=self.cfg.graphs, act_dtype=self.cfg.act_dtype,
+                           prep_priority=self.cfg.prep_priority)
+            self._evaluators[key] = ev
+        return ev.run(ids)
+
+    @torch.no_grad()
+    def evaluate_eager(self, ids: np.ndarray, fanouts: FanoutSpec | None = None,
+                       batch_size: int | None = None) -> tuple[int, int]:
+        """Sampled inference through the public prep API (run_epoch_prep ->
+        materialised features -> FusedSAGE.predict), one batch at a time; the
+        comparator of the Evaluator fast path (this rank's ids only)."""
         from .prep import EpochPlan, PrepConfig, run_epoch_prep
         from .sampler import SeedBatch
         fan = fanouts or self.cfg.fanouts
@@ -450,3 +469,162 @@ class Trainer:
             correct += (logits.argmax(dim=-1) == pb.labels).sum()
             total += len(pb.labels)
         return int(correct.item()), total
+
+
+class Evaluator:
+    """Sampled inference over a node set on the device pipeline (SURVEY §8 f1;
+    PAPER.md:1428-1439, inference fanout (20,20,20) in the paper).
+
+    Batches are `ids` chunked in order (batch_id = chunk index, no shuffle),
+    sampled with `global_seed`; chunk b runs on rank b % world.  Each step is
+    {prep(k+1) on the prep stream: plan cursor -> MFG (last hop edges only) ->
+    destination rows -> labels  ||  forward(k) without dropout: layer-0 mean
+    straight from the fp16 table, SAGE layers, argmax + correct count}, captured
+    as one CUDA graph per slot parity.  The (correct, total) pair stays on the
+    device until the end of the pass (one D2H; one all-reduce when world > 1).
+    """
+
+    def __init__(self, dg: DeviceGraph, model: FusedSAGE, fanouts: FanoutSpec, batch_size: int,
+                 global_seed: int, rank: int = 0, world: int = 1, rng_policy: str = "splitmix",
+                 graphs: bool = True, act_dtype: torch.dtype = torch.bfloat16,
+                 prep_priority: int = -1):
+        _lib.require_cuda()
+        self.dg, self.model = dg, model
+        self.fanouts, self.batch_size, self.global_seed = fanouts, int(batch_size), int(global_seed)
+        self.rank, self.world = rank, world
+        self.device = dg.device
+        self.nh = len(fanouts)
+        self.policy = RNG_POLICIES[rng_policy]
+        self.use_graphs = graphs
+        cfg = TrainConfig(fanouts=fanouts, batch_size=self.batch_size, gather_free=True,
+                          act_dtype=act_dtype)
+        self.slots = [_Slot(dg, cfg, self.device, backward=False) for _ in range(2)]
+        self.prep_stream = torch.cuda.Stream(device=self.device, priority=prep_priority)
+        self.x_table = dg.feature_view()
+        self.cursor = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.counts = torch.zeros(2, dtype=torch.int64, device=self.device)
+        self.seeds_all = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.desc_all = torch.zeros((1, 3), dtype=torch.int64, device=self.device)
+        self.n_steps = 0
+        self.graphs = {}
+        self.graph_kernels = {}
+        self.kernel_launches = 0
+
+    def set_ids(self, ids: np.ndarray) -> int:
+        """Chunk and shard `ids`, upload seeds + descriptors; returns this rank's steps."""
+        from .prep import EpochPlan
+        from .sampler import SeedBatch
+        ids = np.asarray(ids, dtype=np.int64)
+        bs = self.batch_size
+        batches = tuple(SeedBatch(i, ids[s:s + bs]) for i, s in enumerate(range(0, len(ids), bs)))
+        plan = EpochPlan(batches=batches, batch_size=bs, shuffle_seed=0)
+        descs, _ = shard_plan(plan, bs, self.rank, self.world)
+        n = len(descs)
+        if self.seeds_all.numel() < max(1, len(ids)):
+            self.seeds_all = torch.zeros(len(ids), dtype=torch.int64, device=self.device)
+            self.graphs.clear()
+        if self.desc_all.shape[0] < max(1, n) or self.n_steps != n:
+            self.desc_all = torch.zeros((max(1, n), 3), dtype=torch.int64, device=self.device)
+            self.graphs.clear()
+        if len(ids):
+            self.seeds_all[:len(ids)].copy_(torch.from_numpy(ids))
+        if n:
+            self.desc_all[:n].copy_(torch.from_numpy(np.asarray(descs, np.int64)))
+        self.n_steps = n
+        return n
+
+    def _prep(self, slot: _Slot) -> None:
+        ws = slot.ws
+        st = torch.cuda.current_stream()
+        L = _lib.lib()
+        _lib.check(L.sal_plan_next(self.desc_all.data_ptr(), self.n_steps, self.cursor.data_ptr(),
+                                   slot.desc.data_ptr(), _lib.stream_ptr(st)), "plan_next")
+        ws.run(self.dg, self.seeds_all, slot.desc, self.global_seed, self.policy, st)
+        nh = self.nh
+        f = self.x_table.shape[1]
+        gather_rows(self.x_table, ws.globals, slot.feats[:, f:], n=ws.node_cap[nh - 1],
+                    n_dev=ws.sizes[nh - 1:nh], stream=st)
+        _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), self.seeds_all.data_ptr(),
+                                       slot.desc.data_ptr(), self.batch_size,
+                                       slot.labels.data_ptr(), _lib.stream_ptr(st)),
+                   "gather_labels")
+
+    def _forward(self, slot: _Slot) -> None:
+        ws = slot.ws
+        adjs = []
+        for i in range(self.nh):
+            h = self.nh - 1 - i
+            adjs.append((ws.dst_indptr[h], ws.src_local[h], ws.node_cap[h], ws.sizes[h:h + 1]))
+        m = self.model
+        was = m.training
+        m.training = False
+        try:
+            logits, _ = m.forward(slot.feats, adjs, x_global=(self.x_table, ws.src_glob))
+        finally:
+            m.training = was
+        _lib.check(_lib.lib().sal_argmax_correct(
+            logits.data_ptr(), logits.stride(0), min(logits.shape[0], self.batch_size),
+            logits.shape[1], _lib.dtype_code(logits.dtype), slot.labels.data_ptr(),
+            self.counts.data_ptr(), None, _lib.stream_ptr()), "argmax_correct")
+
+    def _pair(self, k: int) -> None:
+        cs = torch.cuda.current_stream()
+        ps = self.prep_stream
+        ps.wait_stream(cs)
+        with torch.cuda.stream(ps):
+            self._prep(self.slots[(k + 1) % 2])
+        self._forward(self.slots[k % 2])
+        cs.wait_stream(ps)
+
+    def _capture(self, parity: int):
+        torch.cuda.synchronize()
+        saved = (self.cursor.clone(), self.counts.clone())
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._prep(self.slots[parity])  # the warm-up forward reads a prepared slot
+            for _ in range(2):
+                self._pair(parity)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = _lib.lib().sal_launch_count()
+        with torch.cuda.graph(g):
+            self._pair(parity)
+        torch.cuda.synchronize()
+        self.graph_kernels[parity] = _lib.lib().sal_launch_count() - n0
+        self.cursor.copy_(saved[0])
+        self.counts.copy_(saved[1])
+        self.graphs[parity] = g
+        return g
+
+    def begin(self) -> None:
+        """Reset the cursor and counters and prepare step 0 into slot 0."""
+        self.cursor.zero_()
+        self.counts.zero_()
+        self._prep(self.slots[0])
+
+    def steps(self, start: int, count: int) -> None:
+        """Enqueue steps [start, start+count) (begin() primed step `start`)."""
+        for k in range(start, start + count):
+            if self.use_graphs:
+                g = self.graphs.get(k % 2) or self._capture(k % 2)
+                g.replay()
+                self.kernel_launches += self.graph_kernels[k % 2]
+            else:
+                n0 = _lib.lib().sal_launch_count()
+                self._pair(k)
+                self.kernel_launches += _lib.lib().sal_launch_count() - n0
+
+    def run(self, ids: np.ndarray) -> tuple[int, int]:
+        n = self.set_ids(ids)
+        if self.use_graphs:  # capture before the pass so it does not disturb the cursor
+            for p in range(min(2, n)):
+                if p not in self.graphs:
+                    self._capture(p)
+        self.begin()
+        self.steps(0, n)
+        if self.world > 1:
+            torch.distributed.all_reduce(self.counts)
+        c, t = self.counts.tolist()
+        return int(c), int(t)
