@@ -296,6 +296,69 @@ int sal_gen_features_uniform(int64_t n, int32_t f, int64_t stride, uint64_t seed
 int sal_gen_labels_uniform(int64_t n, int32_t num_classes, uint64_t seed, int64_t* out_dev,
                            void* stream);
 
+/* ---- f2: binary files straight into HBM (graph.py:194-249) -------------- *
+ * MFGC: "MFGC" u32 version=1, u64 num_nodes, u64 num_edges, u64 indptr[n+1],
+ *       u32 indices[E]                       (save_csr / load_csr, :194-214)
+ * FEAT: "FEAT" u32 version, u64 rows, u32 cols, u8 dtype (1 = f16, else f32),
+ *       3 pad bytes, row-major payload        (save_features / load_features, :217-232)
+ * LABL: "LABL" u32 version, u64 rows, u32 num_classes, u32 values[rows]
+ *                                            (save_labels / load_labels, :235-249)
+ * Header errors mirror graph.py:23-36 and _check_header/_read_exact (:176-191):
+ * SAL_EBADMAGIC (BadMagicError), SAL_EVERSION (VersionMismatchError),
+ * SAL_ETRUNC (TruncatedFileError, message "truncated file while reading <what>"
+ * with the reference's field names), SAL_EIO (OSError). */
+#define SAL_EBADMAGIC (-10)
+#define SAL_EVERSION (-11)
+#define SAL_ETRUNC (-12)
+#define SAL_EIO (-13)
+
+#define SAL_FILE_CSR 1
+#define SAL_FILE_FEAT 2
+#define SAL_FILE_LABL 3
+
+typedef struct {
+  int32_t kind;            /* SAL_FILE_*                                   */
+  uint32_t version;
+  uint8_t magic[4];        /* as read (for the BadMagicError message)      */
+  int64_t rows;            /* CSR: num_nodes; FEAT / LABL: rows            */
+  int64_t cols;            /* CSR: num_edges; FEAT: cols; LABL: classes    */
+  int32_t dtype;           /* FEAT: SAL_F16 / SAL_F32 (code 1 = f16)       */
+  int32_t elem_bytes;      /* FEAT: 2 / 4; LABL / CSR indices: 4           */
+  int64_t payload_offset;  /* first byte after the fixed header            */
+  int64_t file_bytes;
+} sal_file_header;
+
+/* Parse + size-check the header of `path` as `kind` (no device work). */
+int sal_file_header_read(const char* path, int32_t kind, sal_file_header* out);
+/* Stream a file's payload into HBM through a caller-provided pinned staging
+ * buffer (split in two halves: read of chunk k+1 by `threads` host threads
+ * overlaps the H2D copy of chunk k on `stream`).  Returns when the last copy
+ * is enqueued and the staging buffer is free again (synchronises on its own
+ * events only).
+ *   CSR : indptr_dev int64[n+1] (u64 bytes), indices_dev int32[E] (u32 bytes)
+ *   FEAT: rows into out_dev with row pitch out_stride_bytes (>= cols*elem);
+ *         a padded pitch goes through scratch_dev (>= pinned_bytes/2 bytes,
+ *         nullable when the pitch equals the row) and a re-pitch kernel
+ *   LABL: u32 chunks into scratch_dev (>= pinned_bytes/2 bytes), widened
+ *         to int64 into out_dev by a kernel                                  */
+int sal_load_csr(const char* path, const sal_file_header* h, int64_t* indptr_dev,
+                 int32_t* indices_dev, void* pinned, int64_t pinned_bytes, int32_t threads,
+                 void* stream);
+int sal_load_features(const char* path, const sal_file_header* h, void* out_dev,
+                      int64_t out_stride_bytes, void* scratch_dev, void* pinned,
+                      int64_t pinned_bytes, int32_t threads, void* stream);
+int sal_load_labels(const char* path, const sal_file_header* h, int64_t* out_dev,
+                    void* scratch_dev, void* pinned, int64_t pinned_bytes, int32_t threads,
+                    void* stream);
+/* CsrGraph.validate (graph.py:58-65) on device: flags_dev int32[3] |= (bad
+ * endpoints, decreasing indptr, neighbour id out of range); caller zeroes. */
+int sal_validate_csr(const int64_t* indptr_dev, const int32_t* indices_dev, int64_t n,
+                     int64_t e, int32_t* flags_dev, void* stream);
+/* LabelVector check (graph.py:96-100): flags_dev[0] |= any value outside
+ * [0, num_classes). */
+int sal_validate_labels(const int64_t* y_dev, int64_t n, int64_t num_classes, int32_t* flags_dev,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,16 @@ class SalMfgLayout(ctypes.Structure):
                 ("scan_bytes", i64), ("total", i64)]
 
 
+class SalFileHeader(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("version", ctypes.c_uint32),
+                ("magic", ctypes.c_uint8 * 4), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+                ("dtype", ctypes.c_int32), ("elem_bytes", ctypes.c_int32),
+                ("payload_offset", ctypes.c_int64), ("file_bytes", ctypes.c_int64)]
+
+
+SAL_EBADMAGIC, SAL_EVERSION, SAL_ETRUNC, SAL_EIO = -10, -11, -12, -13
+SAL_FILE_CSR, SAL_FILE_FEAT, SAL_FILE_LABL = 1, 2, 3
+
 P = ctypes.POINTER
 
 # name -> (restype, argtypes); every symbol declared in include/salient_b200.h
@@ -108,6 +118,14 @@ SIGNATURES = {
     "sal_gen_pairing": (ctypes.c_int, [vp, i64, u64, vp, vp]),
     "sal_gen_features_uniform": (ctypes.c_int, [i64, i32, i64, u64, vp, vp]),
     "sal_gen_labels_uniform": (ctypes.c_int, [i64, i32, u64, vp, vp]),
+    "sal_file_header_read": (ctypes.c_int, [ctypes.c_char_p, i32, P(SalFileHeader)]),
+    "sal_load_csr": (ctypes.c_int, [ctypes.c_char_p, P(SalFileHeader), vp, vp, vp, i64, i32, vp]),
+    "sal_load_features": (ctypes.c_int, [ctypes.c_char_p, P(SalFileHeader), vp, i64, vp, vp, i64,
+                                         i32, vp]),
+    "sal_load_labels": (ctypes.c_int, [ctypes.c_char_p, P(SalFileHeader), vp, vp, vp, i64, i32,
+                                       vp]),
+    "sal_validate_csr": (ctypes.c_int, [vp, vp, i64, i64, vp, vp]),
+    "sal_validate_labels": (ctypes.c_int, [vp, i64, i64, vp, vp]),
 }
 
 

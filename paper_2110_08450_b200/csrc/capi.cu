@@ -35,6 +35,18 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+}  // namespace
+namespace sal {
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+}  // namespace sal
+namespace {
+
 int cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return SAL_OK;
   return fail(SAL_ECUDA, "%s: %s", what, cudaGetErrorString(e));

@@ -36,6 +36,8 @@ struct HopKey {
 };
 
 int num_sms();
+// thread-local error message of sal_last_error(); returns `code`
+int set_error(int code, const char* fmt, ...);
 void count_launch(int kernels);
 int log2_exact(int64_t cap);
 size_t scan_ws_bytes(int64_t max_items);

@@ -192,7 +192,83 @@ def gen_config1():
     save("config1", **out)
 
 
+def _malformed_cases(good: bytes, magic: bytes):
+    """(tag, bytes) variants of one good file: bad magic, bad version, and a
+    truncation inside every field (magic, version, counts/shape, payloads)."""
+    cases = [("badmagic", b"XXXX" + good[4:]),
+             ("badversion", good[:4] + (2).to_bytes(4, "little") + good[8:])]
+    for cut in (2, 6, 12, 30, len(good) - 1):
+        if cut < len(good):
+            cases.append((f"trunc{cut}", good[:cut]))
+    return cases
+
+
+def gen_files():
+    """f2 loaders: small MFGC / FEAT / LABL files written by the reference's own
+    writers (graph.py:194-240), the arrays its loaders return, and the
+    exception class + message its loaders raise on malformed variants."""
+    import tempfile
+    d = OUT / "files"
+    d.mkdir(exist_ok=True)
+    g = M.synth_graph(700, 6, 3.0, seed=5)
+    fh = M.generate_features(700, 20, "f16", seed=5)
+    ff = M.generate_features(700, 7, "f32", seed=5)
+    y = M.generate_labels(700, 13, seed=5)
+    M.save_csr(g, d / "g.mfgc")
+    M.save_features(fh, d / "x16.feat")
+    M.save_features(ff, d / "x32.feat")
+    M.save_labels(y, d / "y.labl")
+    out = {"indptr": M.load_csr(d / "g.mfgc").indptr, "indices": M.load_csr(d / "g.mfgc").indices,
+           "num_nodes": np.array(g.num_nodes),
+           "x16": M.load_features(d / "x16.feat").data, "x32": M.load_features(d / "x32.feat").data,
+           "y": M.load_labels(d / "y.labl").values,
+           "num_classes": np.array(M.load_labels(d / "y.labl").num_classes)}
+    errs = []
+    loaders = {"g.mfgc": M.load_csr, "x16.feat": M.load_features, "y.labl": M.load_labels}
+    with tempfile.TemporaryDirectory() as td:
+        for name, fn in loaders.items():
+            good = (d / name).read_bytes()
+            for tag, data in _malformed_cases(good, good[:4]):
+                p = Path(td) / f"{tag}_{name}"
+                p.write_bytes(data)
+                try:
+                    fn(p)
+                    errs.append((name, tag, "", ""))
+                except Exception as e:  # noqa: BLE001 — recording the reference's behaviour
+                    errs.append((name, tag, type(e).__name__, str(e)))
+        # semantic faults the loaders' validation catches (graph.py:58-65, 96-100)
+        good = bytearray((d / "g.mfgc").read_bytes())
+        n, e = g.num_nodes, g.num_edges
+        ip0 = 4 + 4 + 16
+        ix0 = ip0 + 8 * (n + 1)
+        sem = {}
+        b = bytearray(good); b[ix0 + 4 * (e - 1): ix0 + 4 * e] = int(n).to_bytes(4, "little")
+        sem["badindex_g.mfgc"] = b
+        b = bytearray(good); b[ip0 + 8 * 5: ip0 + 8 * 6] = int(e + 3).to_bytes(8, "little")
+        sem["decreasing_g.mfgc"] = b
+        b = bytearray(good); b[ip0 + 8 * n: ip0 + 8 * (n + 1)] = int(e - 1).to_bytes(8, "little")
+        sem["endpoint_g.mfgc"] = b
+        b = bytearray(good); b[ip0: ip0 + 8] = int(1).to_bytes(8, "little")
+        sem["start_g.mfgc"] = b
+        lb = bytearray((d / "y.labl").read_bytes())
+        lb[8 + 12 + 4 * 9: 8 + 12 + 4 * 10] = (13).to_bytes(4, "little")
+        sem["badlabel_y.labl"] = lb
+        for key, data in sem.items():
+            tag, name = key.split("_", 1)
+            p = Path(td) / key
+            p.write_bytes(bytes(data))
+            (d / key).write_bytes(bytes(data))
+            try:
+                loaders[name](p)
+                errs.append((name, tag, "", ""))
+            except Exception as ex:  # noqa: BLE001
+                errs.append((name, tag, type(ex).__name__, str(ex)))
+    out["errors"] = np.array(errs)
+    save("files", **out)
+
+
 if __name__ == "__main__":
+    gen_files()
     gen_rng()
     gen_graphs()
     gen_small_mfgs()
