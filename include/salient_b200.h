@@ -84,6 +84,11 @@ typedef struct {
   int64_t table_cap;
   int32_t flags;                        /* SAL_MFG_* plan flags            */
   int32_t reserved;
+  /* sampler launch shape (sal_hop_sample_tuned; 0 = default), set by the
+   * caller after sal_mfg_plan_init; the caller may also raise table_cap (a
+   * power of two) before sal_mfg_layout_init to lower the id-table load */
+  int32_t sample_lanes;
+  int32_t sample_blocks_per_sm;
 } sal_mfg_plan;
 
 /* Plan flag: the last hop emits its edges as global ids only (layout.src_glob);
@@ -164,6 +169,17 @@ int sal_hop_sample(const sal_graph* g, const sal_idmap* m, const int64_t* n_dst_
                    const int64_t* inject_pos_dev, const int32_t* dst_indptr_dev,
                    int32_t* src_glob_dev, int32_t* slot_dev, int32_t* draws_out_dev,
                    void* stream);
+/* sal_hop_sample with the launch shape pinned, for the f3 design-space sweep
+ * (bench.py:142-189 sweep over SamplerVariant): lanes = threads cooperating on
+ * one destination (8 / 16 / 32; 0 = smallest group holding the fanout),
+ * blocks_per_sm = grid cap per SM (0 = 8).  Output is identical for every
+ * setting (the sweep checks digests). */
+int sal_hop_sample_tuned(const sal_graph* g, const sal_idmap* m, const int64_t* n_dst_dev,
+                         int64_t max_dst, int32_t fanout, uint64_t key_prefix,
+                         int32_t rng_policy, uint64_t global_seed, int64_t batch_id, int32_t hop,
+                         const int64_t* inject_pos_dev, const int32_t* dst_indptr_dev,
+                         int32_t* src_glob_dev, int32_t* slot_dev, int32_t* draws_out_dev,
+                         int32_t lanes, int32_t blocks_per_sm, void* stream);
 /* relabel half of hop_kernel (_map_get_or_insert, _kernels.py:76-99). */
 int sal_hop_relabel(const sal_idmap* m, const int64_t* e_total_dev, int64_t max_edges,
                     const int64_t* size_old_dev, int64_t* size_new_dev,

@@ -44,7 +44,8 @@ class SalIdMap(ctypes.Structure):
 class SalMfgPlan(ctypes.Structure):
     _fields_ = [("num_hops", i32), ("fanout", i32 * SAL_MAX_HOPS), ("max_seeds", i64),
                 ("node_cap", i64 * (SAL_MAX_HOPS + 1)), ("edge_cap", i64 * SAL_MAX_HOPS),
-                ("table_cap", i64), ("flags", i32), ("reserved", i32)]
+                ("table_cap", i64), ("flags", i32), ("reserved", i32), ("sample_lanes", i32),
+                ("sample_blocks_per_sm", i32)]
 
 
 class SalMfgLayout(ctypes.Structure):
@@ -85,6 +86,8 @@ SIGNATURES = {
     "sal_hop_count": (ctypes.c_int, [P(SalGraph), vp, vp, i64, i32, vp, vp, vp, vp]),
     "sal_hop_sample": (ctypes.c_int, [P(SalGraph), P(SalIdMap), vp, i64, i32, u64, i32, u64, i64,
                                       i32, vp, vp, vp, vp, vp, vp]),
+    "sal_hop_sample_tuned": (ctypes.c_int, [P(SalGraph), P(SalIdMap), vp, i64, i32, u64, i32,
+                                            u64, i64, i32, vp, vp, vp, vp, vp, i32, i32, vp]),
     "sal_hop_relabel": (ctypes.c_int, [P(SalIdMap), vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "sal_gather_rows": (ctypes.c_int, [vp, i64, i32, i64, i32, vp, i32, vp, i64, vp, i64, i32,
                                        vp]),

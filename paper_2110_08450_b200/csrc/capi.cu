@@ -219,12 +219,13 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
       none.size_out = sizes + h + 1;
       e = sal::launch_hop_sample(gd, none, sizes + h, plan->node_cap[h], plan->fanout[h], hk,
                                  desc, rng_policy, nullptr, dst_indptr, src_glob, nullptr,
-                                 nullptr, st);
+                                 nullptr, st, plan->sample_lanes, plan->sample_blocks_per_sm);
       if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
       return counted(SAL_OK, 4 * plan->num_hops - 1);
     }
     e = sal::launch_hop_sample(gd, m, sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
-                               rng_policy, nullptr, dst_indptr, src_glob, slot, nullptr, st);
+                               rng_policy, nullptr, dst_indptr, src_glob, slot, nullptr, st,
+                               plan->sample_lanes, plan->sample_blocks_per_sm);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
     e = sal::launch_hop_relabel(m, etot + h, plan->edge_cap[h], sizes + h, sizes + h + 1,
                                 src_glob, slot, rank, src_local, scan, st);
@@ -293,6 +294,21 @@ int sal_hop_sample(const sal_graph* g, const sal_idmap* m, const int64_t* n_dst_
                    uint64_t global_seed, int64_t batch_id, int32_t hop,
                    const int64_t* inject_pos, const int32_t* dst_indptr, int32_t* src_glob,
                    int32_t* slot, int32_t* draws_out, void* stream) {
+  return sal_hop_sample_tuned(g, m, n_dst_dev, max_dst, fanout, key_prefix, rng_policy,
+                              global_seed, batch_id, hop, inject_pos, dst_indptr, src_glob, slot,
+                              draws_out, 0, 0, stream);
+}
+
+int sal_hop_sample_tuned(const sal_graph* g, const sal_idmap* m, const int64_t* n_dst_dev,
+                         int64_t max_dst, int32_t fanout, uint64_t key_prefix,
+                         int32_t rng_policy, uint64_t global_seed, int64_t batch_id, int32_t hop,
+                         const int64_t* inject_pos, const int32_t* dst_indptr,
+                         int32_t* src_glob, int32_t* slot, int32_t* draws_out, int32_t lanes,
+                         int32_t blocks_per_sm, void* stream) {
+  if (lanes != 0 && lanes != 8 && lanes != 16 && lanes != 32)
+    return fail(SAL_EINVAL, "hop_sample: lanes must be 0 (auto), 8, 16 or 32, got %d", lanes);
+  if (blocks_per_sm < 0 || blocks_per_sm > 32)
+    return fail(SAL_EINVAL, "hop_sample: blocks_per_sm must be in [0, 32], got %d", blocks_per_sm);
   sal::IdMapDev d;
   int rc = idmap_dev(m, &d);
   if (rc) return rc;
@@ -309,7 +325,8 @@ int sal_hop_sample(const sal_graph* g, const sal_idmap* m, const int64_t* n_dst_
   hk.derive = 0;
   return counted(cuda_status(sal::launch_hop_sample(to_dev(g), d, n_dst_dev, max_dst, fanout, hk, nullptr,
                                             rng_policy, inject_pos, dst_indptr, src_glob, slot,
-                                            draws_out, (cudaStream_t)stream),
+                                            draws_out, (cudaStream_t)stream, lanes,
+                                            blocks_per_sm),
                      "hop_sample"), 1);
 }
 

@@ -403,13 +403,17 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
                               int64_t max_dst, int32_t fanout, HopKey hk, const BatchDesc* desc,
                               int32_t policy, const int64_t* inject_pos,
                               const int32_t* dst_indptr, int32_t* src_glob, int32_t* slot,
-                              int32_t* draws_out, cudaStream_t st) {
+                              int32_t* draws_out, cudaStream_t st, int lanes,
+                              int blocks_per_sm) {
   const int64_t warps_needed = max_dst > 0 ? max_dst : 1;
   int64_t grid = (warps_needed + 7) / 8;
-  const int64_t cap = (int64_t)num_sms() * 8;  // 8 blocks x 8 warps per SM, grid-stride
+  // default 8 blocks x 8 warps per SM, grid-stride
+  const int64_t cap = (int64_t)num_sms() * (blocks_per_sm > 0 ? blocks_per_sm : 8);
   if (grid > cap) grid = cap;
-  // lanes per destination: the smallest group that holds the fanout
-  const int G = fanout <= 8 ? 8 : (fanout <= 16 ? 16 : 32);
+  // lanes per destination: by default the smallest group that holds the fanout
+  const int G = lanes == 8 || lanes == 16 || lanes == 32
+                    ? lanes
+                    : (fanout <= 8 ? 8 : (fanout <= 16 ? 16 : 32));
   grid = (warps_needed * G / 32 + 7) / 8;
   if (grid < 1) grid = 1;
   if (grid > cap) grid = cap;

@@ -51,7 +51,8 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
                               int64_t max_dst, int32_t fanout, HopKey hk, const BatchDesc* desc,
                               int32_t policy, const int64_t* inject_pos,
                               const int32_t* dst_indptr, int32_t* src_glob, int32_t* slot,
-                              int32_t* draws_out, cudaStream_t st);
+                              int32_t* draws_out, cudaStream_t st, int lanes = 0,
+                              int blocks_per_sm = 0);
 cudaError_t launch_rehash(const IdMapDev& m, int64_t n, cudaStream_t st);
 cudaError_t launch_keys_insert(const int64_t* keys, int64_t n, const IdMapDev& m,
                                int32_t* src_glob, int32_t* slot, int64_t* e_total,

@@ -349,7 +349,8 @@ class MfgWorkspace:
     """
 
     def __init__(self, num_nodes: int, fanouts: FanoutSpec, max_seeds: int, device=None,
-                 last_hop_edges: bool = False):
+                 last_hop_edges: bool = False, sample_lanes: int = 0, sample_bps: int = 0,
+                 table_factor: int = 1):
         """last_hop_edges: SAL_MFG_LAST_HOP_EDGES — the last hop only emits global
         source ids (src_glob); its relabel is skipped (training with the
         layer-0 mean read straight from the feature table)."""
@@ -366,6 +367,12 @@ class MfgWorkspace:
         _lib.check(L.sal_mfg_plan_init_ex(ctypes.byref(self.plan), self.num_hops, per,
                                           self.max_seeds, int(num_nodes), flags),
                    "mfg_plan_init")
+        # design-space knobs (tools/sweep.py): sampler launch shape, id-table load
+        if table_factor < 1 or table_factor & (table_factor - 1):
+            raise ValueError("table_factor must be a power of two")
+        self.plan.sample_lanes = int(sample_lanes)
+        self.plan.sample_blocks_per_sm = int(sample_bps)
+        self.plan.table_cap = int(self.plan.table_cap) * int(table_factor)
         self.layout = _lib.SalMfgLayout()
         _lib.check(L.sal_mfg_layout_init(ctypes.byref(self.plan), ctypes.byref(self.layout)),
                    "mfg_layout_init")

@@ -53,6 +53,9 @@ class TrainConfig:
     tc_wgrad: bool = True          # tcgen05 weight gradients where the shapes allow
     late_prep: bool = True         # labels + reverse adjacency built beside the forward pass
     prep_mean0: bool = False       # gather-free: layer-0 mean on the prep stream (measured slower)
+    sampler_lanes: int = 0         # lanes per destination (0 = smallest group holding the fanout)
+    sampler_bps: int = 0           # sampler grid cap in blocks per SM (0 = 8)
+    table_factor: int = 1          # id-table capacity multiplier (lower load, fewer probes)
 
 
 def shard_plan(plan, batch_size: int, rank: int, world: int):
@@ -94,7 +97,8 @@ class _Slot:
     def __init__(self, dg: DeviceGraph, cfg: TrainConfig, device, backward: bool = True):
         # gather-free: layer 0 reads rows by global id, so the last hop needs no relabel
         self.ws = MfgWorkspace(dg.num_nodes, cfg.fanouts, cfg.batch_size, device=device,
-                               last_hop_edges=cfg.gather_free)
+                               last_hop_edges=cfg.gather_free, sample_lanes=cfg.sampler_lanes,
+                               sample_bps=cfg.sampler_bps, table_factor=cfg.table_factor)
         ws = self.ws
         nh = ws.num_hops
         rows = ws.node_cap[-1] if not cfg.gather_free else ws.node_cap[-2]

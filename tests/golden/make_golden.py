@@ -267,7 +267,46 @@ def gen_files():
     save("files", **out)
 
 
+def gen_trace():
+    """f3 hop replay: a TRCE file written by the reference's record_trace
+    (bench.py:46-79), the digest its replay_variant computes (bench.py:104-139)
+    and the errors load_trace raises on malformed copies."""
+    import tempfile
+    from mfgprep import bench as RB
+    d = OUT / "files"
+    d.mkdir(exist_ok=True)
+    g = M.synth_graph(5000, 9, 3.0, seed=8)
+    batches = M.make_epoch_plan(np.arange(0, 5000, 3), 128, 2).batches[:4]
+
+    class _Plan:  # record_trace only reads plan.batches
+        pass
+    p = _Plan()
+    p.batches = batches
+    tr = RB.record_trace(g, p, M.FanoutSpec((15, 10, 5)), 11, path=d / "trace.trce")
+    rep = RB.replay_variant(tr, g, M.SamplerVariant(), repetitions=1, warmup=False)
+    good = (d / "trace.trce").read_bytes()
+    errs = []
+    with tempfile.TemporaryDirectory() as td:
+        for tag, data in (("badmagic", b"XXXX" + good[4:]),
+                          ("badversion", good[:4] + (2).to_bytes(4, "little") + good[8:]),
+                          ("trunc10", good[:10]), ("trunc40", good[:40]),
+                          ("trunc60", good[:60]), ("truncm1", good[:-1])):
+            q = Path(td) / tag
+            q.write_bytes(data)
+            try:
+                RB.load_trace(q)
+                errs.append((tag, "", ""))
+            except Exception as e:  # noqa: BLE001
+                errs.append((tag, type(e).__name__, str(e)))
+    save("trace", digest=np.array(rep.digest), checksum=np.array(g.checksum(), dtype=np.int64),
+         indptr=g.indptr, indices=g.indices.astype(np.int32),
+         batch_ids=np.array([b.batch_id for b in batches]),
+         seeds=np.concatenate([b.dst_ids for b in batches]),
+         nrec=np.array(len(tr.records)), errors=np.array(errs))
+
+
 if __name__ == "__main__":
+    gen_trace()
     gen_files()
     gen_rng()
     gen_graphs()
