@@ -30,6 +30,15 @@ SAL_DEVINL uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// Dropout stream of the training step (relu_dropout_fwd_kernel and the fused
+// tcgen05 epilogue must agree).  General p: 16 bits of uniform per element,
+// two splitmix64 draws per group of 8 elements.  p == 0.5 exactly (the
+// paper's setting): one keep bit per element, 64 elements per draw —
+// keep(e) = bit (e % 64) of dropout_word64(key, e / 64), e = row * cols + col.
+SAL_DEVINL uint64_t dropout_word64(uint64_t key_base, uint64_t e64) {
+  return mix64(key_base ^ 0x6A09E667F3BCC909ull ^ (e64 * 0xD1B54A32D192ED03ull));
+}
+
 __host__ __device__ inline uint64_t mix64_hd(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;

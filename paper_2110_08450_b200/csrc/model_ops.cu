@@ -95,6 +95,20 @@ __global__ void relu_dropout_fwd_kernel(const T* __restrict__ x, int64_t sx, T* 
     const int c = (int)(i - r * c8) * 8;
     float v[8];
     ld8<T>(x + (int64_t)r * sx + c, v);
+    if (p == 0.5f) {  // one keep bit per element (common.cuh dropout_word64)
+      const uint32_t keep =
+          (uint32_t)(dropout_word64(key_base, (uint64_t)(i >> 3)) >> (8 * (i & 7))) & 0xFFu;
+      uint8_t bits = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool on = ((keep >> j) & 1u) && v[j] > 0.f;
+        bits |= (uint8_t)on << j;
+        v[j] = on ? v[j] * 2.f : 0.f;
+      }
+      st8<T>(y + (int64_t)r * sy + c, v);
+      mask[i] = bits;
+      continue;
+    }
     // dropout stream: two splitmix64 draws per 8 elements, keyed on
     // (seed, step salt, element group) — 16 bits of uniform per element
     uint64_t r0 = ~0ull, r1 = ~0ull;

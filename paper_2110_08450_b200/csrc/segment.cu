@@ -36,6 +36,16 @@ template <> struct Cvt<__nv_bfloat16> {
   static SAL_DEVINL __nv_bfloat16 out(float v) { return __float2bfloat16_rn(v); }
 };
 
+// acc[0..7] += the 8 16-bit values packed in v (convert, then fp32 add).  The
+// sm_100 mixed-precision add.rn.f32.{f16,bf16} (FHADD) halves the instruction
+// count but measured 5% slower on the layer-0 mean (40.1 vs 38.3 us).
+template <typename T>
+SAL_DEVINL void acc_row8(float* acc, const uint4& v) {
+  const T* t = reinterpret_cast<const T*>(&v);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] += Cvt<T>::in(t[j]);
+}
+
 template <typename T, int V>
 SAL_DEVINL void load_row(const T* p, float* f) {
   constexpr int B = V * (int)sizeof(T);
@@ -203,11 +213,7 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          if (e0 + u * RPI + grp < end) {
-            const TIn* v = reinterpret_cast<const TIn*>(&buf[u]);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] += Cvt<TIn>::in(v[j]);
-          }
+          if (e0 + u * RPI + grp < end) acc_row8<TIn>(acc, buf[u]);
         }
       }
 #pragma unroll
@@ -221,6 +227,113 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
       }
     }
     if (grp == 0) store_row<TOut, 8>(out + (int64_t)d * out_stride + sub * 8, acc);
+  }
+}
+
+// Software-pipelined variant for wide rows (LPR >= 8: 2-4 rows per warp
+// instruction).  Per destination the plain kernel pays three dependent memory
+// latencies (indptr -> source ids -> rows) for one round of row loads; here
+// the source ids of destination d+W and the row pointers of d+2W are loaded
+// while d's rows are in flight, so the steady state waits on the row loads
+// alone.  Same summation order as segment_mean_rows_kernel.
+template <typename TIn, typename TOut, int LPR, bool kGlobal>
+__global__ void __launch_bounds__(kSegThreads, 3)
+segment_mean_rows_pipe_kernel(const int32_t* __restrict__ indptr,
+                              const int32_t* __restrict__ src,
+                              const int32_t* __restrict__ globals,
+                              const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
+                              const TIn* __restrict__ h, int64_t h_stride,
+                              TOut* __restrict__ out, int64_t out_stride) {
+  constexpr int RPI = 32 / LPR;
+  constexpr int kU = 8;
+  constexpr int W = RPI * kU;  // edges per round
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / LPR, sub = lane % LPR;
+  const int n_dst = (int)(n_dst_dev ? *n_dst_dev : n_pad);
+  const int npad = (int)n_pad;
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  int d = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (d >= npad) return;
+  int beg = 0, end = 0;
+  if (d < n_dst) {
+    beg = __ldg(indptr + d);
+    end = __ldg(indptr + d + 1);
+  }
+  int ids[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int e = beg + u * RPI + grp;
+    ids[u] = e < end ? load_id<kGlobal>(src, globals, e) : 0;
+  }
+  int dn = d + nwarps, nbeg = 0, nend = 0;
+  if (dn < n_dst) {
+    nbeg = __ldg(indptr + dn);
+    nend = __ldg(indptr + dn + 1);
+  }
+  while (true) {
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    uint4 buf[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (beg + u * RPI + grp < end) {
+        const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + (int64_t)ids[u] * h_stride) + sub);
+        buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
+      }
+    }
+    // next destination's first-round ids and the row pointers after it
+    int nids[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = nbeg + u * RPI + grp;
+      nids[u] = e < nend ? load_id<kGlobal>(src, globals, e) : 0;
+    }
+    const int dnn = dn + nwarps;
+    int nnbeg = 0, nnend = 0;
+    if (dnn < n_dst) {
+      nnbeg = __ldg(indptr + dnn);
+      nnend = __ldg(indptr + dnn + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (beg + u * RPI + grp < end) acc_row8<TIn>(acc, buf[u]);
+    }
+    // rare: destinations with more than W edges finish unpipelined
+    for (int e0 = beg + W; e0 < end; e0 += W) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * RPI + grp;
+        if (e < end) {
+          const int64_t s = load_id<kGlobal>(src, globals, e);
+          const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + s * h_stride) + sub);
+          buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (e0 + u * RPI + grp < end) acc_row8<TIn>(acc, buf[u]);
+      }
+    }
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+    if (end > beg) {
+      const float inv = 1.f / (float)(end - beg);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] *= inv;
+    }
+    if (grp == 0) store_row<TOut, 8>(out + (int64_t)d * out_stride + sub * 8, acc);
+    d = dn;
+    if (d >= npad) break;
+    beg = nbeg;
+    end = nend;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) ids[u] = nids[u];
+    dn = dnn;
+    nbeg = nnbeg;
+    nend = nnend;
   }
 }
 
@@ -295,9 +408,25 @@ static bool fwd_rows(const int32_t* indptr, const int32_t* src, const int32_t* g
   if (h_stride % 8 != 0 || out_stride % 8 != 0 || ((uintptr_t)h % 16) != 0 ||
       ((uintptr_t)out % 16) != 0)
     return false;
-  const int grid = seg_grid(n_pad);
   const TIn* hp = (const TIn*)h;
   TOut* op = (TOut*)out;
+  if (lpr >= 8) {  // software-pipelined (tools/l0mean_bench.py: 42.3 -> 38.3 us)
+    int64_t blocks = (n_pad + 7) / 8;
+    const int64_t cap = (int64_t)num_sms() * 3;  // one resident wave
+    if (blocks > cap) blocks = cap;
+    const int g = (int)(blocks < 1 ? 1 : blocks);
+    if (lpr == 8)
+      segment_mean_rows_pipe_kernel<TIn, TOut, 8, kGlobal><<<g, kSegThreads, 0, st>>>(
+          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);
+    else if (lpr == 16)
+      segment_mean_rows_pipe_kernel<TIn, TOut, 16, kGlobal><<<g, kSegThreads, 0, st>>>(
+          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);
+    else
+      segment_mean_rows_pipe_kernel<TIn, TOut, 32, kGlobal><<<g, kSegThreads, 0, st>>>(
+          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);
+    return true;
+  }
+  const int grid = seg_grid(n_pad);
 #define SAL_ROWS_CASE(L)                                                                     \
   case L:                                                                                    \
     segment_mean_rows_kernel<TIn, TOut, L, kGlobal><<<grid, kSegThreads, 0, st>>>(            \

@@ -2,16 +2,16 @@
 //
 // Forward:  y = relu_dropout( A[M, K] @ W[N, K]^T )  with A the layer-0 "cat"
 //           buffer [mean | h_dst] (bf16, K = 2f = 256) and W = [W_neigh |
-//           W_self] (N = 256).  One CTA per SM, persistent over 128-row tiles;
-//           W stays resident in shared memory (128 KB, loaded once), each A
-//           tile (64 KB) is fetched with cp.async into the 128-byte-swizzled
-//           K-major layout the UMMA descriptor describes, one elected thread
-//           issues 16 tcgen05.mma (M=128, N=256, K=16) into a TMEM accumulator,
-//           tcgen05.commit signals an mbarrier, and the epilogue (8 warps,
-//           tcgen05.ld 32x32b) applies ReLU + dropout, writes bf16 rows into the
-//           next layer's cat buffer and the keep/relu bit mask — the GEMM output
-//           never round-trips through HBM.  The next tile's cp.async is issued
-//           before the epilogue so the copy overlaps it.
+//           W_self] (N = 256).  Production kernel (sage_fwd_tma_st_kernel):
+//           one CTA per SM, persistent over 128-row tiles; warp 0 streams A
+//           K-blocks with TMA into a 4-stage SWIZZLE_128B ring (W stays
+//           resident, 128 KB, loaded once); warp 1 issues tcgen05.mma (M=128,
+//           N=256, K=16) into one of two TMEM accumulators; 16 epilogue warps
+//           drain TMEM (tcgen05.ld 32x32b), apply ReLU + dropout, stage bf16
+//           32x32 chunks in shared memory and write them with TMA bulk tensor
+//           stores, plus the keep/relu bit mask — the GEMM output never
+//           round-trips through HBM.  sage_fwd_kernel is the single-warpgroup
+//           cp.async version kept as a reference point (tools/tc_bench.py).
 //
 // Weight gradient: dW[N, K] += dz[M, N]^T @ A[M, K] with both operands read
 //           MN-major (row-major in HBM): each CTA reduces a contiguous range of
@@ -118,6 +118,54 @@ constexpr uint32_t kBBytes = kFN * kFK * 2;     // 128 KB
 constexpr uint32_t kABytes = kFM * kFK * 2;     // 64 KB
 constexpr uint32_t kFSmem = kBBytes + kABytes + 1024 + 64;
 
+// Epilogue element math shared by the forward kernels: 32 consecutive fp32
+// accumulator columns [c, c+32) of one row -> relu + dropout (scaled) in bf16
+// plus the 32 keep bits; the dropout stream is relu_dropout_fwd_kernel's
+// (common.cuh dropout_word64 for p == 0.5, 16-bit uniforms otherwise).
+SAL_DEVINL uint32_t relu_dropout32(const uint32_t* r, int64_t row, int c, int relu_dropout,
+                                   float p, float scale, uint32_t thresh, uint64_t key_base,
+                                   __nv_bfloat16* o) {
+  uint32_t bits = 0;
+  if (!relu_dropout) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+    return 0;
+  }
+  if (p == 0.5f) {  // one draw covers the 32 columns
+    const uint64_t e0 = (uint64_t)row * kFN + (uint64_t)c;
+    const uint32_t keep = (uint32_t)(dropout_word64(key_base, e0 >> 6) >> (e0 & 63));
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float v = __uint_as_float(r[j]);
+      const bool on = ((keep >> j) & 1u) && v > 0.f;
+      bits |= (uint32_t)on << j;
+      o[j] = __float2bfloat16_rn(on ? v * 2.f : 0.f);
+    }
+    return bits;
+  }
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    uint64_t r0 = ~0ull, r1 = ~0ull;
+    if (p > 0.f) {  // group i = row * 32 + col / 8
+      const uint64_t i = (uint64_t)row * (kFN / 8) + (uint64_t)((c >> 3) + g);
+      const uint64_t kk = key_base ^ (i * 0xD1B54A32D192ED03ull);
+      r0 = mix64(kk);
+      r1 = mix64(kk + kGolden);
+    }
+    const uint32_t rr[4] = {(uint32_t)r0, (uint32_t)(r0 >> 32), (uint32_t)r1,
+                            (uint32_t)(r1 >> 32)};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = __uint_as_float(r[g * 8 + j]);
+      const uint32_t u16 = (rr[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+      const bool on = (u16 >= thresh) && v > 0.f;
+      bits |= (uint32_t)on << (g * 8 + j);
+      o[g * 8 + j] = __float2bfloat16_rn(on ? v * scale : 0.f);
+    }
+  }
+  return bits;
+}
+
 // load a [rows x 256] bf16 row-major block into 4 K-major SW128 K-block tiles
 SAL_DEVINL void load_kmajor(uint32_t sbase, const __nv_bfloat16* g, int64_t ldg, int rows,
                             int valid_rows, int tid, int nthreads) {
@@ -210,38 +258,13 @@ sage_fwd_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda, int M,
       if (row < M) {
         const int c = col0 + cc;
         alignas(16) __nv_bfloat16 o[32];
-        uint8_t bits[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          // dropout stream identical to relu_dropout_fwd_kernel: group i = row*32 + col/8
-          uint64_t r0 = ~0ull, r1 = ~0ull;
-          if (relu_dropout && p > 0.f) {
-            const uint64_t i = (uint64_t)row * (kFN / 8) + (uint64_t)((c >> 3) + g);
-            const uint64_t kk = key_base ^ (i * 0xD1B54A32D192ED03ull);
-            r0 = mix64(kk);
-            r1 = mix64(kk + kGolden);
-          }
-          const uint32_t rr[4] = {(uint32_t)r0, (uint32_t)(r0 >> 32), (uint32_t)r1,
-                                  (uint32_t)(r1 >> 32)};
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float v = __uint_as_float(r[g * 8 + j]);
-            if (relu_dropout) {
-              const uint32_t u16 = (rr[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
-              const bool on = (u16 >= thresh) && v > 0.f;
-              bits[g] |= (uint8_t)on << j;
-              v = on ? v * scale : 0.f;
-            }
-            o[g * 8 + j] = __float2bfloat16_rn(v);
-          }
-        }
+        const uint32_t bits =
+            relu_dropout32(r, row, c, relu_dropout, p, scale, thresh, key_base, o);
         uint4* dst = reinterpret_cast<uint4*>(Y + (int64_t)row * ldy + c);
 #pragma unroll
         for (int q = 0; q < 4; ++q) dst[q] = reinterpret_cast<const uint4*>(o)[q];
         if (relu_dropout)
-          *reinterpret_cast<uint32_t*>(mask + (int64_t)row * (kFN / 8) + (c >> 3)) =
-              (uint32_t)bits[0] | ((uint32_t)bits[1] << 8) | ((uint32_t)bits[2] << 16) |
-              ((uint32_t)bits[3] << 24);
+          *reinterpret_cast<uint32_t*>(mask + (int64_t)row * (kFN / 8) + (c >> 3)) = bits;
       }
     }
     tc_fence_before();
@@ -404,46 +427,69 @@ SAL_DEVINL bool elect_one() {
   return pred != 0;
 }
 
-// forward: warp 0 = TMA producer, warp 1 = MMA issuer, warps 2..9 = epilogue
-// (two warps per TMEM lane group, each draining half of the 256 columns)
-constexpr int kPStages = 5;                      // A K-block ring (16 KB each)
-constexpr int kPThreads = 320;
-constexpr int kPEpiWarps = 8;
-constexpr uint32_t kPABlk = kFM * kFKB * 2;      // 16 KB
-constexpr uint32_t kPSmem = kBBytes + kPStages * kPABlk + 1024 + 256;
+// A K-block of the TMA forward: 128 rows x 64 K (16 KB, SWIZZLE_128B)
+constexpr uint32_t kPABlk = kFM * kFKB * 2;
 
-__global__ void __launch_bounds__(kPThreads, 1)
-sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
-                    const __grid_constant__ CUtensorMap mapW, int M,
-                    __nv_bfloat16* __restrict__ Y, int64_t ldy, uint8_t* __restrict__ mask,
-                    float p, uint64_t seed, const int64_t* __restrict__ salt, int relu_dropout) {
+// forward v2: the epilogue stores through shared memory with TMA.  In v1 each
+// epilogue lane writes its own TMEM row straight to HBM (st.global.v4 of 32
+// different rows per instruction), so every store request costs 32 L1 tag
+// cycles: 2.7 M of them per launch, ~9.6 us per SM at papers shape (ncu).
+// Here each warp converts a 32-row x 32-column chunk, writes it into a 2 KB
+// SWIZZLE_64B staging tile (conflict-free 16-byte shared stores) and one lane
+// issues a bulk tensor store.  16 epilogue warps (4 per SM sub-partition,
+// v1 had 2) hide the tcgen05.ld and RNG latency; the A ring keeps 4 K-blocks
+// (one full tile) in flight.
+constexpr int kSStages = 4;
+constexpr int kSEpiWarps = 16;
+constexpr int kSThreads = (2 + kSEpiWarps) * 32;
+constexpr uint32_t kSStage = 32 * 32 * 2;         // 2 KB staging per epilogue warp
+constexpr uint32_t kSSmem = kBBytes + kSStages * kPABlk + kSEpiWarps * kSStage + 1024 + 256;
+
+SAL_DEVINL void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+      "r"(src), "r"(c0), "r"(c1)
+      : "memory");
+}
+SAL_DEVINL void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+SAL_DEVINL void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+SAL_DEVINL void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kSThreads, 1)
+sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
+                       const __grid_constant__ CUtensorMap mapW,
+                       const __grid_constant__ CUtensorMap mapY, int M,
+                       uint8_t* __restrict__ mask, float p, uint64_t seed,
+                       const int64_t* __restrict__ salt, int relu_dropout) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sB = smem;
   uint8_t* sA = smem + kBBytes;
-  uint64_t* bars = (uint64_t*)(sA + kPStages * kPABlk);
-  uint64_t* full = bars;                    // [kPStages]
-  uint64_t* empty = bars + kPStages;        // [kPStages]
-  uint64_t* bfull = bars + 2 * kPStages;    // W resident
-  uint64_t* tfull = bars + 2 * kPStages + 1;   // [2] accumulator ready
-  uint64_t* tempty = bars + 2 * kPStages + 3;  // [2] accumulator drained
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kPStages + 5);
+  uint8_t* sY = sA + kSStages * kPABlk;
+  uint64_t* bars = (uint64_t*)(sY + kSEpiWarps * kSStage);
+  uint64_t* full = bars;                    // [kSStages]
+  uint64_t* empty = bars + kSStages;        // [kSStages]
+  uint64_t* bfull = bars + 2 * kSStages;    // W resident
+  uint64_t* tfull = bars + 2 * kSStages + 1;   // [2] accumulator ready
+  uint64_t* tempty = bars + 2 * kSStages + 3;  // [2] accumulator drained
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kSStages + 5);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (M + kFM - 1) / kFM;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < kPStages; ++i) {
+    for (int i = 0; i < kSStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     mbar_init(bfull, 1);
     mbar_init(&tfull[0], 1);
     mbar_init(&tfull[1], 1);
-    mbar_init(&tempty[0], kPEpiWarps);
-    mbar_init(&tempty[1], kPEpiWarps);
+    mbar_init(&tempty[0], kSEpiWarps);
+    mbar_init(&tempty[1], kSEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapY) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -458,7 +504,6 @@ sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
 
   if (warp == 0) {
     if (elect_one()) {
-      // resident weights: 4 K-blocks of [256 rows x 64]
       mbar_expect_tx(bfull, kBBytes);
 #pragma unroll
       for (int kb = 0; kb < kFK / kFKB; ++kb)
@@ -470,7 +515,7 @@ sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
           mbar_wait(&empty[stage], ph ^ 1);
           mbar_expect_tx(&full[stage], kPABlk);
           tma_load_2d(smem_u32(sA) + stage * kPABlk, &mapA, kb * kFKB, t * kFM, &full[stage]);
-          if (++stage == kPStages) { stage = 0; ph ^= 1; }
+          if (++stage == kSStages) { stage = 0; ph ^= 1; }
         }
       }
     }
@@ -483,7 +528,7 @@ sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int buf = it & 1;
       const uint32_t tph = (uint32_t)((it >> 1) & 1);
-      mbar_wait(&tempty[buf], tph ^ 1);  // epilogue drained this accumulator
+      mbar_wait(&tempty[buf], tph ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < kFK / kFKB; ++kb) {
         mbar_wait(&full[stage], ph);
@@ -499,13 +544,16 @@ sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
           if (kb == kFK / kFKB - 1) mma_commit(&tfull[buf]);
         }
         __syncwarp();
-        if (++stage == kPStages) { stage = 0; ph ^= 1; }
+        if (++stage == kSStages) { stage = 0; ph ^= 1; }
       }
     }
   } else {
-    // epilogue warps 2..9 -> TMEM lane group (warp % 4), column half (warp - 2) / 4
+    // epilogue warp e = 0..15: TMEM lane group (warp % 4), column quarter e / 4
+    const int e = warp - 2;
     const int lg = warp & 3;
-    const int chalf = (warp - 2) >> 2;
+    const int cq = e >> 2;
+    uint8_t* stg = sY + e * kSStage;
+    const uint32_t stg_s = smem_u32(stg);
     const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
     const uint32_t thresh = (uint32_t)(p * 65536.0f);
     const uint64_t key_base = mix64(seed ^ mix64((salt ? (uint64_t)*salt : 0ull) + 0x5EEDull));
@@ -514,50 +562,37 @@ sage_fwd_tma_kernel(const __grid_constant__ CUtensorMap mapA,
       const int buf = it & 1;
       mbar_wait(&tfull[buf], (uint32_t)((it >> 1) & 1));
       tc_fence_after();
-      const int row = t * kFM + lg * 32 + lane;
+      const int row0 = t * kFM + lg * 32;
+      const int row = row0 + lane;
 #pragma unroll 1
-      for (int c = chalf * (kFN / 2); c < (chalf + 1) * (kFN / 2); c += 32) {
+      for (int c = cq * (kFN / 4); c < (cq + 1) * (kFN / 4); c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * 256 + c), r);
-        if (row < M) {
-          alignas(16) __nv_bfloat16 o[32];
-          uint8_t bits[4] = {0, 0, 0, 0};
+        alignas(16) __nv_bfloat16 o[32];
+        const uint32_t bits =
+            relu_dropout32(r, row, c, relu_dropout, p, scale, thresh, key_base, o);
+        // staging tile free again (the previous bulk store has read it)
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        // SWIZZLE_64B: 16-byte chunk q of row `lane` at lane*64 + ((q ^ ((lane>>1)&3)) << 4)
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            uint64_t r0 = ~0ull, r1 = ~0ull;
-            if (relu_dropout && p > 0.f) {
-              const uint64_t i = (uint64_t)row * (kFN / 8) + (uint64_t)((c >> 3) + g);
-              const uint64_t kk = key_base ^ (i * 0xD1B54A32D192ED03ull);
-              r0 = mix64(kk);
-              r1 = mix64(kk + kGolden);
-            }
-            const uint32_t rr[4] = {(uint32_t)r0, (uint32_t)(r0 >> 32), (uint32_t)r1,
-                                    (uint32_t)(r1 >> 32)};
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float v = __uint_as_float(r[g * 8 + j]);
-              if (relu_dropout) {
-                const uint32_t u16 = (rr[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
-                const bool on = (u16 >= thresh) && v > 0.f;
-                bits[g] |= (uint8_t)on << j;
-                v = on ? v * scale : 0.f;
-              }
-              o[g * 8 + j] = __float2bfloat16_rn(v);
-            }
-          }
-          uint4* dst = reinterpret_cast<uint4*>(Y + (int64_t)row * ldy + c);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) dst[q] = reinterpret_cast<const uint4*>(o)[q];
-          if (relu_dropout)
-            *reinterpret_cast<uint32_t*>(mask + (int64_t)row * (kFN / 8) + (c >> 3)) =
-                (uint32_t)bits[0] | ((uint32_t)bits[1] << 8) | ((uint32_t)bits[2] << 16) |
-                ((uint32_t)bits[3] << 24);
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(stg + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+              reinterpret_cast<const uint4*>(o)[q];
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&mapY, stg_s, c, row0);
+          bulk_commit();
         }
+        if (relu_dropout && row < M)
+          *reinterpret_cast<uint32_t*>(mask + (int64_t)row * (kFN / 8) + (c >> 3)) = bits;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
     }
+    if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -684,7 +719,8 @@ sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
-                     uint64_t row_stride_elems, uint32_t box_cols, uint32_t box_rows) {
+                     uint64_t row_stride_elems, uint32_t box_cols, uint32_t box_rows,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   if (g_encode == nullptr) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -699,7 +735,7 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -716,22 +752,25 @@ int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const void* W, int32_
   if (lda % 8 || ldy % 8 || ((uintptr_t)A & 15) || ((uintptr_t)W & 15) || ((uintptr_t)Y & 15))
     return SAL_EINVAL;
   if (M <= 0) return SAL_OK;
-  CUtensorMap mA, mW;
+  CUtensorMap mA, mW, mY;
   if (!sal::tc::make_map(&mA, A, (uint64_t)M, 256, (uint64_t)lda, 64, 128) ||
       !sal::tc::make_map(&mW, W, 256, 256, 256, 64, 256))
     return SAL_ECUDA;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sal::tc::sage_fwd_tma_kernel,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, sal::tc::kPSmem);
-    attr = true;
-  }
   const int ntiles = (int)((M + 127) / 128);
   int grid = sal::num_sms();
   if (grid > ntiles) grid = ntiles;
-  sal::tc::sage_fwd_tma_kernel<<<grid, sal::tc::kPThreads, sal::tc::kPSmem,
-                                 (cudaStream_t)stream>>>(mA, mW, (int)M, (__nv_bfloat16*)Y, ldy,
-                                                         mask, p, seed, salt_dev, relu_dropout);
+  if (!sal::tc::make_map(&mY, Y, (uint64_t)M, 256, (uint64_t)ldy, 32, 32,
+                         CU_TENSOR_MAP_SWIZZLE_64B))
+    return SAL_ECUDA;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sal::tc::sage_fwd_tma_st_kernel,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sal::tc::kSSmem);
+    attr = true;
+  }
+  sal::tc::sage_fwd_tma_st_kernel<<<grid, sal::tc::kSThreads, sal::tc::kSSmem,
+                                    (cudaStream_t)stream>>>(mA, mW, mY, (int)M, mask, p, seed,
+                                                            salt_dev, relu_dropout);
   if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
   sal::count_launch(1);
   return SAL_OK;
