@@ -63,6 +63,9 @@ def parse():
     p.add_argument("--hidden", type=int, default=256)
     p.add_argument("--no-graphs", action="store_true")
     p.add_argument("--prep-priority", type=int, default=-1)
+    p.add_argument("--prep-split", type=int, default=None,
+                   help="three-slot pipeline: hops [0, s) of batch i+2 beside hops [s, L) of "
+                        "batch i+1 (0 = two slots)")
     p.add_argument("--materialise", action="store_true",
                    help="train on the materialised feature gather instead of the gather-free "
                         "layer-0 path")
@@ -337,6 +340,8 @@ def run_ours(args):
     dg, train, test, gen_s = build_data(args.shape)
     cfg = TrainConfig(fanouts=fan, hidden=args.hidden, gather_free=not args.materialise,
                       graphs=not args.no_graphs, prep_priority=args.prep_priority)
+    if args.prep_split is not None:
+        cfg.prep_split = args.prep_split
     tr = Trainer(dg, train, cfg, rank=rank, world=world)
     spe = tr.set_epoch(0)
     K = args.steps if args.steps > 0 else spe
@@ -420,16 +425,18 @@ def run_ours(args):
             "sampled_edges_per_s": kp["sampled_edges_per_s"],
             "gather_GBps": kp["gather_GBps"],
             "kernels": kp,
-            "roofline": {"kernel": "segment_mean_rows_kernel (layer-0 mean over the sampled "
-                                   "edges, rows read from the HBM feature table)",
+            "roofline": {"kernel": "segment_mean_rows_pipe_kernel (layer-0 mean over the "
+                                   "sampled edges, rows read from the HBM feature table)",
                          "bound": "hbm", "achieved": round(kp["l0_mean_GBps"], 1), "peak": peak,
                          "unit": "GB/s", "frac": round(kp["l0_mean_GBps"] / peak, 4),
                          "peak_source": peak_src,
-                         "traffic": ncu_traffic("segment_mean_rows_kernel<__half"),
+                         "traffic": ncu_traffic("segment_mean_rows_pipe_kernel<__half"),
                          "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one "
                                            "layer-0 launch)",
                          "bytes_per_launch": kp["l0_mean_bytes_per_launch"],
-                         "ms_per_launch": kp["l0_mean_ms_per_launch"]},
+                         "ms_per_launch": kp["l0_mean_ms_per_launch"],
+                         "timing": "CUDA events around each launch on its stream, prep + "
+                                   "kernel pass over the epoch's first batches, in this run"},
             "gather_roofline": {"kernel": "gather_rows_warp_kernel (fp16 rows, 128-bit)",
                                 "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                                 "unit": "GB/s", "frac": round(ach / peak, 4),

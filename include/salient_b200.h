@@ -138,6 +138,16 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
                    void* ws_dev, const int64_t* seeds_base_dev, const sal_batch_desc* desc_dev,
                    uint64_t global_seed, int32_t rng_policy, void* stream);
 
+/* Hops [hop_begin, hop_end) of sal_sample_mfg (hop_begin == 0 also resets the
+ * map and inserts the seeds): lets a pipeline run the early hops of batch
+ * i+2 beside the late hops of batch i+1.  Ranges must be issued in order on
+ * one workspace. */
+int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan,
+                         const sal_mfg_layout* layout, void* ws_dev,
+                         const int64_t* seeds_base_dev, const sal_batch_desc* desc_dev,
+                         uint64_t global_seed, int32_t rng_policy, int32_t hop_begin,
+                         int32_t hop_end, void* stream);
+
 /* ---- hop-level operators (the _kernels.py operator layer) --------------- */
 size_t sal_scan_ws_bytes(int64_t max_items);
 /* reset every slot of the map to empty (IdMap.__init__, sampler.py:113-129) */

@@ -78,6 +78,8 @@ SIGNATURES = {
     "sal_mfg_layout_init": (ctypes.c_int, [P(SalMfgPlan), P(SalMfgLayout)]),
     "sal_sample_mfg": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp, vp,
                                       u64, i32, vp]),
+    "sal_sample_mfg_range": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp,
+                                            vp, u64, i32, i32, i32, vp]),
     "sal_scan_ws_bytes": (ctypes.c_size_t, [i64]),
     "sal_idmap_reset": (ctypes.c_int, [P(SalIdMap), vp]),
     "sal_idmap_rehash": (ctypes.c_int, [P(SalIdMap), i64, vp]),

@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "salient_internal.h"
@@ -37,6 +38,22 @@ int fail(int code, const char* fmt, ...) {
 
 }  // namespace
 namespace sal {
+int train_sms() {
+  static const int v = [] {
+    const char* e = getenv("SAL_TRAIN_SMS_RESERVE");
+    const int r = e ? atoi(e) : 0;
+    const int n = num_sms() - r;
+    return n > 1 ? n : 1;
+  }();
+  return v;
+}
+int l0_blocks_per_sm() {
+  static const int v = [] {
+    const char* e = getenv("SAL_L0_BPS");
+    return e ? atoi(e) : 3;
+  }();
+  return v;
+}
 int set_error(int code, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -176,6 +193,15 @@ int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* L) {
 int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
                    void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
                    uint64_t global_seed, int32_t rng_policy, void* stream) {
+  if (plan == nullptr) return fail(SAL_EINVAL, "sample_mfg: null argument");
+  return sal_sample_mfg_range(g, plan, L, ws, seeds_base, desc, global_seed, rng_policy, 0,
+                              plan->num_hops, stream);
+}
+
+int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
+                         void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
+                         uint64_t global_seed, int32_t rng_policy, int32_t hop_begin,
+                         int32_t hop_end, void* stream) {
   if (g == nullptr || plan == nullptr || L == nullptr || ws == nullptr || seeds_base == nullptr ||
       desc == nullptr)
     return fail(SAL_EINVAL, "sample_mfg: null argument");
@@ -196,11 +222,19 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
   int32_t* rank = (int32_t*)(base + L->rank);
   void* scan = base + L->scan;
 
-  cudaError_t e = cudaMemsetAsync(m.table, 0xFF, plan->table_cap * 8, st);
-  if (e != cudaSuccess) return cuda_status(e, "sample_mfg: table reset");
-  e = sal::launch_seed_insert(seeds_base, desc, m, plan->max_seeds, st);
-  if (e != cudaSuccess) return cuda_status(e, "sample_mfg: seed insert");
-  for (int h = 0; h < plan->num_hops; ++h) {
+  if (hop_begin < 0 || hop_end > plan->num_hops || hop_begin > hop_end)
+    return fail(SAL_EINVAL, "sample_mfg: hop range [%d, %d) outside [0, %d]", hop_begin, hop_end,
+                plan->num_hops);
+  cudaError_t e = cudaSuccess;
+  int kernels = 0;
+  if (hop_begin == 0) {
+    e = cudaMemsetAsync(m.table, 0xFF, plan->table_cap * 8, st);
+    if (e != cudaSuccess) return cuda_status(e, "sample_mfg: table reset");
+    e = sal::launch_seed_insert(seeds_base, desc, m, plan->max_seeds, st);
+    if (e != cudaSuccess) return cuda_status(e, "sample_mfg: seed insert");
+    kernels = 1;
+  }
+  for (int h = hop_begin; h < hop_end; ++h) {
     int32_t* dst_indptr = (int32_t*)(base + L->dst_indptr[h]);
     int32_t* src_local = (int32_t*)(base + L->src_local[h]);
     e = sal::launch_hop_count(gd, m.globals, sizes + h, plan->node_cap[h], plan->fanout[h],
@@ -221,7 +255,7 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
                                  desc, rng_policy, nullptr, dst_indptr, src_glob, nullptr,
                                  nullptr, st, plan->sample_lanes, plan->sample_blocks_per_sm);
       if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
-      return counted(SAL_OK, 4 * plan->num_hops - 1);
+      return counted(SAL_OK, kernels + 2);
     }
     e = sal::launch_hop_sample(gd, m, sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
                                rng_policy, nullptr, dst_indptr, src_glob, slot, nullptr, st,
@@ -230,8 +264,9 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
     e = sal::launch_hop_relabel(m, etot + h, plan->edge_cap[h], sizes + h, sizes + h + 1,
                                 src_glob, slot, rank, src_local, scan, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop relabel");
+    kernels += 4;
   }
-  return counted(SAL_OK, 1 + 4 * plan->num_hops);
+  return counted(SAL_OK, kernels);
 }
 
 // ---------------------------------------------------------------------------

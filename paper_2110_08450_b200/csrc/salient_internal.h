@@ -36,6 +36,10 @@ struct HopKey {
 };
 
 int num_sms();
+// experiment knobs (env, read once): SMs the persistent training kernels use,
+// blocks per SM of the layer-0 mean
+int train_sms();
+int l0_blocks_per_sm();
 // thread-local error message of sal_last_error(); returns `code`
 int set_error(int code, const char* fmt, ...);
 void count_launch(int kernels);

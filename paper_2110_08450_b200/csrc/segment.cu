@@ -17,6 +17,8 @@
 // input is the (frozen) feature table.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "salient_internal.h"
 
@@ -412,8 +414,13 @@ static bool fwd_rows(const int32_t* indptr, const int32_t* src, const int32_t* g
   TOut* op = (TOut*)out;
   if (lpr >= 8) {  // software-pipelined (tools/l0mean_bench.py: 42.3 -> 38.3 us)
     int64_t blocks = (n_pad + 7) / 8;
-    const int64_t cap = (int64_t)num_sms() * 3;  // one resident wave
-    if (blocks > cap) blocks = cap;
+    const int64_t cap = (int64_t)num_sms() * l0_blocks_per_sm();  // one resident wave
+    static const int dpw = [] {
+      const char* e = getenv("SAL_L0_DPW");
+      return e ? atoi(e) : 0;
+    }();
+    if (dpw > 0) blocks = (n_pad + 8 * dpw - 1) / (8 * dpw);  // short-lived blocks
+    else if (blocks > cap) blocks = cap;
     const int g = (int)(blocks < 1 ? 1 : blocks);
     if (lpr == 8)
       segment_mean_rows_pipe_kernel<TIn, TOut, 8, kGlobal><<<g, kSegThreads, 0, st>>>(

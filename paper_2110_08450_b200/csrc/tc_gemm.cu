@@ -757,7 +757,7 @@ int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const void* W, int32_
       !sal::tc::make_map(&mW, W, 256, 256, 256, 64, 256))
     return SAL_ECUDA;
   const int ntiles = (int)((M + 127) / 128);
-  int grid = sal::num_sms();
+  int grid = sal::train_sms();
   if (grid > ntiles) grid = ntiles;
   if (!sal::tc::make_map(&mY, Y, (uint64_t)M, 256, (uint64_t)ldy, 32, 32,
                          CU_TENSOR_MAP_SWIZZLE_64B))
@@ -823,7 +823,7 @@ int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, i
   // one CTA per SM: tiles x splits ~ #SMs, splits of whole 64-row chunks
   const int tiles_k = K / 128;
   const int tiles = (N / 128) * tiles_k;
-  int splits = sal::num_sms() / tiles;
+  int splits = sal::train_sms() / tiles;
   if (splits < 1) splits = 1;
   int rows = (int)((M + splits - 1) / splits);
   rows = (rows + 63) / 64 * 64;

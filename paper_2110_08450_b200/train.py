@@ -56,6 +56,8 @@ class TrainConfig:
     sampler_lanes: int = 0         # lanes per destination (0 = smallest group holding the fanout)
     sampler_bps: int = 0           # sampler grid cap in blocks per SM (0 = 8)
     table_factor: int = 1          # id-table capacity multiplier (lower load, fewer probes)
+    prep_split: int = 0            # 0: two-slot pipeline; s in [1, L): three slots, hops [0, s)
+                                   # of batch i+2 run beside hops [s, L) of batch i+1
 
 
 def shard_plan(plan, batch_size: int, rank: int, world: int):
@@ -154,8 +156,15 @@ class Trainer:
             torch.distributed.broadcast(self.model.flat, src=0)
             self.model.refresh_shadow()
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
-        self.slots = [_Slot(dg, cfg, self.device) for _ in range(2)]
-        self.staging = [_Staging(cfg.batch_size) for _ in range(4)]
+        if not 0 <= cfg.prep_split < self.nh:
+            raise ValueError(f"prep_split must be in [0, {self.nh})")
+        # pipeline depth: batches in flight (trained, tail-prepared, head-prepared)
+        self.depth = 3 if cfg.prep_split else 2
+        self.slots = [_Slot(dg, cfg, self.device) for _ in range(self.depth)]
+        self.ring = 2 * self.depth   # pinned staging buffers of the end-to-end path
+        self.staging = [_Staging(cfg.batch_size) for _ in range(self.ring)]
+        self.head_stream = torch.cuda.Stream(device=self.device, priority=cfg.prep_priority) \
+            if cfg.prep_split else None
         # high priority: the prep chain is latency-bound (many small dependent kernels), so
         # it should take SMs first as the bandwidth-bound training kernels drain
         self.prep_stream = torch.cuda.Stream(device=self.device, priority=cfg.prep_priority)
@@ -213,6 +222,14 @@ class Trainer:
     def _prep(self, slot: _Slot, stage: "_Staging | None", late: bool = False) -> None:
         """Enqueue one batch preparation on the current stream (capturable): seeds ->
         MFG -> layer-0 feature rows, plus (late=True) what _prep_late builds."""
+        self._prep_head(slot, stage, whole=True)
+        self._prep_tail(slot, stage is not None, whole=True)
+        if late:
+            self._prep_late(slot, stage is not None)
+
+    def _prep_head(self, slot: _Slot, stage: "_Staging | None", whole: bool = False) -> None:
+        """Seeds + descriptor of the next batch and its hops [0, prep_split) (all
+        hops when `whole`)."""
         ws = slot.ws
         st = torch.cuda.current_stream()
         L = _lib.lib()
@@ -225,7 +242,19 @@ class Trainer:
                                        self.cursor.data_ptr(), slot.desc.data_ptr(),
                                        _lib.stream_ptr(st)), "plan_next")
             seeds_base = self.seeds_all
-        ws.run(self.dg, seeds_base, slot.desc, self.cfg.global_seed, self.policy, st)
+        ws.run(self.dg, seeds_base, slot.desc, self.cfg.global_seed, self.policy, st,
+               hops=None if whole else (0, self.cfg.prep_split))
+
+    def _prep_tail(self, slot: _Slot, host_inputs: bool = False, whole: bool = False) -> None:
+        """Hops [prep_split, L) (none when `whole`: _prep_head ran them all) and the
+        layer-0 rows."""
+        ws = slot.ws
+        st = torch.cuda.current_stream()
+        L = _lib.lib()
+        if not whole:
+            seeds_base = slot.seeds if host_inputs else self.seeds_all  # unread past hop 0
+            ws.run(self.dg, seeds_base, slot.desc, self.cfg.global_seed, self.policy, st,
+                   hops=(self.cfg.prep_split, self.nh))
         nh = self.nh
         rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
         n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
@@ -242,8 +271,6 @@ class Trainer:
                 _lib.dtype_code(self.x_table.dtype), self.x_table.stride(0), f, a0.data_ptr(),
                 _lib.dtype_code(a0.dtype), a0.stride(0), _lib.stream_ptr(st)),
                 "segment_mean_fwd(table)")
-        if late:
-            self._prep_late(slot, stage is not None)
 
     def _prep_late(self, slot: _Slot, host_inputs: bool) -> None:
         """The inputs only the loss / backward read: labels and the reverse adjacency
@@ -299,9 +326,12 @@ class Trainer:
                                                 _lib.stream_ptr()), "step_tail")
 
     def _pair(self, k: int, host_inputs: bool, part: str = "all") -> None:
-        """{prep(slot k+1) on the prep stream || train(slot k)} on the current stream."""
+        """{prep(slot k+1) on the prep stream || train(slot k)} on the current stream.
+
+        Depth 3 (prep_split): {head(slot k+2) || tail(slot k+1) || train(slot k)}."""
+        D = self.depth
         if part == "post":
-            self._train(self.slots[k % 2], "post")
+            self._train(self.slots[k % D], "post")
             return
         cs = torch.cuda.current_stream()
         ps = self.prep_stream or cs  # None: prep serialised on the compute stream
@@ -312,12 +342,26 @@ class Trainer:
             ls = self.late_stream
             ls.wait_stream(cs)
             with torch.cuda.stream(ls):
-                self._prep_late(self.slots[k % 2], host_inputs)
-        with torch.cuda.stream(ps):
-            self._prep(self.slots[(k + 1) % 2],
-                       self.staging[(k + 1) % 4] if host_inputs else None, late=not split)
-        self._train(self.slots[k % 2], part, late=ls)
+                self._prep_late(self.slots[k % D], host_inputs)
+        if D == 3:
+            hs = self.head_stream
+            hs.wait_stream(cs)
+            with torch.cuda.stream(hs):
+                self._prep_head(self.slots[(k + 2) % 3],
+                                self.staging[(k + 2) % self.ring] if host_inputs else None)
+            with torch.cuda.stream(ps):
+                self._prep_tail(self.slots[(k + 1) % 3], host_inputs)
+                if not split:
+                    self._prep_late(self.slots[(k + 1) % 3], host_inputs)
+        else:
+            with torch.cuda.stream(ps):
+                self._prep(self.slots[(k + 1) % 2],
+                           self.staging[(k + 1) % self.ring] if host_inputs else None,
+                           late=not split)
+        self._train(self.slots[k % D], part, late=ls)
         cs.wait_stream(ps)
+        if D == 3:
+            cs.wait_stream(self.head_stream)
 
     # ---------------------------------------------------------------- driver
     def _stage_host(self, stage: _Staging, step: int) -> None:
@@ -331,17 +375,24 @@ class Trainer:
             stage.seeds[:n].copy_(torch.from_numpy(self.perm_host[off:off + n]))
 
     def begin_epoch(self, host_inputs: bool = False) -> None:
-        """Prepare batch 0 into slot 0 (eager) before the first step."""
-        stage = None
-        if host_inputs:
-            stage = self.staging[0]
-            stage.ev.synchronize()
-            self._stage_host(stage, 0)
+        """Prime the pipeline (eager): batch 0 into slot 0, and with depth 3 also
+        the head hops of batch 1 into slot 1."""
+        late = not (self.cfg.late_prep and self.prep_stream is not None)
+        stages = []
+        for j in range(self.depth - 1):
+            stage = None
+            if host_inputs:
+                stage = self.staging[j]
+                stage.ev.synchronize()
+                self._stage_host(stage, j)
+            stages.append(stage)
         # with the late split, pair 0 builds slot 0's labels / reverse adjacency
-        self._prep(self.slots[0], stage,
-                   late=not (self.cfg.late_prep and self.prep_stream is not None))
-        if stage is not None:
-            stage.ev.record()
+        self._prep(self.slots[0], stages[0], late=late)
+        if self.depth == 3:
+            self._prep_head(self.slots[1], stages[1])
+        for stage in stages:
+            if stage is not None:
+                stage.ev.record()
 
     def run_steps(self, start: int, count: int, host_inputs: bool = False,
                   loss_out: torch.Tensor | None = None) -> None:
@@ -349,17 +400,19 @@ class Trainer:
 
         begin_epoch() must have prepared step `start` (the pipeline is primed
         once per epoch).  With host_inputs each step stages its successor's
-        seeds in pinned host memory (4-deep ring, so the host runs ahead of
+        seeds in pinned host memory (2*depth ring, so the host runs ahead of
         the GPU) and copies its loss back to `loss_out[k]` (pinned) — the
         end-to-end path.
         """
-        P = 4 if host_inputs else 2
+        D = self.depth
+        P = self.ring if host_inputs else D
         for k in range(start, start + count):
             stage = None
             if host_inputs:
-                stage = self.staging[(k + 1) % 4]
+                ahead = k + D - 1             # the step whose seeds this replay consumes
+                stage = self.staging[ahead % self.ring]
                 stage.ev.synchronize()  # the replay that last read this staging buffer
-                self._stage_host(stage, k + 1)
+                self._stage_host(stage, ahead)
             if self.cfg.graphs:
                 if self.graph_allreduce:
                     key = (k % P, host_inputs, "all")
@@ -391,6 +444,8 @@ class Trainer:
         all-reduce cannot be captured."""
         torch.cuda.synchronize()
         state = [self.cursor, self.step_ctr] + self.model.optimizer_tensors()
+        # the slots too: a warm-up re-runs a tail on a half-prepared slot (depth 3)
+        state += [t for sl in self.slots for t in (sl.ws.buf, sl.desc)]
         saved = [s.clone() for s in state]
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream())

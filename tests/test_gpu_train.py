@@ -86,14 +86,15 @@ def test_fused_logits_fp32_within_1e3_of_autograd_on_config_shape():
     assert err < 1e-3, err
 
 
-def _small_trainer(graphs, gather_free=False, seed=0):
+def _small_trainer(graphs, gather_free=False, seed=0, fanouts=(10, 5), prep_split=0):
     g = synth_graph(30000, 10, 3.0, seed=4)
     fm = generate_features(30000, 64, "f16", seed=4)
     y = planted_labels(fm.data, 8, seed=4)
     dg = DeviceGraph.from_host(g, fm, y)
     train = np.arange(0, 30000, 2)
-    cfg = TrainConfig(fanouts=FanoutSpec((10, 5)), batch_size=512, hidden=64, lr=0.01,
-                      graphs=graphs, gather_free=gather_free, model_seed=seed)
+    cfg = TrainConfig(fanouts=FanoutSpec(fanouts), batch_size=512, hidden=64, lr=0.01,
+                      graphs=graphs, gather_free=gather_free, model_seed=seed,
+                      prep_split=prep_split)
     return Trainer(dg, train, cfg), dg
 
 
@@ -151,3 +152,35 @@ def test_training_learns_planted_labels():
     correct, total = tr.evaluate(test_ids)
     assert total == 4000
     assert correct / total > 0.5, correct / total
+
+
+@pytest.mark.parametrize("gather_free", [False, True])
+@pytest.mark.parametrize("split", [1, 2])
+def test_three_slot_pipeline_matches_two_slot(gather_free, split):
+    """prep_split: hops [0, s) of batch i+2 beside hops [s, L) of batch i+1 —
+    the same batches in the same order, eager and graph-replayed, device plan
+    and host inputs, across an epoch boundary."""
+    ref, _ = _small_trainer(False, gather_free, fanouts=(10, 5, 3))
+    ref.set_epoch(0)
+    ref.begin_epoch()
+    n = ref.steps_per_epoch
+    ref.run_steps(0, n)
+    torch.cuda.synchronize()
+    want = ref.losses[:n].cpu().numpy()
+    for graphs in (False, True):
+        tr, _ = _small_trainer(graphs, gather_free, fanouts=(10, 5, 3), prep_split=split)
+        assert tr.depth == 3
+        tr.set_epoch(0)
+        tr.begin_epoch()
+        tr.run_steps(0, n)
+        torch.cuda.synchronize()
+        got = tr.losses[:n].cpu().numpy()
+        assert np.allclose(got, want, rtol=2e-2, atol=1e-3), (graphs, got[:6], want[:6])
+        assert int(tr.cursor.item()) == n + 2   # one plan_next per batch, two past the end
+    tr, _ = _small_trainer(True, gather_free, fanouts=(10, 5, 3), prep_split=split)
+    tr.set_epoch(0)
+    tr.begin_epoch(host_inputs=True)
+    out = torch.zeros(n).pin_memory()
+    tr.run_steps(0, n, host_inputs=True, loss_out=out)
+    torch.cuda.synchronize()
+    assert np.allclose(out.numpy(), want, rtol=2e-2, atol=1e-3)

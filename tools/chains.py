@@ -49,7 +49,7 @@ def main():
     tr.begin_epoch(False)
     tr.run_steps(0, 8)
     torch.cuda.synchronize()
-    s0, s1 = tr.slots
+    s0, s1 = tr.slots[:2]
     print(f"prep alone   {graph_time(lambda: tr._prep(s1, None, late=True)):7.1f} us")
     print(f"train alone  {graph_time(lambda: tr._train(s0)):7.1f} us")
     print(f"pair         {graph_time(lambda: tr._pair(0, False)):7.1f} us")
