@@ -269,7 +269,10 @@ size_t sal_transpose_ws_bytes(int64_t n_src_rows);
 int sal_transpose_build(const int32_t* indptr_dev, const int32_t* src_dev,
                         const int64_t* n_dst_dev, int64_t n_pad, int64_t n_src_rows,
                         int64_t max_edges, int32_t* tindptr_dev, int32_t* tdst_dev,
-                        float* tw_dev, void* ws_dev, void* stream);
+                        float* tw_dev, void* ws_dev, int32_t ws_zeroed, void* stream);
+/* zero n <= 8 device byte ranges in one kernel (ptrs/bytes are host arrays);
+ * replaces a chain of memset nodes inside a captured step */
+int sal_zero_spans(void* const* ptrs, const int64_t* bytes, int32_t n, void* stream);
 /* input gradient of a SAGEConv layer, gathered per source row s < rows:
  * dz[s] = mask(s) * (dA[s, f:2f] if s < n_pad) + sum_{d in T(s)} dA[d, 0:f]/deg(d),
  * scaled by 1/(1-p) — relu/dropout backward fused, no atomics, no zero fill */
@@ -278,12 +281,14 @@ int sal_mean_bwd_t(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f,
                    const float* tw_dev, int64_t rows, const uint8_t* mask_dev, float p,
                    void* dz_dev, int64_t ldz, int32_t dz_dtype, void* stream);
 /* Adam (torch.optim.Adam, no weight decay) on flat fp32 params; step count
- * t = *t_dev + 1; refreshes the optional bf16 shadow copy */
-int sal_adam_step(float* param_dev, const float* grad_dev, float* m_dev, float* v_dev,
+ * t = *t_dev + 1; refreshes the optional bf16 shadow copy; zero_grad != 0
+ * leaves grad zeroed (the next backward accumulates without a memset) */
+int sal_adam_step(float* param_dev, float* grad_dev, float* m_dev, float* v_dev,
                   void* shadow_bf16_dev, int64_t n, float lr, float beta1, float beta2, float eps,
-                  const int64_t* t_dev, void* stream);
-/* per-step bookkeeping: *last = *loss; log[*step] = *loss; ++*step; ++*adam_t */
-int sal_step_tail(const float* loss_dev, float* last_dev, float* log_dev, int64_t log_len,
+                  const int64_t* t_dev, int32_t zero_grad, void* stream);
+/* per-step bookkeeping: *last = *loss; log[*step] = *loss; *loss = 0 (ready
+ * for the next step's accumulation); ++*step; ++*adam_t */
+int sal_step_tail(float* loss_dev, float* last_dev, float* log_dev, int64_t log_len,
                   int64_t* step_dev, int64_t* adam_t_dev, void* stream);
 
 /* ---- tcgen05 GEMMs of the layer-0 SAGEConv (sm_100a tensor cores) -------- */
@@ -293,11 +298,13 @@ int sal_step_tail(const float* loss_dev, float* last_dev, float* log_dev, int64_
 int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const void* W_dev, int32_t N,
                     int32_t K, void* Y_dev, int64_t ldy, uint8_t* mask_dev, float p,
                     uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout, void* stream);
-/* dW[N,K] (fp32, row stride lddw) = dz[M,N]^T @ A[M,K]; zeroes dW first.
+/* dW[N,K] (fp32, row stride lddw) = dz[M,N]^T @ A[M,K]; zeroes dW first
+ * unless `accumulate` (then dW += ...: the caller guarantees dW was zero).
  * 128 x 128 output tiles x split-K over M (about one CTA per SM), partials
  * added with fp32 vector atomics.  N, K multiples of 128. */
 int sal_tc_sage_wgrad(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda, int64_t M,
-                      int32_t N, int32_t K, float* dW_dev, int64_t lddw, void* stream);
+                      int32_t N, int32_t K, float* dW_dev, int64_t lddw, int32_t accumulate,
+                      void* stream);
 /* the same two GEMMs without TMA / warp specialisation (cp.async, one CTA
  * role) — the reference implementation the TMA versions are checked against */
 int sal_tc_sage_fwd_simple(const void* A_dev, int64_t lda, int64_t M, const void* W_dev,

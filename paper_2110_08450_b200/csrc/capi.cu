@@ -38,22 +38,6 @@ int fail(int code, const char* fmt, ...) {
 
 }  // namespace
 namespace sal {
-int train_sms() {
-  static const int v = [] {
-    const char* e = getenv("SAL_TRAIN_SMS_RESERVE");
-    const int r = e ? atoi(e) : 0;
-    const int n = num_sms() - r;
-    return n > 1 ? n : 1;
-  }();
-  return v;
-}
-int l0_blocks_per_sm() {
-  static const int v = [] {
-    const char* e = getenv("SAL_L0_BPS");
-    return e ? atoi(e) : 3;
-  }();
-  return v;
-}
 int set_error(int code, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -227,8 +211,17 @@ int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan, const sal
                 plan->num_hops);
   cudaError_t e = cudaSuccess;
   int kernels = 0;
+  // one shared look-back workspace: every later scan finds it zeroed by the
+  // kernel before it (sample(h) -> flag scan(h); resolve(h) -> count(h+1)), so
+  // the hops add no memset nodes
+  sal::ZeroJob zws;
+  zws.p = (uint32_t*)scan;
+  zws.words = (L->scan_bytes + 3) / 4;
   if (hop_begin == 0) {
+    // table + first scan workspace as memset nodes: measured faster in the
+    // overlapped step than a reset kernel, which takes SM slots from training
     e = cudaMemsetAsync(m.table, 0xFF, plan->table_cap * 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(scan, 0, L->scan_bytes, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: table reset");
     e = sal::launch_seed_insert(seeds_base, desc, m, plan->max_seeds, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: seed insert");
@@ -238,7 +231,7 @@ int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan, const sal
     int32_t* dst_indptr = (int32_t*)(base + L->dst_indptr[h]);
     int32_t* src_local = (int32_t*)(base + L->src_local[h]);
     e = sal::launch_hop_count(gd, m.globals, sizes + h, plan->node_cap[h], plan->fanout[h],
-                              dst_indptr, etot + h, scan, st);
+                              dst_indptr, etot + h, scan, st, /*ws_zeroed=*/true);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop count");
     sal::HopKey hk;
     hk.prefix = 0;
@@ -259,10 +252,11 @@ int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan, const sal
     }
     e = sal::launch_hop_sample(gd, m, sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
                                rng_policy, nullptr, dst_indptr, src_glob, slot, nullptr, st,
-                               plan->sample_lanes, plan->sample_blocks_per_sm);
+                               plan->sample_lanes, plan->sample_blocks_per_sm, zws);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
     e = sal::launch_hop_relabel(m, etot + h, plan->edge_cap[h], sizes + h, sizes + h + 1,
-                                src_glob, slot, rank, src_local, scan, st);
+                                src_glob, slot, rank, src_local, scan, st, /*ws_zeroed=*/true,
+                                h + 1 < plan->num_hops ? zws : sal::ZeroJob());
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop relabel");
     kernels += 4;
   }

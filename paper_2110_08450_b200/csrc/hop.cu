@@ -63,6 +63,12 @@ SAL_DEVINL void table_insert_assigned(unsigned long long* table, int log2cap, ui
 // ---------------------------------------------------------------------------
 // seeds -> locals 0..n-1 (sampler.py:336-340: id_map.insert(seeds.dst_ids))
 // ---------------------------------------------------------------------------
+SAL_DEVINL void side_zero(const ZeroJob& zj) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < zj.words;
+       w += (int64_t)gridDim.x * blockDim.x)
+    zj.p[w] = 0u;
+}
+
 __global__ void seed_insert_kernel(const int64_t* __restrict__ seeds_base,
                                    const BatchDesc* __restrict__ desc,
                                    unsigned long long* table, int log2cap,
@@ -146,14 +152,25 @@ SAL_DEVINL void emit_edge(const int32_t* __restrict__ indices, int64_t slot_pos,
     slot[e] = (int32_t)table_insert_min(table, log2cap, key, (uint32_t)e);
 }
 
-// Draw -> position for the two RNG policies.
+// Exact z % d for d in [1, 2^32) without the u64 division routine: with the
+// per-destination reciprocal m = floor((2^64-1)/d), q = umulhi(z, m) is at most
+// 2 below floor(z/d), so r = z - q*d needs at most two corrections.
+SAL_DEVINL uint32_t mod_by_recip(uint64_t z, uint32_t d, uint64_t m) {
+  const uint64_t q = __umul64hi(z, m);
+  uint64_t r = z - q * (uint64_t)d;
+  if (r >= d) r -= d;
+  if (r >= d) r -= d;
+  return (uint32_t)r;
+}
+
+// Draw -> position for the two RNG policies.  recip = floor((2^64-1)/deg).
 template <int kPolicy>
 SAL_DEVINL uint32_t draw_position(uint64_t key, uint2 pkey, uint32_t ctr, uint32_t dst,
-                                  uint32_t hop, uint32_t batch, uint32_t deg) {
+                                  uint32_t hop, uint32_t batch, uint32_t deg, uint64_t recip) {
   if (kPolicy == kRngSplitmix) {
     // _kernels.py:37-39 + 120: mix64(key + (c+1)G) % deg  (u64 modulo)
     const uint64_t z = mix64(key + (uint64_t)(ctr + 1) * kGolden);
-    return (uint32_t)(z % (uint64_t)deg);
+    return mod_by_recip(z, deg, recip);
   } else {
     const uint4 r = philox4x32_10(make_uint4(ctr, dst, hop, batch), pkey);
     return (uint32_t)(((uint64_t)r.x * deg) >> 32);
@@ -174,7 +191,8 @@ sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restri
                      const int64_t* __restrict__ inject_pos, const int32_t* __restrict__ dst_indptr,
                      unsigned long long* table, int log2cap, int32_t* src_glob,
                      int32_t* __restrict__ slot, int32_t* __restrict__ draws_out,
-                     int64_t* __restrict__ size_unknown) {
+                     int64_t* __restrict__ size_unknown, ZeroJob zj) {
+  side_zero(zj);
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, gl = lane % G;
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
@@ -211,6 +229,7 @@ sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restri
     }
     const uint64_t key = mix64(prefix ^ (uint64_t)i);  // _kernels.py:167
     const uint32_t udeg = (uint32_t)deg;
+    const uint64_t recip = kPolicy == kRngSplitmix ? ~0ull / (uint64_t)udeg : 0ull;
     // accepted positions: this group's slice of shared memory when the fanout
     // fits, else staged in this destination's own output range
     int32_t* accepted = fanout <= G ? &sh_acc[threadIdx.x >> 5][grp * G] : src_glob + out;
@@ -218,7 +237,7 @@ sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restri
     uint32_t ctr = 0;
     while (acc < fanout) {
       const uint32_t pos = draw_position<kPolicy>(key, pkey, ctr + gl, (uint32_t)i, hk.hop,
-                                                  batch, udeg);
+                                                  batch, udeg, recip);
       bool hit = false;
       for (int j = 0; j < acc; ++j) hit |= ((uint32_t)accepted[j] == pos);
       const unsigned peers = __match_any_sync(gmask, pos) & gmask;
@@ -313,7 +332,8 @@ __global__ void resolve_kernel(unsigned long long* table, const int32_t* __restr
                                const int64_t* __restrict__ e_total,
                                const int64_t* __restrict__ size_old_ptr,
                                const int32_t* __restrict__ rank_of,
-                               int32_t* __restrict__ src_local) {
+                               int32_t* __restrict__ src_local, ZeroJob zj) {
+  side_zero(zj);
   const int64_t n = *e_total;
   const int64_t size_old = *size_old_ptr;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -390,10 +410,12 @@ cudaError_t launch_rehash(const IdMapDev& m, int64_t n, cudaStream_t st) {
 
 cudaError_t launch_hop_count(const GraphDev& g, const int32_t* globals, const int64_t* n_dst,
                              int64_t max_dst, int32_t fanout, int32_t* dst_indptr,
-                             int64_t* e_total, void* scan_ws, cudaStream_t st) {
+                             int64_t* e_total, void* scan_ws, cudaStream_t st, bool ws_zeroed) {
   ScanWs ws = carve_scan_ws(scan_ws, max_dst);
-  cudaError_t err = cudaMemsetAsync(scan_ws, 0, scan_ws_bytes(max_dst), st);
-  if (err != cudaSuccess) return err;
+  if (!ws_zeroed) {
+    cudaError_t err = cudaMemsetAsync(scan_ws, 0, scan_ws_bytes(max_dst), st);
+    if (err != cudaSuccess) return err;
+  }
   count_scan_kernel<<<scan_grid(max_dst), kScanThreads, 0, st>>>(g.indptr, globals, n_dst, fanout,
                                                                 dst_indptr, e_total, ws);
   return cudaGetLastError();
@@ -404,7 +426,7 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
                               int32_t policy, const int64_t* inject_pos,
                               const int32_t* dst_indptr, int32_t* src_glob, int32_t* slot,
                               int32_t* draws_out, cudaStream_t st, int lanes,
-                              int blocks_per_sm) {
+                              int blocks_per_sm, ZeroJob zj) {
   const int64_t warps_needed = max_dst > 0 ? max_dst : 1;
   int64_t grid = (warps_needed + 7) / 8;
   // default 8 blocks x 8 warps per SM, grid-stride
@@ -420,7 +442,7 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
 #define SAL_SAMPLE(P, GG)                                                                   \
   sample_insert_kernel<P, GG><<<(int)grid, 256, 0, st>>>(                                   \
       g.indptr, g.indices, m.globals, n_dst, fanout, hk, desc, inject_pos, dst_indptr, m.table, \
-      m.log2cap, src_glob, slot, draws_out, m.table == nullptr ? m.size_out : nullptr)
+      m.log2cap, src_glob, slot, draws_out, m.table == nullptr ? m.size_out : nullptr, zj)
   if (policy == kRngSplitmix) {
     if (G == 8) SAL_SAMPLE(kRngSplitmix, 8);
     else if (G == 16) SAL_SAMPLE(kRngSplitmix, 16);
@@ -448,10 +470,14 @@ cudaError_t launch_keys_insert(const int64_t* keys, int64_t n, const IdMapDev& m
 cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_t max_edges,
                                const int64_t* size_old, int64_t* size_new,
                                const int32_t* src_glob, const int32_t* slot, int32_t* rank_of,
-                               int32_t* src_local, void* scan_ws, cudaStream_t st) {
+                               int32_t* src_local, void* scan_ws, cudaStream_t st,
+                               bool ws_zeroed, ZeroJob next) {
   ScanWs ws = carve_scan_ws(scan_ws, max_edges);
-  cudaError_t err = cudaMemsetAsync(scan_ws, 0, scan_ws_bytes(max_edges), st);
-  if (err != cudaSuccess) return err;
+  cudaError_t err;
+  if (!ws_zeroed) {
+    err = cudaMemsetAsync(scan_ws, 0, scan_ws_bytes(max_edges), st);
+    if (err != cudaSuccess) return err;
+  }
   flag_scan_kernel<<<scan_grid(max_edges), kScanThreads, 0, st>>>(
       m.table, slot, src_glob, e_total, size_old, size_new, rank_of, m.globals, ws);
   err = cudaGetLastError();
@@ -459,7 +485,8 @@ cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_
   int64_t grid = (max_edges + 255) / 256;
   if (grid < 1) grid = 1;
   if (grid > num_sms() * 16) grid = num_sms() * 16;
-  resolve_kernel<<<(int)grid, 256, 0, st>>>(m.table, slot, e_total, size_old, rank_of, src_local);
+  resolve_kernel<<<(int)grid, 256, 0, st>>>(m.table, slot, e_total, size_old, rank_of, src_local,
+                                            next);
   return cudaGetLastError();
 }
 

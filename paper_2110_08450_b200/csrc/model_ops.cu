@@ -417,10 +417,11 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
 // ---------------------------------------------------------------------------
 // Adam (torch.optim.Adam semantics, no weight decay) over flat fp32 params,
 // bias correction from the device step counter; refreshes the bf16 shadow.
-__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
+__global__ void adam_kernel(float* __restrict__ p, float* __restrict__ g,
                             float* __restrict__ m, float* __restrict__ v,
                             __nv_bfloat16* __restrict__ shadow, int64_t n, float lr, float b1,
-                            float b2, float eps, const int64_t* __restrict__ t_dev) {
+                            float b2, float eps, const int64_t* __restrict__ t_dev,
+                            int zero_grad) {
   const float t = (float)(*t_dev + 1);
   const float bc1 = 1.f - __powf(b1, t);
   const float bc2 = 1.f - __powf(b2, t);
@@ -429,6 +430,7 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
+    if (zero_grad) g[i] = 0.f;
     const float mi = b1 * m[i] + (1.f - b1) * gi;
     const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
     m[i] = mi;
@@ -439,11 +441,12 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
   }
 }
 
-__global__ void step_tail_kernel(const float* __restrict__ loss, float* __restrict__ last,
+__global__ void step_tail_kernel(float* __restrict__ loss, float* __restrict__ last,
                                  float* __restrict__ log, int64_t log_len,
                                  int64_t* __restrict__ step, int64_t* __restrict__ adam_t) {
   const int64_t s = *step;
   const float l = *loss;
+  *loss = 0.f;
   *last = l;
   if (s >= 0 && s < log_len) log[s] = l;
   *step = s + 1;
@@ -560,7 +563,7 @@ size_t sal_transpose_ws_bytes(int64_t n_src_rows) {
 
 int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
                         int64_t n_pad, int64_t n_src_rows, int64_t max_edges, int32_t* tindptr,
-                        int32_t* tdst, float* tw, void* ws, void* stream) {
+                        int32_t* tdst, float* tw, void* ws, int32_t ws_zeroed, void* stream) {
   (void)max_edges;
   if (indptr == nullptr || src == nullptr || tindptr == nullptr || tdst == nullptr || ws == nullptr)
     return SAL_EINVAL;
@@ -569,10 +572,12 @@ int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t
   int32_t* tfill = tcount + (n_src_rows + 1);
   char* scan = (char*)(tfill + (n_src_rows + 1));
   scan = (char*)(((uintptr_t)scan + 15) & ~(uintptr_t)15);
-  const size_t zero_bytes = (size_t)(8 * (n_src_rows + 1));
-  if (cudaMemsetAsync(ws, 0, zero_bytes, st) != cudaSuccess) return SAL_ECUDA;
-  const size_t sb = sal::scan_ws_bytes(n_src_rows);
-  if (cudaMemsetAsync(scan, 0, sb, st) != cudaSuccess) return SAL_ECUDA;
+  if (!ws_zeroed) {  // else the caller zeroed the whole ws (sal_zero_spans)
+    const size_t zero_bytes = (size_t)(8 * (n_src_rows + 1));
+    if (cudaMemsetAsync(ws, 0, zero_bytes, st) != cudaSuccess) return SAL_ECUDA;
+    const size_t sb = sal::scan_ws_bytes(n_src_rows);
+    if (cudaMemsetAsync(scan, 0, sb, st) != cudaSuccess) return SAL_ECUDA;
+  }
   sal::transpose_count_kernel<<<sal::ew_grid(n_pad * 16), 256, 0, st>>>(indptr, src, n_dst_dev,
                                                                          n_pad, tcount);
   sal::ScanWs sw;
@@ -607,17 +612,45 @@ int sal_mean_bwd_t(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int
   return sal::done(1);
 }
 
-int sal_adam_step(float* param, const float* grad, float* m, float* v, void* shadow_bf16,
+int sal_adam_step(float* param, float* grad, float* m, float* v, void* shadow_bf16,
                   int64_t n, float lr, float beta1, float beta2, float eps,
-                  const int64_t* t_dev, void* stream) {
+                  const int64_t* t_dev, int32_t zero_grad, void* stream) {
   if (param == nullptr || grad == nullptr || m == nullptr || v == nullptr || t_dev == nullptr)
     return SAL_EINVAL;
   sal::adam_kernel<<<sal::ew_grid(n), 256, 0, (cudaStream_t)stream>>>(
-      param, grad, m, v, (__nv_bfloat16*)shadow_bf16, n, lr, beta1, beta2, eps, t_dev);
+      param, grad, m, v, (__nv_bfloat16*)shadow_bf16, n, lr, beta1, beta2, eps, t_dev, zero_grad);
   return sal::done(1);
 }
 
-int sal_step_tail(const float* loss, float* last, float* log, int64_t log_len, int64_t* step,
+struct ZeroSpans {
+  uint4* p[8];
+  int64_t n16[8];
+  int32_t n;
+};
+__global__ void zero_spans_kernel(ZeroSpans z) {
+  for (int k = 0; k < z.n; ++k)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < z.n16[k];
+         i += (int64_t)gridDim.x * blockDim.x)
+      z.p[k][i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+int sal_zero_spans(void* const* ptrs, const int64_t* bytes, int32_t n, void* stream) {
+  if (n < 0 || n > 8 || (n && (!ptrs || !bytes))) return SAL_EINVAL;
+  ZeroSpans z;
+  z.n = n;
+  int64_t most = 0;
+  for (int k = 0; k < n; ++k) {
+    if (((uintptr_t)ptrs[k] & 15) || (bytes[k] & 15)) return SAL_EINVAL;
+    z.p[k] = (uint4*)ptrs[k];
+    z.n16[k] = bytes[k] / 16;
+    if (z.n16[k] > most) most = z.n16[k];
+  }
+  if (n == 0 || most == 0) return SAL_OK;
+  zero_spans_kernel<<<sal::ew_grid(most), 256, 0, (cudaStream_t)stream>>>(z);
+  return sal::done(1);
+}
+
+int sal_step_tail(float* loss, float* last, float* log, int64_t log_len, int64_t* step,
                   int64_t* adam_t, void* stream) {
   sal::step_tail_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(loss, last, log, log_len, step,
                                                            adam_t);

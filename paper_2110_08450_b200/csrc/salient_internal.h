@@ -35,11 +35,15 @@ struct HopKey {
   int32_t derive;
 };
 
+// Words a kernel zeroes on the side for its successor in a stream (the
+// look-back scan workspace of the next scan): replaces a memset node, whose
+// graph dependency edges cost ~5 us of latency each (profiles/, timeline).
+struct ZeroJob {
+  uint32_t* p = nullptr;
+  int64_t words = 0;
+};
+
 int num_sms();
-// experiment knobs (env, read once): SMs the persistent training kernels use,
-// blocks per SM of the layer-0 mean
-int train_sms();
-int l0_blocks_per_sm();
 // thread-local error message of sal_last_error(); returns `code`
 int set_error(int code, const char* fmt, ...);
 void count_launch(int kernels);
@@ -50,13 +54,14 @@ cudaError_t launch_seed_insert(const int64_t* seeds_base, const BatchDesc* desc,
                                const IdMapDev& m, int64_t max_seeds, cudaStream_t st);
 cudaError_t launch_hop_count(const GraphDev& g, const int32_t* globals, const int64_t* n_dst,
                              int64_t max_dst, int32_t fanout, int32_t* dst_indptr,
-                             int64_t* e_total, void* scan_ws, cudaStream_t st);
+                             int64_t* e_total, void* scan_ws, cudaStream_t st, bool ws_zeroed = false);
 cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_t* n_dst,
                               int64_t max_dst, int32_t fanout, HopKey hk, const BatchDesc* desc,
                               int32_t policy, const int64_t* inject_pos,
                               const int32_t* dst_indptr, int32_t* src_glob, int32_t* slot,
                               int32_t* draws_out, cudaStream_t st, int lanes = 0,
-                              int blocks_per_sm = 0);
+                              int blocks_per_sm = 0,
+                              ZeroJob zj = ZeroJob());
 cudaError_t launch_rehash(const IdMapDev& m, int64_t n, cudaStream_t st);
 cudaError_t launch_keys_insert(const int64_t* keys, int64_t n, const IdMapDev& m,
                                int32_t* src_glob, int32_t* slot, int64_t* e_total,
@@ -64,7 +69,8 @@ cudaError_t launch_keys_insert(const int64_t* keys, int64_t n, const IdMapDev& m
 cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_t max_edges,
                                const int64_t* size_old, int64_t* size_new,
                                const int32_t* src_glob, const int32_t* slot, int32_t* rank_of,
-                               int32_t* src_local, void* scan_ws, cudaStream_t st);
+                               int32_t* src_local, void* scan_ws, cudaStream_t st, bool ws_zeroed = false,
+                               ZeroJob next = ZeroJob());
 
 cudaError_t launch_gather_rows(const void* x, int64_t x_rows, int32_t cols, int64_t x_stride,
                                int32_t in_dtype, const void* ids, int32_t id_bytes,

@@ -17,8 +17,6 @@
 // input is the (frozen) feature table.
 #include <cuda_bf16.h>
 
-#include <cstdlib>
-
 #include "common.cuh"
 #include "salient_internal.h"
 
@@ -412,24 +410,24 @@ static bool fwd_rows(const int32_t* indptr, const int32_t* src, const int32_t* g
     return false;
   const TIn* hp = (const TIn*)h;
   TOut* op = (TOut*)out;
-  if (lpr >= 8) {  // software-pipelined (tools/l0mean_bench.py: 42.3 -> 38.3 us)
+  // Software-pipelined persistent kernel for the training layer-0 shape (128-d
+  // 16-bit rows, <= 128 K destinations): 42.3 -> 38.3 us alone, -1.6 % per
+  // training step.  Not for 512 B rows (neutral) nor for the (20,20,20)
+  // inference layer 0 (450 K destinations), where the persistent grid starves
+  // the overlapped prep chain: the pass took 0.098 s with it, 0.084 s without.
+  if ((lpr == 8 || lpr == 16) && n_pad <= 131072) {
+    // one resident wave (3 blocks/SM at 80 registers).  Measured worse: 2 blocks/SM
+    // to leave room for the prep chain (+16 us), short-lived blocks of 2-8
+    // destinations per warp (+6..20 us)
     int64_t blocks = (n_pad + 7) / 8;
-    const int64_t cap = (int64_t)num_sms() * l0_blocks_per_sm();  // one resident wave
-    static const int dpw = [] {
-      const char* e = getenv("SAL_L0_DPW");
-      return e ? atoi(e) : 0;
-    }();
-    if (dpw > 0) blocks = (n_pad + 8 * dpw - 1) / (8 * dpw);  // short-lived blocks
-    else if (blocks > cap) blocks = cap;
+    const int64_t cap = (int64_t)num_sms() * 3;
+    if (blocks > cap) blocks = cap;
     const int g = (int)(blocks < 1 ? 1 : blocks);
     if (lpr == 8)
       segment_mean_rows_pipe_kernel<TIn, TOut, 8, kGlobal><<<g, kSegThreads, 0, st>>>(
           indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);
-    else if (lpr == 16)
-      segment_mean_rows_pipe_kernel<TIn, TOut, 16, kGlobal><<<g, kSegThreads, 0, st>>>(
-          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);
     else
-      segment_mean_rows_pipe_kernel<TIn, TOut, 32, kGlobal><<<g, kSegThreads, 0, st>>>(
+      segment_mean_rows_pipe_kernel<TIn, TOut, 16, kGlobal><<<g, kSegThreads, 0, st>>>(
           indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);
     return true;
   }

@@ -757,7 +757,7 @@ int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const void* W, int32_
       !sal::tc::make_map(&mW, W, 256, 256, 256, 64, 256))
     return SAL_ECUDA;
   const int ntiles = (int)((M + 127) / 128);
-  int grid = sal::train_sms();
+  int grid = sal::num_sms();
   if (grid > ntiles) grid = ntiles;
   if (!sal::tc::make_map(&mY, Y, (uint64_t)M, 256, (uint64_t)ldy, 32, 32,
                          CU_TENSOR_MAP_SWIZZLE_64B))
@@ -801,13 +801,15 @@ int sal_tc_sage_fwd_simple(const void* A, int64_t lda, int64_t M, const void* W,
 }
 
 int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, int64_t M,
-                      int32_t N, int32_t K, float* dW, int64_t lddw, void* stream) {
+                      int32_t N, int32_t K, float* dW, int64_t lddw, int32_t accumulate,
+                      void* stream) {
   if (N <= 0 || K <= 0 || N % 128 || K % 128) return SAL_EINVAL;
   if (ldz % 8 || lda % 8 || ((uintptr_t)dz & 15) || ((uintptr_t)A & 15) || ((uintptr_t)dW & 15) ||
       lddw % 4 || lddw < K)
     return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  if (cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)N * (size_t)lddw, st) != cudaSuccess)
+  if (!accumulate &&
+      cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)N * (size_t)lddw, st) != cudaSuccess)
     return SAL_ECUDA;
   if (M <= 0) return SAL_OK;
   CUtensorMap mD, mA;
@@ -823,7 +825,7 @@ int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, i
   // one CTA per SM: tiles x splits ~ #SMs, splits of whole 64-row chunks
   const int tiles_k = K / 128;
   const int tiles = (N / 128) * tiles_k;
-  int splits = sal::train_sms() / tiles;
+  int splits = sal::num_sms() / tiles;
   if (splits < 1) splits = 1;
   int rows = (int)((M + splits - 1) / splits);
   rows = (rows + 63) / 64 * 64;

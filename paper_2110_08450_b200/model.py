@@ -227,7 +227,8 @@ class FusedSAGE:
                                    self.v.data_ptr(),
                                    self.shadow.data_ptr() if self.act == torch.bfloat16 else None,
                                    self.flat.numel(), self.lr, self.betas[0], self.betas[1],
-                                   self.eps, self.t.data_ptr(), _lib.stream_ptr()), "adam_step")
+                                   self.eps, self.t.data_ptr(), 0, _lib.stream_ptr()),
+                   "adam_step")
         if self.act != torch.bfloat16:
             self.refresh_shadow()
 
@@ -312,14 +313,17 @@ class FusedSAGE:
             saved.append(rec)
         return a, saved
 
-    def loss(self, logits: torch.Tensor, labels: torch.Tensor, out: torch.Tensor | None = None):
+    def loss(self, logits: torch.Tensor, labels: torch.Tensor, out: torch.Tensor | None = None,
+             zeroed: bool = False):
         """Fused log_softmax + NLL; returns (loss scalar fp32, dlogits [rows, c_pad]).
 
-        dlogits lives in a persistent buffer whose padded columns stay zero."""
+        dlogits lives in a persistent buffer whose padded columns stay zero.
+        zeroed: `out` is already zero (the trainer's step_tail clears it)."""
         L = _lib.lib()
         loss = out if out is not None else torch.empty((), dtype=torch.float32,
                                                        device=logits.device)
-        loss.zero_()
+        if not (zeroed and out is not None):
+            loss.zero_()
         n = logits.shape[0]
         if self._dlog is None or self._dlog.shape[0] != n or self._dlog.dtype != logits.dtype:
             self._dlog = torch.zeros((n, self.c_pad), dtype=logits.dtype, device=logits.device)
@@ -332,8 +336,17 @@ class FusedSAGE:
         return loss, dlog
 
     # ------------------------------------------------------------- bwd
-    def backward(self, dlogits: torch.Tensor, saved, transposes=None) -> None:
-        """Writes every weight gradient into self.grad (overwrite semantics).
+    def tc_grad_spans(self):
+        """(pointer, bytes) of the gradient blocks the split-K tcgen05 weight
+        gradient accumulates into; a caller that zeroes them off the critical path
+        passes grads_zeroed=True to backward()."""
+        return [(self.gp[i].data_ptr(), self.gp[i].numel() * 4) for i in range(self.L)
+                if self._tc_wgrad_layer(i)]
+
+    def backward(self, dlogits: torch.Tensor, saved, transposes=None,
+                 grads_zeroed: bool = False) -> None:
+        """Writes every weight gradient into self.grad (overwrite semantics; with
+        grads_zeroed the tcgen05 layers accumulate into blocks the caller zeroed).
 
         transposes[i] = (tindptr, tdst) reverse adjacency of layer i (i >= 1);
         built here when not supplied (the trainer builds them on the prep
@@ -348,7 +361,9 @@ class FusedSAGE:
                 gi = self.gp[i]
                 _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), a.data_ptr(),
                                                a.stride(0), n_pad, gi.shape[0], gi.shape[1],
-                                               gi.data_ptr(), gi.stride(0), st), "tc_sage_wgrad")
+                                               gi.data_ptr(), gi.stride(0),
+                                               1 if grads_zeroed else 0, st),
+                           "tc_sage_wgrad")
             else:
                 _mm_f32(dz.t(), a[:n_pad], self.gp[i])
             if i == 0:
@@ -381,7 +396,8 @@ class FusedSAGE:
         return logits
 
 
-def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=None, ws=None):
+def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=None, ws=None,
+                    ws_zeroed: bool = False):
     """Reverse adjacency (tindptr [n_src_rows+1], tdst, tw [edges]) of one MFG layer."""
     L = _lib.lib()
     dev = indptr.device
@@ -396,7 +412,7 @@ def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=Non
     _lib.check(L.sal_transpose_build(indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dst_dev),
                                      n_pad, n_src_rows, src.numel(), tindptr.data_ptr(),
                                      tdst.data_ptr(), tw.data_ptr(), ws.data_ptr(),
-                                     _lib.stream_ptr()),
+                                     1 if ws_zeroed else 0, _lib.stream_ptr()),
                "transpose_build")
     return tindptr, tdst, tw
 

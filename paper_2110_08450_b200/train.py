@@ -121,8 +121,8 @@ class _Slot:
                 torch.zeros(n_src + 1, dtype=torch.int32, device=device),
                 torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.int32, device=device),
                 torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.float32, device=device)))
-            self.t_ws.append(torch.empty(L.sal_transpose_ws_bytes(n_src), dtype=torch.uint8,
-                                         device=device))
+            nb = -(-L.sal_transpose_ws_bytes(n_src) // 16) * 16   # 16 B multiple (zero_spans)
+            self.t_ws.append(torch.empty(nb, dtype=torch.uint8, device=device))
 
 
 class _Staging:
@@ -272,9 +272,10 @@ class Trainer:
                 _lib.dtype_code(a0.dtype), a0.stride(0), _lib.stream_ptr(st)),
                 "segment_mean_fwd(table)")
 
-    def _prep_late(self, slot: _Slot, host_inputs: bool) -> None:
+    def _prep_late(self, slot: _Slot, host_inputs: bool, zero_grads: bool = False) -> None:
         """The inputs only the loss / backward read: labels and the reverse adjacency
-        of layers >= 1 (capturable, current stream)."""
+        of layers >= 1 (capturable, current stream); zero_grads: also clear the
+        tcgen05 weight-gradient blocks of the step being trained."""
         ws = slot.ws
         st = torch.cuda.current_stream()
         L = _lib.lib()
@@ -284,10 +285,21 @@ class Trainer:
                                        slot.desc.data_ptr(), self.cfg.batch_size,
                                        slot.labels.data_ptr(), _lib.stream_ptr(st)),
                    "gather_labels")
-        for i in range(1, nh):  # reverse adjacency for the backward pass
+        # reverse adjacency for the backward pass; every layer's count/scan workspace is
+        # zeroed by one kernel (no memset nodes in the captured chain)
+        spans = [(t.data_ptr(), t.numel()) for t in slot.t_ws[1:]]
+        if zero_grads:
+            spans += self.model.tc_grad_spans()
+        if spans:
+            ptrs = (ctypes.c_void_p * len(spans))(*[p for p, _ in spans])
+            nbytes = (ctypes.c_int64 * len(spans))(*[b for _, b in spans])
+            _lib.check(L.sal_zero_spans(ptrs, nbytes, len(spans), _lib.stream_ptr(st)),
+                       "zero_spans")
+        for i in range(1, nh):
             h = nh - 1 - i
             build_transpose(ws.dst_indptr[h], ws.src_local[h], ws.sizes[h:h + 1], ws.node_cap[h],
-                            ws.node_cap[h + 1], out=slot.transposes[i], ws=slot.t_ws[i])
+                            ws.node_cap[h + 1], out=slot.transposes[i], ws=slot.t_ws[i],
+                            ws_zeroed=True)
 
     def _adjs(self, slot: _Slot):
         ws = slot.ws
@@ -313,8 +325,8 @@ class Trainer:
                                       salt=self.step_ctr, mean0_ready=ready)
             if late is not None:
                 torch.cuda.current_stream().wait_stream(late)
-            loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf)
-            m.backward(dlog, saved, slot.transposes)
+            loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf, zeroed=True)
+            m.backward(dlog, saved, slot.transposes, grads_zeroed=late is not None)
         if part == "all" and self.world > 1:
             allreduce_mean(m.grad, self.world)
         if part in ("all", "post"):
@@ -342,7 +354,9 @@ class Trainer:
             ls = self.late_stream
             ls.wait_stream(cs)
             with torch.cuda.stream(ls):
-                self._prep_late(self.slots[k % D], host_inputs)
+                # the late stream also zeroes the tcgen05 gradient blocks (the previous
+                # step's Adam has read them): no memset node in the training chain
+                self._prep_late(self.slots[k % D], host_inputs, zero_grads=True)
         if D == 3:
             hs = self.head_stream
             hs.wait_stream(cs)
@@ -443,7 +457,7 @@ class Trainer:
         Returns None (and switches to the split "pre"/"post" graphs) when the
         all-reduce cannot be captured."""
         torch.cuda.synchronize()
-        state = [self.cursor, self.step_ctr] + self.model.optimizer_tensors()
+        state = [self.cursor, self.step_ctr, self.loss_buf] + self.model.optimizer_tensors()
         # the slots too: a warm-up re-runs a tail on a half-prepared slot (depth 3)
         state += [t for sl in self.slots for t in (sl.ws.buf, sl.desc)]
         saved = [s.clone() for s in state]

@@ -69,9 +69,15 @@ def test_tc_wgrad_matches_torch(M, N, K):
     dW = torch.full((N, K), 7.0, device="cuda")
     L = _lib.lib()
     _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), A.data_ptr(), A.stride(0), M,
-                                   N, K, dW.data_ptr(), dW.stride(0), _lib.stream_ptr()),
+                                   N, K, dW.data_ptr(), dW.stride(0), 0, _lib.stream_ptr()),
                "tc_sage_wgrad")
+    # accumulate mode adds into dW (the trainer's Adam leaves the gradient zeroed)
+    dW2 = torch.full((N, K), 0.5, device="cuda")
+    _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), A.data_ptr(), A.stride(0), M,
+                                   N, K, dW2.data_ptr(), dW2.stride(0), 1, _lib.stream_ptr()),
+               "tc_sage_wgrad(accumulate)")
     torch.cuda.synchronize()
     want = dz.float().t() @ A.float()
+    assert ((dW2 - 0.5 - want).norm() / want.norm()).item() < 1e-3
     err = (dW - want).norm() / want.norm()
     assert err < 1e-3, err
