@@ -81,15 +81,24 @@ def parse():
 
 # ---------------------------------------------------------------------------
 def dist_setup(args):
+    """One process per GPU (torchrun env).  SAL_DIST_BACKEND=gloo with fewer GPUs than
+    ranks maps every rank onto the visible GPUs round-robin: a functional test of
+    the N > 1 path on a single-GPU box (tests/test_gpu_dist.py), never a
+    measurement."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("SAL_DIST_BACKEND", "nccl")
+    dev = local % max(torch.cuda.device_count(), 1)
     if world > 1:
-        torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            torch.distributed.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
-    return rank, world, local
+    return rank, world, dev
 
 
 def barrier(world):
