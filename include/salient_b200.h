@@ -262,6 +262,15 @@ int sal_lsm_nll(const void* logits_dev, int64_t ld, int64_t rows, int32_t num_cl
 int sal_argmax_correct(const void* logits_dev, int64_t ld, int64_t rows, int32_t num_classes,
                        int32_t dtype, const int64_t* labels_dev, int64_t* counts_dev,
                        int64_t* pred_dev, void* stream);
+/* fused output layer (training): A = act[0:n_rows, 0:2f] ([mean | h_dst], bf16,
+ * mean already written), logits = A @ W^T (W [c_pad, 2f] bf16, rows >= classes
+ * zero), *loss += mean NLL over labels >= 0 (count over labels[0:n_labels]),
+ * dlogits = (softmax - onehot)/count, dA[n_rows, 2f] = dlogits @ W (bf16),
+ * dW[c_pad, 2f] += dlogits^T @ A (fp32; caller zeroes).  2f <= 512, c_pad <= 256. */
+int sal_sage_head(const void* act_dev, int64_t lda, int32_t f, int64_t n_rows, const void* W_dev,
+                  int32_t num_classes, int32_t c_pad, const int64_t* labels_dev, int64_t n_labels,
+                  float* loss_dev, float* dW_dev, int64_t lddw, void* dA_dev, int64_t ldda,
+                  void* stream);
 /* reverse adjacency of an MFG layer: tindptr[n_src_rows+1], tdst[edges] lists
  * for every source row the destinations that sampled it (order within a list
  * is unspecified); tw (nullable) receives each entry's 1/deg(dst) */

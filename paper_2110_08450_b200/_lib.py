@@ -106,6 +106,8 @@ SIGNATURES = {
                                             ctypes.c_float, vp]),
     "sal_lsm_nll": (ctypes.c_int, [vp, i64, i64, i32, i32, vp, vp, vp, i64, vp]),
     "sal_argmax_correct": (ctypes.c_int, [vp, i64, i64, i32, i32, vp, vp, vp, vp]),
+    "sal_sage_head": (ctypes.c_int, [vp, i64, i32, i64, vp, i32, i32, vp, i64, vp, vp, i64, vp,
+                                     i64, vp]),
     "sal_transpose_ws_bytes": (ctypes.c_size_t, [i64]),
     "sal_transpose_build": (ctypes.c_int, [vp, vp, vp, i64, i64, i64, vp, vp, vp, vp, i32, vp]),
     "sal_zero_spans": (ctypes.c_int, [vp, vp, i32, vp]),

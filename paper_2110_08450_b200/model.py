@@ -203,6 +203,9 @@ class FusedSAGE:
         # tcgen05 weight gradients (tiled split-K, sal_tc_sage_wgrad) where the
         # shapes allow; cuBLAS for the rest
         self.tc_wgrad = True
+        # fused output layer + loss + backward (sal_sage_head): off — mma.sync-bound on
+        # 16 SMs, 51 us against ~20 us for the unfused kernels (csrc/head.cu)
+        self.use_head = False
 
     # ------------------------------------------------------------- weights
     def refresh_shadow(self):
@@ -255,14 +258,15 @@ class FusedSAGE:
 
     # ------------------------------------------------------------- fwd
     def forward(self, a0: torch.Tensor, adjs, x_global=None, salt: torch.Tensor | None = None,
-                mean0_ready: bool = False):
+                mean0_ready: bool = False, head: bool = False):
         """a0: layer-0 cat buffer (right half = features in local order).
 
         adjs[i] = (indptr, src, n_pad, n_dst_dev).  With x_global = (table,
         edge_global_ids) layer 0's mean is read straight from the feature table
         (the sampler's per-edge global ids of the last hop).  mean0_ready: the
         left half of a0 already holds layer 0's mean (computed by the prep stream).
-        Returns (logits [n_pad_last, C], saved)."""
+        head: stop after the output layer's mean (loss_backward runs the rest).
+        Returns (logits [n_pad_last, C] or None with head, saved)."""
         L = _lib.lib()
         st = _lib.stream_ptr()
         a = a0
@@ -308,6 +312,8 @@ class FusedSAGE:
                         st), "relu_dropout_fwd")
                 rec["mask"] = mask
                 a = nxt
+            elif head:  # the fused output layer (loss_backward) computes the logits
+                a = None
             else:
                 a = torch.mm(a[:n_pad], self.wb[i].t())[:, :self.dims[-1]]
             saved.append(rec)
@@ -351,38 +357,89 @@ class FusedSAGE:
         transposes[i] = (tindptr, tdst) reverse adjacency of layer i (i >= 1);
         built here when not supplied (the trainer builds them on the prep
         stream)."""
-        L = _lib.lib()
-        st = _lib.stream_ptr()
         dz = dlogits
         for i in reversed(range(self.L)):
-            rec = saved[i]
-            a, n_pad = rec["a"], rec["n_pad"]
-            if self._tc_wgrad_layer(i):
-                gi = self.gp[i]
-                _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), a.data_ptr(),
-                                               a.stride(0), n_pad, gi.shape[0], gi.shape[1],
-                                               gi.data_ptr(), gi.stride(0),
-                                               1 if grads_zeroed else 0, st),
-                           "tc_sage_wgrad")
-            else:
-                _mm_f32(dz.t(), a[:n_pad], self.gp[i])
+            self._wgrad(i, dz, saved, grads_zeroed)
             if i == 0:
                 break
-            f = self.dims[i]
-            dA = torch.mm(dz, self.wb[i])                 # [n_pad, 2f]: [dmean | dh_dst]
-            indptr, src, _, n_dev = rec["adj"]
-            rows = a.shape[0]
-            if transposes is not None and transposes[i] is not None:
-                tindptr, tdst, tw = transposes[i]
-            else:
-                tindptr, tdst, tw = build_transpose(indptr, src, n_dev, n_pad, rows)
-            dzp = torch.empty((rows, f), dtype=self.act, device=a.device)
-            _lib.check(L.sal_mean_bwd_t(
-                dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
-                indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows,
-                saved[i - 1]["mask"].data_ptr(), self.p if self.training else 0.0,
-                dzp.data_ptr(), dzp.stride(0), _lib.dtype_code(self.act), st), "mean_bwd_t")
-            dz = dzp
+            dz = self._input_grad(i, torch.mm(dz, self.wb[i]), saved, transposes)
+
+    def _wgrad(self, i: int, dz, saved, grads_zeroed: bool) -> None:
+        L = _lib.lib()
+        rec = saved[i]
+        a, n_pad = rec["a"], rec["n_pad"]
+        if self._tc_wgrad_layer(i):
+            gi = self.gp[i]
+            _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), a.data_ptr(),
+                                           a.stride(0), n_pad, gi.shape[0], gi.shape[1],
+                                           gi.data_ptr(), gi.stride(0),
+                                           1 if grads_zeroed else 0, _lib.stream_ptr()),
+                       "tc_sage_wgrad")
+        else:
+            _mm_f32(dz.t(), a[:n_pad], self.gp[i])
+
+    def _input_grad(self, i: int, dA, saved, transposes):
+        """dz of layer i-1 from dA = [dmean | dh_dst] of layer i (mean_bwd_t over the
+        reverse adjacency, ReLU/dropout backward fused)."""
+        L = _lib.lib()
+        rec = saved[i]
+        a, n_pad = rec["a"], rec["n_pad"]
+        f = self.dims[i]
+        indptr, src, _, n_dev = rec["adj"]
+        rows = a.shape[0]
+        if transposes is not None and transposes[i] is not None:
+            tindptr, tdst, tw = transposes[i]
+        else:
+            tindptr, tdst, tw = build_transpose(indptr, src, n_dev, n_pad, rows)
+        dzp = torch.empty((rows, f), dtype=self.act, device=a.device)
+        _lib.check(L.sal_mean_bwd_t(
+            dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
+            indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows,
+            saved[i - 1]["mask"].data_ptr(), self.p if self.training else 0.0,
+            dzp.data_ptr(), dzp.stride(0), _lib.dtype_code(self.act), _lib.stream_ptr()),
+            "mean_bwd_t")
+        return dzp
+
+    # ------------------------------------------------------------- fused output layer
+    def head_ok(self) -> bool:
+        """The output layer, its loss and its backward run as one kernel
+        (sal_sage_head): bf16, 2 f_in <= 512, padded classes <= 256."""
+        f = self.dims[self.L - 1]
+        return (self.use_head and self.act == torch.bfloat16 and self.L >= 2 and f % 8 == 0
+                and 2 * f <= 512 and self.c_pad <= 256)
+
+    def head_grad_span(self):
+        """(pointer, bytes) of the output layer's gradient block (sal_sage_head accumulates)."""
+        g = self.gp[self.L - 1]
+        return (g.data_ptr(), g.numel() * 4)
+
+    def loss_backward(self, saved, labels: torch.Tensor, out: torch.Tensor, transposes=None,
+                      grads_zeroed: bool = False, loss_zeroed: bool = False) -> torch.Tensor:
+        """Fused output layer after forward(..., head=True): loss, the output layer's
+        weight gradient and dA in one kernel, then the backward of the layers below.
+        grads_zeroed: the caller zeroed the tcgen05 and output-layer gradient blocks."""
+        L = _lib.lib()
+        i = self.L - 1
+        rec = saved[i]
+        a, n_pad = rec["a"], rec["n_pad"]
+        f = self.dims[i]
+        if not loss_zeroed:
+            out.zero_()
+        gi = self.gp[i]
+        if not grads_zeroed:
+            gi.zero_()
+        dA = torch.empty((n_pad, 2 * f), dtype=self.act, device=a.device)
+        _lib.check(L.sal_sage_head(a.data_ptr(), a.stride(0), f, n_pad, self.wb[i].data_ptr(),
+                                   self.dims[-1], self.c_pad, labels.data_ptr(), labels.numel(),
+                                   out.data_ptr(), gi.data_ptr(), gi.stride(0), dA.data_ptr(),
+                                   dA.stride(0), _lib.stream_ptr()), "sage_head")
+        dz = self._input_grad(i, dA, saved, transposes)
+        for j in reversed(range(i)):
+            self._wgrad(j, dz, saved, grads_zeroed)
+            if j == 0:
+                break
+            dz = self._input_grad(j, torch.mm(dz, self.wb[j]), saved, transposes)
+        return out
 
     @torch.no_grad()
     def predict(self, x, adjs, x_global=None, cat: bool = False):

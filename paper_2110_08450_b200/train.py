@@ -290,6 +290,8 @@ class Trainer:
         spans = [(t.data_ptr(), t.numel()) for t in slot.t_ws[1:]]
         if zero_grads:
             spans += self.model.tc_grad_spans()
+            if self.model.head_ok():
+                spans.append(self.model.head_grad_span())
         if spans:
             ptrs = (ctypes.c_void_p * len(spans))(*[p for p, _ in spans])
             nbytes = (ctypes.c_int64 * len(spans))(*[b for _, b in spans])
@@ -321,12 +323,17 @@ class Trainer:
         if part in ("all", "pre"):
             ready = self.cfg.gather_free and self.cfg.prep_mean0
             xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free and not ready else None
+            head = m.head_ok()
             logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg,
-                                      salt=self.step_ctr, mean0_ready=ready)
+                                      salt=self.step_ctr, mean0_ready=ready, head=head)
             if late is not None:
                 torch.cuda.current_stream().wait_stream(late)
-            loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf, zeroed=True)
-            m.backward(dlog, saved, slot.transposes, grads_zeroed=late is not None)
+            if head:  # output layer + loss + its backward in one kernel
+                m.loss_backward(saved, slot.labels, self.loss_buf, slot.transposes,
+                                grads_zeroed=late is not None, loss_zeroed=True)
+            else:
+                loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf, zeroed=True)
+                m.backward(dlog, saved, slot.transposes, grads_zeroed=late is not None)
         if part == "all" and self.world > 1:
             allreduce_mean(m.grad, self.world)
         if part in ("all", "post"):

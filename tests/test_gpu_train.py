@@ -184,3 +184,80 @@ def test_three_slot_pipeline_matches_two_slot(gather_free, split):
     tr.run_steps(0, n, host_inputs=True, loss_out=out)
     torch.cuda.synchronize()
     assert np.allclose(out.numpy(), want, rtol=2e-2, atol=1e-3)
+
+
+@pytest.mark.parametrize("fin,hid,classes", [(128, 256, 172), (64, 64, 10), (32, 96, 47)])
+def test_fused_head_matches_unfused_and_autograd(fin, hid, classes):
+    """sal_sage_head (output layer + log_softmax/NLL + its backward in one kernel)
+    against the unfused GEMM / lsm_nll / GEMM path and a torch fp32 autograd model."""
+    g = synth_graph(3000, 8, 3.0, seed=5)
+    fm = generate_features(3000, fin, "f32", seed=5)
+    dg = DeviceGraph.from_host(g)
+    seeds = SeedBatch(0, np.random.default_rng(3).choice(3000, 200, replace=False))
+    mfg = multihop_mfg(dg, seeds, FanoutSpec((10, 5, 3)), 7)
+    x = torch.from_numpy(fm.data).cuda()[mfg.id_map.global_ids.long()]
+    labels = torch.from_numpy(np.random.default_rng(4).integers(0, classes, 200)).cuda()
+    labels[::9] = -1                         # ignored rows
+    m = FusedSAGE(fin, hid, classes, 3, dropout=0.0, seed=6, act_dtype=torch.bfloat16)
+    m.use_head = True
+    assert m.head_ok()
+    adjs = [(l.indptr, l.src_local, l.num_dst, None) for l in mfg.layers]
+    a0 = m.cat_input(x.to(torch.bfloat16))
+    logits, saved = m.forward(a0, adjs)
+    loss_u, dlog = m.loss(logits, labels)
+    m.backward(dlog, saved)
+    grads_u = [gi.clone() for gi in m.g]
+    m.grad.fill_(3.0)                        # loss_backward zeroes what it accumulates into
+    _, saved = m.forward(m.cat_input(x.to(torch.bfloat16)), adjs, head=True)
+    out = torch.full((), 5.0, device="cuda")
+    m.loss_backward(saved, labels, out)
+    torch.cuda.synchronize()
+    assert abs(out.item() - loss_u.item()) / loss_u.item() < 1e-2, (out.item(), loss_u.item())
+    for i in range(3):
+        r = ((m.g[i] - grads_u[i]).norm() / grads_u[i].norm().clamp_min(1e-12)).item()
+        assert r < 2e-2, (i, r)
+    weights = [(m.w_neigh(i).clone(), m.w_self(i).clone()) for i in range(3)]
+    keep = labels >= 0
+    _, want_loss, want_grads = _torch_reference_masked(weights, x, mfg.layers, labels, keep)
+    assert abs(out.item() - want_loss.item()) / want_loss.item() < 5e-2
+    for i in range(3):
+        f = m.dims[i]
+        for got, gw in ((m.g[i][:, :f], want_grads[2 * i]), (m.g[i][:, f:], want_grads[2 * i + 1])):
+            r = ((got - gw).norm() / gw.norm().clamp_min(1e-12)).item()
+            assert r < 8e-2, (i, r)
+
+
+def _torch_reference_masked(weights, x, layers, labels, keep):
+    """_torch_reference with the loss averaged over rows whose label is >= 0."""
+    h = x.clone()
+    params = []
+    for i, (l, (wn, ws)) in enumerate(zip(layers, weights)):
+        wn = wn.clone().requires_grad_(True)
+        ws = ws.clone().requires_grad_(True)
+        params += [wn, ws]
+        ip = l.indptr.long()
+        deg = (ip[1:] - ip[:-1])
+        dst = torch.repeat_interleave(torch.arange(l.num_dst, device=x.device), deg)
+        acc = torch.zeros((l.num_dst, h.shape[1]), device=x.device).index_add(
+            0, dst, h[l.src_local.long()])
+        mean = acc / deg.clamp_min(1).unsqueeze(1).float()
+        h = h[:l.num_dst] @ ws.t() + mean @ wn.t()
+        if i != len(layers) - 1:
+            h = torch.relu(h)
+    logp = torch.log_softmax(h, dim=-1)
+    loss = torch.nn.functional.nll_loss(logp[keep], labels[keep])
+    loss.backward()
+    return h.detach(), loss.detach(), [p.grad for p in params]
+
+
+def test_trainer_with_fused_head_matches_default():
+    a, _ = _small_trainer(True)
+    b, _ = _small_trainer(True)
+    b.model.use_head = True
+    for tr in (a, b):
+        tr.set_epoch(0)
+        tr.begin_epoch()
+        tr.run_steps(0, 8)
+        torch.cuda.synchronize()
+    la, lb = a.losses[:8].cpu().numpy(), b.losses[:8].cpu().numpy()
+    assert np.allclose(la, lb, rtol=2e-2, atol=1e-3), (la, lb)
