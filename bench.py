@@ -73,6 +73,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--kernel-batches", type=int, default=20)
+    p.add_argument("--prep-batches", type=int, default=160,
+                   help="batches of the drop-in run_epoch_prep measurement (0 = skip)")
     p.add_argument("--mode", choices=["train", "infer"], default="train",
                    help="infer: sampled inference over all test ids (config c5, fanout "
                         "--fanouts, default 20,20,20 in this mode)")
@@ -266,6 +268,37 @@ def kernel_profile(trainer, nbatches: int):
     }
 
 
+def prep_epoch_profile(trainer, nbatches: int, workers=(1, 8)):
+    """The drop-in path of the reference's headline (batch preparation only):
+    run_epoch_prep over the first `nbatches` batches of the epoch plan with the
+    reference's output contract (full MFG, features gathered to f32, labels),
+    `num_workers` batches prepared concurrently; extrapolated to the epoch."""
+    from paper_2110_08450_b200 import PrepConfig, run_epoch_prep
+    from paper_2110_08450_b200.prep import EpochPlan
+    plan = trainer.plan
+    sub = EpochPlan(batches=plan.batches[:nbatches], batch_size=plan.batch_size,
+                    shuffle_seed=plan.shuffle_seed)
+    x = trainer.dg.feature_view()
+    out = {}
+    for p in workers:
+        cfg = PrepConfig(num_workers=p, fanouts=trainer.cfg.fanouts, feature_dtype="f32")
+        for _ in run_epoch_prep(trainer.dg, x, trainer.dg.labels,
+                                EpochPlan(batches=plan.batches[:2 * p], batch_size=plan.batch_size,
+                                          shuffle_seed=0), cfg, trainer.cfg.global_seed):
+            pass  # warm-up (workspaces, streams)
+        torch.cuda.synchronize()
+        run = run_epoch_prep(trainer.dg, x, trainer.dg.labels, sub, cfg, trainer.cfg.global_seed)
+        edges = 0
+        t0 = time.perf_counter()
+        for b in run:
+            edges += b.num_edges
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        out[f"P{p}"] = {"epoch_s": wall * len(plan) / len(sub), "sampled_edges_per_s": edges / wall,
+                        "batches": len(sub)}
+    return out
+
+
 def cpu_baseline(dg, trainer, fanouts, target_s: float, global_seed: int):
     """Reference CPU prep path (oracle port) on all host cores, bounded sample."""
     sys.path.insert(0, str(REPO / "oracle"))
@@ -405,6 +438,7 @@ def run_ours(args):
                "path": "Trainer.run_steps(host_inputs=True): each step's seeds + batch "
                        "descriptor H2D from pinned host memory, loss D2H to pinned memory"}
     kp = kernel_profile(tr, args.kernel_batches) if rank == 0 else None
+    pe = prep_epoch_profile(tr, args.prep_batches) if rank == 0 and args.prep_batches else None
     line = None
     if rank == 0:
         peaks = measured_peaks()
@@ -434,6 +468,10 @@ def run_ours(args):
             "sampled_edges_per_s": kp["sampled_edges_per_s"],
             "gather_GBps": kp["gather_GBps"],
             "kernels": kp,
+            "prep_epoch": None if pe is None else dict(
+                pe, what="drop-in run_epoch_prep (reference contract: full MFG, f32 features, "
+                         "labels), num_workers batches on concurrent streams, first batches of "
+                         "the plan extrapolated to the epoch; compare cpu_baseline"),
             "roofline": {"kernel": "segment_mean_rows_pipe_kernel (layer-0 mean over the "
                                    "sampled edges, rows read from the HBM feature table)",
                          "bound": "hbm", "achieved": round(kp["l0_mean_GBps"], 1), "peak": peak,

@@ -2,8 +2,9 @@
 
 The reference prepares batches with P CPU threads, a bounded queue and a
 pool of reusable host buffers (prep.py:226-334).  Here every batch is
-prepared by GPU-wide kernels on a dedicated CUDA stream; `depth` batches are
-in flight ahead of the consumer, each in its own device slot (MFG workspace
+prepared by GPU-wide kernels; `num_workers` batches are prepared concurrently
+on their own CUDA streams and `depth` batches are in flight ahead of the
+consumer, each in its own device slot (MFG workspace
 + feature + label buffers), so sampling/slicing of batch i+1.. overlaps
 whatever the consumer runs for batch i on its own stream.  A slot is
 recycled only after the consumer stream has passed an event recorded when
@@ -60,7 +61,7 @@ def make_epoch_plan(train_ids, batch_size: int, shuffle_seed: int) -> EpochPlan:
 @dataclass
 class PrepConfig:
     """prep.py:55-72.  On the GPU `num_workers` is the number of batches
-    prepared ahead of the consumer (prefetch depth)."""
+    prepared concurrently (one CUDA stream each) and ahead of the consumer."""
 
     num_workers: int = 1
     queue_capacity: int = 0
@@ -350,7 +351,10 @@ class EpochPrepRun:
         depth = cfg.depth
         slots = [_Slot(dg, cfg, max_seeds, cols, dg.device) for _ in range(depth + 1)]
         self._free = list(slots)
-        stream = torch.cuda.Stream(device=dg.device)
+        # num_workers batches are prepared concurrently, one CUDA stream each (the
+        # reference's P worker threads, prep.py:255-287)
+        streams = [torch.cuda.Stream(device=dg.device)
+                   for _ in range(max(1, min(cfg.num_workers, depth)))]
         # the whole plan goes to HBM once: seeds + one sal_batch_desc per batch
         lens = np.array([len(b) for b in plan.batches], dtype=np.int64)
         offs = np.zeros(nb, dtype=np.int64)
@@ -370,7 +374,7 @@ class EpochPrepRun:
             slot.index = nxt
             try:
                 _prep_one(dg, x, yv, slot, plan.batches[nxt], seeds_all, desc_all[nxt],
-                          self._seed, policy, stream)
+                          self._seed, policy, streams[nxt % len(streams)])
             except Exception as exc:
                 raise RuntimeError("batch preparation worker failed") from exc
             pending.append(slot)
@@ -399,8 +403,9 @@ class EpochPrepRun:
         finally:
             if current is not None:
                 current.release()
-            torch.cuda.current_stream().wait_stream(stream)
-            stream.synchronize()
+            for st in streams:
+                torch.cuda.current_stream().wait_stream(st)
+                st.synchronize()
             self.report.both_s = time.perf_counter() - t0
 
 
