@@ -303,10 +303,13 @@ int sal_step_tail(float* loss_dev, float* last_dev, float* log_dev, int64_t log_
 /* ---- tcgen05 GEMMs of the layer-0 SAGEConv (sm_100a tensor cores) -------- */
 /* Y = act(A[M,K] @ W[N,K]^T), bf16 in, fp32 TMEM accumulate, bf16 out; with
  * relu_dropout != 0 the epilogue applies ReLU + dropout (same stream as
- * sal_relu_dropout_fwd) and writes the bit mask [M, N/8].  N = K = 256. */
-int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const void* W_dev, int32_t N,
-                    int32_t K, void* Y_dev, int64_t ldy, uint8_t* mask_dev, float p,
-                    uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout, void* stream);
+ * sal_relu_dropout_fwd) and writes the bit mask [M, N/8].  N = K = 256.
+ * m_dev (nullable): true row count on the device; 128-row tiles past it are
+ * zero-filled (Y and mask) without loading A or running the MMA. */
+int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const int64_t* m_dev,
+                    const void* W_dev, int32_t N, int32_t K, void* Y_dev, int64_t ldy,
+                    uint8_t* mask_dev, float p, uint64_t seed, const int64_t* salt_dev,
+                    int32_t relu_dropout, void* stream);
 /* dW[N,K] (fp32, row stride lddw) = dz[M,N]^T @ A[M,K]; zeroes dW first
  * unless `accumulate` (then dW += ...: the caller guarantees dW was zero).
  * 128 x 128 output tiles x split-K over M (about one CTA per SM), partials

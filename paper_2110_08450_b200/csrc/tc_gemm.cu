@@ -459,8 +459,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
 sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
                        const __grid_constant__ CUtensorMap mapW,
                        const __grid_constant__ CUtensorMap mapY, int M,
-                       uint8_t* __restrict__ mask, float p, uint64_t seed,
-                       const int64_t* __restrict__ salt, int relu_dropout) {
+                       const int64_t* __restrict__ m_dev, uint8_t* __restrict__ mask, float p,
+                       uint64_t seed, const int64_t* __restrict__ salt, int relu_dropout) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sB = smem;
@@ -475,6 +475,10 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kSStages + 5);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (M + kFM - 1) / kFM;
+  // tiles past the true row count (*m_dev, static shapes pad to M) are only
+  // zero-filled: no TMA loads, no MMA
+  const int m_true = m_dev ? (int)min((int64_t)M, *m_dev) : M;
+  const int nfull = (m_true + kFM - 1) / kFM;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < kSStages; ++i) {
@@ -510,7 +514,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
         tma_load_2d(smem_u32(sB) + kb * (kFN * 128), &mapW, kb * kFKB, 0, bfull);
       int stage = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = blockIdx.x; t < nfull; t += gridDim.x) {
         for (int kb = 0; kb < kFK / kFKB; ++kb) {
           mbar_wait(&empty[stage], ph ^ 1);
           mbar_expect_tx(&full[stage], kPABlk);
@@ -525,7 +529,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
     int stage = 0;
     uint32_t ph = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (int t = blockIdx.x; t < nfull; t += gridDim.x, ++it) {
       const int buf = it & 1;
       const uint32_t tph = (uint32_t)((it >> 1) & 1);
       mbar_wait(&tempty[buf], tph ^ 1);
@@ -558,7 +562,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
     const uint32_t thresh = (uint32_t)(p * 65536.0f);
     const uint64_t key_base = mix64(seed ^ mix64((salt ? (uint64_t)*salt : 0ull) + 0x5EEDull));
     int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (int t = blockIdx.x; t < nfull; t += gridDim.x, ++it) {
       const int buf = it & 1;
       mbar_wait(&tfull[buf], (uint32_t)((it >> 1) & 1));
       tc_fence_after();
@@ -591,6 +595,31 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+    // padding tiles: zero rows (finite, zero-gradient) without touching A or TMEM
+    const int first_pad = blockIdx.x + ((nfull - (int)blockIdx.x + (int)gridDim.x - 1) /
+                                        (int)gridDim.x) * (int)gridDim.x;
+    if (first_pad < ntiles) {
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(stg + lane * 64 + (q << 4)) = make_uint4(0, 0, 0, 0);
+      fence_async_smem();
+      __syncwarp();
+      for (int t = first_pad > (int)blockIdx.x ? first_pad : (int)blockIdx.x; t < ntiles;
+           t += gridDim.x) {
+        if (t < nfull) continue;
+        const int row0 = t * kFM + lg * 32;
+        for (int c = cq * (kFN / 4); c < (cq + 1) * (kFN / 4); c += 32) {
+          if (lane == 0) {
+            tma_store_2d(&mapY, stg_s, c, row0);
+            bulk_commit();
+          }
+          if (relu_dropout && row0 + lane < M)
+            *reinterpret_cast<uint32_t*>(mask + (int64_t)(row0 + lane) * (kFN / 8) + (c >> 3)) = 0u;
+        }
+      }
     }
     if (lane == 0) bulk_wait0();
   }
@@ -745,9 +774,9 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t
 
 extern "C" {
 
-int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const void* W, int32_t N, int32_t K,
-                    void* Y, int64_t ldy, uint8_t* mask, float p, uint64_t seed,
-                    const int64_t* salt_dev, int32_t relu_dropout, void* stream) {
+int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const int64_t* m_dev, const void* W,
+                    int32_t N, int32_t K, void* Y, int64_t ldy, uint8_t* mask, float p,
+                    uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout, void* stream) {
   if (N != sal::tc::kFN || K != sal::tc::kFK) return SAL_EINVAL;
   if (lda % 8 || ldy % 8 || ((uintptr_t)A & 15) || ((uintptr_t)W & 15) || ((uintptr_t)Y & 15))
     return SAL_EINVAL;
@@ -769,8 +798,8 @@ int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const void* W, int32_
     attr = true;
   }
   sal::tc::sage_fwd_tma_st_kernel<<<grid, sal::tc::kSThreads, sal::tc::kSSmem,
-                                    (cudaStream_t)stream>>>(mA, mW, mY, (int)M, mask, p, seed,
-                                                            salt_dev, relu_dropout);
+                                    (cudaStream_t)stream>>>(mA, mW, mY, (int)M, m_dev, mask, p,
+                                                            seed, salt_dev, relu_dropout);
   if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
   sal::count_launch(1);
   return SAL_OK;

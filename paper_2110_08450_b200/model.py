@@ -301,7 +301,8 @@ class FusedSAGE:
                 if self._tc_layer(i):
                     # tcgen05 GEMM with the ReLU/dropout epilogue: z never reaches HBM
                     _lib.check(L.sal_tc_sage_fwd(
-                        a.data_ptr(), a.stride(0), n_pad, self.wb[i].data_ptr(), fo, 2 * f,
+                        a.data_ptr(), a.stride(0), n_pad, _lib.ptr(n_dev), self.wb[i].data_ptr(),
+                        fo, 2 * f,
                         nxt[:, fo:].data_ptr(), nxt.stride(0), mask.data_ptr(), p, seed,
                         _lib.ptr(salt), 1, st), "tc_sage_fwd")
                 else:

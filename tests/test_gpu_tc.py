@@ -7,12 +7,13 @@ from paper_2110_08450_b200 import _lib
 pytestmark = pytest.mark.gpu
 
 
-def _fwd(A, W, p=0.0, relu=True, seed=7, salt=None, out_cols=256):
+def _fwd(A, W, p=0.0, relu=True, seed=7, salt=None, out_cols=256, m_dev=None, fill=0.0):
     M = A.shape[0]
-    Y = torch.zeros((M, 2 * out_cols), dtype=torch.bfloat16, device="cuda")[:, out_cols:]
-    mask = torch.zeros(M * 256 // 8, dtype=torch.uint8, device="cuda")
+    Y = torch.full((M, 2 * out_cols), fill, dtype=torch.bfloat16, device="cuda")[:, out_cols:]
+    mask = torch.full((M * 256 // 8,), 255 if fill else 0, dtype=torch.uint8, device="cuda")
     L = _lib.lib()
-    _lib.check(L.sal_tc_sage_fwd(A.data_ptr(), A.stride(0), M, W.data_ptr(), 256, 256,
+    _lib.check(L.sal_tc_sage_fwd(A.data_ptr(), A.stride(0), M, _lib.ptr(m_dev), W.data_ptr(),
+                                 256, 256,
                                  Y.data_ptr(), Y.stride(0), mask.data_ptr(), p, seed,
                                  _lib.ptr(salt), int(relu), _lib.stream_ptr()), "tc_sage_fwd")
     torch.cuda.synchronize()
@@ -81,3 +82,21 @@ def test_tc_wgrad_matches_torch(M, N, K):
     assert ((dW2 - 0.5 - want).norm() / want.norm()).item() < 1e-3
     err = (dW - want).norm() / want.norm()
     assert err < 1e-3, err
+
+
+@pytest.mark.parametrize("m_true", [0, 1, 300, 1000, 4096])
+def test_tc_fwd_true_row_count_zero_fills_padding(m_true):
+    """Static shapes pad to M; rows past *m_dev come out zero (Y and mask) and the
+    rows before it equal the full computation."""
+    M = 4096
+    g = torch.Generator(device="cuda").manual_seed(9)
+    A = (torch.randn(M, 256, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(256, 256, device="cuda", generator=g) * 0.06).to(torch.bfloat16)
+    salt = torch.tensor([3], dtype=torch.int64, device="cuda")
+    Yf, mf = _fwd(A, W, p=0.5, relu=True, seed=11, salt=salt)
+    md = torch.tensor([m_true], dtype=torch.int64, device="cuda")
+    Yp, mp = _fwd(A, W, p=0.5, relu=True, seed=11, salt=salt, m_dev=md, fill=7.0)
+    tile_end = min(M, -(-m_true // 128) * 128)   # whole 128-row tiles are computed
+    assert torch.equal(Yp[:tile_end], Yf[:tile_end])
+    assert torch.equal(mp[:tile_end * 32], mf[:tile_end * 32])
+    assert (Yp[tile_end:] == 0).all() and (mp[tile_end * 32:] == 0).all()

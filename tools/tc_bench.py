@@ -42,7 +42,7 @@ def t(fn, it=50):
 
 
 def fwd_tma():
-    _lib.check(L.sal_tc_sage_fwd(A.data_ptr(), A.stride(0), M, W.data_ptr(), 256, 256,
+    _lib.check(L.sal_tc_sage_fwd(A.data_ptr(), A.stride(0), M, None, W.data_ptr(), 256, 256,
                                  Y.data_ptr(), Y.stride(0), mask.data_ptr(), 0.5, 1,
                                  salt.data_ptr(), 1, st()))
 
