@@ -412,7 +412,9 @@ static bool fwd_rows(const int32_t* indptr, const int32_t* src, const int32_t* g
   TOut* op = (TOut*)out;
   // Software-pipelined persistent kernel for the training layer-0 shape (128-d
   // 16-bit rows, <= 128 K destinations): 42.3 -> 38.3 us alone, -1.6 % per
-  // training step.  Not for 512 B rows (neutral) nor for the (20,20,20)
+  // training step (random 256 B row reads alone take 32.8 us, tools/randread_bench.cu).
+  // A variant streaming the rows into shared memory with one cp.async.bulk per
+  // row, S = 3 stages of 32 rows per warp, was correct but took 93 us.  Not for 512 B rows (neutral) nor for the (20,20,20)
   // inference layer 0 (450 K destinations), where the persistent grid starves
   // the overlapped prep chain: the pass took 0.098 s with it, 0.084 s without.
   if ((lpr == 8 || lpr == 16) && n_pad <= 131072) {
