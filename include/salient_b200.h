@@ -305,7 +305,9 @@ int sal_step_tail(float* loss_dev, float* last_dev, float* log_dev, int64_t log_
  * relu_dropout != 0 the epilogue applies ReLU + dropout (same stream as
  * sal_relu_dropout_fwd) and writes the bit mask [M, N/8].  N = K = 256.
  * m_dev (nullable): true row count on the device; 128-row tiles past it are
- * zero-filled (Y and mask) without loading A or running the MMA. */
+ * zero-filled (Y and mask) without loading A or running the MMA, or left
+ * unwritten when relu_dropout has bit 1 set (a caller that never reads the
+ * padding rows, e.g. inference). */
 int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const int64_t* m_dev,
                     const void* W_dev, int32_t N, int32_t K, void* Y_dev, int64_t ldy,
                     uint8_t* mask_dev, float p, uint64_t seed, const int64_t* salt_dev,

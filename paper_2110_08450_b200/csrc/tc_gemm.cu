@@ -118,6 +118,10 @@ constexpr uint32_t kBBytes = kFN * kFK * 2;     // 128 KB
 constexpr uint32_t kABytes = kFM * kFK * 2;     // 64 KB
 constexpr uint32_t kFSmem = kBBytes + kABytes + 1024 + 64;
 
+// sal_tc_sage_fwd flags (the relu_dropout argument): bit 0 = ReLU + dropout
+// epilogue, bit 1 = leave the padding tiles past *m_dev unwritten
+constexpr int kReluDropout = 1, kNoPadFill = 2;
+
 // Epilogue element math shared by the forward kernels: 32 consecutive fp32
 // accumulator columns [c, c+32) of one row -> relu + dropout (scaled) in bf16
 // plus the 32 keep bits; the dropout stream is relu_dropout_fwd_kernel's
@@ -126,7 +130,7 @@ SAL_DEVINL uint32_t relu_dropout32(const uint32_t* r, int64_t row, int c, int re
                                    float p, float scale, uint32_t thresh, uint64_t key_base,
                                    __nv_bfloat16* o) {
   uint32_t bits = 0;
-  if (!relu_dropout) {
+  if (!(relu_dropout & kReluDropout)) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) o[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
     return 0;
@@ -589,17 +593,18 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
           tma_store_2d(&mapY, stg_s, c, row0);
           bulk_commit();
         }
-        if (relu_dropout && row < M)
+        if ((relu_dropout & kReluDropout) && row < M)
           *reinterpret_cast<uint32_t*>(mask + (int64_t)row * (kFN / 8) + (c >> 3)) = bits;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
     }
-    // padding tiles: zero rows (finite, zero-gradient) without touching A or TMEM
+    // padding tiles: zero rows (finite, zero-gradient) without touching A or TMEM;
+    // skipped entirely when the caller does not consume padding rows (kNoPadFill)
     const int first_pad = blockIdx.x + ((nfull - (int)blockIdx.x + (int)gridDim.x - 1) /
                                         (int)gridDim.x) * (int)gridDim.x;
-    if (first_pad < ntiles) {
+    if (first_pad < ntiles && !(relu_dropout & kNoPadFill)) {
       if (lane == 0) bulk_wait_read0();
       __syncwarp();
 #pragma unroll
@@ -616,7 +621,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
             tma_store_2d(&mapY, stg_s, c, row0);
             bulk_commit();
           }
-          if (relu_dropout && row0 + lane < M)
+          if ((relu_dropout & kReluDropout) && row0 + lane < M)
             *reinterpret_cast<uint32_t*>(mask + (int64_t)(row0 + lane) * (kFN / 8) + (c >> 3)) = 0u;
         }
       }

@@ -308,7 +308,8 @@ class FusedSAGE:
                         a.data_ptr(), a.stride(0), n_pad, _lib.ptr(n_dev), self.wb[i].data_ptr(),
                         fo, 2 * f,
                         nxt[:, fo:].data_ptr(), nxt.stride(0), mask.data_ptr(), p, seed,
-                        _lib.ptr(salt), 1, st), "tc_sage_fwd")
+                        # eval: nothing reads the padding rows (no backward), skip filling
+                        _lib.ptr(salt), 1 if self.training else 3, st), "tc_sage_fwd")
                 else:
                     z = torch.mm(a[:n_pad], self.wb[i].t())
                     _lib.check(L.sal_relu_dropout_fwd(
