@@ -249,6 +249,34 @@ def kernel_profile(trainer, nbatches: int):
         e0 += etot[h0]
         d0 += sizes[h0]
     k = nbatches - 1
+    # the MFG build as the pipelines run it: captured in a CUDA graph (plan cursor ->
+    # sal_sample_mfg), batches 1..k of the plan replayed back to back
+    cursor = torch.ones(1, dtype=torch.int64, device=trainer.device)
+    gdesc = torch.zeros(3, dtype=torch.int64, device=trainer.device)
+
+    def build():
+        _lib.check(Lb.sal_plan_next(trainer.desc_all.data_ptr(), trainer.n_steps_dev,
+                                    cursor.data_ptr(), gdesc.data_ptr(),
+                                    _lib.stream_ptr(torch.cuda.current_stream())), "plan_next")
+        ws.run(trainer.dg, trainer.seeds_all, gdesc, trainer.cfg.global_seed, trainer.policy,
+               torch.cuda.current_stream())
+    side = torch.cuda.Stream(device=trainer.device)
+    side.wait_stream(st)
+    with torch.cuda.stream(side):
+        build()
+    st.wait_stream(side)
+    torch.cuda.synchronize()
+    gmfg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gmfg):
+        for _ in range(k):
+            build()
+    cursor.fill_(1)
+    torch.cuda.synchronize()
+    ev[0].record(st)
+    gmfg.replay()
+    ev[1].record(st)
+    torch.cuda.synchronize()
+    t_mfg_graph = ev[0].elapsed_time(ev[1]) / 1e3
     # batch-parallel MFG build: P batches sampled concurrently on P streams (the
     # throughput the epoch prep and inference pipelines can draw on)
     P = 8
@@ -290,6 +318,8 @@ def kernel_profile(trainer, nbatches: int):
         "l0_mean_bytes_per_launch": mean_bytes / k,
         "l0_edges_per_batch": e0 / k,
         "sampled_edges_per_s_8_concurrent": e_par / t_par,
+        "sampled_edges_per_s_graph": edges / t_mfg_graph,
+        "mfg_ms_per_batch_graph": 1e3 * t_mfg_graph / k,
     }
 
 
@@ -490,7 +520,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "e2e": e2e,
-            "sampled_edges_per_s": kp["sampled_edges_per_s"],
+            "sampled_edges_per_s": kp["sampled_edges_per_s_graph"],
             "gather_GBps": kp["gather_GBps"],
             "kernels": kp,
             "prep_epoch": None if pe is None else dict(
