@@ -201,10 +201,11 @@ def kernel_profile(trainer, nbatches: int):
     """Prep-only pass timed with CUDA events on the launching stream.
 
     Per batch: the MFG build (sal_sample_mfg: count/sample/relabel x 3 hops),
-    the full row gather of all N sampled nodes (sal_gather_rows, fp16 -> fp16,
-    the drop-in slice_features kernel) and the layer-0 mean aggregation read
-    straight from the HBM feature table (sal_segment_mean_fwd over the last
-    hop's edges — the largest kernel of the training step)."""
+    the layer-0 mean aggregation read straight from the HBM feature table
+    (sal_segment_mean_fwd over the last hop's edges — the largest kernel of the
+    training step, which also runs right after the sampler there) and the full
+    row gather of all N sampled nodes (sal_gather_rows, fp16 -> fp16, the
+    drop-in slice_features kernel)."""
     from paper_2110_08450_b200 import _lib
     from paper_2110_08450_b200.prep import gather_rows
     from paper_2110_08450_b200.sampler import MfgWorkspace
@@ -230,20 +231,22 @@ def kernel_profile(trainer, nbatches: int):
         ws.run(trainer.dg, trainer.seeds_all, trainer.desc_all[step], trainer.cfg.global_seed,
                trainer.policy, st)
         ev[1].record(st)
-        gather_rows(x, ws.globals, out_buf, n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
-                    stream=st)
-        ev[2].record(st)
+        # the layer-0 mean right after the sampler, as in the training step (its edge
+        # ids are still in L2); then the drop-in full row gather
         _lib.check(Lb.sal_segment_mean_fwd(
             ws.dst_indptr[h0].data_ptr(), ws.src_glob.data_ptr(), ws.sizes[h0:h0 + 1].data_ptr(),
             ws.node_cap[h0], x.data_ptr(), _lib.SAL_F16, x.stride(0), f, mean_buf.data_ptr(),
             _lib.SAL_BF16, mean_buf.stride(0), _lib.stream_ptr(st)), "segment_mean_fwd")
+        ev[2].record(st)
+        gather_rows(x, ws.globals, out_buf, n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
+                    stream=st)
         ev[3].record(st)
         sizes, etot = ws.read_extents()
         if b == 0:
             continue  # warm-up
         t_mfg += ev[0].elapsed_time(ev[1]) / 1e3
-        t_gat += ev[1].elapsed_time(ev[2]) / 1e3
-        t_mean += ev[2].elapsed_time(ev[3]) / 1e3
+        t_mean += ev[1].elapsed_time(ev[2]) / 1e3
+        t_gat += ev[2].elapsed_time(ev[3]) / 1e3
         edges += sum(etot)
         nodes += sizes[-1]
         e0 += etot[h0]
