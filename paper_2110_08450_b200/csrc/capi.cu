@@ -141,6 +141,25 @@ int sal_mfg_plan_init_ex(sal_mfg_plan* plan, int32_t num_hops, const int32_t* pe
   return SAL_OK;
 }
 
+// The look-back scan workspaces of one MFG build: hop h's count scan and its
+// flag scan each get their own region inside layout.scan, so a single memset at
+// hop 0 zeroes all of them and no scan waits on a reset.
+static int64_t scan_region(const sal_mfg_plan* plan, int h, int flag, int64_t* bytes) {
+  int64_t off = 0;
+  for (int k = 0; k < plan->num_hops; ++k)
+    for (int q = 0; q < 2; ++q) {
+      const int64_t items = q ? plan->edge_cap[k] : plan->node_cap[k];
+      const int64_t b = ((int64_t)sal::scan_ws_bytes(items > 0 ? items : 1) + 255) / 256 * 256;
+      if (k == h && q == flag) {
+        if (bytes) *bytes = b;
+        return off;
+      }
+      off += b;
+    }
+  if (bytes) *bytes = 0;
+  return off;  // total
+}
+
 int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* L) {
   if (plan == nullptr || L == nullptr) return fail(SAL_EINVAL, "layout: null argument");
   memset(L, 0, sizeof(*L));
@@ -167,8 +186,8 @@ int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* L) {
   L->src_glob = take(max_e * 4 + 4);
   L->slot = take(max_e * 4 + 4);
   L->rank = take(max_e * 4 + 4);
-  const int64_t scan_items = max_e > max_d ? max_e : max_d;
-  L->scan_bytes = (int64_t)sal::scan_ws_bytes(scan_items);
+  (void)max_d;
+  L->scan_bytes = scan_region(plan, plan->num_hops, 0, nullptr);
   L->scan = take(L->scan_bytes);
   L->total = off;
   return SAL_OK;
@@ -211,28 +230,26 @@ int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan, const sal
                 plan->num_hops);
   cudaError_t e = cudaSuccess;
   int kernels = 0;
-  // one shared look-back workspace: every later scan finds it zeroed by the
-  // kernel before it (sample(h) -> flag scan(h); resolve(h) -> count(h+1)), so
-  // the hops add no memset nodes
-  sal::ZeroJob zws;
-  zws.p = (uint32_t*)scan;
-  zws.words = (L->scan_bytes + 3) / 4;
+  // every scan has its own zeroed region (scan_region); hop 0's count runs on its
+  // own, each later count rides in the previous hop's resolve launch
+  auto scan_ws = [&](int h, int flag) { return (void*)(scan + scan_region(plan, h, flag, nullptr)); };
   if (hop_begin == 0) {
-    // table + first scan workspace as memset nodes: measured faster in the
+    // table + all scan workspaces as memset nodes: measured faster in the
     // overlapped step than a reset kernel, which takes SM slots from training
     e = cudaMemsetAsync(m.table, 0xFF, plan->table_cap * 8, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(scan, 0, L->scan_bytes, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: table reset");
     e = sal::launch_seed_insert(seeds_base, desc, m, plan->max_seeds, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: seed insert");
-    kernels = 1;
+    e = sal::launch_hop_count(gd, m.globals, sizes, plan->node_cap[0], plan->fanout[0],
+                              (int32_t*)(base + L->dst_indptr[0]), etot, scan_ws(0, 0), st,
+                              /*ws_zeroed=*/true);
+    if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop count");
+    kernels = 2;
   }
   for (int h = hop_begin; h < hop_end; ++h) {
     int32_t* dst_indptr = (int32_t*)(base + L->dst_indptr[h]);
     int32_t* src_local = (int32_t*)(base + L->src_local[h]);
-    e = sal::launch_hop_count(gd, m.globals, sizes + h, plan->node_cap[h], plan->fanout[h],
-                              dst_indptr, etot + h, scan, st, /*ws_zeroed=*/true);
-    if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop count");
     sal::HopKey hk;
     hk.prefix = 0;
     hk.global_seed = global_seed;
@@ -248,17 +265,27 @@ int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan, const sal
                                  desc, rng_policy, nullptr, dst_indptr, src_glob, nullptr,
                                  nullptr, st, plan->sample_lanes, plan->sample_blocks_per_sm);
       if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
-      return counted(SAL_OK, kernels + 2);
+      return counted(SAL_OK, kernels + 1);
     }
     e = sal::launch_hop_sample(gd, m, sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
                                rng_policy, nullptr, dst_indptr, src_glob, slot, nullptr, st,
-                               plan->sample_lanes, plan->sample_blocks_per_sm, zws);
+                               plan->sample_lanes, plan->sample_blocks_per_sm);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
+    sal::NextCount nc;
+    const bool has_next = h + 1 < plan->num_hops;
+    if (has_next) {
+      nc.g = gd;
+      nc.fanout = plan->fanout[h + 1];
+      nc.max_dst = plan->node_cap[h + 1];
+      nc.dst_indptr = (int32_t*)(base + L->dst_indptr[h + 1]);
+      nc.e_total = etot + h + 1;
+      nc.scan_ws = scan_ws(h + 1, 0);
+    }
     e = sal::launch_hop_relabel(m, etot + h, plan->edge_cap[h], sizes + h, sizes + h + 1,
-                                src_glob, slot, rank, src_local, scan, st, /*ws_zeroed=*/true,
-                                h + 1 < plan->num_hops ? zws : sal::ZeroJob());
+                                src_glob, slot, rank, src_local, scan_ws(h, 1), st,
+                                /*ws_zeroed=*/true, has_next ? &nc : nullptr);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop relabel");
-    kernels += 4;
+    kernels += 3;
   }
   return counted(SAL_OK, kernels);
 }

@@ -63,11 +63,6 @@ SAL_DEVINL void table_insert_assigned(unsigned long long* table, int log2cap, ui
 // ---------------------------------------------------------------------------
 // seeds -> locals 0..n-1 (sampler.py:336-340: id_map.insert(seeds.dst_ids))
 // ---------------------------------------------------------------------------
-SAL_DEVINL void side_zero(const ZeroJob& zj) {
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < zj.words;
-       w += (int64_t)gridDim.x * blockDim.x)
-    zj.p[w] = 0u;
-}
 
 __global__ void seed_insert_kernel(const int64_t* __restrict__ seeds_base,
                                    const BatchDesc* __restrict__ desc,
@@ -99,10 +94,11 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-__global__ void __launch_bounds__(kScanThreads)
-count_scan_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ globals,
-                  const int64_t* __restrict__ n_dst_ptr, int32_t fanout,
-                  int32_t* __restrict__ dst_indptr, int64_t* __restrict__ e_total, ScanWs ws) {
+SAL_DEVINL void count_scan_tile(const int64_t* __restrict__ indptr,
+                                const int32_t* __restrict__ globals,
+                                const int64_t* __restrict__ n_dst_ptr, int32_t fanout,
+                                int32_t* __restrict__ dst_indptr, int64_t* __restrict__ e_total,
+                                ScanWs ws) {
   __shared__ uint64_t sh_scan[kScanThreads / kWarp + 1];
   __shared__ uint64_t sh_prefix;
   __shared__ int sh_tile;
@@ -138,6 +134,13 @@ count_scan_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
     dst_indptr[n] = (int32_t)(prefix + tile_total);
     *e_total = (int64_t)(prefix + tile_total);
   }
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+count_scan_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ globals,
+                  const int64_t* __restrict__ n_dst_ptr, int32_t fanout,
+                  int32_t* __restrict__ dst_indptr, int64_t* __restrict__ e_total, ScanWs ws) {
+  count_scan_tile(indptr, globals, n_dst_ptr, fanout, dst_indptr, e_total, ws);
 }
 
 // ---------------------------------------------------------------------------
@@ -191,8 +194,7 @@ sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restri
                      const int64_t* __restrict__ inject_pos, const int32_t* __restrict__ dst_indptr,
                      unsigned long long* table, int log2cap, int32_t* src_glob,
                      int32_t* __restrict__ slot, int32_t* __restrict__ draws_out,
-                     int64_t* __restrict__ size_unknown, ZeroJob zj) {
-  side_zero(zj);
+                     int64_t* __restrict__ size_unknown) {
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, gl = lane % G;
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
@@ -328,16 +330,14 @@ flag_scan_kernel(const unsigned long long* __restrict__ table, const int32_t* __
 
 // relabel pass 2: every edge resolves its local id; first occurrences
 // finalize their slot so the next hop sees an assigned entry.
-__global__ void resolve_kernel(unsigned long long* table, const int32_t* __restrict__ slot,
-                               const int64_t* __restrict__ e_total,
-                               const int64_t* __restrict__ size_old_ptr,
-                               const int32_t* __restrict__ rank_of,
-                               int32_t* __restrict__ src_local, ZeroJob zj) {
-  side_zero(zj);
+SAL_DEVINL void resolve_range(unsigned long long* table, const int32_t* __restrict__ slot,
+                              const int64_t* __restrict__ e_total,
+                              const int64_t* __restrict__ size_old_ptr,
+                              const int32_t* __restrict__ rank_of,
+                              int32_t* __restrict__ src_local, int64_t first, int64_t stride) {
   const int64_t n = *e_total;
   const int64_t size_old = *size_old_ptr;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = first; e < n; e += stride) {
     const int32_t s = slot[e];
     const unsigned long long w = *((volatile unsigned long long*)&table[s]);
     const uint32_t lo = (uint32_t)w;
@@ -351,6 +351,40 @@ __global__ void resolve_kernel(unsigned long long* table, const int32_t* __restr
     }
     if (src_local != nullptr) src_local[e] = (int32_t)local;
   }
+}
+
+__global__ void resolve_kernel(unsigned long long* table, const int32_t* __restrict__ slot,
+                               const int64_t* __restrict__ e_total,
+                               const int64_t* __restrict__ size_old_ptr,
+                               const int32_t* __restrict__ rank_of,
+                               int32_t* __restrict__ src_local) {
+  resolve_range(table, slot, e_total, size_old_ptr, rank_of, src_local,
+                blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
+// resolve of hop h and the count + scan of hop h+1 in one launch: both read only
+// what flag_scan(h) wrote (the new locals' global ids, the new map size), so the
+// first `resolve_blocks` blocks resolve edges while the rest scan destinations
+struct CountJob {
+  const int64_t* indptr;
+  const int32_t* globals;
+  const int64_t* n_dst;
+  int32_t fanout;
+  int32_t* dst_indptr;
+  int64_t* e_total;
+  ScanWs ws;
+};
+__global__ void __launch_bounds__(kScanThreads)
+resolve_count_kernel(unsigned long long* table, const int32_t* __restrict__ slot,
+                     const int64_t* __restrict__ e_total, const int64_t* __restrict__ size_old_ptr,
+                     const int32_t* __restrict__ rank_of, int32_t* __restrict__ src_local,
+                     int resolve_blocks, CountJob cj) {
+  if ((int)blockIdx.x < resolve_blocks)
+    resolve_range(table, slot, e_total, size_old_ptr, rank_of, src_local,
+                  blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                  (int64_t)resolve_blocks * blockDim.x);
+  else
+    count_scan_tile(cj.indptr, cj.globals, cj.n_dst, cj.fanout, cj.dst_indptr, cj.e_total, cj.ws);
 }
 
 // ---------------------------------------------------------------------------
@@ -426,7 +460,7 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
                               int32_t policy, const int64_t* inject_pos,
                               const int32_t* dst_indptr, int32_t* src_glob, int32_t* slot,
                               int32_t* draws_out, cudaStream_t st, int lanes,
-                              int blocks_per_sm, ZeroJob zj) {
+                              int blocks_per_sm) {
   const int64_t warps_needed = max_dst > 0 ? max_dst : 1;
   int64_t grid = (warps_needed + 7) / 8;
   // default 8 blocks x 8 warps per SM, grid-stride
@@ -442,7 +476,7 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
 #define SAL_SAMPLE(P, GG)                                                                   \
   sample_insert_kernel<P, GG><<<(int)grid, 256, 0, st>>>(                                   \
       g.indptr, g.indices, m.globals, n_dst, fanout, hk, desc, inject_pos, dst_indptr, m.table, \
-      m.log2cap, src_glob, slot, draws_out, m.table == nullptr ? m.size_out : nullptr, zj)
+      m.log2cap, src_glob, slot, draws_out, m.table == nullptr ? m.size_out : nullptr)
   if (policy == kRngSplitmix) {
     if (G == 8) SAL_SAMPLE(kRngSplitmix, 8);
     else if (G == 16) SAL_SAMPLE(kRngSplitmix, 16);
@@ -471,7 +505,7 @@ cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_
                                const int64_t* size_old, int64_t* size_new,
                                const int32_t* src_glob, const int32_t* slot, int32_t* rank_of,
                                int32_t* src_local, void* scan_ws, cudaStream_t st,
-                               bool ws_zeroed, ZeroJob next) {
+                               bool ws_zeroed, const NextCount* next) {
   ScanWs ws = carve_scan_ws(scan_ws, max_edges);
   cudaError_t err;
   if (!ws_zeroed) {
@@ -485,8 +519,23 @@ cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_
   int64_t grid = (max_edges + 255) / 256;
   if (grid < 1) grid = 1;
   if (grid > num_sms() * 16) grid = num_sms() * 16;
-  resolve_kernel<<<(int)grid, 256, 0, st>>>(m.table, slot, e_total, size_old, rank_of, src_local,
-                                            next);
+  if (next == nullptr) {
+    resolve_kernel<<<(int)grid, 256, 0, st>>>(m.table, slot, e_total, size_old, rank_of,
+                                              src_local);
+    return cudaGetLastError();
+  }
+  // the next hop's count + scan rides in the same launch (its workspace is zeroed)
+  CountJob cj;
+  cj.indptr = next->g.indptr;
+  cj.globals = m.globals;
+  cj.n_dst = size_new;
+  cj.fanout = next->fanout;
+  cj.dst_indptr = next->dst_indptr;
+  cj.e_total = next->e_total;
+  cj.ws = carve_scan_ws(next->scan_ws, next->max_dst);
+  const int cgrid = scan_grid(next->max_dst);
+  resolve_count_kernel<<<(int)grid + cgrid, 256, 0, st>>>(m.table, slot, e_total, size_old,
+                                                          rank_of, src_local, (int)grid, cj);
   return cudaGetLastError();
 }
 

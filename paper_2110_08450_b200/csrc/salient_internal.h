@@ -35,13 +35,6 @@ struct HopKey {
   int32_t derive;
 };
 
-// Words a kernel zeroes on the side for its successor in a stream (the
-// look-back scan workspace of the next scan): replaces a memset node, whose
-// graph dependency edges cost ~5 us of latency each (profiles/, timeline).
-struct ZeroJob {
-  uint32_t* p = nullptr;
-  int64_t words = 0;
-};
 
 int num_sms();
 // thread-local error message of sal_last_error(); returns `code`
@@ -60,17 +53,25 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
                               int32_t policy, const int64_t* inject_pos,
                               const int32_t* dst_indptr, int32_t* src_glob, int32_t* slot,
                               int32_t* draws_out, cudaStream_t st, int lanes = 0,
-                              int blocks_per_sm = 0,
-                              ZeroJob zj = ZeroJob());
+                              int blocks_per_sm = 0);
 cudaError_t launch_rehash(const IdMapDev& m, int64_t n, cudaStream_t st);
 cudaError_t launch_keys_insert(const int64_t* keys, int64_t n, const IdMapDev& m,
                                int32_t* src_glob, int32_t* slot, int64_t* e_total,
                                cudaStream_t st);
+// the next hop's count + scan, fused into the resolve launch of this hop
+struct NextCount {
+  GraphDev g;
+  int32_t fanout;
+  int64_t max_dst;
+  int32_t* dst_indptr;
+  int64_t* e_total;
+  void* scan_ws;  // zeroed by the caller
+};
 cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_t max_edges,
                                const int64_t* size_old, int64_t* size_new,
                                const int32_t* src_glob, const int32_t* slot, int32_t* rank_of,
-                               int32_t* src_local, void* scan_ws, cudaStream_t st, bool ws_zeroed = false,
-                               ZeroJob next = ZeroJob());
+                               int32_t* src_local, void* scan_ws, cudaStream_t st,
+                               bool ws_zeroed = false, const NextCount* next = nullptr);
 
 cudaError_t launch_gather_rows(const void* x, int64_t x_rows, int32_t cols, int64_t x_stride,
                                int32_t in_dtype, const void* ids, int32_t id_bytes,
