@@ -13,7 +13,11 @@ from ncu_summary import load  # noqa: E402
 def main(path, which=-2):
     rows = load(path)
     starts = [i for i, (_, name, _) in enumerate(rows) if "plan_next_kernel" in name]
-    a, b = starts[which - 1], starts[which]
+    # training steps only: intervals that contain the optimizer (the bench's prep-only
+    # passes also launch plan_next)
+    steps = [(a, b) for a, b in zip(starts, starts[1:])
+             if any("adam_kernel" in n for _, n, _ in rows[a:b])]
+    a, b = steps[which]
     step = rows[a:b]
     tot = sum(us for _, _, us in step)
     for _, name, us in step:
