@@ -232,7 +232,9 @@ int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan, const sal
   int kernels = 0;
   // every scan has its own zeroed region (scan_region); hop 0's count runs on its
   // own, each later count rides in the previous hop's resolve launch
-  auto scan_ws = [&](int h, int flag) { return (void*)(scan + scan_region(plan, h, flag, nullptr)); };
+  auto scan_ws = [&](int h, int flag) {
+    return (void*)((char*)scan + scan_region(plan, h, flag, nullptr));
+  };
   if (hop_begin == 0) {
     // table + all scan workspaces as memset nodes: measured faster in the
     // overlapped step than a reset kernel, which takes SM slots from training
