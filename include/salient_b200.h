@@ -314,11 +314,13 @@ int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const int64_t* m_
                     int32_t relu_dropout, void* stream);
 /* dW[N,K] (fp32, row stride lddw) = dz[M,N]^T @ A[M,K]; zeroes dW first
  * unless `accumulate` (then dW += ...: the caller guarantees dW was zero).
+ * m_dev (nullable): true row count on the device (rows past it are skipped;
+ * the caller guarantees their contributions are zero).
  * 128 x 128 output tiles x split-K over M (about one CTA per SM), partials
  * added with fp32 vector atomics.  N, K multiples of 128. */
 int sal_tc_sage_wgrad(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda, int64_t M,
-                      int32_t N, int32_t K, float* dW_dev, int64_t lddw, int32_t accumulate,
-                      void* stream);
+                      const int64_t* m_dev, int32_t N, int32_t K, float* dW_dev, int64_t lddw,
+                      int32_t accumulate, void* stream);
 /* the same two GEMMs without TMA / warp specialisation (cp.async, one CTA
  * role) — the reference implementation the TMA versions are checked against */
 int sal_tc_sage_fwd_simple(const void* A_dev, int64_t lda, int64_t M, const void* W_dev,

@@ -118,7 +118,7 @@ SIGNATURES = {
     "sal_step_tail": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
     "sal_tc_sage_fwd": (ctypes.c_int, [vp, i64, i64, vp, vp, i32, i32, vp, i64, vp, ctypes.c_float,
                                        u64, vp, i32, vp]),
-    "sal_tc_sage_wgrad": (ctypes.c_int, [vp, i64, vp, i64, i64, i32, i32, vp, i64, i32, vp]),
+    "sal_tc_sage_wgrad": (ctypes.c_int, [vp, i64, vp, i64, i64, vp, i32, i32, vp, i64, i32, vp]),
     "sal_tc_sage_fwd_simple": (ctypes.c_int, [vp, i64, i64, vp, i32, i32, vp, i64, vp,
                                               ctypes.c_float, u64, vp, i32, vp]),
     "sal_tc_sage_wgrad_simple": (ctypes.c_int, [vp, i64, vp, i64, i64, i32, i32, vp, i64, vp]),

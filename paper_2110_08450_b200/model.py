@@ -389,8 +389,10 @@ class FusedSAGE:
         a, n_pad = rec["a"], rec["n_pad"]
         if self._tc_wgrad_layer(i):
             gi = self.gp[i]
+            # rows past the layer's true destination count carry zero dz
             _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), a.data_ptr(),
-                                           a.stride(0), n_pad, gi.shape[0], gi.shape[1],
+                                           a.stride(0), n_pad, _lib.ptr(rec["adj"][3]),
+                                           gi.shape[0], gi.shape[1],
                                            gi.data_ptr(), gi.stride(0),
                                            1 if grads_zeroed else 0, _lib.stream_ptr()),
                        "tc_sage_wgrad")

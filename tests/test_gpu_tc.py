@@ -70,12 +70,12 @@ def test_tc_wgrad_matches_torch(M, N, K):
     dW = torch.full((N, K), 7.0, device="cuda")
     L = _lib.lib()
     _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), A.data_ptr(), A.stride(0), M,
-                                   N, K, dW.data_ptr(), dW.stride(0), 0, _lib.stream_ptr()),
+                                   None, N, K, dW.data_ptr(), dW.stride(0), 0, _lib.stream_ptr()),
                "tc_sage_wgrad")
     # accumulate mode adds into dW (the trainer's Adam leaves the gradient zeroed)
     dW2 = torch.full((N, K), 0.5, device="cuda")
     _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), A.data_ptr(), A.stride(0), M,
-                                   N, K, dW2.data_ptr(), dW2.stride(0), 1, _lib.stream_ptr()),
+                                   None, N, K, dW2.data_ptr(), dW2.stride(0), 1, _lib.stream_ptr()),
                "tc_sage_wgrad(accumulate)")
     torch.cuda.synchronize()
     want = dz.float().t() @ A.float()
@@ -100,3 +100,28 @@ def test_tc_fwd_true_row_count_zero_fills_padding(m_true):
     assert torch.equal(Yp[:tile_end], Yf[:tile_end])
     assert torch.equal(mp[:tile_end * 32], mf[:tile_end * 32])
     assert (Yp[tile_end:] == 0).all() and (mp[tile_end * 32:] == 0).all()
+
+
+@pytest.mark.parametrize("m_true", [0, 100, 3000, 4096])
+def test_tc_wgrad_true_row_count(m_true):
+    """With *m_dev the split-K ranges cover only the first m_true rows (in whole
+    64-row chunks: the contract is that dz rows past m_true are zero, as the
+    trainer's padding rows are)."""
+    M, N, K = 4096, 256, 256
+    g = torch.Generator(device="cuda").manual_seed(17)
+    dz = (torch.randn(M, N, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    dz[m_true:] = 0
+    dz[-(-m_true // 64) * 64:] = float("nan")   # chunks past the last partial one: never read
+    A = (torch.randn(M, K, device="cuda", generator=g)).to(torch.bfloat16)
+    dW = torch.full((N, K), 3.0, device="cuda")
+    md = torch.tensor([m_true], dtype=torch.int64, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), A.data_ptr(), A.stride(0), M,
+                                   md.data_ptr(), N, K, dW.data_ptr(), dW.stride(0), 0,
+                                   _lib.stream_ptr()), "tc_sage_wgrad(m_dev)")
+    torch.cuda.synchronize()
+    want = dz[:m_true].float().t() @ A[:m_true].float()
+    if m_true == 0:
+        assert (dW == 0).all()
+    else:
+        assert ((dW - want).norm() / want.norm()).item() < 1e-3

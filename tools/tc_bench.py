@@ -62,7 +62,7 @@ def fwd_cublas():
 
 def wg_tma():
     _lib.check(L.sal_tc_sage_wgrad(dz.data_ptr(), dz.stride(0), A.data_ptr(), A.stride(0), M,
-                                   256, 256, dW.data_ptr(), dW.stride(0), 0, st()))
+                                   None, 256, 256, dW.data_ptr(), dW.stride(0), 0, st()))
 
 
 def wg_simple():
