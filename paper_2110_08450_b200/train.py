@@ -126,12 +126,18 @@ class _Slot:
 
 
 class _Staging:
-    """Pinned host inputs of one step for the end-to-end path."""
+    """One step's host inputs for the end-to-end path: [desc(3) | seeds] in pinned
+    memory, copied H2D as one block into a device mirror that the captured step
+    graphs read (no memcpy node inside the graph)."""
 
-    def __init__(self, batch_size: int):
-        self.desc = torch.zeros(3, dtype=torch.int64).pin_memory()
-        self.seeds = torch.zeros(max(batch_size, 1), dtype=torch.int64).pin_memory()
-        self.ev = torch.cuda.Event()
+    def __init__(self, batch_size: int, device):
+        self.host = torch.zeros(3 + max(batch_size, 1), dtype=torch.int64).pin_memory()
+        self.np = self.host.numpy()
+        self.dev = torch.zeros(3 + max(batch_size, 1), dtype=torch.int64, device=device)
+        self.ddesc = self.dev[:3]
+        self.dseeds = self.dev[3:]
+        self.ev = torch.cuda.Event()       # the last replay that read `dev` has finished
+        self.copied = torch.cuda.Event()   # `dev` holds this step's inputs
 
 
 class Trainer:
@@ -162,7 +168,9 @@ class Trainer:
         self.depth = 3 if cfg.prep_split else 2
         self.slots = [_Slot(dg, cfg, self.device) for _ in range(self.depth)]
         self.ring = 2 * self.depth   # pinned staging buffers of the end-to-end path
-        self.staging = [_Staging(cfg.batch_size) for _ in range(self.ring)]
+        self.staging = [_Staging(cfg.batch_size, self.device) for _ in range(self.ring)]
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self._loss_ev = [torch.cuda.Event() for _ in range(8)]
         self.head_stream = torch.cuda.Stream(device=self.device, priority=cfg.prep_priority) \
             if cfg.prep_split else None
         # high priority: the prep chain is latency-bound (many small dependent kernels), so
@@ -223,9 +231,9 @@ class Trainer:
         """Enqueue one batch preparation on the current stream (capturable): seeds ->
         MFG -> layer-0 feature rows, plus (late=True) what _prep_late builds."""
         self._prep_head(slot, stage, whole=True)
-        self._prep_tail(slot, stage is not None, whole=True)
+        self._prep_tail(slot, stage, whole=True)
         if late:
-            self._prep_late(slot, stage is not None)
+            self._prep_late(slot, stage)
 
     def _prep_head(self, slot: _Slot, stage: "_Staging | None", whole: bool = False) -> None:
         """Seeds + descriptor of the next batch and its hops [0, prep_split) (all
@@ -233,27 +241,27 @@ class Trainer:
         ws = slot.ws
         st = torch.cuda.current_stream()
         L = _lib.lib()
-        if stage is not None:
-            slot.desc.copy_(stage.desc, non_blocking=True)
-            slot.seeds.copy_(stage.seeds, non_blocking=True)
-            seeds_base = slot.seeds
+        if stage is not None:  # this step's inputs, already copied H2D (run_steps)
+            desc, seeds_base = stage.ddesc, stage.dseeds
         else:
             _lib.check(L.sal_plan_next(self.desc_all.data_ptr(), self.n_steps_dev,
                                        self.cursor.data_ptr(), slot.desc.data_ptr(),
                                        _lib.stream_ptr(st)), "plan_next")
-            seeds_base = self.seeds_all
-        ws.run(self.dg, seeds_base, slot.desc, self.cfg.global_seed, self.policy, st,
+            desc, seeds_base = slot.desc, self.seeds_all
+        ws.run(self.dg, seeds_base, desc, self.cfg.global_seed, self.policy, st,
                hops=None if whole else (0, self.cfg.prep_split))
 
-    def _prep_tail(self, slot: _Slot, host_inputs: bool = False, whole: bool = False) -> None:
+    def _prep_tail(self, slot: _Slot, stage: "_Staging | None" = None,
+                   whole: bool = False) -> None:
         """Hops [prep_split, L) (none when `whole`: _prep_head ran them all) and the
         layer-0 rows."""
         ws = slot.ws
         st = torch.cuda.current_stream()
         L = _lib.lib()
         if not whole:
-            seeds_base = slot.seeds if host_inputs else self.seeds_all  # unread past hop 0
-            ws.run(self.dg, seeds_base, slot.desc, self.cfg.global_seed, self.policy, st,
+            desc = stage.ddesc if stage is not None else slot.desc
+            seeds_base = stage.dseeds if stage is not None else self.seeds_all  # unread past hop 0
+            ws.run(self.dg, seeds_base, desc, self.cfg.global_seed, self.policy, st,
                    hops=(self.cfg.prep_split, self.nh))
         nh = self.nh
         rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
@@ -272,7 +280,7 @@ class Trainer:
                 _lib.dtype_code(a0.dtype), a0.stride(0), _lib.stream_ptr(st)),
                 "segment_mean_fwd(table)")
 
-    def _prep_late(self, slot: _Slot, host_inputs: bool, zero_grads: bool = False) -> None:
+    def _prep_late(self, slot: _Slot, stage: "_Staging | None", zero_grads: bool = False) -> None:
         """The inputs only the loss / backward read: labels and the reverse adjacency
         of layers >= 1 (capturable, current stream); zero_grads: also clear the
         tcgen05 weight-gradient blocks of the step being trained."""
@@ -280,9 +288,10 @@ class Trainer:
         st = torch.cuda.current_stream()
         L = _lib.lib()
         nh = self.nh
-        seeds_base = slot.seeds if host_inputs else self.seeds_all
+        seeds_base = stage.dseeds if stage is not None else self.seeds_all
+        desc = stage.ddesc if stage is not None else slot.desc
         _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), seeds_base.data_ptr(),
-                                       slot.desc.data_ptr(), self.cfg.batch_size,
+                                       desc.data_ptr(), self.cfg.batch_size,
                                        slot.labels.data_ptr(), _lib.stream_ptr(st)),
                    "gather_labels")
         # reverse adjacency for the backward pass; every layer's count/scan workspace is
@@ -352,6 +361,9 @@ class Trainer:
         if part == "post":
             self._train(self.slots[k % D], "post")
             return
+
+        def stg(j):  # the staging slot holding step j's inputs (end-to-end mode)
+            return self.staging[j % self.ring] if host_inputs else None
         cs = torch.cuda.current_stream()
         ps = self.prep_stream or cs  # None: prep serialised on the compute stream
         split = self.cfg.late_prep and self.prep_stream is not None
@@ -363,22 +375,19 @@ class Trainer:
             with torch.cuda.stream(ls):
                 # the late stream also zeroes the tcgen05 gradient blocks (the previous
                 # step's Adam has read them): no memset node in the training chain
-                self._prep_late(self.slots[k % D], host_inputs, zero_grads=True)
+                self._prep_late(self.slots[k % D], stg(k), zero_grads=True)
         if D == 3:
             hs = self.head_stream
             hs.wait_stream(cs)
             with torch.cuda.stream(hs):
-                self._prep_head(self.slots[(k + 2) % 3],
-                                self.staging[(k + 2) % self.ring] if host_inputs else None)
+                self._prep_head(self.slots[(k + 2) % 3], stg(k + 2))
             with torch.cuda.stream(ps):
-                self._prep_tail(self.slots[(k + 1) % 3], host_inputs)
+                self._prep_tail(self.slots[(k + 1) % 3], stg(k + 1))
                 if not split:
-                    self._prep_late(self.slots[(k + 1) % 3], host_inputs)
+                    self._prep_late(self.slots[(k + 1) % 3], stg(k + 1))
         else:
             with torch.cuda.stream(ps):
-                self._prep(self.slots[(k + 1) % 2],
-                           self.staging[(k + 1) % self.ring] if host_inputs else None,
-                           late=not split)
+                self._prep(self.slots[(k + 1) % 2], stg(k + 1), late=not split)
         self._train(self.slots[k % D], part, late=ls)
         cs.wait_stream(ps)
         if D == 3:
@@ -391,49 +400,63 @@ class Trainer:
             bid, off, n = (int(v) for v in self.desc_host[step])
         else:
             bid, off, n = -1, 0, 0
-        stage.desc[0], stage.desc[1], stage.desc[2] = bid, 0, n
+        stage.np[0], stage.np[1], stage.np[2] = bid, 0, n
         if n:
-            stage.seeds[:n].copy_(torch.from_numpy(self.perm_host[off:off + n]))
+            stage.np[3:3 + n] = self.perm_host[off:off + n]
+
+    def _push(self, stage: _Staging) -> None:
+        """H2D of one staged step on the copy stream, a step before the replay that
+        consumes it (which waits on `stage.copied`, long satisfied by then): no copy
+        sits between two replays and no memcpy node inside the graph."""
+        cps = self.copy_stream
+        cps.wait_event(stage.ev)      # the last replay that read the device mirror
+        with torch.cuda.stream(cps):
+            stage.dev.copy_(stage.host, non_blocking=True)
+            stage.copied.record(cps)
+
+    def _stage_and_push(self, step: int) -> None:
+        stage = self.staging[step % self.ring]
+        stage.ev.synchronize()  # the replay that last read this staging slot
+        self._stage_host(stage, step)
+        self._push(stage)
 
     def begin_epoch(self, host_inputs: bool = False) -> None:
         """Prime the pipeline (eager): batch 0 into slot 0, and with depth 3 also
         the head hops of batch 1 into slot 1."""
         late = not (self.cfg.late_prep and self.prep_stream is not None)
         stages = []
+        if host_inputs:  # steps 0 .. depth-1 (the first replay preps step depth-1)
+            for j in range(self.depth):
+                self._stage_and_push(j)
         for j in range(self.depth - 1):
             stage = None
             if host_inputs:
                 stage = self.staging[j]
-                stage.ev.synchronize()
-                self._stage_host(stage, j)
+                torch.cuda.current_stream().wait_event(stage.copied)
             stages.append(stage)
         # with the late split, pair 0 builds slot 0's labels / reverse adjacency
         self._prep(self.slots[0], stages[0], late=late)
         if self.depth == 3:
             self._prep_head(self.slots[1], stages[1])
-        for stage in stages:
-            if stage is not None:
-                stage.ev.record()
 
     def run_steps(self, start: int, count: int, host_inputs: bool = False,
                   loss_out: torch.Tensor | None = None) -> None:
         """Steps [start, start+count): step k trains slot k%2 and prepares k+1.
 
         begin_epoch() must have prepared step `start` (the pipeline is primed
-        once per epoch).  With host_inputs each step stages its successor's
-        seeds in pinned host memory (2*depth ring, so the host runs ahead of
-        the GPU) and copies its loss back to `loss_out[k]` (pinned) — the
-        end-to-end path.
+        once per epoch).  With host_inputs each step stages the seeds + descriptor
+        of step k+depth in pinned host memory and copies them H2D on the copy
+        stream (a ring of 2*depth slots, so the host runs ahead of the GPU), and
+        copies its loss back to `loss_out[k]` (pinned) — the end-to-end path.
         """
         D = self.depth
         P = self.ring if host_inputs else D
+        cs = torch.cuda.current_stream()
         for k in range(start, start + count):
-            stage = None
             if host_inputs:
-                ahead = k + D - 1             # the step whose seeds this replay consumes
-                stage = self.staging[ahead % self.ring]
-                stage.ev.synchronize()  # the replay that last read this staging buffer
-                self._stage_host(stage, ahead)
+                # replay k preps step k+D-1 (pushed one iteration ago); push step k+D now
+                self._stage_and_push(k + D)
+                cs.wait_event(self.staging[(k + D - 1) % self.ring].copied)
             if self.cfg.graphs:
                 if self.graph_allreduce:
                     key = (k % P, host_inputs, "all")
@@ -453,10 +476,17 @@ class Trainer:
                 n0 = _lib.lib().sal_launch_count()
                 self._pair(k % P, host_inputs)
                 self.kernel_launches += _lib.lib().sal_launch_count() - n0
+            if host_inputs:
+                # step k's inputs are fully consumed (prep of k, labels of k in this replay)
+                self.staging[k % self.ring].ev.record(cs)
             if loss_out is not None:
-                loss_out[k - start].copy_(self.last_loss, non_blocking=True)
-            if stage is not None:
-                stage.ev.record()
+                # loss D2H on the copy stream from the step's slot of the device log, so
+                # the next replay does not queue behind it
+                done = self._loss_ev[k % len(self._loss_ev)]
+                done.record(cs)
+                self.copy_stream.wait_event(done)
+                with torch.cuda.stream(self.copy_stream):
+                    loss_out[k - start].copy_(self.losses[k], non_blocking=True)
 
     def _capture(self, parity: int, host_inputs: bool, part: str = "all"):
         """Capture one step variant without disturbing the training state.
