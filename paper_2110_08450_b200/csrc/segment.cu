@@ -185,7 +185,7 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
                          const int32_t* __restrict__ globals,
                          const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
                          const TIn* __restrict__ h, int64_t h_stride, TOut* __restrict__ out,
-                         int64_t out_stride) {
+                         int64_t out_stride, int vpr) {
   constexpr int RPI = 32 / LPR;
   constexpr int kU = LPR >= 32 ? 4 : (LPR < 8 ? LPR : 8);
   const int lane = threadIdx.x & 31;
@@ -205,7 +205,7 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const int e = e0 + u * RPI + grp;
-          if (e < end) {
+          if (e < end && sub < vpr) {
             const int64_t s = load_id<kGlobal>(src, globals, e);
             const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + s * h_stride) + sub);
             buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
@@ -213,7 +213,7 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          if (e0 + u * RPI + grp < end) acc_row8<TIn>(acc, buf[u]);
+          if (e0 + u * RPI + grp < end && sub < vpr) acc_row8<TIn>(acc, buf[u]);
         }
       }
 #pragma unroll
@@ -226,7 +226,7 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
         for (int j = 0; j < 8; ++j) acc[j] *= inv;
       }
     }
-    if (grp == 0) store_row<TOut, 8>(out + (int64_t)d * out_stride + sub * 8, acc);
+    if (grp == 0 && sub < vpr) store_row<TOut, 8>(out + (int64_t)d * out_stride + sub * 8, acc);
   }
 }
 
@@ -243,7 +243,7 @@ segment_mean_rows_pipe_kernel(const int32_t* __restrict__ indptr,
                               const int32_t* __restrict__ globals,
                               const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
                               const TIn* __restrict__ h, int64_t h_stride,
-                              TOut* __restrict__ out, int64_t out_stride) {
+                              TOut* __restrict__ out, int64_t out_stride, int vpr) {
   constexpr int RPI = 32 / LPR;
   constexpr int kU = 8;
   constexpr int W = RPI * kU;  // edges per round
@@ -277,7 +277,7 @@ segment_mean_rows_pipe_kernel(const int32_t* __restrict__ indptr,
     uint4 buf[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      if (beg + u * RPI + grp < end) {
+      if (beg + u * RPI + grp < end && sub < vpr) {
         const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + (int64_t)ids[u] * h_stride) + sub);
         buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
       }
@@ -297,14 +297,14 @@ segment_mean_rows_pipe_kernel(const int32_t* __restrict__ indptr,
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      if (beg + u * RPI + grp < end) acc_row8<TIn>(acc, buf[u]);
+      if (beg + u * RPI + grp < end && sub < vpr) acc_row8<TIn>(acc, buf[u]);
     }
     // rare: destinations with more than W edges finish unpipelined
     for (int e0 = beg + W; e0 < end; e0 += W) {
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int e = e0 + u * RPI + grp;
-        if (e < end) {
+        if (e < end && sub < vpr) {
           const int64_t s = load_id<kGlobal>(src, globals, e);
           const int4 t = ld_stream_v4(reinterpret_cast<const int4*>(h + s * h_stride) + sub);
           buf[u] = make_uint4((unsigned)t.x, (unsigned)t.y, (unsigned)t.z, (unsigned)t.w);
@@ -312,7 +312,7 @@ segment_mean_rows_pipe_kernel(const int32_t* __restrict__ indptr,
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        if (e0 + u * RPI + grp < end) acc_row8<TIn>(acc, buf[u]);
+        if (e0 + u * RPI + grp < end && sub < vpr) acc_row8<TIn>(acc, buf[u]);
       }
     }
 #pragma unroll
@@ -324,7 +324,7 @@ segment_mean_rows_pipe_kernel(const int32_t* __restrict__ indptr,
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] *= inv;
     }
-    if (grp == 0) store_row<TOut, 8>(out + (int64_t)d * out_stride + sub * 8, acc);
+    if (grp == 0 && sub < vpr) store_row<TOut, 8>(out + (int64_t)d * out_stride + sub * 8, acc);
     d = dn;
     if (d >= npad) break;
     beg = nbeg;
@@ -403,8 +403,12 @@ static bool fwd_rows(const int32_t* indptr, const int32_t* src, const int32_t* g
                      const int64_t* n_dst_dev, int64_t n_pad, const void* h, int64_t h_stride,
                      int32_t f, void* out, int64_t out_stride, cudaStream_t st) {
   if (sizeof(TIn) != 2 || f % 8 != 0) return false;
-  const int lpr = f / 8;
-  if (lpr > 32 || (32 % lpr) != 0) return false;
+  // lanes per row: the power of two holding the row's 16-byte vectors (vpr of
+  // them; e.g. 104 padded fp16 columns = 13 vectors on 16 lanes)
+  const int vpr = f / 8;
+  int lpr = 1;
+  while (lpr < vpr) lpr <<= 1;
+  if (lpr > 32) return false;
   if (h_stride % 8 != 0 || out_stride % 8 != 0 || ((uintptr_t)h % 16) != 0 ||
       ((uintptr_t)out % 16) != 0)
     return false;
@@ -427,17 +431,17 @@ static bool fwd_rows(const int32_t* indptr, const int32_t* src, const int32_t* g
     const int g = (int)(blocks < 1 ? 1 : blocks);
     if (lpr == 8)
       segment_mean_rows_pipe_kernel<TIn, TOut, 8, kGlobal><<<g, kSegThreads, 0, st>>>(
-          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);
+          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride, vpr);
     else
       segment_mean_rows_pipe_kernel<TIn, TOut, 16, kGlobal><<<g, kSegThreads, 0, st>>>(
-          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);
+          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride, vpr);
     return true;
   }
   const int grid = seg_grid(n_pad);
 #define SAL_ROWS_CASE(L)                                                                     \
   case L:                                                                                    \
     segment_mean_rows_kernel<TIn, TOut, L, kGlobal><<<grid, kSegThreads, 0, st>>>(            \
-        indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride);              \
+        indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride, vpr);         \
     return true;
   switch (lpr) {
     SAL_ROWS_CASE(1)

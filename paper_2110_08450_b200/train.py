@@ -95,6 +95,21 @@ def allreduce_mean(t: torch.Tensor, world: int) -> None:
         t.div_(world)
 
 
+def _model_width(dg: DeviceGraph) -> int:
+    """Feature width the model consumes: the table's padded row (16-byte multiple),
+    so every layer-0 row is whole 16-byte vectors for the fast kernels (products'
+    100 fp16 columns -> 104; the padding columns are zero and their weights get
+    zero gradient, so the model is the unpadded one)."""
+    return dg.features.shape[1]
+
+
+def _model_table(dg: DeviceGraph) -> torch.Tensor:
+    f, fp = dg.num_features, dg.features.shape[1]
+    if fp != f:
+        dg.features[:, f:].zero_()
+    return dg.features
+
+
 class _Slot:
     def __init__(self, dg: DeviceGraph, cfg: TrainConfig, device, backward: bool = True):
         # gather-free: layer 0 reads rows by global id, so the last hop needs no relabel
@@ -104,7 +119,7 @@ class _Slot:
         ws = self.ws
         nh = ws.num_hops
         rows = ws.node_cap[-1] if not cfg.gather_free else ws.node_cap[-2]
-        f = dg.num_features
+        f = _model_width(dg)
         # layer-0 "cat" buffer: right half = gathered features, left = mean
         self.feats = torch.zeros((max(rows, 1), 2 * f), dtype=cfg.act_dtype, device=device)
         self.labels = torch.full((cfg.batch_size,), -1, dtype=torch.int64, device=device)
@@ -154,7 +169,7 @@ class Trainer:
         self.train_ids = np.asarray(train_ids, dtype=np.int64)
         self.num_classes = num_classes or dg.num_classes
         self.nh = len(cfg.fanouts)
-        self.model = FusedSAGE(dg.num_features, cfg.hidden, self.num_classes, self.nh,
+        self.model = FusedSAGE(_model_width(dg), cfg.hidden, self.num_classes, self.nh,
                                cfg.dropout, device=self.device, seed=cfg.model_seed,
                                act_dtype=cfg.act_dtype, lr=cfg.lr)
         self.model.tc_wgrad = cfg.tc_wgrad
@@ -180,7 +195,7 @@ class Trainer:
         # are built on a third stream while its forward pass runs
         self.late_stream = torch.cuda.Stream(device=self.device, priority=cfg.prep_priority)
         self.policy = RNG_POLICIES[cfg.rng_policy]
-        self.x_table = dg.feature_view()
+        self.x_table = _model_table(dg)
         self.cursor = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.step_ctr = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.losses = torch.zeros(1, dtype=torch.float32, device=self.device)
@@ -571,7 +586,7 @@ class Trainer:
         plan = EpochPlan(batches=batches, batch_size=bs, shuffle_seed=0)
         correct = torch.zeros((), dtype=torch.int64, device=self.device)
         total = 0
-        x = self.dg.feature_view()
+        x = _model_table(self.dg)   # the model's (padded) input width
         cfg = PrepConfig(num_workers=2, fanouts=fan, feature_dtype="bf16")
         for pb in run_epoch_prep(self.dg, x, self.dg.labels, plan, cfg, self.cfg.global_seed + 7):
             adjs = [(l.indptr, l.src_local, l.num_dst, None) for l in pb.mfg.layers]
@@ -610,7 +625,7 @@ class Evaluator:
                           act_dtype=act_dtype)
         self.slots = [_Slot(dg, cfg, self.device, backward=False) for _ in range(2)]
         self.prep_stream = torch.cuda.Stream(device=self.device, priority=prep_priority)
-        self.x_table = dg.feature_view()
+        self.x_table = _model_table(dg)
         self.cursor = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.counts = torch.zeros(2, dtype=torch.int64, device=self.device)
         self.seeds_all = torch.zeros(1, dtype=torch.int64, device=self.device)

@@ -29,9 +29,13 @@ def test_segment_mean_bit_exact_fp32():
         assert np.array_equal(got.cpu().numpy(), want), f
 
 
-def test_segment_mean_fp16_input_and_padding():
+@pytest.mark.parametrize("f,n_pad", [(128, 256), (104, 256), (24, 256), (128, 200000),
+                                     (256, 256)])
+def test_segment_mean_fp16_input_and_padding(f, n_pad):
+    """16-bit rows: the warp-row kernels (pipelined for the training layer-0 shape,
+    plain otherwise), including rows of 13 vectors on 16 lanes (products' 104)."""
     rng = np.random.default_rng(1)
-    n_dst, n_src, f = 200, 500, 128
+    n_dst, n_src = 200, 500
     deg = rng.integers(0, 20, size=n_dst)
     indptr = np.zeros(n_dst + 1, dtype=np.int64)
     indptr[1:] = np.cumsum(deg)
@@ -41,7 +45,7 @@ def test_segment_mean_fp16_input_and_padding():
     nd = torch.tensor([n_dst], dtype=torch.int64, device="cuda")
     got = segment_mean(torch.from_numpy(indptr.astype(np.int32)).cuda(),
                        torch.from_numpy(src.astype(np.int32)).cuda(),
-                       torch.from_numpy(h).cuda(), n_dst, n_pad=256, n_dst_dev=nd)
+                       torch.from_numpy(h).cuda(), n_dst, n_pad=n_pad, n_dst_dev=nd)
     # 16-bit rows take the warp-row kernel: per-lane-group partial sums, so the
     # fp32 summation order differs from strict edge order (tolerance, not bits)
     assert np.allclose(got[:n_dst].cpu().numpy(), want, rtol=1e-6, atol=1e-6)

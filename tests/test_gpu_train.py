@@ -86,9 +86,9 @@ def test_fused_logits_fp32_within_1e3_of_autograd_on_config_shape():
     assert err < 1e-3, err
 
 
-def _small_trainer(graphs, gather_free=False, seed=0, fanouts=(10, 5), prep_split=0):
+def _small_trainer(graphs, gather_free=False, seed=0, fanouts=(10, 5), prep_split=0, f=64):
     g = synth_graph(30000, 10, 3.0, seed=4)
-    fm = generate_features(30000, 64, "f16", seed=4)
+    fm = generate_features(30000, f, "f16", seed=4)
     y = planted_labels(fm.data, 8, seed=4)
     dg = DeviceGraph.from_host(g, fm, y)
     train = np.arange(0, 30000, 2)
@@ -117,9 +117,11 @@ def test_graph_replay_matches_eager():
     assert ("pre" in {k[2] for k in tr_s.graphs}) and ("all" in {k[2] for k in tr_g.graphs})
 
 
-def test_gather_free_matches_materialised():
-    a, _ = _small_trainer(False, gather_free=False)
-    b, _ = _small_trainer(False, gather_free=True)
+@pytest.mark.parametrize("f", [64, 100])
+def test_gather_free_matches_materialised(f):
+    """f = 100 fp16 (products): the model runs on the table's 104-column padded rows."""
+    a, _ = _small_trainer(False, gather_free=False, f=f)
+    b, _ = _small_trainer(False, gather_free=True, f=f)
     for tr in (a, b):
         tr.set_epoch(0)
         tr.begin_epoch()
@@ -261,3 +263,14 @@ def test_trainer_with_fused_head_matches_default():
         torch.cuda.synchronize()
     la, lb = a.losses[:8].cpu().numpy(), b.losses[:8].cpu().numpy()
     assert np.allclose(la, lb, rtol=2e-2, atol=1e-3), (la, lb)
+
+
+def test_padded_feature_width_trains_and_evaluates():
+    tr, dg = _small_trainer(True, gather_free=True, f=100)
+    assert tr.model.dims[0] == 104 and dg.num_features == 100
+    first = tr.train_epoch(0)
+    last = tr.train_epoch(1)
+    assert np.isfinite(last) and last < first
+    c, t = tr.evaluate(np.arange(1, 30000, 2)[:3000])
+    ce, te = tr.evaluate_eager(np.arange(1, 30000, 2)[:3000])
+    assert t == te == 3000 and abs(c - ce) <= 0.003 * 3000
