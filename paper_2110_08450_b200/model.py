@@ -255,9 +255,11 @@ class FusedSAGE:
 
     # ------------------------------------------------------------- buffers
     def cat_input(self, x: torch.Tensor) -> torch.Tensor:
-        """Copy a plain [N, f] layer-0 input into a fresh cat buffer [N, 2f]."""
-        a = torch.zeros((x.shape[0], 2 * x.shape[1]), dtype=self.act, device=x.device)
-        a[:, x.shape[1]:] = x
+        """Copy a plain [N, f] layer-0 input into a fresh cat buffer [N, 2 f_in]
+        (f <= f_in; columns past f stay zero)."""
+        fm = self.dims[0]
+        a = torch.zeros((x.shape[0], 2 * fm), dtype=self.act, device=x.device)
+        a[:, fm:fm + x.shape[1]] = x
         return a
 
     # ------------------------------------------------------------- fwd
@@ -285,11 +287,12 @@ class FusedSAGE:
             elif i == 0 and x_global is not None:
                 # gather-free layer 0: edges carry global ids, rows come from the table
                 table, gsrc = x_global
+                # the table may be narrower than the model's (zero-padded) input width
                 _lib.check(L.sal_segment_mean_fwd(
                     indptr.data_ptr(), gsrc.data_ptr(), _lib.ptr(n_dev), n_pad,
-                    table.data_ptr(), _lib.dtype_code(table.dtype), table.stride(0), f,
-                    mean.data_ptr(), _lib.dtype_code(self.act), a.stride(0), st),
-                    "segment_mean_fwd(table)")
+                    table.data_ptr(), _lib.dtype_code(table.dtype), table.stride(0),
+                    min(f, table.shape[1]), mean.data_ptr(), _lib.dtype_code(self.act),
+                    a.stride(0), st), "segment_mean_fwd(table)")
             else:
                 _lib.check(L.sal_segment_mean_fwd(
                     indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dev), n_pad, h.data_ptr(),

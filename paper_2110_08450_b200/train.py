@@ -96,11 +96,16 @@ def allreduce_mean(t: torch.Tensor, world: int) -> None:
 
 
 def _model_width(dg: DeviceGraph) -> int:
-    """Feature width the model consumes: the table's padded row (16-byte multiple),
-    so every layer-0 row is whole 16-byte vectors for the fast kernels (products'
-    100 fp16 columns -> 104; the padding columns are zero and their weights get
-    zero gradient, so the model is the unpadded one)."""
-    return dg.features.shape[1]
+    """Feature width the model consumes: at least the table's padded row (16-byte
+    multiple), so every layer-0 row is whole 16-byte vectors for the fast kernels,
+    and 128 for 16-bit tables between 64 and 128 columns, so layer 0 runs on the
+    tcgen05 kernels (K = 2 x 128).  Products' 100 fp16 columns: table 104, model
+    128.  The padding columns are zero and their weights get zero gradient, so
+    the model is the unpadded one."""
+    fp = dg.features.shape[1]
+    if dg.features.element_size() == 2 and 64 < fp < 128:
+        return 128
+    return fp
 
 
 def _model_table(dg: DeviceGraph) -> torch.Tensor:
@@ -281,8 +286,9 @@ class Trainer:
         nh = self.nh
         rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
         n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
-        f = self.x_table.shape[1]
-        gather_rows(self.x_table, ws.globals, slot.feats[:, f:], n=rows, n_dev=n_dev, stream=st)
+        f, fx = self.model.dims[0], self.x_table.shape[1]
+        gather_rows(self.x_table, ws.globals, slot.feats[:, f:f + fx], n=rows, n_dev=n_dev,
+                    stream=st)
         if self.cfg.gather_free and self.cfg.prep_mean0:
             # layer-0 mean over the last hop's edges, rows read by global id from the
             # table, written into the left half of the layer-0 cat buffer
@@ -291,7 +297,7 @@ class Trainer:
             _lib.check(L.sal_segment_mean_fwd(
                 ws.dst_indptr[h0].data_ptr(), ws.src_glob.data_ptr(),
                 ws.sizes[h0:h0 + 1].data_ptr(), ws.node_cap[h0], self.x_table.data_ptr(),
-                _lib.dtype_code(self.x_table.dtype), self.x_table.stride(0), f, a0.data_ptr(),
+                _lib.dtype_code(self.x_table.dtype), self.x_table.stride(0), fx, a0.data_ptr(),
                 _lib.dtype_code(a0.dtype), a0.stride(0), _lib.stream_ptr(st)),
                 "segment_mean_fwd(table)")
 
@@ -666,8 +672,8 @@ class Evaluator:
                                    slot.desc.data_ptr(), _lib.stream_ptr(st)), "plan_next")
         ws.run(self.dg, self.seeds_all, slot.desc, self.global_seed, self.policy, st)
         nh = self.nh
-        f = self.x_table.shape[1]
-        gather_rows(self.x_table, ws.globals, slot.feats[:, f:], n=ws.node_cap[nh - 1],
+        f, fx = self.model.dims[0], self.x_table.shape[1]
+        gather_rows(self.x_table, ws.globals, slot.feats[:, f:f + fx], n=ws.node_cap[nh - 1],
                     n_dev=ws.sizes[nh - 1:nh], stream=st)
         _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), self.seeds_all.data_ptr(),
                                        slot.desc.data_ptr(), self.batch_size,

@@ -119,7 +119,7 @@ def test_graph_replay_matches_eager():
 
 @pytest.mark.parametrize("f", [64, 100])
 def test_gather_free_matches_materialised(f):
-    """f = 100 fp16 (products): the model runs on the table's 104-column padded rows."""
+    """f = 100 fp16 (products): table rows padded to 104, the model to 128."""
     a, _ = _small_trainer(False, gather_free=False, f=f)
     b, _ = _small_trainer(False, gather_free=True, f=f)
     for tr in (a, b):
@@ -267,7 +267,7 @@ def test_trainer_with_fused_head_matches_default():
 
 def test_padded_feature_width_trains_and_evaluates():
     tr, dg = _small_trainer(True, gather_free=True, f=100)
-    assert tr.model.dims[0] == 104 and dg.num_features == 100
+    assert tr.model.dims[0] == 128 and dg.num_features == 100   # table 104, model 128
     first = tr.train_epoch(0)
     last = tr.train_epoch(1)
     assert np.isfinite(last) and last < first
