@@ -218,6 +218,14 @@ int sal_segment_mean_fwd(const int32_t* indptr_dev, const int32_t* src_dev,
                          const int64_t* n_dst_dev, int64_t n_pad, const void* h_dev,
                          int32_t h_dtype, int64_t h_stride, int32_t f, void* out_dev,
                          int32_t out_dtype, int64_t out_stride, void* stream);
+/* sal_segment_mean_fwd with flags: SAL_SEG_NO_PAD_FILL leaves rows
+ * [*n_dst_dev, n_pad) untouched (a consumer that never reads them, or a buffer
+ * that already holds finite values there). */
+#define SAL_SEG_NO_PAD_FILL 1
+int sal_segment_mean_fwd_ex(const int32_t* indptr_dev, const int32_t* src_dev,
+                            const int64_t* n_dst_dev, int64_t n_pad, const void* h_dev,
+                            int32_t h_dtype, int64_t h_stride, int32_t f, void* out_dev,
+                            int32_t out_dtype, int64_t out_stride, int32_t flags, void* stream);
 /* gradient of the above w.r.t. h: g_h[src[e],:] += g_out[d,:] / deg(d).
  * g_h (fp32, n_src rows) must be zeroed by the caller. */
 int sal_segment_mean_bwd(const int32_t* indptr_dev, const int32_t* src_dev,

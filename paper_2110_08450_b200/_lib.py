@@ -17,6 +17,7 @@ SAL_MAX_HOPS = 8
 SAL_RNG_SPLITMIX = 0
 SAL_RNG_PHILOX = 1
 SAL_MFG_LAST_HOP_EDGES = 1
+SAL_SEG_NO_PAD_FILL = 1
 SAL_F16 = 1
 SAL_F32 = 2
 SAL_BF16 = 3
@@ -96,6 +97,8 @@ SIGNATURES = {
     "sal_gather_labels": (ctypes.c_int, [vp, vp, vp, i64, vp, vp]),
     "sal_segment_mean_fwd": (ctypes.c_int, [vp, vp, vp, i64, vp, i32, i64, i32, vp, i32, i64,
                                             vp]),
+    "sal_segment_mean_fwd_ex": (ctypes.c_int, [vp, vp, vp, i64, vp, i32, i64, i32, vp, i32, i64,
+                                               i32, vp]),
     "sal_segment_mean_bwd": (ctypes.c_int, [vp, vp, vp, i64, vp, i32, i64, i32, vp, i64, vp]),
     "sal_segment_mean_fwd_global": (ctypes.c_int, [vp, vp, vp, vp, i64, vp, i32, i64, i32, vp,
                                                    i32, i64, vp]),

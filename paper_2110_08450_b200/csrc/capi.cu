@@ -443,6 +443,15 @@ int sal_segment_mean_fwd(const int32_t* indptr, const int32_t* src, const int64_
                          int64_t n_pad, const void* h, int32_t h_dtype, int64_t h_stride,
                          int32_t f, void* out, int32_t out_dtype, int64_t out_stride,
                          void* stream) {
+  return sal_segment_mean_fwd_ex(indptr, src, n_dst_dev, n_pad, h, h_dtype, h_stride, f, out,
+                                 out_dtype, out_stride, 0, stream);
+}
+
+int sal_segment_mean_fwd_ex(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
+                            int64_t n_pad, const void* h, int32_t h_dtype, int64_t h_stride,
+                            int32_t f, void* out, int32_t out_dtype, int64_t out_stride,
+                            int32_t flags, void* stream) {
+  if (flags & ~SAL_SEG_NO_PAD_FILL) return fail(SAL_EINVAL, "segment_mean_fwd: bad flags");
   if (!valid_dtype(h_dtype) || !valid_dtype(out_dtype))
     return fail(SAL_EINVAL, "segment_mean_fwd: unsupported dtype");
   if (f < 0 || n_pad < 0) return fail(SAL_EINVAL, "segment_mean_fwd: bad shape");
@@ -451,7 +460,8 @@ int sal_segment_mean_fwd(const int32_t* indptr, const int32_t* src, const int64_
     return fail(SAL_EINVAL, "segment_mean_fwd: null argument");
   return counted(cuda_status(sal::launch_segment_mean_fwd(indptr, src, nullptr, n_dst_dev, n_pad, h,
                                                   h_dtype, h_stride, f, out, out_dtype,
-                                                  out_stride, (cudaStream_t)stream),
+                                                  out_stride, (cudaStream_t)stream,
+                                                  !(flags & SAL_SEG_NO_PAD_FILL)),
                      "segment_mean_fwd"), 1);
 }
 

@@ -85,7 +85,7 @@ cudaError_t launch_segment_mean_fwd(const int32_t* indptr, const int32_t* src,
                                     const int32_t* globals, const int64_t* n_dst_dev,
                                     int64_t n_pad, const void* h, int32_t h_dtype,
                                     int64_t h_stride, int32_t f, void* out, int32_t out_dtype,
-                                    int64_t out_stride, cudaStream_t st);
+                                    int64_t out_stride, cudaStream_t st, bool pad_fill = true);
 cudaError_t launch_segment_mean_bwd(const int32_t* indptr, const int32_t* src,
                                     const int64_t* n_dst_dev, int64_t n_pad, const void* g_out,
                                     int32_t g_dtype, int64_t g_stride, int32_t f, float* g_h,

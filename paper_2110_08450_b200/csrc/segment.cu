@@ -93,9 +93,10 @@ __global__ void __launch_bounds__(kSegThreads)
 segment_mean_fwd_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
                         const int32_t* __restrict__ globals, const int64_t* __restrict__ n_dst_dev,
                         int64_t n_pad, const TIn* __restrict__ h, int64_t h_stride, int32_t f,
-                        TOut* __restrict__ out, int64_t out_stride) {
+                        TOut* __restrict__ out, int64_t out_stride, int pad_fill) {
   const int lane = threadIdx.x & 31;
   const int64_t n_dst = n_dst_dev ? *n_dst_dev : n_pad;
+  if (!pad_fill) n_pad = n_pad < n_dst ? n_pad : n_dst;  // padding rows left as they are
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t d = warp; d < n_pad; d += nwarps) {
@@ -185,13 +186,13 @@ segment_mean_rows_kernel(const int32_t* __restrict__ indptr, const int32_t* __re
                          const int32_t* __restrict__ globals,
                          const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
                          const TIn* __restrict__ h, int64_t h_stride, TOut* __restrict__ out,
-                         int64_t out_stride, int vpr) {
+                         int64_t out_stride, int vpr, int pad_fill) {
   constexpr int RPI = 32 / LPR;
   constexpr int kU = LPR >= 32 ? 4 : (LPR < 8 ? LPR : 8);
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPR, sub = lane % LPR;
   const int n_dst = (int)(n_dst_dev ? *n_dst_dev : n_pad);
-  const int npad = (int)n_pad;
+  const int npad = pad_fill ? (int)n_pad : min((int)n_pad, n_dst);
   const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
   for (int d = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); d < npad; d += nwarps) {
     float acc[8];
@@ -243,14 +244,15 @@ segment_mean_rows_pipe_kernel(const int32_t* __restrict__ indptr,
                               const int32_t* __restrict__ globals,
                               const int64_t* __restrict__ n_dst_dev, int64_t n_pad,
                               const TIn* __restrict__ h, int64_t h_stride,
-                              TOut* __restrict__ out, int64_t out_stride, int vpr) {
+                              TOut* __restrict__ out, int64_t out_stride, int vpr,
+                              int pad_fill) {
   constexpr int RPI = 32 / LPR;
   constexpr int kU = 8;
   constexpr int W = RPI * kU;  // edges per round
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPR, sub = lane % LPR;
   const int n_dst = (int)(n_dst_dev ? *n_dst_dev : n_pad);
-  const int npad = (int)n_pad;
+  const int npad = pad_fill ? (int)n_pad : min((int)n_pad, n_dst);
   const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
   int d = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (d >= npad) return;
@@ -401,7 +403,7 @@ static int seg_grid(int64_t rows) {
 template <typename TIn, typename TOut, bool kGlobal>
 static bool fwd_rows(const int32_t* indptr, const int32_t* src, const int32_t* globals,
                      const int64_t* n_dst_dev, int64_t n_pad, const void* h, int64_t h_stride,
-                     int32_t f, void* out, int64_t out_stride, cudaStream_t st) {
+                     int32_t f, void* out, int64_t out_stride, cudaStream_t st, int pad_fill) {
   if (sizeof(TIn) != 2 || f % 8 != 0) return false;
   // lanes per row: the power of two holding the row's 16-byte vectors (vpr of
   // them; e.g. 104 padded fp16 columns = 13 vectors on 16 lanes)
@@ -431,17 +433,17 @@ static bool fwd_rows(const int32_t* indptr, const int32_t* src, const int32_t* g
     const int g = (int)(blocks < 1 ? 1 : blocks);
     if (lpr == 8)
       segment_mean_rows_pipe_kernel<TIn, TOut, 8, kGlobal><<<g, kSegThreads, 0, st>>>(
-          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride, vpr);
+          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride, vpr, pad_fill);
     else
       segment_mean_rows_pipe_kernel<TIn, TOut, 16, kGlobal><<<g, kSegThreads, 0, st>>>(
-          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride, vpr);
+          indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride, vpr, pad_fill);
     return true;
   }
   const int grid = seg_grid(n_pad);
 #define SAL_ROWS_CASE(L)                                                                     \
   case L:                                                                                    \
     segment_mean_rows_kernel<TIn, TOut, L, kGlobal><<<grid, kSegThreads, 0, st>>>(            \
-        indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride, vpr);         \
+        indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, op, out_stride, vpr, pad_fill);         \
     return true;
   switch (lpr) {
     SAL_ROWS_CASE(1)
@@ -459,9 +461,9 @@ template <typename TIn, typename TOut, bool kGlobal>
 static cudaError_t fwd_typed(const int32_t* indptr, const int32_t* src, const int32_t* globals,
                              const int64_t* n_dst_dev, int64_t n_pad, const void* h,
                              int64_t h_stride, int32_t f, void* out, int64_t out_stride,
-                             cudaStream_t st) {
+                             cudaStream_t st, int pad_fill) {
   if (fwd_rows<TIn, TOut, kGlobal>(indptr, src, globals, n_dst_dev, n_pad, h, h_stride, f, out,
-                                    out_stride, st))
+                                    out_stride, st, pad_fill))
     return cudaGetLastError();
   // vector width: 16 B of the narrower side, capped so one pass covers f
   const int max_v = 16 / (int)(sizeof(TIn) < sizeof(TOut) ? sizeof(TIn) : sizeof(TOut));
@@ -473,7 +475,7 @@ static cudaError_t fwd_typed(const int32_t* indptr, const int32_t* src, const in
 #define SAL_SEG_CASE(VV)                                                                     \
   case VV:                                                                                   \
     segment_mean_fwd_kernel<TIn, TOut, VV, kGlobal><<<grid, kSegThreads, 0, st>>>(           \
-        indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, f, op, out_stride);           \
+        indptr, src, globals, n_dst_dev, n_pad, hp, h_stride, f, op, out_stride, pad_fill); \
     break;
   switch (v) {
     SAL_SEG_CASE(8)
@@ -490,10 +492,11 @@ template <bool kGlobal>
 static cudaError_t fwd_dispatch(const int32_t* indptr, const int32_t* src, const int32_t* globals,
                                 const int64_t* n_dst_dev, int64_t n_pad, const void* h,
                                 int32_t h_dtype, int64_t h_stride, int32_t f, void* out,
-                                int32_t out_dtype, int64_t out_stride, cudaStream_t st) {
+                                int32_t out_dtype, int64_t out_stride, cudaStream_t st,
+                                int pad_fill) {
 #define SAL_FWD(TI, TO) \
   return fwd_typed<TI, TO, kGlobal>(indptr, src, globals, n_dst_dev, n_pad, h, h_stride, f, out, \
-                                    out_stride, st)
+                                    out_stride, st, pad_fill)
   if (h_dtype == SAL_F16) {
     if (out_dtype == SAL_F32) SAL_FWD(__half, float);
     if (out_dtype == SAL_BF16) SAL_FWD(__half, __nv_bfloat16);
@@ -512,12 +515,12 @@ cudaError_t launch_segment_mean_fwd(const int32_t* indptr, const int32_t* src,
                                     const int32_t* globals, const int64_t* n_dst_dev,
                                     int64_t n_pad, const void* h, int32_t h_dtype,
                                     int64_t h_stride, int32_t f, void* out, int32_t out_dtype,
-                                    int64_t out_stride, cudaStream_t st) {
+                                    int64_t out_stride, cudaStream_t st, bool pad_fill) {
   if (globals != nullptr)
     return fwd_dispatch<true>(indptr, src, globals, n_dst_dev, n_pad, h, h_dtype, h_stride, f,
-                              out, out_dtype, out_stride, st);
+                              out, out_dtype, out_stride, st, pad_fill ? 1 : 0);
   return fwd_dispatch<false>(indptr, src, globals, n_dst_dev, n_pad, h, h_dtype, h_stride, f,
-                             out, out_dtype, out_stride, st);
+                             out, out_dtype, out_stride, st, pad_fill ? 1 : 0);
 }
 
 template <typename TG>

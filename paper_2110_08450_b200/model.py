@@ -287,12 +287,17 @@ class FusedSAGE:
             elif i == 0 and x_global is not None:
                 # gather-free layer 0: edges carry global ids, rows come from the table
                 table, gsrc = x_global
-                # the table may be narrower than the model's (zero-padded) input width
-                _lib.check(L.sal_segment_mean_fwd(
+                # the table may be narrower than the model's (zero-padded) input width.
+                # Padding rows are left as they are: the layer-0 buffers start zeroed and
+                # only ever hold finite values, the tcgen05 forward reads them only inside
+                # the last partial tile and the weight gradient pairs them with zero dz
+                # (451 K padded vs 175 K real rows at the (20,20,20) inference shape)
+                _lib.check(L.sal_segment_mean_fwd_ex(
                     indptr.data_ptr(), gsrc.data_ptr(), _lib.ptr(n_dev), n_pad,
                     table.data_ptr(), _lib.dtype_code(table.dtype), table.stride(0),
                     min(f, table.shape[1]), mean.data_ptr(), _lib.dtype_code(self.act),
-                    a.stride(0), st), "segment_mean_fwd(table)")
+                    a.stride(0), _lib.SAL_SEG_NO_PAD_FILL if n_dev is not None else 0, st),
+                    "segment_mean_fwd(table)")
             else:
                 _lib.check(L.sal_segment_mean_fwd(
                     indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dev), n_pad, h.data_ptr(),
