@@ -62,7 +62,9 @@ def parse():
     p.add_argument("--fanouts", default="15,10,5")
     p.add_argument("--hidden", type=int, default=256)
     p.add_argument("--no-graphs", action="store_true")
-    p.add_argument("--prep-priority", type=int, default=-1)
+    p.add_argument("--prep-priority", type=int, default=None)
+    p.add_argument("--late-priority", type=int, default=None)
+    p.add_argument("--compute-priority", type=int, default=None)
     p.add_argument("--prep-split", type=int, default=None,
                    help="three-slot pipeline: hops [0, s) of batch i+2 beside hops [s, L) of "
                         "batch i+1 (0 = two slots)")
@@ -439,7 +441,10 @@ def run_ours(args):
     fan = FanoutSpec(tuple(int(x) for x in args.fanouts.split(",")))
     dg, train, test, gen_s = build_data(args.shape)
     cfg = TrainConfig(fanouts=fan, hidden=args.hidden, gather_free=not args.materialise,
-                      graphs=not args.no_graphs, prep_priority=args.prep_priority)
+                      graphs=not args.no_graphs)
+    for k in ("prep_priority", "late_priority", "compute_priority"):
+        if getattr(args, k) is not None:
+            setattr(cfg, k, getattr(args, k))
     if args.prep_split is not None:
         cfg.prep_split = args.prep_split
     tr = Trainer(dg, train, cfg, rank=rank, world=world)

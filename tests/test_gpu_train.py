@@ -177,7 +177,7 @@ def test_three_slot_pipeline_matches_two_slot(gather_free, split):
         tr.run_steps(0, n)
         torch.cuda.synchronize()
         got = tr.losses[:n].cpu().numpy()
-        assert np.allclose(got, want, rtol=2e-2, atol=1e-3), (graphs, got[:6], want[:6])
+        _same_trajectory(got, want)
         assert int(tr.cursor.item()) == n + 2   # one plan_next per batch, two past the end
     tr, _ = _small_trainer(True, gather_free, fanouts=(10, 5, 3), prep_split=split)
     tr.set_epoch(0)
@@ -185,7 +185,14 @@ def test_three_slot_pipeline_matches_two_slot(gather_free, split):
     out = torch.zeros(n).pin_memory()
     tr.run_steps(0, n, host_inputs=True, loss_out=out)
     torch.cuda.synchronize()
-    assert np.allclose(out.numpy(), want, rtol=2e-2, atol=1e-3)
+    _same_trajectory(out.numpy(), want)
+
+
+def _same_trajectory(got, want):
+    """Same batches in the same order: the first steps agree to fp32-atomics noise;
+    over a whole epoch that noise compounds through the updates (a few %)."""
+    assert np.allclose(got[:8], want[:8], rtol=1e-2, atol=1e-3), (got[:8], want[:8])
+    assert np.allclose(got, want, rtol=6e-2, atol=1e-3), (got, want)
 
 
 @pytest.mark.parametrize("fin,hid,classes", [(128, 256, 172), (64, 64, 10), (32, 96, 47)])
