@@ -3,10 +3,14 @@
 The paper's training loop (PAPER.md:407-416 listing, 2562-2586 model) with
 SALIENT's pipeline moved onto the GPU:
 
-  prep stream   : plan cursor -> sample MFG (sal_sample_mfg) -> gather features
-                  (fp16 table -> bf16 rows) -> labels, for batch i+1, into
-                  device slot (i+1) % 2
-  compute stream: GraphSAGE fwd/bwd on slot i % 2 (FusedSAGE), gradient
+  prep stream   : plan cursor -> sample MFG (sal_sample_mfg) -> destination
+                  feature rows (fp16 table -> bf16), for batch i+1, into device
+                  slot (i+1) % 2
+  late stream   : labels + reverse adjacency of batch i (+ zeroing of the
+                  tcgen05 gradient blocks), beside batch i's forward pass
+  compute stream: GraphSAGE fwd/bwd on slot i % 2 (FusedSAGE; layer 0 reads its
+                  sampled rows straight from the table when gather_free), weight
+                  gradients of the upper layers on a side stream, gradient
                   all-reduce (NCCL over NVLink when world > 1), fused Adam
 
 Shapes are static: each layer is padded to the plan's worst-case destination
@@ -16,7 +20,10 @@ a step has no host synchronisation.  With `graphs=True` the pair
 device epoch cursor (sal_plan_next) makes every replay prepare the next batch
 of the plan.  Seed nodes are sharded across ranks: step s trains plan batch
 s*W + r on rank r (effective batch 1024*W); a rank
-without a batch in the last step contributes a zero gradient.
+without a batch in the last step contributes a zero gradient.  The
+end-to-end mode (host_inputs) feeds each step's seeds from pinned host memory
+and reads each loss back (Trainer.run_steps).  Evaluator runs sampled
+inference on the same machinery.
 """
 
 from __future__ import annotations
