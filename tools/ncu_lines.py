@@ -21,7 +21,10 @@ def main(rep, kernel=None, top=30):
     lines = []
     for r in rows:
         if len(r) > si and r[0] not in ("", "Line No") and r[si] not in ("-", ""):
-            lines.append((int(r[0]), float(r[si]), r[ex], r[1].strip()))
+            try:  # source lines with embedded quotes can shift columns: skip them
+                lines.append((int(r[0]), float(r[si]), r[ex], r[1].strip()))
+            except ValueError:
+                continue
     tot = sum(v for _, v, _, _ in lines) or 1.0
     print(f"total samples {tot:.0f}")
     for ln, v, e, src in sorted(lines, key=lambda t: -t[1])[:int(top)]:
