@@ -114,3 +114,31 @@ def test_segment_mean_backward_vs_autograd():
     want = M.T @ g.double()
     assert torch.allclose(h.grad.double(), want, atol=1e-5)
     assert torch.allclose(out.double(), M @ h.detach().double(), atol=1e-5)
+
+
+@pytest.mark.parametrize("f,n_pad", [(128, 512), (104, 512), (128, 200000), (256, 512)])
+def test_segment_mean_no_pad_fill_leaves_padding(f, n_pad):
+    """sal_segment_mean_fwd_ex(SAL_SEG_NO_PAD_FILL): rows [n_dst, n_pad) keep what
+    the buffer held; rows below n_dst equal the zero-filling call."""
+    from paper_2110_08450_b200 import _lib
+    rng = np.random.default_rng(2)
+    n_dst, n_src = 300, 700
+    deg = rng.integers(0, 16, size=n_dst)
+    indptr = np.zeros(n_dst + 1, dtype=np.int32)
+    indptr[1:] = np.cumsum(deg)
+    src = rng.integers(0, n_src, size=int(indptr[-1])).astype(np.int32)
+    h = torch.from_numpy(rng.uniform(-1, 1, (n_src, f)).astype(np.float16)).cuda()
+    ip, sr = torch.from_numpy(indptr).cuda(), torch.from_numpy(src).cuda()
+    nd = torch.tensor([n_dst], dtype=torch.int64, device="cuda")
+    L = _lib.lib()
+    outs = []
+    for flags in (0, _lib.SAL_SEG_NO_PAD_FILL):
+        out = torch.full((n_pad, f), 7.0, dtype=torch.bfloat16, device="cuda")
+        _lib.check(L.sal_segment_mean_fwd_ex(ip.data_ptr(), sr.data_ptr(), nd.data_ptr(), n_pad,
+                                             h.data_ptr(), _lib.SAL_F16, h.stride(0), f,
+                                             out.data_ptr(), _lib.SAL_BF16, out.stride(0),
+                                             flags, _lib.stream_ptr()), "segment_mean_fwd_ex")
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][:n_dst], outs[1][:n_dst])
+    assert (outs[0][n_dst:] == 0).all() and (outs[1][n_dst:] == 7.0).all()
