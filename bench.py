@@ -68,6 +68,8 @@ def parse():
     p.add_argument("--prep-split", type=int, default=None,
                    help="three-slot pipeline: hops [0, s) of batch i+2 beside hops [s, L) of "
                         "batch i+1 (0 = two slots)")
+    p.add_argument("--bwd-parts", type=int, default=None,
+                   help="row parts of the mean_bwd_t -> layer-0 weight-gradient pipeline")
     p.add_argument("--materialise", action="store_true",
                    help="train on the materialised feature gather instead of the gather-free "
                         "layer-0 path")
@@ -447,6 +449,8 @@ def run_ours(args):
             setattr(cfg, k, getattr(args, k))
     if args.prep_split is not None:
         cfg.prep_split = args.prep_split
+    if args.bwd_parts is not None:
+        cfg.bwd_parts = args.bwd_parts
     tr = Trainer(dg, train, cfg, rank=rank, world=world)
     spe = tr.set_epoch(0)
     K = args.steps if args.steps > 0 else spe

@@ -297,6 +297,16 @@ int sal_mean_bwd_t(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f,
                    const int32_t* indptr_dev, const int32_t* tindptr_dev, const int32_t* tdst_dev,
                    const float* tw_dev, int64_t rows, const uint8_t* mask_dev, float p,
                    void* dz_dev, int64_t ldz, int32_t dz_dtype, void* stream);
+/* part `part` of nparts of the same: source rows [b, e) where the first
+ * *m_dev (true row count) rows are cut at multiples of 64 and the last part
+ * runs to `rows` — the cut sal_tc_sage_wgrad_part uses, so the weight gradient
+ * of part k can run while part k+1 of dz is still being gathered */
+int sal_mean_bwd_t_part(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f,
+                        int64_t n_pad, const int32_t* indptr_dev, const int32_t* tindptr_dev,
+                        const int32_t* tdst_dev, const float* tw_dev, int64_t rows,
+                        const int64_t* m_dev, int32_t part, int32_t nparts,
+                        const uint8_t* mask_dev, float p, void* dz_dev, int64_t ldz,
+                        int32_t dz_dtype, void* stream);
 /* Adam (torch.optim.Adam, no weight decay) on flat fp32 params; step count
  * t = *t_dev + 1; refreshes the optional bf16 shadow copy; zero_grad != 0
  * leaves grad zeroed (the next backward accumulates without a memset) */
@@ -329,6 +339,12 @@ int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const int64_t* m_
 int sal_tc_sage_wgrad(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda, int64_t M,
                       const int64_t* m_dev, int32_t N, int32_t K, float* dW_dev, int64_t lddw,
                       int32_t accumulate, void* stream);
+/* the same over part `part` of nparts of the rows (sal_mean_bwd_t_part's cut);
+ * accumulate = 0 zeroes dW first, so parts after the first pass 1 */
+int sal_tc_sage_wgrad_part(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda,
+                           int64_t M, const int64_t* m_dev, int32_t part, int32_t nparts,
+                           int32_t N, int32_t K, float* dW_dev, int64_t lddw,
+                           int32_t accumulate, void* stream);
 /* the same two GEMMs without TMA / warp specialisation (cp.async, one CTA
  * role) — the reference implementation the TMA versions are checked against */
 int sal_tc_sage_fwd_simple(const void* A_dev, int64_t lda, int64_t M, const void* W_dev,

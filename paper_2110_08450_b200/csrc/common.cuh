@@ -30,6 +30,26 @@ SAL_DEVINL uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// Row range [*b, *e) of part k of nparts over `rows` rows whose first *m_dev
+// are live (static shapes pad to `rows`): the live rows are cut at multiples
+// of 64, the last part runs to `rows`.  mean_bwd_t and the tcgen05 weight
+// gradient agree on it, so part k of one can start as part k of the other ends
+// (inner cuts never pass the 64-row chunk holding the last live row, so a
+// weight-gradient chunk never reads rows a later mean_bwd_t part writes).
+SAL_DEVINL void part_rows(const int64_t* m_dev, int64_t rows, int k, int nparts, int* b, int* e) {
+  const int64_t mt = m_dev ? (*m_dev < rows ? *m_dev : rows) : rows;
+  const int64_t cap = (mt + 63) / 64 * 64 < rows ? (mt + 63) / 64 * 64 : rows;
+  auto bound = [&](int j) -> int {
+    if (j <= 0) return 0;
+    if (j >= nparts) return (int)rows;
+    int64_t x = (mt * j + nparts - 1) / nparts;
+    x = (x + 63) / 64 * 64;
+    return (int)(x < cap ? x : cap);
+  };
+  *b = bound(k);
+  *e = bound(k + 1);
+}
+
 // Dropout stream of the training step (relu_dropout_fwd_kernel and the fused
 // tcgen05 epilogue must agree).  General p: 16 bits of uniform per element,
 // two splitmix64 draws per group of 8 elements.  p == 0.5 exactly (the

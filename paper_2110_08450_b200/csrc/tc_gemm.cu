@@ -650,8 +650,8 @@ constexpr uint32_t kQSmem = kQStages * kQStage + 1024 + 256;
 __global__ void __launch_bounds__(kQThreads, 1)
 sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
                       const __grid_constant__ CUtensorMap mapA, int M,
-                      const int64_t* __restrict__ m_dev, int tiles_k, float* __restrict__ dW,
-                      int64_t lddw) {
+                      const int64_t* __restrict__ m_dev, int part, int nparts, int tiles_k,
+                      float* __restrict__ dW, int64_t lddw) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + kQStages * kQStage);
@@ -664,10 +664,14 @@ sage_wgrad_tma_kernel(const __grid_constant__ CUtensorMap mapDz,
   const int n0 = (tile / tiles_k) * 128, k0 = (tile % tiles_k) * 128;
   // GEMM-K rows: the true row count when given (rows past it are zero / padding),
   // split evenly over the grid's splits in whole 64-row chunks
-  const int Me = m_dev ? (int)min((int64_t)M, *m_dev) : M;
+  // (of part `part` of nparts: rows [pb, pe), part_rows)
+  int pb = 0, pe = M;
+  if (nparts > 1) part_rows(m_dev, M, part, nparts, &pb, &pe);
+  const int Me = min(pe, m_dev ? (int)min((int64_t)M, *m_dev) : M);
   const int splits = (int)gridDim.y;
-  const int rows_per_split = ((Me + splits - 1) / splits + kGC - 1) / kGC * kGC;
-  const int m0 = split * rows_per_split;
+  const int span = max(Me - pb, 0);
+  const int rows_per_split = ((span + splits - 1) / splits + kGC - 1) / kGC * kGC;
+  const int m0 = pb + split * rows_per_split;
   const int m1 = min(Me, m0 + rows_per_split);
   const int nchunks = m1 > m0 ? (m1 - m0 + kGC - 1) / kGC : 0;
 
@@ -840,10 +844,12 @@ int sal_tc_sage_fwd_simple(const void* A, int64_t lda, int64_t M, const void* W,
   return SAL_OK;
 }
 
-int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, int64_t M,
-                      const int64_t* m_dev, int32_t N, int32_t K, float* dW, int64_t lddw,
-                      int32_t accumulate, void* stream) {
+int sal_tc_sage_wgrad_part(const void* dz, int64_t ldz, const void* A, int64_t lda, int64_t M,
+                           const int64_t* m_dev, int32_t part, int32_t nparts, int32_t N,
+                           int32_t K, float* dW, int64_t lddw, int32_t accumulate,
+                           void* stream) {
   if (N <= 0 || K <= 0 || N % 128 || K % 128) return SAL_EINVAL;
+  if (nparts < 1 || part < 0 || part >= nparts) return SAL_EINVAL;
   if (ldz % 8 || lda % 8 || ((uintptr_t)dz & 15) || ((uintptr_t)A & 15) || ((uintptr_t)dW & 15) ||
       lddw % 4 || lddw < K)
     return SAL_EINVAL;
@@ -867,14 +873,22 @@ int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, i
   const int tiles = (N / 128) * tiles_k;
   int splits = sal::num_sms() / tiles;
   if (splits < 1) splits = 1;
-  int rows = (int)((M + splits - 1) / splits);
+  const int64_t Mp = (M + nparts - 1) / nparts;
+  int rows = (int)((Mp + splits - 1) / splits);
   rows = (rows + 63) / 64 * 64;
-  splits = (int)((M + rows - 1) / rows);
+  splits = (int)((Mp + rows - 1) / rows);
   sal::tc::sage_wgrad_tma_kernel<<<dim3(tiles, splits), sal::tc::kQThreads, sal::tc::kQSmem, st>>>(
-      mD, mA, (int)M, m_dev, tiles_k, dW, lddw);
+      mD, mA, (int)M, m_dev, part, nparts, tiles_k, dW, lddw);
   if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
   sal::count_launch(1);
   return SAL_OK;
+}
+
+int sal_tc_sage_wgrad(const void* dz, int64_t ldz, const void* A, int64_t lda, int64_t M,
+                      const int64_t* m_dev, int32_t N, int32_t K, float* dW, int64_t lddw,
+                      int32_t accumulate, void* stream) {
+  return sal_tc_sage_wgrad_part(dz, ldz, A, lda, M, m_dev, 0, 1, N, K, dW, lddw, accumulate,
+                                stream);
 }
 
 int sal_tc_sage_wgrad_simple(const void* dz, int64_t ldz, const void* A, int64_t lda, int64_t M,

@@ -209,6 +209,9 @@ class FusedSAGE:
         # weight gradients of the layers above 0 on a second stream, beside the
         # input-gradient chain
         self.overlap_wgrad = True   # measured 0.233 -> 0.228 s per papers epoch
+        # the last input gradient and layer 0's weight gradient as a pipeline of
+        # row parts (1 = off)
+        self.bwd_parts = 1
         self._wgrad_stream = torch.cuda.Stream(device=dev)
 
     # ------------------------------------------------------------- weights
@@ -371,11 +374,17 @@ class FusedSAGE:
         transposes[i] = (tindptr, tdst) reverse adjacency of layer i (i >= 1);
         built here when not supplied (the trainer builds them on the prep
         stream)."""
-        dz = dlogits
+        self._backward_below(self.L - 1, dlogits, saved, transposes, grads_zeroed)
+
+    def _backward_below(self, top: int, dz, saved, transposes, grads_zeroed: bool):
+        """Weight gradients of layers top..0 from dz of layer top, and the input
+        gradients between them.  With bwd_parts > 1 the last input gradient
+        (mean_bwd_t into dz_0) and layer 0's tcgen05 weight gradient run as a
+        pipeline of row parts on two streams."""
         cs = torch.cuda.current_stream()
         ws = self._wgrad_stream if self.overlap_wgrad else None
         forked = False
-        for i in reversed(range(self.L)):
+        for i in reversed(range(top + 1)):
             if ws is not None and i != 0:
                 # the weight gradient of layer i only reads dz_i: it runs beside the
                 # input-gradient chain (dA GEMM -> mean_bwd_t) on a second stream
@@ -387,9 +396,36 @@ class FusedSAGE:
                 self._wgrad(i, dz, saved, grads_zeroed)
             if i == 0:
                 break
-            dz = self._input_grad(i, torch.mm(dz, self.wb[i]), saved, transposes)
+            dA = torch.mm(dz, self.wb[i])
+            if i == 1 and ws is not None and self.bwd_parts > 1 and self._tc_wgrad_layer(0):
+                self._input_grad_wgrad0_parts(dA, saved, transposes, grads_zeroed, ws)
+                forked = True
+                break
+            dz = self._input_grad(i, dA, saved, transposes)
         if forked:
             cs.wait_stream(ws)
+
+    def _input_grad_wgrad0_parts(self, dA, saved, transposes, grads_zeroed, ws) -> None:
+        """dz_0 = mean_bwd_t(dA of layer 1) in bwd_parts row parts on the current
+        stream; layer 0's weight gradient of part k follows on `ws` as soon as
+        part k is written (sal_mean_bwd_t_part / sal_tc_sage_wgrad_part cut the
+        rows identically)."""
+        L = _lib.lib()
+        cs = torch.cuda.current_stream()
+        P = self.bwd_parts
+        dzp = self._input_grad(1, dA, saved, transposes, parts=P)
+        rec0 = saved[0]
+        a0, n0 = rec0["a"], rec0["n_pad"]
+        m0 = rec0["adj"][3]
+        gi = self.gp[0]
+        for k in range(P):
+            dzp.launch(k)
+            ws.wait_stream(cs)
+            with torch.cuda.stream(ws):
+                _lib.check(L.sal_tc_sage_wgrad_part(
+                    dzp.out.data_ptr(), dzp.out.stride(0), a0.data_ptr(), a0.stride(0), n0,
+                    _lib.ptr(m0), k, P, gi.shape[0], gi.shape[1], gi.data_ptr(), gi.stride(0),
+                    1 if (grads_zeroed or k > 0) else 0, _lib.stream_ptr()), "tc_sage_wgrad_part")
 
     def _wgrad(self, i: int, dz, saved, grads_zeroed: bool) -> None:
         L = _lib.lib()
@@ -407,9 +443,10 @@ class FusedSAGE:
         else:
             _mm_f32(dz.t(), a[:n_pad], self.gp[i])
 
-    def _input_grad(self, i: int, dA, saved, transposes):
+    def _input_grad(self, i: int, dA, saved, transposes, parts: int = 0):
         """dz of layer i-1 from dA = [dmean | dh_dst] of layer i (mean_bwd_t over the
-        reverse adjacency, ReLU/dropout backward fused)."""
+        reverse adjacency, ReLU/dropout backward fused).  parts > 0: returns a
+        _PartLauncher whose launch(k) writes row part k (sal_mean_bwd_t_part)."""
         L = _lib.lib()
         rec = saved[i]
         a, n_pad = rec["a"], rec["n_pad"]
@@ -421,12 +458,19 @@ class FusedSAGE:
         else:
             tindptr, tdst, tw = build_transpose(indptr, src, n_dev, n_pad, rows)
         dzp = torch.empty((rows, f), dtype=self.act, device=a.device)
-        _lib.check(L.sal_mean_bwd_t(
-            dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
-            indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows,
-            saved[i - 1]["mask"].data_ptr(), self.p if self.training else 0.0,
-            dzp.data_ptr(), dzp.stride(0), _lib.dtype_code(self.act), _lib.stream_ptr()),
-            "mean_bwd_t")
+        p = self.p if self.training else 0.0
+        mask = saved[i - 1]["mask"]
+        m_rows = saved[i - 1]["adj"][3]   # true rows of dz = layer i-1's destinations
+
+        def launch(k: int, nparts: int) -> None:
+            _lib.check(L.sal_mean_bwd_t_part(
+                dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
+                indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows,
+                _lib.ptr(m_rows), k, nparts, mask.data_ptr(), p, dzp.data_ptr(), dzp.stride(0),
+                _lib.dtype_code(self.act), _lib.stream_ptr()), "mean_bwd_t")
+        if parts:
+            return _PartLauncher(dzp, lambda k: launch(k, parts))
+        launch(0, 1)
         return dzp
 
     # ------------------------------------------------------------- fused output layer
@@ -462,23 +506,15 @@ class FusedSAGE:
                                    self.dims[-1], self.c_pad, labels.data_ptr(), labels.numel(),
                                    out.data_ptr(), gi.data_ptr(), gi.stride(0), dA.data_ptr(),
                                    dA.stride(0), _lib.stream_ptr()), "sage_head")
+        if i == 0:
+            return out
+        if i == 1 and self.overlap_wgrad and self.bwd_parts > 1 and self._tc_wgrad_layer(0):
+            self._input_grad_wgrad0_parts(dA, saved, transposes, grads_zeroed,
+                                          self._wgrad_stream)
+            torch.cuda.current_stream().wait_stream(self._wgrad_stream)
+            return out
         dz = self._input_grad(i, dA, saved, transposes)
-        cs = torch.cuda.current_stream()
-        ws = self._wgrad_stream if self.overlap_wgrad else None
-        forked = False
-        for j in reversed(range(i)):
-            if ws is not None and j != 0:
-                ws.wait_stream(cs)
-                with torch.cuda.stream(ws):
-                    self._wgrad(j, dz, saved, grads_zeroed)
-                forked = True
-            else:
-                self._wgrad(j, dz, saved, grads_zeroed)
-            if j == 0:
-                break
-            dz = self._input_grad(j, torch.mm(dz, self.wb[j]), saved, transposes)
-        if forked:
-            cs.wait_stream(ws)
+        self._backward_below(i - 1, dz, saved, transposes, grads_zeroed)
         return out
 
     @torch.no_grad()
@@ -491,6 +527,13 @@ class FusedSAGE:
         finally:
             self.training = was
         return logits
+
+
+class _PartLauncher:
+    """dz buffer of a parted mean_bwd_t and the launcher of its parts."""
+
+    def __init__(self, out, launch):
+        self.out, self.launch = out, launch
 
 
 def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=None, ws=None,

@@ -125,3 +125,31 @@ def test_tc_wgrad_true_row_count(m_true):
         assert (dW == 0).all()
     else:
         assert ((dW - want).norm() / want.norm()).item() < 1e-3
+
+
+@pytest.mark.parametrize("m_true,parts", [(0, 2), (100, 2), (3000, 3), (4096, 4), (1000, 8),
+                                          (4000, 5)])
+def test_tc_wgrad_parts_sum_to_whole(m_true, parts):
+    """sal_tc_sage_wgrad_part over parts 0..P-1 (the first zeroing dW) equals the
+    whole weight gradient; no part reads a row past the 64-row chunk holding
+    the last live row."""
+    M, N, K = 4096, 256, 256
+    g = torch.Generator(device="cuda").manual_seed(19)
+    dz = (torch.randn(M, N, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    dz[m_true:] = 0
+    dz[-(-m_true // 64) * 64:] = float("nan")
+    A = (torch.randn(M, K, device="cuda", generator=g)).to(torch.bfloat16)
+    dW = torch.full((N, K), 3.0, device="cuda")
+    md = torch.tensor([m_true], dtype=torch.int64, device="cuda")
+    L = _lib.lib()
+    for k in range(parts):
+        _lib.check(L.sal_tc_sage_wgrad_part(dz.data_ptr(), dz.stride(0), A.data_ptr(),
+                                            A.stride(0), M, md.data_ptr(), k, parts, N, K,
+                                            dW.data_ptr(), dW.stride(0), 1 if k else 0,
+                                            _lib.stream_ptr()), "tc_sage_wgrad_part")
+    torch.cuda.synchronize()
+    want = dz[:m_true].float().t() @ A[:m_true].float()
+    if m_true == 0:
+        assert (dW == 0).all()
+    else:
+        assert ((dW - want).norm() / want.norm()).item() < 1e-3

@@ -86,15 +86,16 @@ def test_fused_logits_fp32_within_1e3_of_autograd_on_config_shape():
     assert err < 1e-3, err
 
 
-def _small_trainer(graphs, gather_free=False, seed=0, fanouts=(10, 5), prep_split=0, f=64):
+def _small_trainer(graphs, gather_free=False, seed=0, fanouts=(10, 5), prep_split=0, f=64,
+                   hidden=64, bwd_parts=1):
     g = synth_graph(30000, 10, 3.0, seed=4)
     fm = generate_features(30000, f, "f16", seed=4)
     y = planted_labels(fm.data, 8, seed=4)
     dg = DeviceGraph.from_host(g, fm, y)
     train = np.arange(0, 30000, 2)
-    cfg = TrainConfig(fanouts=FanoutSpec(fanouts), batch_size=512, hidden=64, lr=0.01,
+    cfg = TrainConfig(fanouts=FanoutSpec(fanouts), batch_size=512, hidden=hidden, lr=0.01,
                       graphs=graphs, gather_free=gather_free, model_seed=seed,
-                      prep_split=prep_split)
+                      prep_split=prep_split, bwd_parts=bwd_parts)
     return Trainer(dg, train, cfg), dg
 
 
@@ -281,3 +282,46 @@ def test_padded_feature_width_trains_and_evaluates():
     c, t = tr.evaluate(np.arange(1, 30000, 2)[:3000])
     ce, te = tr.evaluate_eager(np.arange(1, 30000, 2)[:3000])
     assert t == te == 3000 and abs(c - ce) <= 0.003 * 3000
+
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_backward_row_parts_match_whole(parts):
+    """bwd_parts: the last mean_bwd_t and layer 0's tcgen05 weight gradient run as
+    a two-stream pipeline of row parts; the gradients equal the one-pass ones
+    (dz_0 is bit-identical, dW_0 differs only in fp32 summation order)."""
+    g = synth_graph(3000, 8, 3.0, seed=5)
+    fm = generate_features(3000, 64, "f32", seed=5)
+    dg = DeviceGraph.from_host(g)
+    seeds = SeedBatch(0, np.random.default_rng(3).choice(3000, 200, replace=False))
+    mfg = multihop_mfg(dg, seeds, FanoutSpec((10, 5, 3)), 7)
+    x = torch.from_numpy(fm.data).cuda()[mfg.id_map.global_ids.long()]
+    labels = torch.from_numpy(np.random.default_rng(4).integers(0, 47, 200)).cuda()
+    grads = []
+    for p in (1, parts):
+        m = FusedSAGE(64, 128, 47, 3, dropout=0.5, seed=6, act_dtype=torch.bfloat16)
+        m.bwd_parts = p
+        assert m._tc_wgrad_layer(0)
+        adjs = [(l.indptr, l.src_local, l.num_dst,
+                 torch.tensor([l.num_dst], dtype=torch.int64, device="cuda"))
+                for l in mfg.layers]
+        logits, saved = m.forward(m.cat_input(x.to(torch.bfloat16)), adjs)
+        _, dlog = m.loss(logits, labels)
+        m.backward(dlog, saved)
+        torch.cuda.synchronize()
+        grads.append([gi.clone() for gi in m.g])
+    for i, (a, b) in enumerate(zip(*grads)):
+        r = ((a - b).norm() / b.norm().clamp_min(1e-12)).item()
+        assert r < 2e-3, (i, r)   # replay-to-replay noise of the bf16 backward is ~2e-4
+
+
+def test_trainer_with_backward_parts_matches_default():
+    a, _ = _small_trainer(True, hidden=128)
+    b, _ = _small_trainer(True, hidden=128, bwd_parts=3)
+    assert b.model.bwd_parts == 3 and b.model._tc_wgrad_layer(0)
+    for tr in (a, b):
+        tr.set_epoch(0)
+        tr.begin_epoch()
+        tr.run_steps(0, 8)
+        torch.cuda.synchronize()
+    la, lb = a.losses[:8].cpu().numpy(), b.losses[:8].cpu().numpy()
+    assert np.allclose(la, lb, rtol=1e-2, atol=1e-3), (la, lb)
