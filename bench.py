@@ -236,11 +236,13 @@ def kernel_profile(trainer, nbatches: int):
                trainer.policy, st)
         ev[1].record(st)
         # the layer-0 mean right after the sampler, as in the training step (its edge
-        # ids are still in L2); then the drop-in full row gather
-        _lib.check(Lb.sal_segment_mean_fwd(
+        # ids are still in L2; padding rows past the true count left alone, as the
+        # step's call does); then the drop-in full row gather
+        _lib.check(Lb.sal_segment_mean_fwd_ex(
             ws.dst_indptr[h0].data_ptr(), ws.src_glob.data_ptr(), ws.sizes[h0:h0 + 1].data_ptr(),
             ws.node_cap[h0], x.data_ptr(), _lib.SAL_F16, x.stride(0), f, mean_buf.data_ptr(),
-            _lib.SAL_BF16, mean_buf.stride(0), _lib.stream_ptr(st)), "segment_mean_fwd")
+            _lib.SAL_BF16, mean_buf.stride(0), _lib.SAL_SEG_NO_PAD_FILL, _lib.stream_ptr(st)),
+            "segment_mean_fwd_ex")
         ev[2].record(st)
         gather_rows(x, ws.globals, out_buf, n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
                     stream=st)
