@@ -209,6 +209,9 @@ class FusedSAGE:
         # weight gradients of the layers above 0 on a second stream, beside the
         # input-gradient chain
         self.overlap_wgrad = True   # measured 0.233 -> 0.228 s per papers epoch
+        # fork each overlapped weight gradient after the layer's dA GEMM (True) or
+        # before it (False)
+        self.wgrad_fork_late = True
         # the last input gradient and layer 0's weight gradient as a pipeline of
         # row parts (1 = off)
         self.bwd_parts = 1
@@ -385,18 +388,29 @@ class FusedSAGE:
         ws = self._wgrad_stream if self.overlap_wgrad else None
         forked = False
         for i in reversed(range(top + 1)):
-            if ws is not None and i != 0:
+            late = self.wgrad_fork_late and i != 0
+            if ws is not None and i != 0 and not late:
                 # the weight gradient of layer i only reads dz_i: it runs beside the
                 # input-gradient chain (dA GEMM -> mean_bwd_t) on a second stream
                 ws.wait_stream(cs)
                 with torch.cuda.stream(ws):
                     self._wgrad(i, dz, saved, grads_zeroed)
+                dz.record_stream(ws)
                 forked = True
-            else:
+            elif ws is None or i == 0:
                 self._wgrad(i, dz, saved, grads_zeroed)
             if i == 0:
                 break
             dA = torch.mm(dz, self.wb[i])
+            if ws is not None and late:
+                # forked after the dA GEMM: the weight gradient (a full-grid tcgen05
+                # kernel) then shares the SMs with the latency-bound mean_bwd_t
+                # gather instead of stretching the small dA GEMM it would displace
+                ws.wait_stream(cs)
+                with torch.cuda.stream(ws):
+                    self._wgrad(i, dz, saved, grads_zeroed)
+                dz.record_stream(ws)
+                forked = True
             if i == 1 and ws is not None and self.bwd_parts > 1 and self._tc_wgrad_layer(0):
                 self._input_grad_wgrad0_parts(dA, saved, transposes, grads_zeroed, ws)
                 forked = True

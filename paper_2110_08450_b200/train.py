@@ -61,6 +61,7 @@ class TrainConfig:
     compute_priority: int = 0      # ... of the training stream (0: the caller's stream)
     tc_wgrad: bool = True          # tcgen05 weight gradients where the shapes allow
     bwd_parts: int = 1             # row parts of the mean_bwd_t -> layer-0 wgrad pipeline
+    wgrad_fork_late: bool = True   # overlapped weight gradients fork after the dA GEMM
     late_prep: bool = True         # labels + reverse adjacency built beside the forward pass
     prep_mean0: bool = False       # gather-free: layer-0 mean on the prep stream (measured slower)
     sampler_lanes: int = 0         # lanes per destination (0 = smallest group holding the fanout)
@@ -189,6 +190,7 @@ class Trainer:
                                act_dtype=cfg.act_dtype, lr=cfg.lr)
         self.model.tc_wgrad = cfg.tc_wgrad
         self.model.bwd_parts = cfg.bwd_parts
+        self.model.wgrad_fork_late = cfg.wgrad_fork_late
         if world > 1:  # identical initial weights on every rank
             torch.distributed.broadcast(self.model.flat, src=0)
             self.model.refresh_shadow()

@@ -325,3 +325,51 @@ def test_trainer_with_backward_parts_matches_default():
         torch.cuda.synchronize()
     la, lb = a.losses[:8].cpu().numpy(), b.losses[:8].cpu().numpy()
     assert np.allclose(la, lb, rtol=1e-2, atol=1e-3), (la, lb)
+
+
+@pytest.mark.parametrize("dtype,f", [(torch.bfloat16, 256), (torch.bfloat16, 32),
+                                     (torch.bfloat16, 512), (torch.bfloat16, 104),
+                                     (torch.float32, 64)])
+@pytest.mark.parametrize("parts", [1, 3])
+def test_mean_bwd_t_matches_scatter_reference(dtype, f, parts):
+    """sal_mean_bwd_t(_part): dz[s] = mask(s) / (1-p) * (dA[s, f:2f] (s < n_pad) +
+    sum over in-edges d of dA[d, :f] / deg(d)), against an fp32 index_add scatter
+    (rows with 0, 1 and several in-edges, self rows, padded rows)."""
+    from paper_2110_08450_b200 import _lib
+    from paper_2110_08450_b200.model import build_transpose
+    rng = np.random.default_rng(7)
+    n_dst, rows, p = 300, 2000, 0.5
+    deg = rng.integers(0, 12, size=n_dst)
+    indptr = np.zeros(n_dst + 1, dtype=np.int32)
+    indptr[1:] = np.cumsum(deg)
+    src = rng.integers(0, rows - 100, size=int(indptr[-1])).astype(np.int32)
+    ip, sr = torch.from_numpy(indptr).cuda(), torch.from_numpy(src).cuda()
+    n_true = 1900                                       # rows past it: padding
+    md = torch.tensor([n_true], dtype=torch.int64, device="cuda")
+    tind, tdst, tw = build_transpose(ip, sr, torch.tensor([n_dst], dtype=torch.int64,
+                                                          device="cuda"), n_dst, rows)
+    dA = (torch.randn(n_dst, 2 * f, device="cuda") * 0.1).to(dtype)
+    mask = torch.from_numpy(rng.integers(0, 256, size=rows * f // 8, dtype=np.uint8)).cuda()
+    dz = torch.full((rows, f), float("nan"), device="cuda", dtype=dtype)
+    L = _lib.lib()
+    for k in range(parts):
+        _lib.check(L.sal_mean_bwd_t_part(dA.data_ptr(), dA.stride(0), _lib.dtype_code(dtype), f,
+                                         n_dst, ip.data_ptr(), tind.data_ptr(), tdst.data_ptr(),
+                                         tw.data_ptr(), rows, md.data_ptr(), k, parts,
+                                         mask.data_ptr(), p, dz.data_ptr(), dz.stride(0),
+                                         _lib.dtype_code(dtype), _lib.stream_ptr()), "mbt")
+    torch.cuda.synchronize()
+    d32 = dA.float()
+    dst_of_edge = torch.repeat_interleave(torch.arange(n_dst, device="cuda"),
+                                          torch.from_numpy(deg).cuda())
+    w = 1.0 / torch.from_numpy(deg).cuda().clamp_min(1).float()
+    want = torch.zeros(rows, f, device="cuda")
+    want.index_add_(0, sr.long(), d32[dst_of_edge, :f] * w[dst_of_edge, None])
+    want[:n_dst] += d32[:, f:]
+    bits = torch.from_numpy(np.unpackbits(mask.cpu().numpy(), bitorder="little")
+                            .reshape(rows, f)).cuda().float()
+    want = want * bits * (1.0 / (1.0 - p))
+    assert not torch.isnan(dz).any()
+    tol = 1e-5 if dtype == torch.float32 else 8e-3
+    assert torch.allclose(dz.float(), want, rtol=tol, atol=tol * 0.1), \
+        (dz.float() - want).abs().max().item()
