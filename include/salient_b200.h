@@ -321,7 +321,9 @@ int sal_step_tail(float* loss_dev, float* last_dev, float* log_dev, int64_t log_
 /* ---- tcgen05 GEMMs of the layer-0 SAGEConv (sm_100a tensor cores) -------- */
 /* Y = act(A[M,K] @ W[N,K]^T), bf16 in, fp32 TMEM accumulate, bf16 out; with
  * relu_dropout != 0 the epilogue applies ReLU + dropout (same stream as
- * sal_relu_dropout_fwd) and writes the bit mask [M, N/8].  N = K = 256.
+ * sal_relu_dropout_fwd) and writes the bit mask [M, N/8].  N = 256 and
+ * K = 256 (layer 0: [mean | h] of 128-d features) or K = 512 (a hidden layer
+ * of width 256: two 128-column blocks per row tile).
  * m_dev (nullable): true row count on the device; 128-row tiles past it are
  * zero-filled (Y and mask) without loading A or running the MMA, or left
  * unwritten when relu_dropout has bit 1 set (a caller that never reads the

@@ -459,14 +459,20 @@ SAL_DEVINL void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "
 SAL_DEVINL void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 SAL_DEVINL void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// BN output columns per CTA (the W block [BN x FK] stays resident: 128 KB for
+// (256, 256) and (128, 512)); blockIdx.y picks the column block n0 = BN * y of
+// the N = kFN = 256 output columns (dropout indices and the mask use the full row)
+template <int BN, int FK>
 __global__ void __launch_bounds__(kSThreads, 1)
 sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
                        const __grid_constant__ CUtensorMap mapW,
                        const __grid_constant__ CUtensorMap mapY, int M,
                        const int64_t* __restrict__ m_dev, uint8_t* __restrict__ mask, float p,
                        uint64_t seed, const int64_t* __restrict__ salt, int relu_dropout) {
+  static_assert(BN * FK * 2 == (int)kBBytes, "resident W block must be 128 KB");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int n0 = (int)blockIdx.y * BN;
   uint8_t* sB = smem;
   uint8_t* sA = smem + kBBytes;
   uint8_t* sY = sA + kSStages * kPABlk;
@@ -514,12 +520,12 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
     if (elect_one()) {
       mbar_expect_tx(bfull, kBBytes);
 #pragma unroll
-      for (int kb = 0; kb < kFK / kFKB; ++kb)
-        tma_load_2d(smem_u32(sB) + kb * (kFN * 128), &mapW, kb * kFKB, 0, bfull);
+      for (int kb = 0; kb < FK / kFKB; ++kb)
+        tma_load_2d(smem_u32(sB) + kb * (BN * 128), &mapW, kb * kFKB, n0, bfull);
       int stage = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < nfull; t += gridDim.x) {
-        for (int kb = 0; kb < kFK / kFKB; ++kb) {
+        for (int kb = 0; kb < FK / kFKB; ++kb) {
           mbar_wait(&empty[stage], ph ^ 1);
           mbar_expect_tx(&full[stage], kPABlk);
           tma_load_2d(smem_u32(sA) + stage * kPABlk, &mapA, kb * kFKB, t * kFM, &full[stage]);
@@ -528,7 +534,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = make_idesc(kFM, kFN, 0, 0);
+    const uint32_t idesc = make_idesc(kFM, BN, 0, 0);
     mbar_wait(bfull, 0);
     int stage = 0;
     uint32_t ph = 0;
@@ -538,18 +544,18 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
       const uint32_t tph = (uint32_t)((it >> 1) & 1);
       mbar_wait(&tempty[buf], tph ^ 1);
       tc_fence_after();
-      for (int kb = 0; kb < kFK / kFKB; ++kb) {
+      for (int kb = 0; kb < FK / kFKB; ++kb) {
         mbar_wait(&full[stage], ph);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kFKB / 16; ++k) {
             const uint64_t a = make_desc(smem_u32(sA) + stage * kPABlk + k * 32, 16, 1024, 2);
-            const uint64_t b = make_desc(smem_u32(sB) + kb * (kFN * 128) + k * 32, 16, 1024, 2);
+            const uint64_t b = make_desc(smem_u32(sB) + kb * (BN * 128) + k * 32, 16, 1024, 2);
             mma_f16(tmem + buf * 256, a, b, idesc, (kb | k) != 0);
           }
           mma_commit(&empty[stage]);
-          if (kb == kFK / kFKB - 1) mma_commit(&tfull[buf]);
+          if (kb == FK / kFKB - 1) mma_commit(&tfull[buf]);
         }
         __syncwarp();
         if (++stage == kSStages) { stage = 0; ph ^= 1; }
@@ -573,9 +579,10 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
       const int row0 = t * kFM + lg * 32;
       const int row = row0 + lane;
 #pragma unroll 1
-      for (int c = cq * (kFN / 4); c < (cq + 1) * (kFN / 4); c += 32) {
+      for (int cl = cq * (BN / 4); cl < (cq + 1) * (BN / 4); cl += 32) {
+        const int c = n0 + cl;   // output column
         uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * 256 + c), r);
+        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * 256 + cl), r);
         alignas(16) __nv_bfloat16 o[32];
         const uint32_t bits =
             relu_dropout32(r, row, c, relu_dropout, p, scale, thresh, key_base, o);
@@ -616,7 +623,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
            t += gridDim.x) {
         if (t < nfull) continue;
         const int row0 = t * kFM + lg * 32;
-        for (int c = cq * (kFN / 4); c < (cq + 1) * (kFN / 4); c += 32) {
+        for (int c = n0 + cq * (BN / 4); c < n0 + (cq + 1) * (BN / 4); c += 32) {
           if (lane == 0) {
             tma_store_2d(&mapY, stg_s, c, row0);
             bulk_commit();
@@ -792,29 +799,33 @@ extern "C" {
 int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const int64_t* m_dev, const void* W,
                     int32_t N, int32_t K, void* Y, int64_t ldy, uint8_t* mask, float p,
                     uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout, void* stream) {
-  if (N != sal::tc::kFN || K != sal::tc::kFK) return SAL_EINVAL;
+  // (N, K) = (256, 256): one 128 x 256 tile per CTA step; (256, 512): two column
+  // blocks of 128 (grid.y), each CTA holding its [128 x 512] W block
+  if (N != sal::tc::kFN || (K != 256 && K != 512)) return SAL_EINVAL;
   if (lda % 8 || ldy % 8 || ((uintptr_t)A & 15) || ((uintptr_t)W & 15) || ((uintptr_t)Y & 15))
     return SAL_EINVAL;
   if (M <= 0) return SAL_OK;
+  const int bn = K == 256 ? 256 : 128;
+  const int nblk = N / bn;
   CUtensorMap mA, mW, mY;
-  if (!sal::tc::make_map(&mA, A, (uint64_t)M, 256, (uint64_t)lda, 64, 128) ||
-      !sal::tc::make_map(&mW, W, 256, 256, 256, 64, 256))
+  if (!sal::tc::make_map(&mA, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, 64, 128) ||
+      !sal::tc::make_map(&mW, W, (uint64_t)N, (uint64_t)K, (uint64_t)K, 64, (uint32_t)bn))
     return SAL_ECUDA;
   const int ntiles = (int)((M + 127) / 128);
-  int grid = sal::num_sms();
+  int grid = sal::num_sms() / nblk;
   if (grid > ntiles) grid = ntiles;
   if (!sal::tc::make_map(&mY, Y, (uint64_t)M, 256, (uint64_t)ldy, 32, 32,
                          CU_TENSOR_MAP_SWIZZLE_64B))
     return SAL_ECUDA;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sal::tc::sage_fwd_tma_st_kernel,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, sal::tc::kSSmem);
-    attr = true;
+  auto kern = K == 256 ? sal::tc::sage_fwd_tma_st_kernel<256, 256>
+                       : sal::tc::sage_fwd_tma_st_kernel<128, 512>;
+  static bool attr[2] = {false, false};
+  if (!attr[K == 512]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sal::tc::kSSmem);
+    attr[K == 512] = true;
   }
-  sal::tc::sage_fwd_tma_st_kernel<<<grid, sal::tc::kSThreads, sal::tc::kSSmem,
-                                    (cudaStream_t)stream>>>(mA, mW, mY, (int)M, m_dev, mask, p,
-                                                            seed, salt_dev, relu_dropout);
+  kern<<<dim3(grid, nblk), sal::tc::kSThreads, sal::tc::kSSmem, (cudaStream_t)stream>>>(
+      mA, mW, mY, (int)M, m_dev, mask, p, seed, salt_dev, relu_dropout);
   if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
   sal::count_launch(1);
   return SAL_OK;

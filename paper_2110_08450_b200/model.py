@@ -200,6 +200,8 @@ class FusedSAGE:
         self.training = True
         self.seed = seed
         self.use_tc = True
+        # K = 2 f_in of the layers on the tcgen05 forward
+        self.tc_fwd_k = (256, 512)
         # tcgen05 weight gradients (tiled split-K, sal_tc_sage_wgrad) where the
         # shapes allow; cuBLAS for the rest
         self.tc_wgrad = True
@@ -249,10 +251,11 @@ class FusedSAGE:
         return [self.flat, self.m, self.v, self.t]
 
     def _tc_layer(self, i: int) -> bool:
-        """Layers the hand-written tcgen05 kernels cover: bf16, K = 2 f_in = 256,
-        N = f_out = 256, with a hidden layer after it (the ReLU/dropout epilogue)."""
+        """Layers the hand-written tcgen05 forward covers: bf16, K = 2 f_in = 256 or
+        512, N = f_out = 256, with a hidden layer after it (the ReLU/dropout
+        epilogue)."""
         return (self.use_tc and self.act == torch.bfloat16 and i != self.L - 1
-                and 2 * self.dims[i] == 256 and self.dims[i + 1] == 256)
+                and 2 * self.dims[i] in self.tc_fwd_k and self.dims[i + 1] == 256)
 
     def _tc_wgrad_layer(self, i: int) -> bool:
         """dW_i on sal_tc_sage_wgrad: bf16 operands, dW rows and cols multiples of 128."""

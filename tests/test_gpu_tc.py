@@ -13,18 +13,21 @@ def _fwd(A, W, p=0.0, relu=True, seed=7, salt=None, out_cols=256, m_dev=None, fi
     mask = torch.full((M * 256 // 8,), 255 if fill else 0, dtype=torch.uint8, device="cuda")
     L = _lib.lib()
     _lib.check(L.sal_tc_sage_fwd(A.data_ptr(), A.stride(0), M, _lib.ptr(m_dev), W.data_ptr(),
-                                 256, 256,
+                                 256, A.shape[1],
                                  Y.data_ptr(), Y.stride(0), mask.data_ptr(), p, seed,
                                  _lib.ptr(salt), int(relu), _lib.stream_ptr()), "tc_sage_fwd")
     torch.cuda.synchronize()
     return Y, mask
 
 
-@pytest.mark.parametrize("M", [128, 1000, 67584])
-def test_tc_fwd_matches_torch(M):
+@pytest.mark.parametrize("M,K", [(128, 256), (1000, 256), (67584, 256), (128, 512),
+                                 (1000, 512), (6144, 512)])
+def test_tc_fwd_matches_torch(M, K):
+    """K = 256: the layer-0 shape; K = 512: a hidden layer's [mean | h] (two
+    128-column blocks per row tile, grid.y)."""
     g = torch.Generator(device="cuda").manual_seed(M)
-    A = (torch.randn(M, 512, device="cuda", generator=g) * 0.5).to(torch.bfloat16)[:, :256]
-    W = (torch.randn(256, 256, device="cuda", generator=g) * 0.06).to(torch.bfloat16)
+    A = (torch.randn(M, 2 * K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)[:, :K]
+    W = (torch.randn(256, K, device="cuda", generator=g) * 0.06).to(torch.bfloat16)
     Y, mask = _fwd(A, W, p=0.0, relu=False)
     want = A.float() @ W.float().t()
     err = (Y.float() - want).norm() / want.norm()
@@ -38,11 +41,12 @@ def test_tc_fwd_matches_torch(M):
     assert agree.all()
 
 
-def test_tc_fwd_dropout_matches_unfused_kernels():
+@pytest.mark.parametrize("K", [256, 512])
+def test_tc_fwd_dropout_matches_unfused_kernels(K):
     M = 4096
     g = torch.Generator(device="cuda").manual_seed(1)
-    A = (torch.randn(M, 256, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
-    W = (torch.randn(256, 256, device="cuda", generator=g) * 0.06).to(torch.bfloat16)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(256, K, device="cuda", generator=g) * 0.06).to(torch.bfloat16)
     salt = torch.tensor([5], dtype=torch.int64, device="cuda")
     Y, mask = _fwd(A, W, p=0.5, relu=True, seed=123, salt=salt)
     # unfused: torch GEMM -> library relu_dropout with the same seed/salt
@@ -84,14 +88,15 @@ def test_tc_wgrad_matches_torch(M, N, K):
     assert err < 1e-3, err
 
 
+@pytest.mark.parametrize("K", [256, 512])
 @pytest.mark.parametrize("m_true", [0, 1, 300, 1000, 4096])
-def test_tc_fwd_true_row_count_zero_fills_padding(m_true):
+def test_tc_fwd_true_row_count_zero_fills_padding(m_true, K):
     """Static shapes pad to M; rows past *m_dev come out zero (Y and mask) and the
     rows before it equal the full computation."""
     M = 4096
     g = torch.Generator(device="cuda").manual_seed(9)
-    A = (torch.randn(M, 256, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
-    W = (torch.randn(256, 256, device="cuda", generator=g) * 0.06).to(torch.bfloat16)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(256, K, device="cuda", generator=g) * 0.06).to(torch.bfloat16)
     salt = torch.tensor([3], dtype=torch.int64, device="cuda")
     Yf, mf = _fwd(A, W, p=0.5, relu=True, seed=11, salt=salt)
     md = torch.tensor([m_true], dtype=torch.int64, device="cuda")

@@ -5,6 +5,7 @@ python tools/step_ab.py [--steps N] [variant ...]   (under gpurun)
 variant = name:key=val,key=val   e.g.  notc:sampler_tcount=0  nofirst:first_edge=0
 """
 import argparse
+import ast
 import gc
 import sys
 from pathlib import Path
@@ -17,10 +18,15 @@ from paper_2110_08450_b200.train import TrainConfig, Trainer  # noqa: E402
 
 
 def parse_variant(s):
+    """name:key=val,...; a key `m.attr` sets FusedSAGE.attr (a Python literal; use
+    `;` for commas inside it, e.g. m.tc_fwd_k=(256;)) after the trainer is built."""
     name, _, kv = s.partition(":")
     out = {}
     for item in filter(None, kv.split(",")):
         k, v = item.split("=")
+        if k.startswith("m."):
+            out[k] = ast.literal_eval(v.replace(";", ","))
+            continue
         f = TrainConfig.__dataclass_fields__[k]
         out[k] = (v not in ("0", "false")) if f.type in (bool, "bool") else type(f.default)(v)
     return name, out
@@ -38,7 +44,11 @@ def main():
     res = {n: [] for n, _ in variants}
     for rep in range(a.reps):
         for name, kw in variants:
-            tr = Trainer(dg, train, TrainConfig(gather_free=True, **kw))
+            tr = Trainer(dg, train, TrainConfig(gather_free=True, **{k: v for k, v in kw.items()
+                                                                    if not k.startswith("m.")}))
+            for k, v in kw.items():
+                if k.startswith("m."):
+                    setattr(tr.model, k[2:], v)
             spe = tr.set_epoch(0)
             n = a.steps or spe
             tr.begin_epoch(False)
