@@ -7,11 +7,15 @@ available when a device entry point is called, the call raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import torch
 
-LIB_PATH = Path(__file__).resolve().parent / "libsalient_b200.so"
+# SAL_LIB: load another build of the same library (A/B of compile-time variants
+# by tools/; the product path uses the in-tree build)
+LIB_PATH = Path(os.environ.get("SAL_LIB") or
+                Path(__file__).resolve().parent / "libsalient_b200.so")
 
 SAL_MAX_HOPS = 8
 SAL_RNG_SPLITMIX = 0

@@ -648,7 +648,10 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
 // the CTAs of one split read the same dz/A rows at the same time, so the
 // second read of each chunk hits L2.  Stage = dz chunk [64 rows x 128] + A
 // chunk [64 x 128], each two TMA boxes of {64 mn, 64 k}.
-constexpr int kQStages = 6;
+#ifndef SAL_WGRAD_STAGES
+#define SAL_WGRAD_STAGES 6
+#endif
+constexpr int kQStages = SAL_WGRAD_STAGES;
 constexpr int kQThreads = 192;
 constexpr uint32_t kQHalf = kGC * 128 * 2;   // 16 KB per operand per stage
 constexpr uint32_t kQStage = 2 * kQHalf;
