@@ -648,6 +648,8 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
 // the CTAs of one split read the same dz/A rows at the same time, so the
 // second read of each chunk hits L2.  Stage = dz chunk [64 rows x 128] + A
 // chunk [64 x 128], each two TMA boxes of {64 mn, 64 k}.
+// stage count (-DSAL_WGRAD_STAGES=N builds the A/B variants of
+// profiles/r1_ab_wgrad_epilogue.txt; 3, 4 and 6 time alike alone, 6 is best in the step)
 #ifndef SAL_WGRAD_STAGES
 #define SAL_WGRAD_STAGES 6
 #endif
