@@ -297,6 +297,15 @@ int sal_mean_bwd_t(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f,
                    const int32_t* indptr_dev, const int32_t* tindptr_dev, const int32_t* tdst_dev,
                    const float* tw_dev, int64_t rows, const uint8_t* mask_dev, float p,
                    void* dz_dev, int64_t ldz, int32_t dz_dtype, void* stream);
+/* the same over the live rows only: source rows [0, ceil64(*m_dev)), m_dev = the
+ * true row count of dz; rows past that 64-row chunk are left unwritten.  For a dz
+ * whose only reader is the split-K weight gradient with the same m_dev (layer 0's
+ * dz: nothing reads its padding rows, the weight gradient reads whole 64-row chunks) */
+int sal_mean_bwd_t_live(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f,
+                        int64_t n_pad, const int32_t* indptr_dev, const int32_t* tindptr_dev,
+                        const int32_t* tdst_dev, const float* tw_dev, int64_t rows,
+                        const int64_t* m_dev, const uint8_t* mask_dev, float p, void* dz_dev,
+                        int64_t ldz, int32_t dz_dtype, void* stream);
 /* part `part` of nparts of the same: source rows [b, e) where the first
  * *m_dev (true row count) rows are cut at multiples of 64 and the last part
  * runs to `rows` — the cut sal_tc_sage_wgrad_part uses, so the weight gradient

@@ -120,6 +120,8 @@ SIGNATURES = {
     "sal_zero_spans": (ctypes.c_int, [vp, vp, i32, vp]),
     "sal_mean_bwd_t": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp,
                                       ctypes.c_float, vp, i64, i32, vp]),
+    "sal_mean_bwd_t_live": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp, vp,
+                                           ctypes.c_float, vp, i64, i32, vp]),
     "sal_mean_bwd_t_part": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp, i32,
                                            i32, vp, ctypes.c_float, vp, i64, i32, vp]),
     "sal_adam_step": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, ctypes.c_float, ctypes.c_float,

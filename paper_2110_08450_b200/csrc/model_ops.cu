@@ -328,7 +328,8 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
                   const int32_t* __restrict__ indptr, const int32_t* __restrict__ tindptr,
                   const int32_t* __restrict__ tdst, const float* __restrict__ tw, int64_t rows,
                   const int64_t* __restrict__ m_dev, int part, int nparts,
-                  const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz, int64_t ldz) {
+                  const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz, int64_t ldz,
+                  int live) {
   constexpr int kRows = 4;
   constexpr int kChunk = 8;  // source rows per warp task (lanes 0..7 fetch metadata)
   const int lane = threadIdx.x & 31;
@@ -336,6 +337,10 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
   // rows [rb, nrows) of this part (part_rows; the whole range when nparts == 1)
   int rb = 0, nrows = (int)rows;
   if (nparts > 1) part_rows(m_dev, rows, part, nparts, &rb, &nrows);
+  if (live && m_dev) {   // only the 64-row chunks holding live rows (sal_mean_bwd_t_live)
+    const int64_t cap = (*m_dev + 63) / 64 * 64;
+    if (cap < nrows) nrows = (int)cap;
+  }
   const int npad = (int)n_pad;
   const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
   for (int base = rb + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kChunk; base < nrows;
@@ -596,11 +601,12 @@ int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t
   return sal::done(3);
 }
 
-int sal_mean_bwd_t_part(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
-                        const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
-                        const float* tw, int64_t rows, const int64_t* m_dev, int32_t part,
-                        int32_t nparts, const uint8_t* mask, float p, void* dz, int64_t ldz,
-                        int32_t dz_dtype, void* stream) {
+static int mean_bwd_t_launch(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f,
+                             int64_t n_pad, const int32_t* indptr, const int32_t* tindptr,
+                             const int32_t* tdst, const float* tw, int64_t rows,
+                             const int64_t* m_dev, int32_t part, int32_t nparts,
+                             const uint8_t* mask, float p, void* dz, int64_t ldz,
+                             int32_t dz_dtype, void* stream, int live) {
   if (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0) return SAL_EINVAL;
   if (nparts < 1 || part < 0 || part >= nparts) return SAL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -608,11 +614,11 @@ int sal_mean_bwd_t_part(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f
   if (dA_dtype == SAL_BF16 && dz_dtype == SAL_BF16)
     sal::mean_bwd_t_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(
         (const __nv_bfloat16*)dA, lda, f, n_pad, indptr, tindptr, tdst, tw, rows, m_dev, part,
-        nparts, mask, p, (__nv_bfloat16*)dz, ldz);
+        nparts, mask, p, (__nv_bfloat16*)dz, ldz, live);
   else if (dA_dtype == SAL_F32 && dz_dtype == SAL_F32)
     sal::mean_bwd_t_kernel<float, float><<<g, 256, 0, st>>>(
         (const float*)dA, lda, f, n_pad, indptr, tindptr, tdst, tw, rows, m_dev, part, nparts,
-        mask, p, (float*)dz, ldz);
+        mask, p, (float*)dz, ldz, live);
   else
     return SAL_EINVAL;
   return sal::done(1);
@@ -622,8 +628,26 @@ int sal_mean_bwd_t(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int
                    const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
                    const float* tw, int64_t rows, const uint8_t* mask, float p, void* dz,
                    int64_t ldz, int32_t dz_dtype, void* stream) {
-  return sal_mean_bwd_t_part(dA, lda, dA_dtype, f, n_pad, indptr, tindptr, tdst, tw, rows,
-                             nullptr, 0, 1, mask, p, dz, ldz, dz_dtype, stream);
+  return mean_bwd_t_launch(dA, lda, dA_dtype, f, n_pad, indptr, tindptr, tdst, tw, rows, nullptr,
+                           0, 1, mask, p, dz, ldz, dz_dtype, stream, 0);
+}
+
+int sal_mean_bwd_t_part(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
+                        const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
+                        const float* tw, int64_t rows, const int64_t* m_dev, int32_t part,
+                        int32_t nparts, const uint8_t* mask, float p, void* dz, int64_t ldz,
+                        int32_t dz_dtype, void* stream) {
+  return mean_bwd_t_launch(dA, lda, dA_dtype, f, n_pad, indptr, tindptr, tdst, tw, rows, m_dev,
+                           part, nparts, mask, p, dz, ldz, dz_dtype, stream, 0);
+}
+
+int sal_mean_bwd_t_live(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
+                        const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
+                        const float* tw, int64_t rows, const int64_t* m_dev, const uint8_t* mask,
+                        float p, void* dz, int64_t ldz, int32_t dz_dtype, void* stream) {
+  if (m_dev == nullptr) return SAL_EINVAL;
+  return mean_bwd_t_launch(dA, lda, dA_dtype, f, n_pad, indptr, tindptr, tdst, tw, rows, m_dev,
+                           0, 1, mask, p, dz, ldz, dz_dtype, stream, 1);
 }
 
 int sal_adam_step(float* param, float* grad, float* m, float* v, void* shadow_bf16,

@@ -214,6 +214,8 @@ class FusedSAGE:
         # fork each overlapped weight gradient after the layer's dA GEMM (True) or
         # before it (False)
         self.wgrad_fork_late = True
+        # the last input gradient writes only the rows layer 0's weight gradient reads
+        self.mbt_live = True
         # the last input gradient and layer 0's weight gradient as a pipeline of
         # row parts (1 = off)
         self.bwd_parts = 1
@@ -487,6 +489,15 @@ class FusedSAGE:
                 _lib.dtype_code(self.act), _lib.stream_ptr()), "mean_bwd_t")
         if parts:
             return _PartLauncher(dzp, lambda k: launch(k, parts))
+        if i == 1 and self.mbt_live and m_rows is not None and self._tc_wgrad_layer(0):
+            # dz_0's only reader is layer 0's split-K weight gradient, which reads
+            # whole 64-row chunks up to its true row count: skip the padding rows
+            _lib.check(L.sal_mean_bwd_t_live(
+                dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
+                indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows,
+                m_rows.data_ptr(), mask.data_ptr(), p, dzp.data_ptr(), dzp.stride(0),
+                _lib.dtype_code(self.act), _lib.stream_ptr()), "mean_bwd_t_live")
+            return dzp
         launch(0, 1)
         return dzp
 

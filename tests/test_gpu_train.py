@@ -373,3 +373,38 @@ def test_mean_bwd_t_matches_scatter_reference(dtype, f, parts):
     tol = 1e-5 if dtype == torch.float32 else 8e-3
     assert torch.allclose(dz.float(), want, rtol=tol, atol=tol * 0.1), \
         (dz.float() - want).abs().max().item()
+
+
+@pytest.mark.parametrize("m_true", [0, 1, 1000, 1900, 1990])
+def test_mean_bwd_t_live_writes_only_live_chunks(m_true):
+    """sal_mean_bwd_t_live: rows below ceil64(m_true) equal sal_mean_bwd_t's, rows past
+    it keep what the buffer held."""
+    from paper_2110_08450_b200 import _lib
+    from paper_2110_08450_b200.model import build_transpose
+    rng = np.random.default_rng(11)
+    n_dst, rows, f = 300, 2000, 256
+    deg = rng.integers(0, 12, size=n_dst)
+    indptr = np.zeros(n_dst + 1, dtype=np.int32)
+    indptr[1:] = np.cumsum(deg)
+    src = rng.integers(0, rows, size=int(indptr[-1])).astype(np.int32)
+    ip, sr = torch.from_numpy(indptr).cuda(), torch.from_numpy(src).cuda()
+    tind, tdst, tw = build_transpose(ip, sr, torch.tensor([n_dst], dtype=torch.int64,
+                                                          device="cuda"), n_dst, rows)
+    dA = (torch.randn(n_dst, 2 * f, device="cuda") * 0.1).to(torch.bfloat16)
+    mask = torch.from_numpy(rng.integers(0, 256, size=rows * f // 8, dtype=np.uint8)).cuda()
+    md = torch.tensor([m_true], dtype=torch.int64, device="cuda")
+    L = _lib.lib()
+    whole = torch.empty(rows, f, device="cuda", dtype=torch.bfloat16)
+    live = torch.full((rows, f), float("nan"), device="cuda", dtype=torch.bfloat16)
+    args = (ip.data_ptr(), tind.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows)
+    _lib.check(L.sal_mean_bwd_t(dA.data_ptr(), dA.stride(0), _lib.SAL_BF16, f, n_dst, *args,
+                                mask.data_ptr(), 0.5, whole.data_ptr(), whole.stride(0),
+                                _lib.SAL_BF16, _lib.stream_ptr()), "whole")
+    _lib.check(L.sal_mean_bwd_t_live(dA.data_ptr(), dA.stride(0), _lib.SAL_BF16, f, n_dst,
+                                     *args, md.data_ptr(), mask.data_ptr(), 0.5,
+                                     live.data_ptr(), live.stride(0), _lib.SAL_BF16,
+                                     _lib.stream_ptr()), "live")
+    torch.cuda.synchronize()
+    cap = min(rows, -(-m_true // 64) * 64)
+    assert torch.equal(live[:cap].view(torch.int16), whole[:cap].view(torch.int16))
+    assert torch.isnan(live[cap:].float()).all()
