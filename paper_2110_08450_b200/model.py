@@ -216,6 +216,8 @@ class FusedSAGE:
         self.wgrad_fork_late = True
         # the last input gradient writes only the rows layer 0's weight gradient reads
         self.mbt_live = True
+        # zero-fill the padding rows of the tcgen05 forward's output and mask in training
+        self.pad_fill = False
         # the last input gradient and layer 0's weight gradient as a pipeline of
         # row parts (1 = off)
         self.bwd_parts = 1
@@ -327,8 +329,12 @@ class FusedSAGE:
                         a.data_ptr(), a.stride(0), n_pad, _lib.ptr(n_dev), self.wb[i].data_ptr(),
                         fo, 2 * f,
                         nxt[:, fo:].data_ptr(), nxt.stride(0), mask.data_ptr(), p, seed,
-                        # eval: nothing reads the padding rows (no backward), skip filling
-                        _lib.ptr(salt), 1 if self.training else 3, st), "tc_sage_fwd")
+                        # padding rows (past the true count) are left unwritten unless
+                        # pad_fill: no kernel reads them (the next layer's mean and GEMMs
+                        # touch only live rows, and mean_bwd_t's sum for a padding row is 0
+                        # whatever its mask bits)
+                        _lib.ptr(salt), 1 if (self.training and self.pad_fill) else 3, st),
+                        "tc_sage_fwd")
                 else:
                     z = torch.mm(a[:n_pad], self.wb[i].t())
                     _lib.check(L.sal_relu_dropout_fwd(
