@@ -156,8 +156,12 @@ template <typename T>
 __global__ void lsm_nll_kernel(const T* __restrict__ logits, int64_t ld, int64_t rows, int32_t C,
                                const int64_t* __restrict__ labels, float* __restrict__ loss,
                                T* __restrict__ grad, int64_t ldg) {
+  // one warp per row; a row of C <= 32 * kV logits is read once into registers
+  // (wider rows re-read it per pass); one loss atomic per block
+  constexpr int kV = 8;
   __shared__ float sh_cnt;
   __shared__ int warp_cnt[32];
+  __shared__ float warp_loss[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int c = 0;
   for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) c += labels[i] >= 0;
@@ -172,27 +176,60 @@ __global__ void lsm_nll_kernel(const T* __restrict__ logits, int64_t ld, int64_t
   __syncthreads();
   const float inv = 1.f / sh_cnt;
   const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
-  if (row >= rows) return;
-  const T* x = logits + row * ld;
-  T* g = grad + row * ldg;
-  const int64_t lab = labels[row];
-  float m = -INFINITY;
-  for (int j = lane; j < C; j += 32) m = fmaxf(m, F<T>::in(x[j]));
+  float my_loss = 0.f;
+  if (row < rows) {
+    const T* x = logits + row * ld;
+    T* g = grad + row * ldg;
+    const int64_t lab = labels[row];
+    if (C <= 32 * kV) {
+      float v[kV];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  float s = 0.f;
-  for (int j = lane; j < C; j += 32) s += __expf(F<T>::in(x[j]) - m);
-  s = warp_reduce_sum(s);
-  const float lse = m + __logf(s);
-  if (lab < 0) {
-    for (int j = lane; j < C; j += 32) g[j] = F<T>::out(0.f);
-    return;
+      for (int k = 0; k < kV; ++k) {
+        const int j = lane + 32 * k;
+        v[k] = j < C ? F<T>::in(x[j]) : -INFINITY;
+      }
+      float m = v[0];
+#pragma unroll
+      for (int k = 1; k < kV; ++k) m = fmaxf(m, v[k]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < kV; ++k)
+        if (lane + 32 * k < C) sum += __expf(v[k] - m);
+      sum = warp_reduce_sum(sum);
+      const float lse = m + __logf(sum);
+#pragma unroll
+      for (int k = 0; k < kV; ++k) {
+        const int j = lane + 32 * k;
+        if (j < C)
+          g[j] = F<T>::out(lab < 0 ? 0.f : (__expf(v[k] - lse) - (j == lab ? 1.f : 0.f)) * inv);
+        if (j == lab) my_loss = (lse - v[k]) * inv;
+      }
+    } else {
+      float m = -INFINITY;
+      for (int j = lane; j < C; j += 32) m = fmaxf(m, F<T>::in(x[j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float sum = 0.f;
+      for (int j = lane; j < C; j += 32) sum += __expf(F<T>::in(x[j]) - m);
+      sum = warp_reduce_sum(sum);
+      const float lse = m + __logf(sum);
+      for (int j = lane; j < C; j += 32) {
+        const float xj = F<T>::in(x[j]);
+        g[j] = F<T>::out(lab < 0 ? 0.f : (__expf(xj - lse) - (j == lab ? 1.f : 0.f)) * inv);
+        if (j == lab) my_loss = (lse - xj) * inv;
+      }
+    }
   }
-  for (int j = lane; j < C; j += 32) {
-    const float pj = __expf(F<T>::in(x[j]) - lse);
-    g[j] = F<T>::out((pj - (j == lab ? 1.f : 0.f)) * inv);
+  my_loss = warp_reduce_sum(my_loss);   // the label's lane holds the row's loss
+  if (lane == 0) warp_loss[warp] = my_loss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += warp_loss[w];
+    atomicAdd(loss, t);
   }
-  if (lane == 0) atomicAdd(loss, (lse - F<T>::in(x[lab])) * inv);
 }
 
 // ---------------------------------------------------------------------------

@@ -408,3 +408,31 @@ def test_mean_bwd_t_live_writes_only_live_chunks(m_true):
     cap = min(rows, -(-m_true // 64) * 64)
     assert torch.equal(live[:cap].view(torch.int16), whole[:cap].view(torch.int16))
     assert torch.isnan(live[cap:].float()).all()
+
+
+@pytest.mark.parametrize("dtype,C", [(torch.bfloat16, 172), (torch.bfloat16, 47),
+                                     (torch.float32, 256), (torch.bfloat16, 300)])
+def test_lsm_nll_matches_torch(dtype, C):
+    """sal_lsm_nll: mean NLL of log_softmax over rows with label >= 0 (added to *loss)
+    and its gradient (softmax - onehot) / count, zero rows for ignored labels."""
+    from paper_2110_08450_b200 import _lib
+    rows = 1000
+    g = torch.Generator(device="cuda").manual_seed(C)
+    logits = (torch.randn(rows, C, device="cuda", generator=g) * 3).to(dtype)
+    labels = torch.randint(0, C, (rows,), device="cuda", generator=g)
+    labels[::7] = -1
+    loss = torch.full((), 0.25, device="cuda")
+    grad = torch.full((rows, C), float("nan"), device="cuda", dtype=dtype)
+    L = _lib.lib()
+    _lib.check(L.sal_lsm_nll(logits.data_ptr(), logits.stride(0), rows, C,
+                             _lib.dtype_code(dtype), labels.data_ptr(), loss.data_ptr(),
+                             grad.data_ptr(), grad.stride(0), _lib.stream_ptr()), "lsm_nll")
+    torch.cuda.synchronize()
+    x = logits.float().requires_grad_(True)
+    keep = labels >= 0
+    want = torch.nn.functional.nll_loss(torch.log_softmax(x, -1)[keep], labels[keep])
+    want.backward()
+    assert abs(loss.item() - 0.25 - want.item()) < 1e-4 * max(1.0, want.item())
+    tol = 1e-6 if dtype == torch.float32 else 2e-2
+    assert torch.allclose(grad.float(), x.grad, rtol=tol, atol=tol * 1e-2)
+    assert (grad[~keep] == 0).all()
