@@ -1,12 +1,14 @@
-// Hand-written tcgen05 GEMMs for the layer-0 SAGEConv (sm_100a).
+// Hand-written tcgen05 GEMMs for the SAGEConv layers (sm_100a).
 //
-// Forward:  y = relu_dropout( A[M, K] @ W[N, K]^T )  with A the layer-0 "cat"
-//           buffer [mean | h_dst] (bf16, K = 2f = 256) and W = [W_neigh |
-//           W_self] (N = 256).  Production kernel (sage_fwd_tma_st_kernel):
-//           one CTA per SM, persistent over 128-row tiles; warp 0 streams A
-//           K-blocks with TMA into a 4-stage SWIZZLE_128B ring (W stays
-//           resident, 128 KB, loaded once); warp 1 issues tcgen05.mma (M=128,
-//           N=256, K=16) into one of two TMEM accumulators; 16 epilogue warps
+// Forward:  y = relu_dropout( A[M, K] @ W[N, K]^T )  with A a "cat" buffer
+//           [mean | h_dst] (bf16, K = 2f = 256 at layer 0, 512 at the hidden
+//           layer) and W = [W_neigh | W_self] (N = 256).  Production kernel
+//           (sage_fwd_tma_st_kernel<BN, K>): one CTA per SM and 128-column
+//           block (grid.y), persistent over 128-row tiles; warp 0 streams A
+//           K-blocks with TMA into a SWIZZLE_128B ring (8 stages at K = 256, 4
+//           at K = 512) while the CTA's W block stays resident (loaded once);
+//           warp 1 issues tcgen05.mma (M=128, N=BN, K=16) into one of two TMEM
+//           accumulators; 16 epilogue warps
 //           drain TMEM (tcgen05.ld 32x32b), apply ReLU + dropout, stage bf16
 //           32x32 chunks in shared memory and write them with TMA bulk tensor
 //           stores, plus the keep/relu bit mask — the GEMM output never
@@ -441,13 +443,19 @@ constexpr uint32_t kPABlk = kFM * kFKB * 2;
 // Here each warp converts a 32-row x 32-column chunk, writes it into a 2 KB
 // SWIZZLE_64B staging tile (conflict-free 16-byte shared stores) and one lane
 // issues a bulk tensor store.  16 epilogue warps (4 per SM sub-partition,
-// v1 had 2) hide the tcgen05.ld and RNG latency; the A ring keeps 4 K-blocks
-// (one full tile) in flight.
-constexpr int kSStages = 4;
+// v1 had 2) hide the tcgen05.ld and RNG latency.
 constexpr int kSEpiWarps = 16;
 constexpr int kSThreads = (2 + kSEpiWarps) * 32;
 constexpr uint32_t kSStage = 32 * 32 * 2;         // 2 KB staging per epilogue warp
-constexpr uint32_t kSSmem = kBBytes + kSStages * kPABlk + kSEpiWarps * kSStage + 1024 + 256;
+// shared memory of an instantiation: W block [BN x FK] + the A ring, filling what
+// the W block leaves (4 stages at 128 KB of W, 8 at 64 KB)
+template <int BN, int FK>
+struct FwdCfg {
+  static constexpr uint32_t kW = (uint32_t)BN * FK * 2;
+  static constexpr int kStages = kW >= 131072u ? 4 : 8;
+  static constexpr uint32_t kSmem = kW + kStages * kPABlk + kSEpiWarps * kSStage + 1024 + 256;
+  static_assert(kSmem <= 232448u, "shared memory");
+};
 
 SAL_DEVINL void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
   asm volatile(
@@ -469,20 +477,21 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
                        const __grid_constant__ CUtensorMap mapY, int M,
                        const int64_t* __restrict__ m_dev, uint8_t* __restrict__ mask, float p,
                        uint64_t seed, const int64_t* __restrict__ salt, int relu_dropout) {
-  static_assert(BN * FK * 2 == (int)kBBytes, "resident W block must be 128 KB");
+  constexpr uint32_t kWB = FwdCfg<BN, FK>::kW;
+  constexpr int kSt = FwdCfg<BN, FK>::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int n0 = (int)blockIdx.y * BN;
   uint8_t* sB = smem;
-  uint8_t* sA = smem + kBBytes;
-  uint8_t* sY = sA + kSStages * kPABlk;
+  uint8_t* sA = smem + kWB;
+  uint8_t* sY = sA + kSt * kPABlk;
   uint64_t* bars = (uint64_t*)(sY + kSEpiWarps * kSStage);
-  uint64_t* full = bars;                    // [kSStages]
-  uint64_t* empty = bars + kSStages;        // [kSStages]
-  uint64_t* bfull = bars + 2 * kSStages;    // W resident
-  uint64_t* tfull = bars + 2 * kSStages + 1;   // [2] accumulator ready
-  uint64_t* tempty = bars + 2 * kSStages + 3;  // [2] accumulator drained
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kSStages + 5);
+  uint64_t* full = bars;                    // [kSt]
+  uint64_t* empty = bars + kSt;        // [kSt]
+  uint64_t* bfull = bars + 2 * kSt;    // W resident
+  uint64_t* tfull = bars + 2 * kSt + 1;   // [2] accumulator ready
+  uint64_t* tempty = bars + 2 * kSt + 3;  // [2] accumulator drained
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * kSt + 5);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (M + kFM - 1) / kFM;
   // tiles past the true row count (*m_dev, static shapes pad to M) are only
@@ -491,7 +500,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
   const int nfull = (m_true + kFM - 1) / kFM;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < kSStages; ++i) {
+    for (int i = 0; i < kSt; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -518,7 +527,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
 
   if (warp == 0) {
     if (elect_one()) {
-      mbar_expect_tx(bfull, kBBytes);
+      mbar_expect_tx(bfull, kWB);
 #pragma unroll
       for (int kb = 0; kb < FK / kFKB; ++kb)
         tma_load_2d(smem_u32(sB) + kb * (BN * 128), &mapW, kb * kFKB, n0, bfull);
@@ -529,7 +538,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
           mbar_wait(&empty[stage], ph ^ 1);
           mbar_expect_tx(&full[stage], kPABlk);
           tma_load_2d(smem_u32(sA) + stage * kPABlk, &mapA, kb * kFKB, t * kFM, &full[stage]);
-          if (++stage == kSStages) { stage = 0; ph ^= 1; }
+          if (++stage == kSt) { stage = 0; ph ^= 1; }
         }
       }
     }
@@ -558,7 +567,7 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
           if (kb == FK / kFKB - 1) mma_commit(&tfull[buf]);
         }
         __syncwarp();
-        if (++stage == kSStages) { stage = 0; ph ^= 1; }
+        if (++stage == kSt) { stage = 0; ph ^= 1; }
       }
     }
   } else {
@@ -804,13 +813,13 @@ extern "C" {
 int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const int64_t* m_dev, const void* W,
                     int32_t N, int32_t K, void* Y, int64_t ldy, uint8_t* mask, float p,
                     uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout, void* stream) {
-  // (N, K) = (256, 256): one 128 x 256 tile per CTA step; (256, 512): two column
-  // blocks of 128 (grid.y), each CTA holding its [128 x 512] W block
+  // two column blocks of 128 (grid.y); each CTA holds its [128 x K] W block
+  // (K = 256: layer 0; K = 512: the hidden layer)
   if (N != sal::tc::kFN || (K != 256 && K != 512)) return SAL_EINVAL;
   if (lda % 8 || ldy % 8 || ((uintptr_t)A & 15) || ((uintptr_t)W & 15) || ((uintptr_t)Y & 15))
     return SAL_EINVAL;
   if (M <= 0) return SAL_OK;
-  const int bn = K == 256 ? 256 : 128;
+  const int bn = 128;
   const int nblk = N / bn;
   CUtensorMap mA, mW, mY;
   if (!sal::tc::make_map(&mA, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, 64, 128) ||
@@ -822,14 +831,19 @@ int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const int64_t* m_dev,
   if (!sal::tc::make_map(&mY, Y, (uint64_t)M, 256, (uint64_t)ldy, 32, 32,
                          CU_TENSOR_MAP_SWIZZLE_64B))
     return SAL_ECUDA;
-  auto kern = K == 256 ? sal::tc::sage_fwd_tma_st_kernel<256, 256>
+  // 128-column blocks for both K: the W block is 64 KB at K = 256, leaving room
+  // for an 8-stage A ring (179.0 against 179.5 us per step with 256-column tiles
+  // and 4 stages; the kernel alone times the same)
+  auto kern = K == 256 ? sal::tc::sage_fwd_tma_st_kernel<128, 256>
                        : sal::tc::sage_fwd_tma_st_kernel<128, 512>;
+  const uint32_t smem =
+      K == 256 ? sal::tc::FwdCfg<128, 256>::kSmem : sal::tc::FwdCfg<128, 512>::kSmem;
   static bool attr[2] = {false, false};
   if (!attr[K == 512]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sal::tc::kSSmem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr[K == 512] = true;
   }
-  kern<<<dim3(grid, nblk), sal::tc::kSThreads, sal::tc::kSSmem, (cudaStream_t)stream>>>(
+  kern<<<dim3(grid, nblk), sal::tc::kSThreads, smem, (cudaStream_t)stream>>>(
       mA, mW, mY, (int)M, m_dev, mask, p, seed, salt_dev, relu_dropout);
   if (cudaGetLastError() != cudaSuccess) return SAL_ECUDA;
   sal::count_launch(1);
