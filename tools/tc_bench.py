@@ -47,6 +47,12 @@ def fwd_tma():
                                  salt.data_ptr(), 1, st()))
 
 
+def fwd_tma_plain():   # no ReLU/dropout: the epilogue only converts (isolates its cost)
+    _lib.check(L.sal_tc_sage_fwd(A.data_ptr(), A.stride(0), M, None, W.data_ptr(), 256, 256,
+                                 Y.data_ptr(), Y.stride(0), mask.data_ptr(), 0.0, 1,
+                                 salt.data_ptr(), 0, st()))
+
+
 def fwd_simple():
     _lib.check(L.sal_tc_sage_fwd_simple(A.data_ptr(), A.stride(0), M, W.data_ptr(), 256, 256,
                                         Y.data_ptr(), Y.stride(0), mask.data_ptr(), 0.5, 1,
@@ -78,6 +84,7 @@ def wg_cublas():
 bytes_fwd = M * 256 * 2 * 2 + M * 32
 bytes_wg = M * 256 * 2 * 2
 for name, fn, nb in [("fwd tma (gemm+relu/dropout)", fwd_tma, bytes_fwd),
+                     ("fwd tma (gemm only)", fwd_tma_plain, bytes_fwd),
                      ("fwd simple", fwd_simple, bytes_fwd),
                      ("fwd cublas + relu_dropout", fwd_cublas, bytes_fwd),
                      ("wgrad tma", wg_tma, bytes_wg), ("wgrad simple", wg_simple, bytes_wg),
