@@ -141,11 +141,26 @@ SAL_DEVINL uint32_t relu_dropout32(const uint32_t* r, int64_t row, int c, int re
     const uint64_t e0 = (uint64_t)row * kFN + (uint64_t)c;
     const uint32_t keep = (uint32_t)(dropout_word64(key_base, e0 >> 6) >> (e0 & 63));
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float v = __uint_as_float(r[j]);
-      const bool on = ((keep >> j) & 1u) && v > 0.f;
-      bits |= (uint32_t)on << j;
-      o[j] = __float2bfloat16_rn(on ? v * 2.f : 0.f);
+    for (int j = 0; j < 32; ++j) bits |= (__uint_as_float(r[j]) > 0.f ? 1u : 0u) << j;
+    bits &= keep;
+    // word arithmetic instead of per-element selects: bf16x2(2 v) of every pair,
+    // ANDed with 0xFFFF halves where the keep/ReLU bit is set.  The 4 bits of a
+    // quad spread to the byte MSBs (one multiply; the 4 shifted copies do not
+    // overlap), prmt's sign replication widens a byte MSB to a 16-bit half.
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(o);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t spread = (((bits >> (4 * q)) & 0xFu) * 0x10204080u) & 0x80808080u;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 4 * q + 2 * h;
+        const __nv_bfloat162 b =
+            __floats2bfloat162_rn(__uint_as_float(r[j]) * 2.f, __uint_as_float(r[j + 1]) * 2.f);
+        uint32_t km;
+        asm("prmt.b32 %0, %1, 0, %2;" : "=r"(km) : "r"(spread), "r"(h ? 0xBBAAu : 0x9988u));
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(&b) & km;
+        o2[j >> 1] = *reinterpret_cast<const __nv_bfloat162*>(&w);
+      }
     }
     return bits;
   }
