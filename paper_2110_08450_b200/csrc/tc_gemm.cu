@@ -137,9 +137,11 @@ SAL_DEVINL uint32_t relu_dropout32(const uint32_t* r, int64_t row, int c, int re
     for (int j = 0; j < 32; ++j) o[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
     return 0;
   }
-  if (p == 0.5f) {  // one draw covers the 32 columns
+  if (p == 0.5f || p == 0.f) {  // p = 0.5: one draw covers the 32 columns; p = 0: ReLU only
     const uint64_t e0 = (uint64_t)row * kFN + (uint64_t)c;
-    const uint32_t keep = (uint32_t)(dropout_word64(key_base, e0 >> 6) >> (e0 & 63));
+    const uint32_t keep =
+        p > 0.f ? (uint32_t)(dropout_word64(key_base, e0 >> 6) >> (e0 & 63)) : 0xFFFFFFFFu;
+    const float mult = p > 0.f ? 2.f : 1.f;
 #pragma unroll
     for (int j = 0; j < 32; ++j) bits |= (__uint_as_float(r[j]) > 0.f ? 1u : 0u) << j;
     bits &= keep;
@@ -155,7 +157,7 @@ SAL_DEVINL uint32_t relu_dropout32(const uint32_t* r, int64_t row, int c, int re
       for (int h = 0; h < 2; ++h) {
         const int j = 4 * q + 2 * h;
         const __nv_bfloat162 b =
-            __floats2bfloat162_rn(__uint_as_float(r[j]) * 2.f, __uint_as_float(r[j + 1]) * 2.f);
+            __floats2bfloat162_rn(__uint_as_float(r[j]) * mult, __uint_as_float(r[j + 1]) * mult);
         uint32_t km;
         asm("prmt.b32 %0, %1, 0, %2;" : "=r"(km) : "r"(spread), "r"(h ? 0xBBAAu : 0x9988u));
         const uint32_t w = *reinterpret_cast<const uint32_t*>(&b) & km;
