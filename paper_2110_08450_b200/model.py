@@ -398,29 +398,30 @@ class FusedSAGE:
         cs = torch.cuda.current_stream()
         ws = self._wgrad_stream if self.overlap_wgrad else None
         forked = False
+
+        def fork_wgrad(i: int, dz) -> None:
+            # the weight gradient of layer i only reads dz_i: it runs on a second
+            # stream beside the input-gradient chain (dA GEMM -> mean_bwd_t)
+            ws.wait_stream(cs)
+            with torch.cuda.stream(ws):
+                self._wgrad(i, dz, saved, grads_zeroed)
+            dz.record_stream(ws)
+
         for i in reversed(range(top + 1)):
-            late = self.wgrad_fork_late and i != 0
+            # fork after the dA GEMM (wgrad_fork_late): the full-grid tcgen05 weight
+            # gradient then shares the SMs with the latency-bound mean_bwd_t gather
+            # instead of stretching the small dA GEMM it would displace
+            late = ws is not None and i != 0 and self.wgrad_fork_late
             if ws is not None and i != 0 and not late:
-                # the weight gradient of layer i only reads dz_i: it runs beside the
-                # input-gradient chain (dA GEMM -> mean_bwd_t) on a second stream
-                ws.wait_stream(cs)
-                with torch.cuda.stream(ws):
-                    self._wgrad(i, dz, saved, grads_zeroed)
-                dz.record_stream(ws)
+                fork_wgrad(i, dz)
                 forked = True
             elif ws is None or i == 0:
                 self._wgrad(i, dz, saved, grads_zeroed)
             if i == 0:
                 break
             dA = torch.mm(dz, self.wb[i])
-            if ws is not None and late:
-                # forked after the dA GEMM: the weight gradient (a full-grid tcgen05
-                # kernel) then shares the SMs with the latency-bound mean_bwd_t
-                # gather instead of stretching the small dA GEMM it would displace
-                ws.wait_stream(cs)
-                with torch.cuda.stream(ws):
-                    self._wgrad(i, dz, saved, grads_zeroed)
-                dz.record_stream(ws)
+            if late:
+                fork_wgrad(i, dz)
                 forked = True
             if i == 1 and ws is not None and self.bwd_parts > 1 and self._tc_wgrad_layer(0):
                 self._input_grad_wgrad0_parts(dA, saved, transposes, grads_zeroed, ws)
@@ -451,6 +452,7 @@ class FusedSAGE:
                     dzp.out.data_ptr(), dzp.out.stride(0), a0.data_ptr(), a0.stride(0), n0,
                     _lib.ptr(m0), k, P, gi.shape[0], gi.shape[1], gi.data_ptr(), gi.stride(0),
                     1 if (grads_zeroed or k > 0) else 0, _lib.stream_ptr()), "tc_sage_wgrad_part")
+        dzp.out.record_stream(ws)
 
     def _wgrad(self, i: int, dz, saved, grads_zeroed: bool) -> None:
         L = _lib.lib()
