@@ -59,6 +59,7 @@ class TrainConfig:
     prep_priority: int = 0         # CUDA stream priority of the prep stream (lower = higher)
     late_priority: int = 0         # ... of the stream building labels / reverse adjacency
     compute_priority: int = 0      # ... of the training stream (0: the caller's stream)
+    wgrad_priority: int = 0        # ... of the model's overlapped weight-gradient stream
     tc_wgrad: bool = True          # tcgen05 weight gradients where the shapes allow
     bwd_parts: int = 1             # row parts of the mean_bwd_t -> layer-0 wgrad pipeline
     wgrad_fork_late: bool = True   # overlapped weight gradients fork after the dA GEMM
@@ -191,6 +192,9 @@ class Trainer:
         self.model.tc_wgrad = cfg.tc_wgrad
         self.model.bwd_parts = cfg.bwd_parts
         self.model.wgrad_fork_late = cfg.wgrad_fork_late
+        if cfg.wgrad_priority != 0:
+            self.model._wgrad_stream = torch.cuda.Stream(device=self.device,
+                                                         priority=cfg.wgrad_priority)
         if world > 1:  # identical initial weights on every rank
             torch.distributed.broadcast(self.model.flat, src=0)
             self.model.refresh_shadow()
