@@ -487,6 +487,46 @@ __global__ void adam_kernel(float* __restrict__ p, float* __restrict__ g,
   }
 }
 
+// the same update, 4 elements per thread (n % 4 == 0, 16-byte aligned buffers):
+// a quarter of the threads, four independent element chains each
+SAL_DEVINL void adam_elem(float& p, float& g, float& m, float& v, float b1, float b2,
+                          float step, float rbc2, float eps, int zero_grad) {
+  const float gi = g;
+  if (zero_grad) g = 0.f;
+  const float mi = b1 * m + (1.f - b1) * gi;
+  const float vi = b2 * v + (1.f - b2) * gi * gi;
+  m = mi;
+  v = vi;
+  p = p - step * mi / (sqrtf(vi) * rbc2 + eps);
+}
+
+__global__ void adam4_kernel(float4* __restrict__ p, float4* __restrict__ g,
+                             float4* __restrict__ m, float4* __restrict__ v,
+                             uint2* __restrict__ shadow, int64_t n4, float lr, float b1,
+                             float b2, float eps, const int64_t* __restrict__ t_dev,
+                             int zero_grad) {
+  const float t = (float)(*t_dev + 1);
+  const float step = lr / (1.f - __powf(b1, t));
+  const float rbc2 = rsqrtf(1.f - __powf(b2, t));
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 pi = p[i], gi = g[i], mi = m[i], vi = v[i];
+    adam_elem(pi.x, gi.x, mi.x, vi.x, b1, b2, step, rbc2, eps, zero_grad);
+    adam_elem(pi.y, gi.y, mi.y, vi.y, b1, b2, step, rbc2, eps, zero_grad);
+    adam_elem(pi.z, gi.z, mi.z, vi.z, b1, b2, step, rbc2, eps, zero_grad);
+    adam_elem(pi.w, gi.w, mi.w, vi.w, b1, b2, step, rbc2, eps, zero_grad);
+    p[i] = pi;
+    m[i] = mi;
+    v[i] = vi;
+    if (zero_grad) g[i] = gi;
+    if (shadow) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(pi.x, pi.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(pi.z, pi.w);
+      shadow[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
+  }
+}
+
 __global__ void step_tail_kernel(float* __restrict__ loss, float* __restrict__ last,
                                  float* __restrict__ log, int64_t log_len,
                                  int64_t* __restrict__ step, int64_t* __restrict__ adam_t) {
@@ -692,8 +732,17 @@ int sal_adam_step(float* param, float* grad, float* m, float* v, void* shadow_bf
                   const int64_t* t_dev, int32_t zero_grad, void* stream) {
   if (param == nullptr || grad == nullptr || m == nullptr || v == nullptr || t_dev == nullptr)
     return SAL_EINVAL;
-  sal::adam_kernel<<<sal::ew_grid(n), 256, 0, (cudaStream_t)stream>>>(
-      param, grad, m, v, (__nv_bfloat16*)shadow_bf16, n, lr, beta1, beta2, eps, t_dev, zero_grad);
+  const bool vec = n % 4 == 0 &&
+                   ((uintptr_t)param | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) % 16 == 0 &&
+                   (uintptr_t)shadow_bf16 % 8 == 0;
+  if (vec)
+    sal::adam4_kernel<<<sal::ew_grid(n / 4), 256, 0, (cudaStream_t)stream>>>(
+        (float4*)param, (float4*)grad, (float4*)m, (float4*)v, (uint2*)shadow_bf16, n / 4, lr,
+        beta1, beta2, eps, t_dev, zero_grad);
+  else
+    sal::adam_kernel<<<sal::ew_grid(n), 256, 0, (cudaStream_t)stream>>>(
+        param, grad, m, v, (__nv_bfloat16*)shadow_bf16, n, lr, beta1, beta2, eps, t_dev,
+        zero_grad);
   return sal::done(1);
 }
 

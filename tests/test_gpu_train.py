@@ -436,3 +436,30 @@ def test_lsm_nll_matches_torch(dtype, C):
     tol = 1e-6 if dtype == torch.float32 else 2e-2
     assert torch.allclose(grad.float(), x.grad, rtol=tol, atol=tol * 1e-2)
     assert (grad[~keep] == 0).all()
+
+
+@pytest.mark.parametrize("n", [4096, 1001])   # vectorised (n % 4 == 0) and scalar paths
+def test_adam_step_matches_torch_adam(n):
+    """sal_adam_step: torch.optim.Adam (no weight decay) over 3 steps, the bf16 shadow
+    equal to the rounded parameters, the gradient zeroed when asked."""
+    from paper_2110_08450_b200 import _lib
+    g0 = torch.Generator(device="cuda").manual_seed(n)
+    p = torch.randn(n, device="cuda", generator=g0)
+    ref = torch.nn.Parameter(p.clone())
+    opt = torch.optim.Adam([ref], lr=0.01, betas=(0.9, 0.999), eps=1e-8)
+    m = torch.zeros_like(p)
+    v = torch.zeros_like(p)
+    shadow = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    L = _lib.lib()
+    for t in range(3):
+        grad = torch.randn(n, device="cuda", generator=g0)
+        ref.grad = grad.clone()
+        opt.step()
+        tdev = torch.tensor([t], dtype=torch.int64, device="cuda")
+        _lib.check(L.sal_adam_step(p.data_ptr(), grad.data_ptr(), m.data_ptr(), v.data_ptr(),
+                                   shadow.data_ptr(), n, 0.01, 0.9, 0.999, 1e-8, tdev.data_ptr(),
+                                   1, _lib.stream_ptr()), "adam")
+        torch.cuda.synchronize()
+        assert (grad == 0).all()
+        assert torch.allclose(p, ref.detach(), rtol=1e-5, atol=1e-6)
+        assert torch.equal(shadow, p.to(torch.bfloat16))
