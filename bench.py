@@ -75,6 +75,10 @@ def parse():
                         "layer-0 path")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-parity", action="store_true",
+                   help="skip the parity gate (device MFGs / batches vs the oracle)")
+    p.add_argument("--no-numba-reference", action="store_true",
+                   help="--impl reference: time only the C port, not the numba reference")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--kernel-batches", type=int, default=20)
     p.add_argument("--prep-batches", type=int, default=160,
@@ -185,19 +189,56 @@ def measured_peaks():
         return {}
 
 
+def split_ids(shape: str, seed: int = 1):
+    """Train / test node ids of a shape: seeded numpy split (host-reproducible, so
+    the reference arm builds the same epoch plan without the device)."""
+    n, _, _, _, ntrain, ntest = SHAPES[shape]
+    perm = np.random.default_rng(seed + 100).permutation(n)
+    return np.sort(perm[:ntrain]), np.sort(perm[ntrain:ntrain + ntest])
+
+
 def build_data(shape: str, seed: int = 1):
+    """The shape's synthetic graph, fp16 features and labels generated in HBM
+    (synth_graph_device; oracle.synth_graph_host rebuilds the same arrays on the
+    host for the reference arm)."""
     from paper_2110_08450_b200.graph import synth_graph_device
     n, slots, f, c, ntrain, ntest = SHAPES[shape]
     t0 = time.perf_counter()
     dg = synth_graph_device(n, slots / n, 3.0, seed=seed, num_features=f, num_classes=c,
                             feature_seed=seed, label_seed=seed)
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(seed + 100)
-    perm = torch.randperm(n, device="cuda", generator=gen)
-    train = perm[:ntrain].sort().values.cpu().numpy()
-    test = perm[ntrain:ntrain + ntest].sort().values.cpu().numpy()
     torch.cuda.synchronize()
-    return dg, train, test, time.perf_counter() - t0
+    gen_s = time.perf_counter() - t0
+    train, test = split_ids(shape, seed)
+    return dg, train, test, gen_s
+
+
+def inputs_digest(indptr, indices, features, labels) -> str:
+    """blake2b over the inputs both arms time on (indptr and labels whole, every
+    64th neighbour slot, every 1024th feature row): equal digests = same graph."""
+    import hashlib
+    h = hashlib.blake2b(digest_size=16)
+    h.update(np.ascontiguousarray(indptr, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(indices[::64], dtype=np.int32).tobytes())
+    h.update(np.ascontiguousarray(features[::1024]).view(np.uint16).tobytes())
+    h.update(np.ascontiguousarray(labels, dtype=np.int64).tobytes())
+    return h.hexdigest()
+
+
+def host_info() -> dict:
+    """CPU model and the cores this process may use (the baselines' `cores`)."""
+    model = None
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    return {"cpu_model": model, "cores": cores, "cpu_count": os.cpu_count()}
 
 
 # ---------------------------------------------------------------------------
@@ -227,6 +268,7 @@ def kernel_profile(trainer, nbatches: int):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     t_mfg = t_gat = t_mean = 0.0
     edges = nodes = e0 = d0 = 0
+    mfg_bytes = 0
     x = trainer.x_table
     f = x.shape[1]
     for b in range(nbatches):
@@ -255,6 +297,9 @@ def kernel_profile(trainer, nbatches: int):
         t_gat += ev[2].elapsed_time(ev[3]) / 1e3
         edges += sum(etot)
         nodes += sizes[-1]
+        for h in range(L):  # SURVEY §8(d) MFG-build bytes per hop
+            nd, e, nn = sizes[h], etot[h], sizes[h + 1] - sizes[h]
+            mfg_bytes += nd * (8 + 16 + 8) + e * (4 + 8) + e * (8 + 12 + 4) + nn * (8 + 12)
         e0 += etot[h0]
         d0 += sizes[h0]
     k = nbatches - 1
@@ -329,6 +374,7 @@ def kernel_profile(trainer, nbatches: int):
         "sampled_edges_per_s_8_concurrent": e_par / t_par,
         "sampled_edges_per_s_graph": edges / t_mfg_graph,
         "mfg_ms_per_batch_graph": 1e3 * t_mfg_graph / k,
+        "mfg_bytes_per_batch": mfg_bytes / k,
     }
 
 
@@ -363,33 +409,38 @@ def prep_epoch_profile(trainer, nbatches: int, workers=(1, 8)):
     return out
 
 
-def cpu_baseline(dg, trainer, fanouts, target_s: float, global_seed: int):
-    """Reference CPU prep path (oracle port) on all host cores, bounded sample."""
+def _oracle():
     sys.path.insert(0, str(REPO / "oracle"))
     import oracle as O
-    t0 = time.perf_counter()
-    indptr = dg.indptr.cpu().numpy()
-    indices = dg.indices.cpu().numpy()
-    feats = dg.feature_view().cpu().numpy()
-    copy_s = time.perf_counter() - t0
-    cores = os.cpu_count() or 1
-    plan = trainer.plan
+    return O
+
+
+def port_baseline(host: dict, plan, per_hop, target_s: float, global_seed: int, cores: int):
+    """The reference CPU prep path as the C port (oracle.c, pinned to the
+    reference's goldens) on `cores` host threads, on a bounded sample of the
+    epoch plan, plus a P = 1 sample."""
+    O = _oracle()
+    indptr, indices, feats = host["indptr"], host["indices"], host["features"]
+    n = len(indptr) - 1
     nb = len(plan)
     order = [(b.batch_id, b.dst_ids) for b in plan.batches]
     probe = order[:cores]
-    wall, stats, _ = O.epoch_prep(indptr, indices, dg.num_nodes, feats, None, probe,
-                                  fanouts.per_hop, global_seed, cores)
+    wall, stats, _ = O.epoch_prep(indptr, indices, n, feats, host["labels"], probe, per_hop,
+                                  global_seed, cores)
     per_batch_wall = wall / len(probe)
     want = int(min(nb, max(len(probe), target_s / max(per_batch_wall, 1e-6))))
     sample = order[:want]
-    wall, stats, _ = O.epoch_prep(indptr, indices, dg.num_nodes, feats, None, sample,
-                                  fanouts.per_hop, global_seed, cores)
+    wall, stats, _ = O.epoch_prep(indptr, indices, n, feats, host["labels"], sample, per_hop,
+                                  global_seed, cores)
     epoch_s = wall * nb / len(sample)
     edges = int(stats[:, 1].sum())
     samp_s = stats[:, 2].sum() / 1e9
     slic_s = stats[:, 3].sum() / 1e9
     nodes = int(stats[:, 0].sum())
     f = feats.shape[1]
+    k1 = max(2, min(16, int(0.25 * target_s / max(per_batch_wall * cores, 1e-6))))
+    wall1, _, _ = O.epoch_prep(indptr, indices, n, feats, host["labels"], order[:k1], per_hop,
+                               global_seed, 1)
     return {
         "value": epoch_s, "unit": "s", "cores": cores, "kind": "port",
         "sample": f"{len(sample)} of {nb} epoch batches (first in plan order), extrapolated "
@@ -399,43 +450,166 @@ def cpu_baseline(dg, trainer, fanouts, target_s: float, global_seed: int):
         "sampled_edges_per_s": edges / wall,
         "sampled_edges_per_s_per_core": edges / samp_s if samp_s else None,
         "gather_GBps_per_core": nodes * f * 6 / slic_s / 1e9 if slic_s else None,
-        "host_copy_s": copy_s,
+        "P1": {"epoch_s": wall1 * nb / k1, "batches": k1},
     }
+
+
+def numba_reference(host: dict, shape: str, train, per_hop, target_s: float, global_seed: int,
+                    cores: int):
+    """The UNMODIFIED reference (`mfgprep` installed into baseline/_ref, numba
+    kernels) through its public API: run_epoch_prep(CsrGraph, FeatureMatrix,
+    LabelVector, plan, PrepConfig(num_workers=P), seed) after a warm-up
+    prepare_batch (prep.py:337-350), on a bounded sample of the same epoch plan,
+    at P = cores and P = 1.  None when baseline/_ref is absent."""
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "mfgprep" / "__init__.py").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+    sys.path.insert(0, str(ref))
+    import mfgprep as R
+    n, _, f, c, _, _ = SHAPES[shape]
+    g = R.CsrGraph(n, host["indptr"], host["indices"].astype(np.int64))
+    fm = R.FeatureMatrix(n, f, np.ascontiguousarray(host["features"][:, :f]))
+    y = R.LabelVector(host["labels"], c)
+    plan = R.make_epoch_plan(train, 1024, 1)
+    fan = R.FanoutSpec(tuple(per_hop))
+    nb = len(plan)
+    t0 = time.perf_counter()
+    R.prepare_batch(g, fm, y, plan.batches[0], fan, R.SamplerVariant(), global_seed)
+    warm_s = time.perf_counter() - t0
+
+    def run(batches, P):
+        sub = R.EpochPlan(batches=tuple(batches), batch_size=1024, shuffle_seed=1)
+        r = R.run_epoch_prep(g, fm, y, sub, R.PrepConfig(num_workers=P, fanouts=fan),
+                             global_seed)
+        edges = 0
+        for b in r:
+            edges += b.num_edges
+        return r.report, edges
+
+    rep, _ = run(plan.batches[:cores], cores)          # probe (JIT of the workers' path warm)
+    per_batch = rep.both_s / cores
+    K = int(min(nb, max(cores, target_s / max(per_batch, 1e-6))))
+    rep, edges = run(plan.batches[:K], cores)
+    k1 = max(2, min(8, int(0.25 * target_s / max(per_batch * cores, 1e-6))))
+    rep1, _ = run(plan.batches[:k1], 1)
+    return {
+        "value": rep.both_s * nb / K, "unit": "s", "cores": cores, "kind": "reference",
+        "sample": f"first {K} of {nb} epoch batches at num_workers={cores} "
+                  f"(mfgprep.run_epoch_prep, numba, baseline/_ref), extrapolated to the epoch; "
+                  f"warm-up prepare_batch {warm_s:.1f} s (JIT) not timed",
+        "batches": K, "both_s": rep.both_s, "sampling_s": rep.sampling_s,
+        "slicing_s": rep.slicing_s, "sampled_edges_per_s": edges / rep.both_s,
+        "P1": {"epoch_s": rep1.both_s * nb / k1, "batches": k1,
+               "sampling_s": rep1.sampling_s, "slicing_s": rep1.slicing_s},
+    }
+
+
+def cpu_leg(dg, train, fan, args, global_seed: int) -> dict:
+    """After the timed region, rank 0 at N = 1: host copies of the device inputs,
+    then the parity gate (the checker: oracle.parity on >= 8 papers batches at
+    (15,10,5), (5,10,15) and (20,20,20), plus f32 prepare_batch digests), then the
+    CPU baseline (the C port timed on the host cores)."""
+    from paper_2110_08450_b200 import make_epoch_plan
+    _oracle()
+    import shape_parity as parity
+    info = host_info()
+    out = {"host": info}
+    t0 = time.perf_counter()
+    host = parity.host_copy(dg)
+    out["host_copy_s"] = round(time.perf_counter() - t0, 1)
+    out["config_inputs_digest"] = inputs_digest(host["indptr"], host["indices"],
+                                                host["features"], host["labels"])
+    plan = make_epoch_plan(train, 1024, 1)
+    if not args.no_parity:
+        batches = parity.pick_batches(plan, k=8, seed=0)
+        fans = [tuple(fan.per_hop), (5, 10, 15), (20, 20, 20)]
+        r = parity.check(dg, host, batches, fans, global_seed)
+        out["parity"] = {
+            "shape": args.shape, "batches": [int(b.batch_id) for b in batches],
+            "fanouts": [list(x) for x in fans],
+            "mfg_checked": r["mfg_checked"], "mfg_equal": r["mfg_equal"],
+            "batch_checked": r["batch_checked"], "batch_equal": r["batch_equal"],
+            "equal": not r["mismatches"] and r["mfg_checked"] > 0,
+            "mismatches": r["mismatches"], "seconds": r["seconds"],
+            "what": "public multihop_mfg digests (sampler.py:228-235) and f32 prepare_batch "
+                    "digests (prep.py:132-137) on the device vs oracle.c on host copies of "
+                    "the same arrays"}
+    if not args.no_cpu_baseline:
+        cb = port_baseline(host, plan, tuple(fan.per_hop), args.cpu_seconds, global_seed,
+                           info["cores"])
+        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        out["cpu_baseline_detail"] = cb
+    return out
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args):
-    """--impl reference: the reference CPU path on the host cores (rank 0 only)."""
-    rank, world, local = dist_setup(args)
+    """--impl reference: the reference CPU path on the host cores, rank 0 only.
+
+    Builds the shape's inputs on the host (oracle.synth_graph_host: the same
+    arrays synth_graph_device makes, no product library loaded), then times the
+    unmodified reference (numba, baseline/_ref) and its C port (oracle.c)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
-        barrier(world)
         return
-    from paper_2110_08450_b200 import FanoutSpec
-    from paper_2110_08450_b200.train import TrainConfig, Trainer
-    fan = FanoutSpec(tuple(int(x) for x in args.fanouts.split(",")))
-    dg, train, _, _ = build_data(args.shape)
-    tr = Trainer(dg, train, TrainConfig(fanouts=fan, hidden=8, graphs=False))
-    spe_1 = tr.set_epoch(0)
-    cb = cpu_baseline(dg, tr, fan, args.cpu_seconds * 2, 1)
-    nb = len(tr.plan)
+    O = _oracle()
+    info = host_info()
+    cores = info["cores"]
+    n, slots, f, c, _, _ = SHAPES[args.shape]
+    per_hop = tuple(int(x) for x in args.fanouts.split(","))
+    t0 = time.perf_counter()
+    host = O.synth_graph_host(n, slots / n, 3.0, seed=1, num_features=f, num_classes=c,
+                              feature_seed=1, label_seed=1, nthreads=cores)
+    gen_s = time.perf_counter() - t0
+    if host["features"].shape[1] != f:
+        host["features"] = np.ascontiguousarray(host["features"][:, :f])
+    train, _ = split_ids(args.shape)
+    digest = inputs_digest(host["indptr"], host["indices"], host["features"][:, :f],
+                           host["labels"])
+    # the epoch plan (prep.py:40-52): the same numpy call as both packages' make_epoch_plan
+    perm = train[np.random.default_rng(1).permutation(len(train))]
+
+    class _B:
+        def __init__(self, i, ids):
+            self.batch_id, self.dst_ids = i, ids
+
+    class _P:
+        batches = [_B(i, perm[s:s + 1024]) for i, s in enumerate(range(0, len(perm), 1024))]
+
+        def __len__(self):
+            return len(self.batches)
+    plan = _P()
+    nb = len(plan)
+    port = port_baseline(host, plan, per_hop, args.cpu_seconds, 1, cores)
+    ref = None
+    if not args.no_numba_reference:
+        ref = numba_reference(host, args.shape, train, per_hop, args.cpu_seconds * 1.5, 1, cores)
+    cb = ref or port
     steps = math.ceil(nb / world)
     line = {
         "metric": "papers100M-shape epoch time (s) at 1/2/4/8 B200; sampled edges/s; gather GB/s",
         "impl": "reference", "value": cb["value"], "unit": "s", "n_gpus": world,
         "steps": args.steps or steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * cb["value"] / nb, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int64/f32", "data": "synthetic (device-generated, copied "
-        "to host)", "config": {"workload": WORKLOAD[args.shape] + " — batch preparation only "
+        "vs_baseline": None, "dtype": "int64/f32",
+        "data": "synthetic, generated on the host (oracle.synth_graph_host = the arrays "
+                "synth_graph_device builds; see inputs_digest)",
+        "config": {"workload": WORKLOAD[args.shape] + " — batch preparation only "
                                "(the reference has no training step)",
-                               "fanouts": args.fanouts, "batch": 1024, "batches_per_epoch": nb},
+                   "fanouts": args.fanouts, "batch": 1024, "batches_per_epoch": nb,
+                   "inputs_digest": digest, "host_gen_s": round(gen_s, 1)},
+        "host": info,
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": "s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "sampled_edges_per_s": cb["sampled_edges_per_s"],
-        "gather_GBps_per_core": cb["gather_GBps_per_core"],
+        "reference_numba": ref,
+        "reference_port": port,
+        "product_library_loaded": "libsalient_b200" in Path("/proc/self/maps").read_text(),
     }
     print(json.dumps(line), flush=True)
-    barrier(world)
 
 
 def run_ours(args):
@@ -553,6 +727,19 @@ def run_ours(args):
                          "ms_per_launch": kp["l0_mean_ms_per_launch"],
                          "timing": "CUDA events around each launch on its stream, prep + "
                                    "kernel pass over the epoch's first batches, in this run"},
+            "mfg_roofline": {"kernel": "MFG build chain (sal_sample_mfg: seed insert, count/"
+                                       "scan, sample+insert, flag scan, resolve x 3 hops), "
+                                       "CUDA graph replay of the plan's batches",
+                             "bound": "hbm", "unit": "GB/s", "peak": peak,
+                             "achieved": round(kp["mfg_bytes_per_batch"]
+                                               / (kp["mfg_ms_per_batch_graph"] * 1e-3) / 1e9, 1),
+                             "frac": round(kp["mfg_bytes_per_batch"]
+                                           / (kp["mfg_ms_per_batch_graph"] * 1e-3) / 1e9 / peak,
+                                           4),
+                             "bytes_per_batch": kp["mfg_bytes_per_batch"],
+                             "ms_per_batch": kp["mfg_ms_per_batch_graph"],
+                             "bytes_formula": "SURVEY 8(d): per hop n_dst*(8+16+8) + E*(4+8) "
+                                              "+ E*(8+12+4) + N_new*(8+12)"},
             "gather_roofline": {"kernel": "gather_rows_warp_kernel (fp16 rows, 128-bit)",
                                 "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                                 "unit": "GB/s", "frac": round(ach / peak, 4),
@@ -560,11 +747,9 @@ def run_ours(args):
                                 "bytes_per_launch": kp["gather_bytes_per_launch"],
                                 "ms_per_launch": kp["gather_ms_per_launch"]},
         }
-        if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_baseline(dg, tr, fan, args.cpu_seconds, cfg.global_seed)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
-                                                       "sample")}
-            line["cpu_baseline_detail"] = cb
+        if world == 1 and not (args.no_cpu_baseline and args.no_parity):
+            line.update(cpu_leg(dg, train, fan, args, cfg.global_seed))
+            line["config"]["inputs_digest"] = line.pop("config_inputs_digest")
         print(json.dumps(line), flush=True)
     barrier(world)
 

@@ -367,6 +367,11 @@ int sal_tc_sage_wgrad_simple(const void* dz_dev, int64_t ldz, const void* A_dev,
                              void* stream);
 
 /* ---- on-device synthetic data (graph.py:252-298 laws) ---- */
+/* Pareto degrees of the synth_graph law (graph.py:262-271): degs[v] =
+ * rint(scale * (1-u_v)^(-1/a)) clipped to [0, n-1], u_v counter-based
+ * (Philox on v); a = exponent - 1, scale = avg_degree (a-1)/a */
+int sal_gen_degrees(int64_t n, uint64_t seed, double scale, double a, int64_t* degs_dev,
+                    void* stream);
 /* owner[s] = v for every slot s in [indptr[v], indptr[v+1]) */
 int sal_gen_owner(const int64_t* indptr_dev, int64_t n, int32_t* owner_dev, void* stream);
 /* configuration-model pairing: indices[s] = owner[partner(s)], partner a

@@ -399,3 +399,237 @@ double orc_epoch_prep(const int64_t* indptr, const int32_t* indices, int64_t num
   free(th);
   return t1 - t0;
 }
+
+/* ---- synthetic inputs: host restatement of the device generator --------- *
+ * paper_2110_08450_b200/csrc/generate.cu (the on-device law of the reference's
+ * synth_graph, graph.py:252-298) rebuilt bit for bit on the host: the checker
+ * of the device generator (tests/test_gpu_generate.py) and the way bench.py's
+ * reference arm builds the same inputs without loading the product library.
+ * Every function takes a thread count and splits its index range. */
+typedef struct {
+  void (*fn)(void* ctx, int64_t b, int64_t e);
+  void* ctx;
+  int64_t n;
+  int t, nt;
+} ParJob;
+
+static void* par_worker(void* arg) {
+  ParJob* j = (ParJob*)arg;
+  const int64_t b = j->n * j->t / j->nt, e = j->n * (j->t + 1) / j->nt;
+  if (e > b) j->fn(j->ctx, b, e);
+  return NULL;
+}
+
+static void par_for(int64_t n, int nthreads, void (*fn)(void*, int64_t, int64_t), void* ctx) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  ParJob jobs[256];
+  for (int t = 0; t < nthreads; ++t) {
+    jobs[t].fn = fn;
+    jobs[t].ctx = ctx;
+    jobs[t].n = n;
+    jobs[t].t = t;
+    jobs[t].nt = nthreads;
+    pthread_create(&th[t], NULL, par_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+}
+
+/* common.cuh philox4x32_10 */
+static inline void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+    const uint32_t n1 = (uint32_t)p1;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+    const uint32_t n3 = (uint32_t)p0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+typedef struct { int64_t n; uint64_t seed; double scale, a; int64_t* degs; } DegCtx;
+
+static void deg_range(void* p, int64_t b, int64_t e) {
+  const DegCtx* c = (const DegCtx*)p;
+  const uint32_t k0 = (uint32_t)c->seed ^ 0xDE6u, k1 = (uint32_t)(c->seed >> 32);
+  for (int64_t v = b; v < e; ++v) {
+    uint32_t r[4] = {(uint32_t)v, (uint32_t)((uint64_t)v >> 32), 0u, 5u};
+    philox4x32_10(r, k0, k1);
+    const uint64_t bits53 = (((uint64_t)r[0] << 21) ^ ((uint64_t)r[1] >> 11)) & ((1ull << 53) - 1);
+    const double w = 1.0 - (double)bits53 * 0x1.0p-53;
+    const double y = c->a == 2.0 ? 1.0 / sqrt(w) : pow(w, -1.0 / c->a);
+    double d = rint(c->scale * y);
+    if (d > (double)(c->n - 1)) d = (double)(c->n - 1);
+    if (d < 0.0) d = 0.0;
+    c->degs[v] = (int64_t)d;
+  }
+}
+
+/* generate.cu degrees_kernel */
+void orc_synth_degrees(int64_t n, uint64_t seed, double scale, double a, int64_t* degs,
+                       int nthreads) {
+  DegCtx c = {n, seed, scale, a, degs};
+  par_for(n, nthreads, deg_range, &c);
+}
+
+typedef struct { int half_bits; uint32_t half_mask; uint32_t keys[6]; } Feistel;
+
+static inline uint32_t feistel_f(uint32_t x, uint32_t k) {
+  uint32_t h = x ^ k;
+  h ^= h >> 16;
+  h *= 0x7feb352du;
+  h ^= h >> 15;
+  h *= 0x846ca68bu;
+  h ^= h >> 16;
+  return h;
+}
+
+static inline uint64_t feistel_fwd(const Feistel* F, uint64_t x) {
+  uint32_t L = (uint32_t)(x >> F->half_bits), R = (uint32_t)x & F->half_mask;
+  for (int r = 0; r < 6; ++r) {
+    const uint32_t nl = R;
+    R = (L ^ feistel_f(R, F->keys[r])) & F->half_mask;
+    L = nl;
+  }
+  return ((uint64_t)L << F->half_bits) | R;
+}
+
+static inline uint64_t feistel_inv(const Feistel* F, uint64_t y) {
+  uint32_t L = (uint32_t)(y >> F->half_bits), R = (uint32_t)y & F->half_mask;
+  for (int r = 5; r >= 0; --r) {
+    const uint32_t nr = L;
+    L = (R ^ feistel_f(L, F->keys[r])) & F->half_mask;
+    R = nr;
+  }
+  return ((uint64_t)L << F->half_bits) | R;
+}
+
+typedef struct {
+  const int64_t* indptr;
+  int64_t n;
+  int32_t* owner;
+  Feistel F;
+  int64_t n_stubs;
+  int32_t* indices;
+} PairCtx;
+
+static void owner_range(void* p, int64_t b, int64_t e) {
+  const PairCtx* c = (const PairCtx*)p;
+  for (int64_t v = b; v < e; ++v)
+    for (int64_t s = c->indptr[v]; s < c->indptr[v + 1]; ++s) c->owner[s] = (int32_t)v;
+}
+
+static void pair_range(void* p, int64_t b, int64_t e) {
+  const PairCtx* c = (const PairCtx*)p;
+  const uint64_t n = (uint64_t)c->n_stubs;
+  for (int64_t s = b; s < e; ++s) {
+    uint64_t q = (uint64_t)s;
+    do { q = feistel_inv(&c->F, q); } while (q >= n);
+    uint64_t x = q ^ 1ull;
+    do { x = feistel_fwd(&c->F, x); } while (x >= n);
+    c->indices[s] = c->owner[x];
+  }
+}
+
+/* generate.cu owner_kernel + pairing_kernel + sal_gen_pairing's key schedule:
+ * indices[s] = owner(P(P^-1(s) ^ 1)).  Returns 0, or -1 for an odd stub count. */
+int orc_synth_pairing(const int64_t* indptr, int64_t n, uint64_t seed, int32_t* indices,
+                      int nthreads) {
+  const int64_t n_stubs = indptr[n];
+  if (n_stubs % 2) return -1;
+  PairCtx c;
+  c.indptr = indptr;
+  c.n = n;
+  c.n_stubs = n_stubs;
+  c.indices = indices;
+  c.owner = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n_stubs > 0 ? n_stubs : 1));
+  if (!c.owner) return -2;
+  int bits = 2;
+  while ((1ull << bits) < (uint64_t)n_stubs) ++bits;
+  if (bits & 1) ++bits;
+  c.F.half_bits = bits / 2;
+  c.F.half_mask = (uint32_t)((1ull << c.F.half_bits) - 1);
+  uint64_t k = seed;
+  for (int r = 0; r < 6; ++r) {
+    k = orc_mix64(k + GOLDEN);
+    c.F.keys[r] = (uint32_t)k;
+  }
+  par_for(n, nthreads, owner_range, &c);
+  par_for(n_stubs, nthreads, pair_range, &c);
+  free(c.owner);
+  return 0;
+}
+
+/* IEEE binary32 -> binary16, round to nearest even (what __float2half_rn does) */
+static inline uint16_t f32_to_f16_rne(float f) {
+  uint32_t x;
+  memcpy(&x, &f, 4);
+  const uint32_t sign = (x >> 16) & 0x8000u;
+  const uint32_t ax = x & 0x7FFFFFFFu;
+  if (ax >= 0x7F800000u) return (uint16_t)(sign | (ax > 0x7F800000u ? 0x7E00u : 0x7C00u));
+  if (ax >= 0x477FF000u) return (uint16_t)(sign | 0x7C00u); /* >= 65520: inf */
+  const uint32_t e = ax >> 23, m = (ax & 0x7FFFFFu) | 0x800000u;
+  if (e < 113) { /* below 2^-14: subnormal half, unit 2^-24 */
+    if (e < 102) return (uint16_t)sign;
+    const int shift = 126 - (int)e; /* 14..24 */
+    uint32_t q = m >> shift;
+    const uint32_t rem = m & ((1u << shift) - 1), half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (q & 1u))) ++q;
+    return (uint16_t)(sign | q);
+  }
+  uint32_t h = ((e - 112) << 10) | ((ax & 0x7FFFFFu) >> 13);
+  const uint32_t rem = ax & 0x1FFFu;
+  if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;
+  return (uint16_t)(sign | h);
+}
+
+uint16_t orc_f32_to_f16(float f) { return f32_to_f16_rne(f); }
+
+typedef struct { int64_t row0; int32_t f; int64_t stride; uint64_t seed; uint16_t* out; } FeatCtx;
+
+static void feat_range(void* p, int64_t b, int64_t e) {
+  const FeatCtx* c = (const FeatCtx*)p;
+  const uint32_t k0 = (uint32_t)c->seed, k1 = (uint32_t)(c->seed >> 32) ^ 0xF3A7u;
+  for (int64_t i = b; i < e; ++i) {
+    const int64_t row = c->row0 + i;
+    uint16_t* dst = c->out + i * c->stride;
+    for (int col = 0; col < c->f; col += 4) {
+      uint32_t r[4] = {(uint32_t)row, (uint32_t)((uint64_t)row >> 32), (uint32_t)col, 7u};
+      philox4x32_10(r, k0, k1);
+      for (int j = 0; j < 4 && col + j < c->f; ++j) {
+        const float u = (float)(r[j] >> 8) * (1.0f / 16777216.0f);
+        dst[col + j] = f32_to_f16_rne(-1.0f + 2.0f * u);
+      }
+    }
+  }
+}
+
+/* generate.cu features_kernel for rows [row0, row0 + nrows) into out (row
+ * stride `stride` fp16 elements; padding columns untouched) */
+void orc_synth_features(int64_t row0, int64_t nrows, int32_t f, int64_t stride, uint64_t seed,
+                        uint16_t* out, int nthreads) {
+  FeatCtx c = {row0, f, stride, seed, out};
+  par_for(nrows, nthreads, feat_range, &c);
+}
+
+typedef struct { int32_t C; uint64_t seed; int64_t* out; } LabCtx;
+
+static void lab_range(void* p, int64_t b, int64_t e) {
+  const LabCtx* c = (const LabCtx*)p;
+  const uint32_t k0 = (uint32_t)c->seed ^ 0x1ABE1u, k1 = (uint32_t)(c->seed >> 32);
+  for (int64_t v = b; v < e; ++v) {
+    uint32_t r[4] = {(uint32_t)v, (uint32_t)((uint64_t)v >> 32), 0u, 11u};
+    philox4x32_10(r, k0, k1);
+    c->out[v] = (int64_t)(((uint64_t)r[0] * (uint32_t)c->C) >> 32);
+  }
+}
+
+/* generate.cu labels_kernel */
+void orc_synth_labels(int64_t n, int32_t num_classes, uint64_t seed, int64_t* out, int nthreads) {
+  LabCtx c = {num_classes, seed, out};
+  par_for(n, nthreads, lab_range, &c);
+}

@@ -67,6 +67,20 @@ def lib():
                                      ctypes.c_int64, _i64p, _i64p, _i64p, _i64p, ctypes.c_int64,
                                      _i32p, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, _i64p,
                                      _u64p]
+        L.orc_synth_degrees.restype = None
+        L.orc_synth_degrees.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_double,
+                                        ctypes.c_double, _i64p, ctypes.c_int]
+        L.orc_synth_pairing.restype = ctypes.c_int
+        L.orc_synth_pairing.argtypes = [_i64p, ctypes.c_int64, ctypes.c_uint64, _i32p, ctypes.c_int]
+        L.orc_synth_features.restype = None
+        L.orc_synth_features.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                         ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p,
+                                         ctypes.c_int]
+        L.orc_synth_labels.restype = None
+        L.orc_synth_labels.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, _i64p,
+                                       ctypes.c_int]
+        L.orc_f32_to_f16.restype = ctypes.c_uint16
+        L.orc_f32_to_f16.argtypes = [ctypes.c_float]
         _LIB = L
     return _LIB
 
@@ -240,3 +254,58 @@ def epoch_prep(indptr, indices, num_nodes, features, labels, batches, per_hop, g
         _p(offs, _i64p), _p(ids, _i64p), len(batches), _p(per, _i32p), len(per),
         global_seed & MASK64, nthreads, _p(stats, _i64p), _p(ck, _u64p))
     return wall, stats, ck
+
+
+# --------------------------------------------------------------------------
+# synthetic inputs: host restatement of the device generator
+# (paper_2110_08450_b200/csrc/generate.cu; law of graph.py:252-298)
+# --------------------------------------------------------------------------
+def _odd_fix_node(n: int, seed: int) -> int:
+    """graph.synth_odd_fix_node (counter-based pick of graph.py:273-274)."""
+    return int(mix64(((int(seed) ^ 0x0DD5EED) + GOLDEN) & MASK64) % n)
+
+
+def synth_degrees(n: int, avg_degree: float, exponent: float, seed: int, nthreads: int = 8):
+    a = exponent - 1.0
+    scale = avg_degree * (a - 1.0) / a
+    degs = np.empty(n, dtype=np.int64)
+    lib().orc_synth_degrees(n, int(seed) & MASK64, scale, a, _p(degs, _i64p), nthreads)
+    return degs
+
+
+def synth_graph_host(n: int, avg_degree: float, exponent: float = 3.0, seed: int = 0,
+                     num_features: int = 0, num_classes: int = 0, feature_seed: int = 1,
+                     label_seed: int = 1, nthreads: int = 8, feature_stride: int | None = None):
+    """The arrays graph.synth_graph_device builds, rebuilt on the host: returns
+    dict(indptr int64 [n+1], indices int32 [E], features fp16 [n, stride] or
+    None, labels int64 [n] or None)."""
+    if np.isfinite(exponent):
+        degs = synth_degrees(n, avg_degree, exponent, seed, nthreads)
+    else:
+        degs = np.full(n, int(round(avg_degree)), dtype=np.int64)
+    if int(degs.sum()) % 2:
+        degs[_odd_fix_node(n, seed)] += 1
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(degs, out=indptr[1:])
+    del degs
+    indices = np.empty(max(int(indptr[-1]), 1), dtype=np.int32)[:int(indptr[-1])]
+    rc = lib().orc_synth_pairing(_p(indptr, _i64p), n, int(seed) & MASK64, _p(indices, _i32p),
+                                 nthreads)
+    if rc != 0:
+        raise RuntimeError(f"orc_synth_pairing failed ({rc})")
+    feats = None
+    if num_features:
+        stride = feature_stride or -(-num_features // 8) * 8
+        feats = np.zeros((n, stride), dtype=np.float16)
+        lib().orc_synth_features(0, n, num_features, stride, int(feature_seed) & MASK64,
+                                 feats.ctypes.data, nthreads)
+    labels = None
+    if num_classes:
+        labels = np.empty(n, dtype=np.int64)
+        lib().orc_synth_labels(n, num_classes, int(label_seed) & MASK64, _p(labels, _i64p),
+                               nthreads)
+    return dict(indptr=indptr, indices=indices, features=feats, labels=labels)
+
+
+def f32_to_f16_bits(x: float) -> int:
+    return int(lib().orc_f32_to_f16(x))

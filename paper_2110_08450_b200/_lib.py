@@ -135,6 +135,7 @@ SIGNATURES = {
     "sal_tc_sage_fwd_simple": (ctypes.c_int, [vp, i64, i64, vp, i32, i32, vp, i64, vp,
                                               ctypes.c_float, u64, vp, i32, vp]),
     "sal_tc_sage_wgrad_simple": (ctypes.c_int, [vp, i64, vp, i64, i64, i32, i32, vp, i64, vp]),
+    "sal_gen_degrees": (ctypes.c_int, [i64, u64, ctypes.c_double, ctypes.c_double, vp, vp]),
     "sal_gen_owner": (ctypes.c_int, [vp, i64, vp, vp]),
     "sal_gen_pairing": (ctypes.c_int, [vp, i64, u64, vp, vp]),
     "sal_gen_features_uniform": (ctypes.c_int, [i64, i32, i64, u64, vp, vp]),

@@ -10,6 +10,13 @@
 // and indices[s] = owner(partner(s)) — one gather, no sort.  With slot s of
 // node v stored at row position s - indptr[v], indptr is simply the exclusive
 // scan of the degrees.
+//
+// Every draw is counter-based (Philox4x32-10 on the node / row index, Feistel
+// keys from splitmix64 of the seed) and every float step is exactly rounded
+// (sqrt and division at exponent 3, exact fp16 rounding of 24-bit uniforms),
+// so oracle/oracle.c regenerates the identical graph on the host
+// (orc_synth_*): the reference arm of bench.py builds its inputs without this
+// library, and tests/test_gpu_generate.py checks the two bit for bit.
 #include "common.cuh"
 #include "salient_internal.h"
 
@@ -61,6 +68,27 @@ SAL_DEVINL uint64_t perm_fwd(const Feistel& F, uint64_t x, uint64_t n) {
 SAL_DEVINL uint64_t perm_inv(const Feistel& F, uint64_t y, uint64_t n) {
   do { y = feistel_inv(F, y); } while (y >= n);
   return y;
+}
+
+// Pareto degrees: deg(v) = rint(scale * (1 - u)^(-1/a)) clipped to [0, n-1]
+// with u = 53-bit uniform of Philox((v, v>>32, 0, 5), key(seed)); numpy's
+// 1 + pareto(a) is (1 - u)^(-1/a) (graph.py:270).  a == 2 (exponent 3, every
+// configuration here) uses 1 / sqrt: both correctly rounded, so the host
+// restatement is bit-exact; other exponents go through pow.
+__global__ void degrees_kernel(int64_t n, uint64_t seed, double scale, double a,
+                               int64_t* __restrict__ degs) {
+  const uint2 key = make_uint2((uint32_t)seed ^ 0xDE6u, (uint32_t)(seed >> 32));
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 r = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(v >> 32), 0u, 5u), key);
+    const uint64_t bits53 = (((uint64_t)r.x << 21) ^ ((uint64_t)r.y >> 11)) & ((1ull << 53) - 1);
+    const double w = 1.0 - (double)bits53 * 0x1.0p-53;   // (0, 1], exact
+    const double y = a == 2.0 ? 1.0 / sqrt(w) : pow(w, -1.0 / a);
+    double d = rint(scale * y);
+    if (d > (double)(n - 1)) d = (double)(n - 1);
+    if (d < 0.0) d = 0.0;
+    degs[v] = (int64_t)d;
+  }
 }
 
 __global__ void owner_kernel(const int64_t* __restrict__ indptr, int64_t n,
@@ -126,6 +154,15 @@ static int gen_grid(int64_t n) {
 }  // namespace sal
 
 extern "C" {
+
+int sal_gen_degrees(int64_t n, uint64_t seed, double scale, double a, int64_t* degs,
+                    void* stream) {
+  if (n < 0 || !(a > 1.0) || !(scale >= 0.0)) return SAL_EINVAL;
+  if (n == 0) return SAL_OK;
+  sal::degrees_kernel<<<sal::gen_grid(n), 256, 0, (cudaStream_t)stream>>>(n, seed, scale, a,
+                                                                           degs);
+  return cudaGetLastError() == cudaSuccess ? SAL_OK : SAL_ECUDA;
+}
 
 int sal_gen_owner(const int64_t* indptr, int64_t n, int32_t* owner, void* stream) {
   sal::owner_kernel<<<sal::gen_grid(n), 256, 0, (cudaStream_t)stream>>>(indptr, n, owner);

@@ -306,34 +306,51 @@ def upload_labels(y: LabelVector, device=None) -> torch.Tensor:
 _LAB_CACHE: dict = {}
 
 
+def synth_odd_fix_node(n: int, seed: int) -> int:
+    """The node whose degree absorbs an odd stub total (graph.py:273-274 law):
+    a counter-based pick, so the host restatement (oracle.synth_graph_host) agrees."""
+    z = (int(seed) ^ 0x0DD5EED) & (2**64 - 1)
+    z = (z + 0x9E3779B97F4A7C15) & (2**64 - 1)
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
+    z ^= z >> 31
+    return int(z % n)
+
+
 def synth_graph_device(n: int, avg_degree: float, exponent: float = 3.0, seed: int = 0,
                        num_features: int = 0, num_classes: int = 0, feature_seed: int = 1,
                        label_seed: int = 1, device=None) -> DeviceGraph:
     """Build a synth_graph-law graph (+ fp16 features, labels) directly in HBM.
 
-    Degrees: rint(scale * (1 + Pareto(a))) clipped to [0, n-1] (torch RNG on
-    device, float64); stubs paired by the library's Feistel matching;
-    features uniform [-1, 1) -> fp16; labels uniform.  Peak extra memory is
-    one int32 owner array of E entries.
+    Degrees: rint(scale * (1 - u)^(-1/a)) clipped to [0, n-1] with u a
+    counter-based (Philox) uniform per node (sal_gen_degrees); an odd stub
+    total adds one stub at synth_odd_fix_node; stubs paired by the library's
+    Feistel matching; features uniform [-1, 1) -> fp16; labels uniform.  Every
+    step is counter-based and exactly rounded, so oracle.synth_graph_host
+    rebuilds the same arrays on the host (tests/test_gpu_generate.py).  Peak
+    extra memory is one int32 owner array of E entries.
     """
     _lib.require_cuda()
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if avg_degree < 0:
+        raise ValueError("avg_degree must be >= 0")
     L = _lib.lib()
     dev = torch.device(device or "cuda")
     st = _lib.stream_ptr()
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(int(seed))
     if np.isfinite(exponent):
+        if exponent <= 2.0:
+            raise ValueError("exponent must be > 2 for a finite mean degree")
         a = exponent - 1.0
         scale = avg_degree * (a - 1.0) / a
-        u = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
-        degs = torch.round(scale * (1.0 - u).pow(-1.0 / a)).clamp_(0, n - 1).to(torch.int64)
-        del u
+        degs = torch.empty(n, dtype=torch.int64, device=dev)
+        _lib.check(L.sal_gen_degrees(n, int(seed) & (2**64 - 1), scale, a, degs.data_ptr(), st),
+                   "gen_degrees")
     else:
         degs = torch.full((n,), int(round(avg_degree)), dtype=torch.int64, device=dev)
     total = int(degs.sum().item())
     if total % 2:
-        v = int(torch.randint(0, n, (1,), device=dev, generator=gen).item())
-        degs[v] += 1
+        degs[synth_odd_fix_node(n, seed)] += 1
         total += 1
     indptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     torch.cumsum(degs, 0, out=indptr[1:])
