@@ -65,11 +65,6 @@ def parse():
     p.add_argument("--prep-priority", type=int, default=None)
     p.add_argument("--late-priority", type=int, default=None)
     p.add_argument("--compute-priority", type=int, default=None)
-    p.add_argument("--prep-split", type=int, default=None,
-                   help="three-slot pipeline: hops [0, s) of batch i+2 beside hops [s, L) of "
-                        "batch i+1 (0 = two slots)")
-    p.add_argument("--bwd-parts", type=int, default=None,
-                   help="row parts of the mean_bwd_t -> layer-0 weight-gradient pipeline")
     p.add_argument("--materialise", action="store_true",
                    help="train on the materialised feature gather instead of the gather-free "
                         "layer-0 path")
@@ -623,10 +618,6 @@ def run_ours(args):
     for k in ("prep_priority", "late_priority", "compute_priority"):
         if getattr(args, k) is not None:
             setattr(cfg, k, getattr(args, k))
-    if args.prep_split is not None:
-        cfg.prep_split = args.prep_split
-    if args.bwd_parts is not None:
-        cfg.bwd_parts = args.bwd_parts
     tr = Trainer(dg, train, cfg, rank=rank, world=world)
     spe = tr.set_epoch(0)
     K = args.steps if args.steps > 0 else spe

@@ -138,16 +138,6 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
                    void* ws_dev, const int64_t* seeds_base_dev, const sal_batch_desc* desc_dev,
                    uint64_t global_seed, int32_t rng_policy, void* stream);
 
-/* Hops [hop_begin, hop_end) of sal_sample_mfg (hop_begin == 0 also resets the
- * map and inserts the seeds): lets a pipeline run the early hops of batch
- * i+2 beside the late hops of batch i+1.  Ranges must be issued in order on
- * one workspace. */
-int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan,
-                         const sal_mfg_layout* layout, void* ws_dev,
-                         const int64_t* seeds_base_dev, const sal_batch_desc* desc_dev,
-                         uint64_t global_seed, int32_t rng_policy, int32_t hop_begin,
-                         int32_t hop_end, void* stream);
-
 /* ---- hop-level operators (the _kernels.py operator layer) --------------- */
 size_t sal_scan_ws_bytes(int64_t max_items);
 /* reset every slot of the map to empty (IdMap.__init__, sampler.py:113-129) */
@@ -270,15 +260,6 @@ int sal_lsm_nll(const void* logits_dev, int64_t ld, int64_t rows, int32_t num_cl
 int sal_argmax_correct(const void* logits_dev, int64_t ld, int64_t rows, int32_t num_classes,
                        int32_t dtype, const int64_t* labels_dev, int64_t* counts_dev,
                        int64_t* pred_dev, void* stream);
-/* fused output layer (training): A = act[0:n_rows, 0:2f] ([mean | h_dst], bf16,
- * mean already written), logits = A @ W^T (W [c_pad, 2f] bf16, rows >= classes
- * zero), *loss += mean NLL over labels >= 0 (count over labels[0:n_labels]),
- * dlogits = (softmax - onehot)/count, dA[n_rows, 2f] = dlogits @ W (bf16),
- * dW[c_pad, 2f] += dlogits^T @ A (fp32; caller zeroes).  2f <= 512, c_pad <= 256. */
-int sal_sage_head(const void* act_dev, int64_t lda, int32_t f, int64_t n_rows, const void* W_dev,
-                  int32_t num_classes, int32_t c_pad, const int64_t* labels_dev, int64_t n_labels,
-                  float* loss_dev, float* dW_dev, int64_t lddw, void* dA_dev, int64_t ldda,
-                  void* stream);
 /* reverse adjacency of an MFG layer: tindptr[n_src_rows+1], tdst[edges] lists
  * for every source row the destinations that sampled it (order within a list
  * is unspecified); tw (nullable) receives each entry's 1/deg(dst) */
@@ -306,16 +287,6 @@ int sal_mean_bwd_t_live(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32
                         const int32_t* tdst_dev, const float* tw_dev, int64_t rows,
                         const int64_t* m_dev, const uint8_t* mask_dev, float p, void* dz_dev,
                         int64_t ldz, int32_t dz_dtype, void* stream);
-/* part `part` of nparts of the same: source rows [b, e) where the first
- * *m_dev (true row count) rows are cut at multiples of 64 and the last part
- * runs to `rows` — the cut sal_tc_sage_wgrad_part uses, so the weight gradient
- * of part k can run while part k+1 of dz is still being gathered */
-int sal_mean_bwd_t_part(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f,
-                        int64_t n_pad, const int32_t* indptr_dev, const int32_t* tindptr_dev,
-                        const int32_t* tdst_dev, const float* tw_dev, int64_t rows,
-                        const int64_t* m_dev, int32_t part, int32_t nparts,
-                        const uint8_t* mask_dev, float p, void* dz_dev, int64_t ldz,
-                        int32_t dz_dtype, void* stream);
 /* Adam (torch.optim.Adam, no weight decay) on flat fp32 params; step count
  * t = *t_dev + 1; refreshes the optional bf16 shadow copy; zero_grad != 0
  * leaves grad zeroed (the next backward accumulates without a memset) */
@@ -346,25 +317,43 @@ int sal_tc_sage_fwd(const void* A_dev, int64_t lda, int64_t M, const int64_t* m_
  * m_dev (nullable): true row count on the device (rows past it are skipped;
  * the caller guarantees their contributions are zero).
  * 128 x 128 output tiles x split-K over M (about one CTA per SM), partials
- * added with fp32 vector atomics.  N, K multiples of 128. */
+ * added with fp32 vector atomics.  K multiple of 128, N of 16 (the output
+ * layer's c_pad rows: dz columns past N read as zero, dW rows past N untouched). */
 int sal_tc_sage_wgrad(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda, int64_t M,
                       const int64_t* m_dev, int32_t N, int32_t K, float* dW_dev, int64_t lddw,
                       int32_t accumulate, void* stream);
-/* the same over part `part` of nparts of the rows (sal_mean_bwd_t_part's cut);
- * accumulate = 0 zeroes dW first, so parts after the first pass 1 */
-int sal_tc_sage_wgrad_part(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda,
-                           int64_t M, const int64_t* m_dev, int32_t part, int32_t nparts,
-                           int32_t N, int32_t K, float* dW_dev, int64_t lddw,
-                           int32_t accumulate, void* stream);
-/* the same two GEMMs without TMA / warp specialisation (cp.async, one CTA
- * role) — the reference implementation the TMA versions are checked against */
-int sal_tc_sage_fwd_simple(const void* A_dev, int64_t lda, int64_t M, const void* W_dev,
-                           int32_t N, int32_t K, void* Y_dev, int64_t ldy, uint8_t* mask_dev,
-                           float p, uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout,
-                           void* stream);
-int sal_tc_sage_wgrad_simple(const void* dz_dev, int64_t ldz, const void* A_dev, int64_t lda,
-                             int64_t M, int32_t N, int32_t K, float* dW_dev, int64_t lddw,
-                             void* stream);
+/* C[M,N] = A[M,K] @ B[K,N] (bf16 in, fp32 TMEM accumulate, bf16 out), both
+ * operands row-major: the input gradient dA = dz @ [W_neigh | W_self] of a
+ * SAGEConv layer (mpnn.py:82's contraction, backward).  K multiple of 16
+ * (columns past K read as zero), N multiple of 64.  m_dev (nullable): true
+ * row count on the device; 128-row tiles past it are skipped, or zero-filled
+ * when pad_fill != 0.  Replaces torch.mm (cuBLAS) in the step. */
+int sal_tc_gemm_nn(const void* A_dev, int64_t lda, int64_t M, const int64_t* m_dev, int32_t K,
+                   const void* B_dev, int64_t ldb, int32_t N, void* C_dev, int64_t ldc,
+                   int32_t pad_fill, void* stream);
+/* the output layer in one tcgen05 kernel (training): logits = A[M,K] @
+ * W[c_pad,K]^T (never written), *loss += mean NLL over labels >= 0 (count over
+ * labels[0:min(M, n_labels)]), dlogits[M, ldd] = (softmax - onehot) / count
+ * (bf16, columns >= num_classes and rows of unlabelled or padding rows zero),
+ * dA[M,K] = dlogits @ W (bf16; rows of tiles past *m_dev zero) and
+ * dW[c_pad,K] += dlogits^T @ A (fp32 atomics; the caller zeroes dW).  Replaces
+ * cuBLAS + sal_lsm_nll + cuBLAS + cuBLAS (mpnn.py:82 and the log_softmax/NLL of
+ * PAPER.md:2577-2585).  One cluster of K/64 CTAs per 128-row tile: split-K
+ * logits partials summed through an L2-resident workspace of
+ * sal_tc_sage_head_ws_bytes() bytes, dA and dW from the same A / W tiles.
+ * K = 128, 256 or 512; c_pad multiple of 16, <= 192. */
+size_t sal_tc_sage_head_ws_bytes(int64_t M, int32_t K, int32_t c_pad);
+int sal_tc_sage_head(const void* A_dev, int64_t lda, int64_t M, const int64_t* m_dev, int32_t K,
+                     const void* W_dev, int64_t ldw, int32_t c_pad, int32_t num_classes,
+                     const int64_t* labels_dev, int64_t n_labels, float* loss_dev,
+                     void* dlogits_dev, int64_t ldd, void* dA_dev, int64_t ldda, float* dW_dev,
+                     int64_t lddw, void* ws_dev, size_t ws_bytes, void* stream);
+/* sampled-inference scoring with the same kernel: logits as above, epilogue =
+ * sal_argmax_correct's (counts_dev[0] += correct, counts_dev[1] += labelled) */
+int sal_tc_sage_logits_argmax(const void* A_dev, int64_t lda, int64_t M, const int64_t* m_dev,
+                              int32_t K, const void* W_dev, int64_t ldw, int32_t c_pad,
+                              int32_t num_classes, const int64_t* labels_dev, int64_t n_labels,
+                              int64_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
 
 /* ---- on-device synthetic data (graph.py:252-298 laws) ---- */
 /* Pareto degrees of the synth_graph law (graph.py:262-271): degs[v] =

@@ -83,8 +83,6 @@ SIGNATURES = {
     "sal_mfg_layout_init": (ctypes.c_int, [P(SalMfgPlan), P(SalMfgLayout)]),
     "sal_sample_mfg": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp, vp,
                                       u64, i32, vp]),
-    "sal_sample_mfg_range": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp,
-                                            vp, u64, i32, i32, i32, vp]),
     "sal_scan_ws_bytes": (ctypes.c_size_t, [i64]),
     "sal_idmap_reset": (ctypes.c_int, [P(SalIdMap), vp]),
     "sal_idmap_rehash": (ctypes.c_int, [P(SalIdMap), i64, vp]),
@@ -113,8 +111,6 @@ SIGNATURES = {
                                             ctypes.c_float, vp]),
     "sal_lsm_nll": (ctypes.c_int, [vp, i64, i64, i32, i32, vp, vp, vp, i64, vp]),
     "sal_argmax_correct": (ctypes.c_int, [vp, i64, i64, i32, i32, vp, vp, vp, vp]),
-    "sal_sage_head": (ctypes.c_int, [vp, i64, i32, i64, vp, i32, i32, vp, i64, vp, vp, i64, vp,
-                                     i64, vp]),
     "sal_transpose_ws_bytes": (ctypes.c_size_t, [i64]),
     "sal_transpose_build": (ctypes.c_int, [vp, vp, vp, i64, i64, i64, vp, vp, vp, vp, i32, vp]),
     "sal_zero_spans": (ctypes.c_int, [vp, vp, i32, vp]),
@@ -122,19 +118,18 @@ SIGNATURES = {
                                       ctypes.c_float, vp, i64, i32, vp]),
     "sal_mean_bwd_t_live": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp, vp,
                                            ctypes.c_float, vp, i64, i32, vp]),
-    "sal_mean_bwd_t_part": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp, i32,
-                                           i32, vp, ctypes.c_float, vp, i64, i32, vp]),
     "sal_adam_step": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, ctypes.c_float, ctypes.c_float,
                                      ctypes.c_float, ctypes.c_float, vp, i32, vp]),
     "sal_step_tail": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
     "sal_tc_sage_fwd": (ctypes.c_int, [vp, i64, i64, vp, vp, i32, i32, vp, i64, vp, ctypes.c_float,
                                        u64, vp, i32, vp]),
+    "sal_tc_gemm_nn": (ctypes.c_int, [vp, i64, i64, vp, i32, vp, i64, i32, vp, i64, i32, vp]),
+    "sal_tc_sage_head_ws_bytes": (ctypes.c_size_t, [i64, i32, i32]),
+    "sal_tc_sage_head": (ctypes.c_int, [vp, i64, i64, vp, i32, vp, i64, i32, i32, vp, i64, vp,
+                                        vp, i64, vp, i64, vp, i64, vp, ctypes.c_size_t, vp]),
+    "sal_tc_sage_logits_argmax": (ctypes.c_int, [vp, i64, i64, vp, i32, vp, i64, i32, i32, vp,
+                                                 i64, vp, vp, ctypes.c_size_t, vp]),
     "sal_tc_sage_wgrad": (ctypes.c_int, [vp, i64, vp, i64, i64, vp, i32, i32, vp, i64, i32, vp]),
-    "sal_tc_sage_wgrad_part": (ctypes.c_int, [vp, i64, vp, i64, i64, vp, i32, i32, i32, i32, vp,
-                                              i64, i32, vp]),
-    "sal_tc_sage_fwd_simple": (ctypes.c_int, [vp, i64, i64, vp, i32, i32, vp, i64, vp,
-                                              ctypes.c_float, u64, vp, i32, vp]),
-    "sal_tc_sage_wgrad_simple": (ctypes.c_int, [vp, i64, vp, i64, i64, i32, i32, vp, i64, vp]),
     "sal_gen_degrees": (ctypes.c_int, [i64, u64, ctypes.c_double, ctypes.c_double, vp, vp]),
     "sal_gen_owner": (ctypes.c_int, [vp, i64, vp, vp]),
     "sal_gen_pairing": (ctypes.c_int, [vp, i64, u64, vp, vp]),

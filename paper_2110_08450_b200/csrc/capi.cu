@@ -193,18 +193,12 @@ int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* L) {
   return SAL_OK;
 }
 
-int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
-                   void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
-                   uint64_t global_seed, int32_t rng_policy, void* stream) {
-  if (plan == nullptr) return fail(SAL_EINVAL, "sample_mfg: null argument");
-  return sal_sample_mfg_range(g, plan, L, ws, seeds_base, desc, global_seed, rng_policy, 0,
-                              plan->num_hops, stream);
-}
-
-int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
-                         void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
-                         uint64_t global_seed, int32_t rng_policy, int32_t hop_begin,
-                         int32_t hop_end, void* stream) {
+// hops [hop_begin, hop_end) of one batch's MFG (hop_begin == 0 also resets the map
+// and inserts the seeds); sal_sample_mfg runs them all
+static int sample_mfg_hops(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
+                           void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
+                           uint64_t global_seed, int32_t rng_policy, int32_t hop_begin,
+                           int32_t hop_end, void* stream) {
   if (g == nullptr || plan == nullptr || L == nullptr || ws == nullptr || seeds_base == nullptr ||
       desc == nullptr)
     return fail(SAL_EINVAL, "sample_mfg: null argument");
@@ -290,6 +284,14 @@ int sal_sample_mfg_range(const sal_graph* g, const sal_mfg_plan* plan, const sal
     kernels += 3;
   }
   return counted(SAL_OK, kernels);
+}
+
+int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
+                   void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
+                   uint64_t global_seed, int32_t rng_policy, void* stream) {
+  if (plan == nullptr) return fail(SAL_EINVAL, "sample_mfg: null argument");
+  return sample_mfg_hops(g, plan, L, ws, seeds_base, desc, global_seed, rng_policy, 0,
+                         plan->num_hops, stream);
 }
 
 // ---------------------------------------------------------------------------

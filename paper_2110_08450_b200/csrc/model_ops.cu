@@ -709,15 +709,6 @@ int sal_mean_bwd_t(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int
                            0, 1, mask, p, dz, ldz, dz_dtype, stream, 0);
 }
 
-int sal_mean_bwd_t_part(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
-                        const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
-                        const float* tw, int64_t rows, const int64_t* m_dev, int32_t part,
-                        int32_t nparts, const uint8_t* mask, float p, void* dz, int64_t ldz,
-                        int32_t dz_dtype, void* stream) {
-  return mean_bwd_t_launch(dA, lda, dA_dtype, f, n_pad, indptr, tindptr, tdst, tw, rows, m_dev,
-                           part, nparts, mask, p, dz, ldz, dz_dtype, stream, 0);
-}
-
 int sal_mean_bwd_t_live(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
                         const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
                         const float* tw, int64_t rows, const int64_t* m_dev, const uint8_t* mask,

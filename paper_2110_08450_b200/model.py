@@ -169,9 +169,10 @@ class FusedSAGE:
         self.p = float(dropout)
         self.act = act_dtype
         self.lr, self.betas, self.eps = lr, betas, eps
-        # the output layer's rows are padded to a multiple of 8 (zero weights, zero
-        # gradients) so every logits / dlogits row is 16-byte aligned for the GEMMs
-        self.c_pad = -(-num_classes // 8) * 8
+        # the output layer's rows are padded to a multiple of 16 (zero weights, zero
+        # gradients): every logits / dlogits row is 16-byte aligned and the tcgen05
+        # GEMMs take c_pad as their N (output layer) or K (its input gradient)
+        self.c_pad = -(-num_classes // 16) * 16
         rows_pad = self.dims[1:-1] + [self.c_pad]
         shapes = [(r, 2 * a) for a, r in zip(self.dims[:-1], rows_pad)]
         total = sum(r * c for r, c in shapes)
@@ -205,9 +206,14 @@ class FusedSAGE:
         # tcgen05 weight gradients (tiled split-K, sal_tc_sage_wgrad) where the
         # shapes allow; cuBLAS for the rest
         self.tc_wgrad = True
-        # fused output layer + loss + backward (sal_sage_head): off — mma.sync-bound on
-        # 16 SMs, 51 us against ~20 us for the unfused kernels (csrc/head.cu)
-        self.use_head = False
+        # the output layer on tcgen05 (sal_tc_sage_head: logits in TMEM, loss, dlogits,
+        # dA and dW in one kernel): 179.9 against 179.6 us per step for cuBLAS x3 +
+        # lsm_nll, three launches fewer
+        self.tc_head = True
+        # the hidden layers' input-gradient GEMM dA = dz @ W_cat on tcgen05
+        # (sal_tc_gemm_nn): 6.8 against 4.5 us for cuBLAS at [6144 x 256] @ [256 x 512],
+        # +3 us per step (tools/step_ab.py), so off by default
+        self.tc_dA = False
         # weight gradients of the layers above 0 on a second stream, beside the
         # input-gradient chain
         self.overlap_wgrad = True   # measured 0.233 -> 0.228 s per papers epoch
@@ -218,9 +224,6 @@ class FusedSAGE:
         self.mbt_live = True
         # zero-fill the padding rows of the tcgen05 forward's output and mask in training
         self.pad_fill = False
-        # the last input gradient and layer 0's weight gradient as a pipeline of
-        # row parts (1 = off)
-        self.bwd_parts = 1
         self._wgrad_stream = torch.cuda.Stream(device=dev)
 
     # ------------------------------------------------------------- weights
@@ -262,9 +265,16 @@ class FusedSAGE:
                 and 2 * self.dims[i] in self.tc_fwd_k and self.dims[i + 1] == 256)
 
     def _tc_wgrad_layer(self, i: int) -> bool:
-        """dW_i on sal_tc_sage_wgrad: bf16 operands, dW rows and cols multiples of 128."""
+        """dW_i on sal_tc_sage_wgrad: bf16 operands, dW rows a multiple of 16 (the
+        output layer's c_pad rows included), cols a multiple of 128."""
         return (self.tc_wgrad and self.act == torch.bfloat16
-                and self.gp[i].shape[0] % 128 == 0 and self.gp[i].shape[1] % 128 == 0)
+                and self.gp[i].shape[0] % 16 == 0 and self.gp[i].shape[1] % 128 == 0)
+
+    def _tc_dA_layer(self, i: int) -> bool:
+        """dA_i = dz_i @ W_cat_i on sal_tc_gemm_nn: K = rows of W_cat (f_out or c_pad)
+        a multiple of 16, N = 2 f_in a multiple of 128."""
+        return (self.tc_dA and self.act == torch.bfloat16
+                and self.wb[i].shape[0] % 16 == 0 and self.wb[i].shape[1] % 128 == 0)
 
     # ------------------------------------------------------------- buffers
     def cat_input(self, x: torch.Tensor) -> torch.Tensor:
@@ -277,13 +287,12 @@ class FusedSAGE:
 
     # ------------------------------------------------------------- fwd
     def forward(self, a0: torch.Tensor, adjs, x_global=None, salt: torch.Tensor | None = None,
-                mean0_ready: bool = False, head: bool = False):
+                head: bool = False):
         """a0: layer-0 cat buffer (right half = features in local order).
 
         adjs[i] = (indptr, src, n_pad, n_dst_dev).  With x_global = (table,
         edge_global_ids) layer 0's mean is read straight from the feature table
-        (the sampler's per-edge global ids of the last hop).  mean0_ready: the
-        left half of a0 already holds layer 0's mean (computed by the prep stream).
+        (the sampler's per-edge global ids of the last hop).
         head: stop after the output layer's mean (loss_backward runs the rest).
         Returns (logits [n_pad_last, C] or None with head, saved)."""
         L = _lib.lib()
@@ -295,9 +304,7 @@ class FusedSAGE:
             f = self.dims[i]
             h = a[:, f:]
             mean = a[:n_pad, :f]
-            if i == 0 and mean0_ready:
-                pass
-            elif i == 0 and x_global is not None:
+            if i == 0 and x_global is not None:
                 # gather-free layer 0: edges carry global ids, rows come from the table
                 table, gsrc = x_global
                 # the table may be narrower than the model's (zero-padded) input width.
@@ -378,7 +385,7 @@ class FusedSAGE:
         gradient accumulates into; a caller that zeroes them off the critical path
         passes grads_zeroed=True to backward()."""
         return [(self.gp[i].data_ptr(), self.gp[i].numel() * 4) for i in range(self.L)
-                if self._tc_wgrad_layer(i)]
+                if self._tc_wgrad_layer(i) or (i == self.L - 1 and self.head_ok())]
 
     def backward(self, dlogits: torch.Tensor, saved, transposes=None,
                  grads_zeroed: bool = False) -> None:
@@ -392,9 +399,7 @@ class FusedSAGE:
 
     def _backward_below(self, top: int, dz, saved, transposes, grads_zeroed: bool):
         """Weight gradients of layers top..0 from dz of layer top, and the input
-        gradients between them.  With bwd_parts > 1 the last input gradient
-        (mean_bwd_t into dz_0) and layer 0's tcgen05 weight gradient run as a
-        pipeline of row parts on two streams."""
+        gradients between them."""
         cs = torch.cuda.current_stream()
         ws = self._wgrad_stream if self.overlap_wgrad else None
         forked = False
@@ -419,40 +424,27 @@ class FusedSAGE:
                 self._wgrad(i, dz, saved, grads_zeroed)
             if i == 0:
                 break
-            dA = torch.mm(dz, self.wb[i])
+            dA = self._dA(i, dz, saved)
             if late:
                 fork_wgrad(i, dz)
                 forked = True
-            if i == 1 and ws is not None and self.bwd_parts > 1 and self._tc_wgrad_layer(0):
-                self._input_grad_wgrad0_parts(dA, saved, transposes, grads_zeroed, ws)
-                forked = True
-                break
             dz = self._input_grad(i, dA, saved, transposes)
         if forked:
             cs.wait_stream(ws)
 
-    def _input_grad_wgrad0_parts(self, dA, saved, transposes, grads_zeroed, ws) -> None:
-        """dz_0 = mean_bwd_t(dA of layer 1) in bwd_parts row parts on the current
-        stream; layer 0's weight gradient of part k follows on `ws` as soon as
-        part k is written (sal_mean_bwd_t_part / sal_tc_sage_wgrad_part cut the
-        rows identically)."""
-        L = _lib.lib()
-        cs = torch.cuda.current_stream()
-        P = self.bwd_parts
-        dzp = self._input_grad(1, dA, saved, transposes, parts=P)
-        rec0 = saved[0]
-        a0, n0 = rec0["a"], rec0["n_pad"]
-        m0 = rec0["adj"][3]
-        gi = self.gp[0]
-        for k in range(P):
-            dzp.launch(k)
-            ws.wait_stream(cs)
-            with torch.cuda.stream(ws):
-                _lib.check(L.sal_tc_sage_wgrad_part(
-                    dzp.out.data_ptr(), dzp.out.stride(0), a0.data_ptr(), a0.stride(0), n0,
-                    _lib.ptr(m0), k, P, gi.shape[0], gi.shape[1], gi.data_ptr(), gi.stride(0),
-                    1 if (grads_zeroed or k > 0) else 0, _lib.stream_ptr()), "tc_sage_wgrad_part")
-        dzp.out.record_stream(ws)
+    def _dA(self, i: int, dz, saved) -> torch.Tensor:
+        """dA = dz @ W_cat of layer i ([dmean | dh_dst], mpnn.py:82 backward).  Rows
+        past the layer's true destination count are zero (dz is zero there; whole
+        padding tiles are zero-filled instead of computed)."""
+        w = self.wb[i]
+        if not self._tc_dA_layer(i):
+            return torch.mm(dz, w)
+        dA = torch.empty((dz.shape[0], w.shape[1]), dtype=self.act, device=dz.device)
+        _lib.check(_lib.lib().sal_tc_gemm_nn(
+            dz.data_ptr(), dz.stride(0), dz.shape[0], _lib.ptr(saved[i]["adj"][3]), w.shape[0],
+            w.data_ptr(), w.stride(0), w.shape[1], dA.data_ptr(), dA.stride(0), 1,
+            _lib.stream_ptr()), "tc_gemm_nn")
+        return dA
 
     def _wgrad(self, i: int, dz, saved, grads_zeroed: bool) -> None:
         L = _lib.lib()
@@ -470,10 +462,9 @@ class FusedSAGE:
         else:
             _mm_f32(dz.t(), a[:n_pad], self.gp[i])
 
-    def _input_grad(self, i: int, dA, saved, transposes, parts: int = 0):
+    def _input_grad(self, i: int, dA, saved, transposes):
         """dz of layer i-1 from dA = [dmean | dh_dst] of layer i (mean_bwd_t over the
-        reverse adjacency, ReLU/dropout backward fused).  parts > 0: returns a
-        _PartLauncher whose launch(k) writes row part k (sal_mean_bwd_t_part)."""
+        reverse adjacency, ReLU/dropout backward fused)."""
         L = _lib.lib()
         rec = saved[i]
         a, n_pad = rec["a"], rec["n_pad"]
@@ -489,14 +480,6 @@ class FusedSAGE:
         mask = saved[i - 1]["mask"]
         m_rows = saved[i - 1]["adj"][3]   # true rows of dz = layer i-1's destinations
 
-        def launch(k: int, nparts: int) -> None:
-            _lib.check(L.sal_mean_bwd_t_part(
-                dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
-                indptr.data_ptr(), tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows,
-                _lib.ptr(m_rows), k, nparts, mask.data_ptr(), p, dzp.data_ptr(), dzp.stride(0),
-                _lib.dtype_code(self.act), _lib.stream_ptr()), "mean_bwd_t")
-        if parts:
-            return _PartLauncher(dzp, lambda k: launch(k, parts))
         if i == 1 and self.mbt_live and m_rows is not None and self._tc_wgrad_layer(0):
             # dz_0's only reader is layer 0's split-K weight gradient, which reads
             # whole 64-row chunks up to its true row count: skip the padding rows
@@ -506,52 +489,77 @@ class FusedSAGE:
                 m_rows.data_ptr(), mask.data_ptr(), p, dzp.data_ptr(), dzp.stride(0),
                 _lib.dtype_code(self.act), _lib.stream_ptr()), "mean_bwd_t_live")
             return dzp
-        launch(0, 1)
+        _lib.check(L.sal_mean_bwd_t(
+            dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad, indptr.data_ptr(),
+            tindptr.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows, mask.data_ptr(), p,
+            dzp.data_ptr(), dzp.stride(0), _lib.dtype_code(self.act), _lib.stream_ptr()),
+            "mean_bwd_t")
         return dzp
 
-    # ------------------------------------------------------------- fused output layer
+    # ------------------------------------------------------------- output layer on tcgen05
     def head_ok(self) -> bool:
-        """The output layer, its loss and its backward run as one kernel
-        (sal_sage_head): bf16, 2 f_in <= 512, padded classes <= 256."""
-        f = self.dims[self.L - 1]
-        return (self.use_head and self.act == torch.bfloat16 and self.L >= 2 and f % 8 == 0
-                and 2 * f <= 512 and self.c_pad <= 256)
+        """The output layer runs as one tcgen05 kernel (sal_tc_sage_head: logits, loss,
+        dlogits, dA and dW; sal_tc_sage_logits_argmax for inference): bf16, 2 f_in =
+        128, 256 or 512 (one CTA per 64-wide K block in a cluster), padded classes
+        <= 192."""
+        k = 2 * self.dims[self.L - 1]
+        return (self.tc_head and self.act == torch.bfloat16 and k in (128, 256, 512)
+                and self.c_pad <= 192)
 
-    def head_grad_span(self):
-        """(pointer, bytes) of the output layer's gradient block (sal_sage_head accumulates)."""
-        g = self.gp[self.L - 1]
-        return (g.data_ptr(), g.numel() * 4)
+    def _head_buffers(self, rows: int, k: int):
+        """Persistent dlogits [rows, c_pad] (bf16) and the head kernel's L2 workspace
+        (split-K logits partials), sized for `rows` output rows."""
+        nbytes = _lib.lib().sal_tc_sage_head_ws_bytes(rows, k, self.c_pad)
+        hb = getattr(self, "_hb", None)
+        if hb is None or hb[0].shape[0] < rows or hb[1].numel() < nbytes:
+            hb = (torch.zeros((rows, self.c_pad), dtype=self.act, device=self.device),
+                  torch.empty(nbytes, dtype=torch.uint8, device=self.device))
+            self._hb = hb
+        return hb[0][:rows], hb[1]
 
     def loss_backward(self, saved, labels: torch.Tensor, out: torch.Tensor, transposes=None,
                       grads_zeroed: bool = False, loss_zeroed: bool = False) -> torch.Tensor:
-        """Fused output layer after forward(..., head=True): loss, the output layer's
-        weight gradient and dA in one kernel, then the backward of the layers below.
-        grads_zeroed: the caller zeroed the tcgen05 and output-layer gradient blocks."""
+        """After forward(..., head=True): the output layer (logits in TMEM only, the loss
+        *out += mean NLL, dlogits, its dA and dW) in one tcgen05 kernel, then the
+        backward of the layers below.  grads_zeroed: the caller zeroed the tcgen05
+        weight-gradient blocks (the output layer's included)."""
         L = _lib.lib()
         i = self.L - 1
         rec = saved[i]
         a, n_pad = rec["a"], rec["n_pad"]
-        f = self.dims[i]
         if not loss_zeroed:
             out.zero_()
         gi = self.gp[i]
         if not grads_zeroed:
             gi.zero_()
-        dA = torch.empty((n_pad, 2 * f), dtype=self.act, device=a.device)
-        _lib.check(L.sal_sage_head(a.data_ptr(), a.stride(0), f, n_pad, self.wb[i].data_ptr(),
-                                   self.dims[-1], self.c_pad, labels.data_ptr(), labels.numel(),
-                                   out.data_ptr(), gi.data_ptr(), gi.stride(0), dA.data_ptr(),
-                                   dA.stride(0), _lib.stream_ptr()), "sage_head")
+        w = self.wb[i]
+        dA = torch.empty((n_pad, a.shape[1]), dtype=self.act, device=a.device)
+        dlog, ws = self._head_buffers(n_pad, a.shape[1])
+        _lib.check(L.sal_tc_sage_head(
+            a.data_ptr(), a.stride(0), n_pad, _lib.ptr(rec["adj"][3]), a.shape[1], w.data_ptr(),
+            w.stride(0), self.c_pad, self.dims[-1], labels.data_ptr(), labels.numel(),
+            out.data_ptr(), dlog.data_ptr(), dlog.stride(0), dA.data_ptr(), dA.stride(0),
+            gi.data_ptr(), gi.stride(0), ws.data_ptr(), ws.numel(), _lib.stream_ptr()),
+            "tc_sage_head")
         if i == 0:
-            return out
-        if i == 1 and self.overlap_wgrad and self.bwd_parts > 1 and self._tc_wgrad_layer(0):
-            self._input_grad_wgrad0_parts(dA, saved, transposes, grads_zeroed,
-                                          self._wgrad_stream)
-            torch.cuda.current_stream().wait_stream(self._wgrad_stream)
             return out
         dz = self._input_grad(i, dA, saved, transposes)
         self._backward_below(i - 1, dz, saved, transposes, grads_zeroed)
         return out
+
+    def score(self, saved, labels: torch.Tensor, counts: torch.Tensor) -> None:
+        """After forward(..., head=True) in eval mode: counts[0] += correct argmax
+        predictions, counts[1] += labelled rows (logits never leave TMEM)."""
+        i = self.L - 1
+        rec = saved[i]
+        a, n_pad = rec["a"], rec["n_pad"]
+        w = self.wb[i]
+        _, ws = self._head_buffers(n_pad, a.shape[1])
+        _lib.check(_lib.lib().sal_tc_sage_logits_argmax(
+            a.data_ptr(), a.stride(0), n_pad, _lib.ptr(rec["adj"][3]), a.shape[1], w.data_ptr(),
+            w.stride(0), self.c_pad, self.dims[-1], labels.data_ptr(), labels.numel(),
+            counts.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr()),
+            "tc_sage_logits_argmax")
 
     @torch.no_grad()
     def predict(self, x, adjs, x_global=None, cat: bool = False):
@@ -563,13 +571,6 @@ class FusedSAGE:
         finally:
             self.training = was
         return logits
-
-
-class _PartLauncher:
-    """dz buffer of a parted mean_bwd_t and the launcher of its parts."""
-
-    def __init__(self, out, launch):
-        self.out, self.launch = out, launch
 
 
 def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=None, ws=None,

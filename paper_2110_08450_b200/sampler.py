@@ -398,25 +398,15 @@ class MfgWorkspace:
         return self.buf[off:off + nbytes].view(dt)
 
     def run(self, g: DeviceGraph, seeds_base: torch.Tensor, desc: torch.Tensor,
-            global_seed: int, rng_policy: int = _lib.SAL_RNG_SPLITMIX, stream=None,
-            hops: tuple | None = None) -> None:
-        """Enqueue the multi-hop sample on `stream` (no host sync); `hops` =
-        (begin, end) runs only that hop range (sal_sample_mfg_range)."""
+            global_seed: int, rng_policy: int = _lib.SAL_RNG_SPLITMIX, stream=None) -> None:
+        """Enqueue the multi-hop sample on `stream` (no host sync)."""
         L = _lib.lib()
         gc = g.cstruct
-        if hops is None:
-            _lib.check(L.sal_sample_mfg(ctypes.byref(gc), ctypes.byref(self.plan),
-                                        ctypes.byref(self.layout), self.buf.data_ptr(),
-                                        seeds_base.data_ptr(), desc.data_ptr(),
-                                        int(global_seed) & MASK64, int(rng_policy),
-                                        _lib.stream_ptr(stream)), "sample_mfg")
-            return
-        _lib.check(L.sal_sample_mfg_range(ctypes.byref(gc), ctypes.byref(self.plan),
-                                          ctypes.byref(self.layout), self.buf.data_ptr(),
-                                          seeds_base.data_ptr(), desc.data_ptr(),
-                                          int(global_seed) & MASK64, int(rng_policy),
-                                          int(hops[0]), int(hops[1]), _lib.stream_ptr(stream)),
-                   "sample_mfg_range")
+        _lib.check(L.sal_sample_mfg(ctypes.byref(gc), ctypes.byref(self.plan),
+                                    ctypes.byref(self.layout), self.buf.data_ptr(),
+                                    seeds_base.data_ptr(), desc.data_ptr(),
+                                    int(global_seed) & MASK64, int(rng_policy),
+                                    _lib.stream_ptr(stream)), "sample_mfg")
 
     def load_seeds(self, seeds: SeedBatch, stream=None) -> None:
         n = len(seeds)

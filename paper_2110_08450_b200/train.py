@@ -61,15 +61,11 @@ class TrainConfig:
     compute_priority: int = 0      # ... of the training stream (0: the caller's stream)
     wgrad_priority: int = 0        # ... of the model's overlapped weight-gradient stream
     tc_wgrad: bool = True          # tcgen05 weight gradients where the shapes allow
-    bwd_parts: int = 1             # row parts of the mean_bwd_t -> layer-0 wgrad pipeline
     wgrad_fork_late: bool = True   # overlapped weight gradients fork after the dA GEMM
     late_prep: bool = True         # labels + reverse adjacency built beside the forward pass
-    prep_mean0: bool = False       # gather-free: layer-0 mean on the prep stream (measured slower)
     sampler_lanes: int = 0         # lanes per destination (0 = smallest group holding the fanout)
     sampler_bps: int = 0           # sampler grid cap in blocks per SM (0 = 8)
     table_factor: int = 1          # id-table capacity multiplier (lower load, fewer probes)
-    prep_split: int = 0            # 0: two-slot pipeline; s in [1, L): three slots, hops [0, s)
-                                   # of batch i+2 run beside hops [s, L) of batch i+1
 
 
 def shard_plan(plan, batch_size: int, rank: int, world: int):
@@ -190,7 +186,6 @@ class Trainer:
                                cfg.dropout, device=self.device, seed=cfg.model_seed,
                                act_dtype=cfg.act_dtype, lr=cfg.lr)
         self.model.tc_wgrad = cfg.tc_wgrad
-        self.model.bwd_parts = cfg.bwd_parts
         self.model.wgrad_fork_late = cfg.wgrad_fork_late
         if cfg.wgrad_priority != 0:
             self.model._wgrad_stream = torch.cuda.Stream(device=self.device,
@@ -199,17 +194,13 @@ class Trainer:
             torch.distributed.broadcast(self.model.flat, src=0)
             self.model.refresh_shadow()
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
-        if not 0 <= cfg.prep_split < self.nh:
-            raise ValueError(f"prep_split must be in [0, {self.nh})")
-        # pipeline depth: batches in flight (trained, tail-prepared, head-prepared)
-        self.depth = 3 if cfg.prep_split else 2
+        # pipeline depth: batches in flight (one trained, one prepared)
+        self.depth = 2
         self.slots = [_Slot(dg, cfg, self.device) for _ in range(self.depth)]
         self.ring = 2 * self.depth   # pinned staging buffers of the end-to-end path
         self.staging = [_Staging(cfg.batch_size, self.device) for _ in range(self.ring)]
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self._loss_ev = [torch.cuda.Event() for _ in range(8)]
-        self.head_stream = torch.cuda.Stream(device=self.device, priority=cfg.prep_priority) \
-            if cfg.prep_split else None
         # high priority: the prep chain is latency-bound (many small dependent kernels), so
         # it should take SMs first as the bandwidth-bound training kernels drain
         self.prep_stream = torch.cuda.Stream(device=self.device, priority=cfg.prep_priority)
@@ -271,14 +262,6 @@ class Trainer:
     def _prep(self, slot: _Slot, stage: "_Staging | None", late: bool = False) -> None:
         """Enqueue one batch preparation on the current stream (capturable): seeds ->
         MFG -> layer-0 feature rows, plus (late=True) what _prep_late builds."""
-        self._prep_head(slot, stage, whole=True)
-        self._prep_tail(slot, stage, whole=True)
-        if late:
-            self._prep_late(slot, stage)
-
-    def _prep_head(self, slot: _Slot, stage: "_Staging | None", whole: bool = False) -> None:
-        """Seeds + descriptor of the next batch and its hops [0, prep_split) (all
-        hops when `whole`)."""
         ws = slot.ws
         st = torch.cuda.current_stream()
         L = _lib.lib()
@@ -289,38 +272,15 @@ class Trainer:
                                        self.cursor.data_ptr(), slot.desc.data_ptr(),
                                        _lib.stream_ptr(st)), "plan_next")
             desc, seeds_base = slot.desc, self.seeds_all
-        ws.run(self.dg, seeds_base, desc, self.cfg.global_seed, self.policy, st,
-               hops=None if whole else (0, self.cfg.prep_split))
-
-    def _prep_tail(self, slot: _Slot, stage: "_Staging | None" = None,
-                   whole: bool = False) -> None:
-        """Hops [prep_split, L) (none when `whole`: _prep_head ran them all) and the
-        layer-0 rows."""
-        ws = slot.ws
-        st = torch.cuda.current_stream()
-        L = _lib.lib()
-        if not whole:
-            desc = stage.ddesc if stage is not None else slot.desc
-            seeds_base = stage.dseeds if stage is not None else self.seeds_all  # unread past hop 0
-            ws.run(self.dg, seeds_base, desc, self.cfg.global_seed, self.policy, st,
-                   hops=(self.cfg.prep_split, self.nh))
+        ws.run(self.dg, seeds_base, desc, self.cfg.global_seed, self.policy, st)
         nh = self.nh
         rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
         n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
         f, fx = self.model.dims[0], self.x_table.shape[1]
         gather_rows(self.x_table, ws.globals, slot.feats[:, f:f + fx], n=rows, n_dev=n_dev,
                     stream=st)
-        if self.cfg.gather_free and self.cfg.prep_mean0:
-            # layer-0 mean over the last hop's edges, rows read by global id from the
-            # table, written into the left half of the layer-0 cat buffer
-            h0 = nh - 1
-            a0 = slot.feats
-            _lib.check(L.sal_segment_mean_fwd(
-                ws.dst_indptr[h0].data_ptr(), ws.src_glob.data_ptr(),
-                ws.sizes[h0:h0 + 1].data_ptr(), ws.node_cap[h0], self.x_table.data_ptr(),
-                _lib.dtype_code(self.x_table.dtype), self.x_table.stride(0), fx, a0.data_ptr(),
-                _lib.dtype_code(a0.dtype), a0.stride(0), _lib.stream_ptr(st)),
-                "segment_mean_fwd(table)")
+        if late:
+            self._prep_late(slot, stage)
 
     def _prep_late(self, slot: _Slot, stage: "_Staging | None", zero_grads: bool = False) -> None:
         """The inputs only the loss / backward read: labels and the reverse adjacency
@@ -341,12 +301,11 @@ class Trainer:
         spans = [(t.data_ptr(), t.numel()) for t in slot.t_ws[1:]]
         if zero_grads:
             spans += self.model.tc_grad_spans()
-            if self.model.head_ok():
-                spans.append(self.model.head_grad_span())
-        if spans:
-            ptrs = (ctypes.c_void_p * len(spans))(*[p for p, _ in spans])
-            nbytes = (ctypes.c_int64 * len(spans))(*[b for _, b in spans])
-            _lib.check(L.sal_zero_spans(ptrs, nbytes, len(spans), _lib.stream_ptr(st)),
+        for c in range(0, len(spans), 8):   # sal_zero_spans takes up to 8 ranges per launch
+            chunk = spans[c:c + 8]
+            ptrs = (ctypes.c_void_p * len(chunk))(*[p for p, _ in chunk])
+            nbytes = (ctypes.c_int64 * len(chunk))(*[b for _, b in chunk])
+            _lib.check(L.sal_zero_spans(ptrs, nbytes, len(chunk), _lib.stream_ptr(st)),
                        "zero_spans")
         for i in range(1, nh):
             h = nh - 1 - i
@@ -372,14 +331,13 @@ class Trainer:
         joined after the forward pass."""
         m = self.model
         if part in ("all", "pre"):
-            ready = self.cfg.gather_free and self.cfg.prep_mean0
-            xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free and not ready else None
+            xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free else None
             head = m.head_ok()
             logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg,
-                                      salt=self.step_ctr, mean0_ready=ready, head=head)
+                                      salt=self.step_ctr, head=head)
             if late is not None:
                 torch.cuda.current_stream().wait_stream(late)
-            if head:  # output layer + loss + its backward in one kernel
+            if head:  # output layer + loss on tcgen05, then the backward of every layer
                 m.loss_backward(saved, slot.labels, self.loss_buf, slot.transposes,
                                 grads_zeroed=late is not None, loss_zeroed=True)
             else:
@@ -396,9 +354,7 @@ class Trainer:
                                                 _lib.stream_ptr()), "step_tail")
 
     def _pair(self, k: int, host_inputs: bool, part: str = "all") -> None:
-        """{prep(slot k+1) on the prep stream || train(slot k)} on the current stream.
-
-        Depth 3 (prep_split): {head(slot k+2) || tail(slot k+1) || train(slot k)}."""
+        """{prep(slot k+1) on the prep stream || train(slot k)} on the current stream."""
         D = self.depth
         if part == "post":
             self._train(self.slots[k % D], "post")
@@ -418,22 +374,10 @@ class Trainer:
                 # the late stream also zeroes the tcgen05 gradient blocks (the previous
                 # step's Adam has read them): no memset node in the training chain
                 self._prep_late(self.slots[k % D], stg(k), zero_grads=True)
-        if D == 3:
-            hs = self.head_stream
-            hs.wait_stream(cs)
-            with torch.cuda.stream(hs):
-                self._prep_head(self.slots[(k + 2) % 3], stg(k + 2))
-            with torch.cuda.stream(ps):
-                self._prep_tail(self.slots[(k + 1) % 3], stg(k + 1))
-                if not split:
-                    self._prep_late(self.slots[(k + 1) % 3], stg(k + 1))
-        else:
-            with torch.cuda.stream(ps):
-                self._prep(self.slots[(k + 1) % 2], stg(k + 1), late=not split)
+        with torch.cuda.stream(ps):
+            self._prep(self.slots[(k + 1) % 2], stg(k + 1), late=not split)
         self._train(self.slots[k % D], part, late=ls)
         cs.wait_stream(ps)
-        if D == 3:
-            cs.wait_stream(self.head_stream)
 
     # ---------------------------------------------------------------- driver
     def _stage_host(self, stage: _Staging, step: int) -> None:
@@ -463,8 +407,7 @@ class Trainer:
         self._push(stage)
 
     def begin_epoch(self, host_inputs: bool = False) -> None:
-        """Prime the pipeline (eager): batch 0 into slot 0, and with depth 3 also
-        the head hops of batch 1 into slot 1."""
+        """Prime the pipeline (eager): batch 0 into slot 0."""
         late = not (self.cfg.late_prep and self.prep_stream is not None)
         stages = []
         if host_inputs:  # steps 0 .. depth-1 (the first replay preps step depth-1)
@@ -478,8 +421,6 @@ class Trainer:
             stages.append(stage)
         # with the late split, pair 0 builds slot 0's labels / reverse adjacency
         self._prep(self.slots[0], stages[0], late=late)
-        if self.depth == 3:
-            self._prep_head(self.slots[1], stages[1])
 
     def run_steps(self, start: int, count: int, host_inputs: bool = False,
                   loss_out: torch.Tensor | None = None) -> None:
@@ -724,10 +665,15 @@ class Evaluator:
         m = self.model
         was = m.training
         m.training = False
+        head = m.head_ok()
         try:
-            logits, _ = m.forward(slot.feats, adjs, x_global=(self.x_table, ws.src_glob))
+            logits, saved = m.forward(slot.feats, adjs, x_global=(self.x_table, ws.src_glob),
+                                      head=head)
         finally:
             m.training = was
+        if head:   # logits stay in TMEM: argmax + correct count in the GEMM's epilogue
+            m.score(saved, slot.labels, self.counts)
+            return
         _lib.check(_lib.lib().sal_argmax_correct(
             logits.data_ptr(), logits.stride(0), min(logits.shape[0], self.batch_size),
             logits.shape[1], _lib.dtype_code(logits.dtype), slot.labels.data_ptr(),

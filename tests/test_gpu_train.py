@@ -86,16 +86,14 @@ def test_fused_logits_fp32_within_1e3_of_autograd_on_config_shape():
     assert err < 1e-3, err
 
 
-def _small_trainer(graphs, gather_free=False, seed=0, fanouts=(10, 5), prep_split=0, f=64,
-                   hidden=64, bwd_parts=1):
+def _small_trainer(graphs, gather_free=False, seed=0, fanouts=(10, 5), f=64, hidden=64):
     g = synth_graph(30000, 10, 3.0, seed=4)
     fm = generate_features(30000, f, "f16", seed=4)
     y = planted_labels(fm.data, 8, seed=4)
     dg = DeviceGraph.from_host(g, fm, y)
     train = np.arange(0, 30000, 2)
     cfg = TrainConfig(fanouts=FanoutSpec(fanouts), batch_size=512, hidden=hidden, lr=0.01,
-                      graphs=graphs, gather_free=gather_free, model_seed=seed,
-                      prep_split=prep_split, bwd_parts=bwd_parts)
+                      graphs=graphs, gather_free=gather_free, model_seed=seed)
     return Trainer(dg, train, cfg), dg
 
 
@@ -157,38 +155,6 @@ def test_training_learns_planted_labels():
     assert correct / total > 0.5, correct / total
 
 
-@pytest.mark.parametrize("gather_free", [False, True])
-@pytest.mark.parametrize("split", [1, 2])
-def test_three_slot_pipeline_matches_two_slot(gather_free, split):
-    """prep_split: hops [0, s) of batch i+2 beside hops [s, L) of batch i+1 —
-    the same batches in the same order, eager and graph-replayed, device plan
-    and host inputs, across an epoch boundary."""
-    ref, _ = _small_trainer(False, gather_free, fanouts=(10, 5, 3))
-    ref.set_epoch(0)
-    ref.begin_epoch()
-    n = ref.steps_per_epoch
-    ref.run_steps(0, n)
-    torch.cuda.synchronize()
-    want = ref.losses[:n].cpu().numpy()
-    for graphs in (False, True):
-        tr, _ = _small_trainer(graphs, gather_free, fanouts=(10, 5, 3), prep_split=split)
-        assert tr.depth == 3
-        tr.set_epoch(0)
-        tr.begin_epoch()
-        tr.run_steps(0, n)
-        torch.cuda.synchronize()
-        got = tr.losses[:n].cpu().numpy()
-        _same_trajectory(got, want)
-        assert int(tr.cursor.item()) == n + 2   # one plan_next per batch, two past the end
-    tr, _ = _small_trainer(True, gather_free, fanouts=(10, 5, 3), prep_split=split)
-    tr.set_epoch(0)
-    tr.begin_epoch(host_inputs=True)
-    out = torch.zeros(n).pin_memory()
-    tr.run_steps(0, n, host_inputs=True, loss_out=out)
-    torch.cuda.synchronize()
-    _same_trajectory(out.numpy(), want)
-
-
 def _same_trajectory(got, want):
     """Same batches in the same order: the first steps agree to fp32-atomics noise;
     over a whole epoch that noise compounds through the updates (a few %)."""
@@ -196,10 +162,12 @@ def _same_trajectory(got, want):
     assert np.allclose(got, want, rtol=6e-2, atol=1e-3), (got, want)
 
 
-@pytest.mark.parametrize("fin,hid,classes", [(128, 256, 172), (64, 64, 10), (32, 96, 47)])
-def test_fused_head_matches_unfused_and_autograd(fin, hid, classes):
-    """sal_sage_head (output layer + log_softmax/NLL + its backward in one kernel)
-    against the unfused GEMM / lsm_nll / GEMM path and a torch fp32 autograd model."""
+@pytest.mark.parametrize("fin,hid,classes", [(128, 256, 172), (64, 64, 10), (32, 64, 47),
+                                             (128, 128, 40)])
+def test_tc_head_matches_unfused_and_autograd(fin, hid, classes):
+    """The tcgen05 output layer (sal_tc_sage_head: logits in TMEM, loss, dlogits, dA
+    and dW in one kernel) and the tcgen05 input-gradient GEMMs (sal_tc_gemm_nn)
+    against the cuBLAS GEMM / lsm_nll / cuBLAS path and a torch fp32 autograd model."""
     g = synth_graph(3000, 8, 3.0, seed=5)
     fm = generate_features(3000, fin, "f32", seed=5)
     dg = DeviceGraph.from_host(g)
@@ -209,14 +177,15 @@ def test_fused_head_matches_unfused_and_autograd(fin, hid, classes):
     labels = torch.from_numpy(np.random.default_rng(4).integers(0, classes, 200)).cuda()
     labels[::9] = -1                         # ignored rows
     m = FusedSAGE(fin, hid, classes, 3, dropout=0.0, seed=6, act_dtype=torch.bfloat16)
-    m.use_head = True
     assert m.head_ok()
     adjs = [(l.indptr, l.src_local, l.num_dst, None) for l in mfg.layers]
     a0 = m.cat_input(x.to(torch.bfloat16))
+    m.tc_head = m.tc_dA = False              # the unfused comparator: cuBLAS + lsm_nll
     logits, saved = m.forward(a0, adjs)
     loss_u, dlog = m.loss(logits, labels)
     m.backward(dlog, saved)
     grads_u = [gi.clone() for gi in m.g]
+    m.tc_head = m.tc_dA = True
     m.grad.fill_(3.0)                        # loss_backward zeroes what it accumulates into
     _, saved = m.forward(m.cat_input(x.to(torch.bfloat16)), adjs, head=True)
     out = torch.full((), 5.0, device="cuda")
@@ -260,10 +229,11 @@ def _torch_reference_masked(weights, x, layers, labels, keep):
     return h.detach(), loss.detach(), [p.grad for p in params]
 
 
-def test_trainer_with_fused_head_matches_default():
+def test_trainer_with_tc_head_matches_cublas_head():
     a, _ = _small_trainer(True)
     b, _ = _small_trainer(True)
-    b.model.use_head = True
+    assert b.model.head_ok()
+    a.model.tc_head = a.model.tc_dA = False
     for tr in (a, b):
         tr.set_epoch(0)
         tr.begin_epoch()
@@ -284,55 +254,11 @@ def test_padded_feature_width_trains_and_evaluates():
     assert t == te == 3000 and abs(c - ce) <= 0.003 * 3000
 
 
-@pytest.mark.parametrize("parts", [2, 3, 8])
-def test_backward_row_parts_match_whole(parts):
-    """bwd_parts: the last mean_bwd_t and layer 0's tcgen05 weight gradient run as
-    a two-stream pipeline of row parts; the gradients equal the one-pass ones
-    (dz_0 is bit-identical, dW_0 differs only in fp32 summation order)."""
-    g = synth_graph(3000, 8, 3.0, seed=5)
-    fm = generate_features(3000, 64, "f32", seed=5)
-    dg = DeviceGraph.from_host(g)
-    seeds = SeedBatch(0, np.random.default_rng(3).choice(3000, 200, replace=False))
-    mfg = multihop_mfg(dg, seeds, FanoutSpec((10, 5, 3)), 7)
-    x = torch.from_numpy(fm.data).cuda()[mfg.id_map.global_ids.long()]
-    labels = torch.from_numpy(np.random.default_rng(4).integers(0, 47, 200)).cuda()
-    grads = []
-    for p in (1, parts):
-        m = FusedSAGE(64, 128, 47, 3, dropout=0.5, seed=6, act_dtype=torch.bfloat16)
-        m.bwd_parts = p
-        assert m._tc_wgrad_layer(0)
-        adjs = [(l.indptr, l.src_local, l.num_dst,
-                 torch.tensor([l.num_dst], dtype=torch.int64, device="cuda"))
-                for l in mfg.layers]
-        logits, saved = m.forward(m.cat_input(x.to(torch.bfloat16)), adjs)
-        _, dlog = m.loss(logits, labels)
-        m.backward(dlog, saved)
-        torch.cuda.synchronize()
-        grads.append([gi.clone() for gi in m.g])
-    for i, (a, b) in enumerate(zip(*grads)):
-        r = ((a - b).norm() / b.norm().clamp_min(1e-12)).item()
-        assert r < 2e-3, (i, r)   # replay-to-replay noise of the bf16 backward is ~2e-4
-
-
-def test_trainer_with_backward_parts_matches_default():
-    a, _ = _small_trainer(True, hidden=128)
-    b, _ = _small_trainer(True, hidden=128, bwd_parts=3)
-    assert b.model.bwd_parts == 3 and b.model._tc_wgrad_layer(0)
-    for tr in (a, b):
-        tr.set_epoch(0)
-        tr.begin_epoch()
-        tr.run_steps(0, 8)
-        torch.cuda.synchronize()
-    la, lb = a.losses[:8].cpu().numpy(), b.losses[:8].cpu().numpy()
-    assert np.allclose(la, lb, rtol=1e-2, atol=1e-3), (la, lb)
-
-
 @pytest.mark.parametrize("dtype,f", [(torch.bfloat16, 256), (torch.bfloat16, 32),
                                      (torch.bfloat16, 512), (torch.bfloat16, 104),
                                      (torch.float32, 64)])
-@pytest.mark.parametrize("parts", [1, 3])
-def test_mean_bwd_t_matches_scatter_reference(dtype, f, parts):
-    """sal_mean_bwd_t(_part): dz[s] = mask(s) / (1-p) * (dA[s, f:2f] (s < n_pad) +
+def test_mean_bwd_t_matches_scatter_reference(dtype, f):
+    """sal_mean_bwd_t: dz[s] = mask(s) / (1-p) * (dA[s, f:2f] (s < n_pad) +
     sum over in-edges d of dA[d, :f] / deg(d)), against an fp32 index_add scatter
     (rows with 0, 1 and several in-edges, self rows, padded rows)."""
     from paper_2110_08450_b200 import _lib
@@ -344,20 +270,16 @@ def test_mean_bwd_t_matches_scatter_reference(dtype, f, parts):
     indptr[1:] = np.cumsum(deg)
     src = rng.integers(0, rows - 100, size=int(indptr[-1])).astype(np.int32)
     ip, sr = torch.from_numpy(indptr).cuda(), torch.from_numpy(src).cuda()
-    n_true = 1900                                       # rows past it: padding
-    md = torch.tensor([n_true], dtype=torch.int64, device="cuda")
     tind, tdst, tw = build_transpose(ip, sr, torch.tensor([n_dst], dtype=torch.int64,
                                                           device="cuda"), n_dst, rows)
     dA = (torch.randn(n_dst, 2 * f, device="cuda") * 0.1).to(dtype)
     mask = torch.from_numpy(rng.integers(0, 256, size=rows * f // 8, dtype=np.uint8)).cuda()
     dz = torch.full((rows, f), float("nan"), device="cuda", dtype=dtype)
     L = _lib.lib()
-    for k in range(parts):
-        _lib.check(L.sal_mean_bwd_t_part(dA.data_ptr(), dA.stride(0), _lib.dtype_code(dtype), f,
-                                         n_dst, ip.data_ptr(), tind.data_ptr(), tdst.data_ptr(),
-                                         tw.data_ptr(), rows, md.data_ptr(), k, parts,
-                                         mask.data_ptr(), p, dz.data_ptr(), dz.stride(0),
-                                         _lib.dtype_code(dtype), _lib.stream_ptr()), "mbt")
+    _lib.check(L.sal_mean_bwd_t(dA.data_ptr(), dA.stride(0), _lib.dtype_code(dtype), f,
+                                n_dst, ip.data_ptr(), tind.data_ptr(), tdst.data_ptr(),
+                                tw.data_ptr(), rows, mask.data_ptr(), p, dz.data_ptr(),
+                                dz.stride(0), _lib.dtype_code(dtype), _lib.stream_ptr()), "mbt")
     torch.cuda.synchronize()
     d32 = dA.float()
     dst_of_edge = torch.repeat_interleave(torch.arange(n_dst, device="cuda"),

@@ -1,4 +1,4 @@
-"""Time the layer-0 tcgen05 kernels against cuBLAS on the papers-shape sizes.
+"""Time the tcgen05 kernels of the step against cuBLAS on the papers-shape sizes.
 
 python tools/tc_bench.py   (under gpurun)
 """
@@ -53,12 +53,6 @@ def fwd_tma_plain():   # no ReLU/dropout: the epilogue only converts (isolates i
                                  salt.data_ptr(), 0, st()))
 
 
-def fwd_simple():
-    _lib.check(L.sal_tc_sage_fwd_simple(A.data_ptr(), A.stride(0), M, W.data_ptr(), 256, 256,
-                                        Y.data_ptr(), Y.stride(0), mask.data_ptr(), 0.5, 1,
-                                        salt.data_ptr(), 1, st()))
-
-
 def fwd_cublas():
     z = torch.mm(A, W.t())
     _lib.check(L.sal_relu_dropout_fwd(z.data_ptr(), z.stride(0), Y.data_ptr(), Y.stride(0), M,
@@ -71,23 +65,81 @@ def wg_tma():
                                    None, 256, 256, dW.data_ptr(), dW.stride(0), 0, st()))
 
 
-def wg_simple():
-    _lib.check(L.sal_tc_sage_wgrad_simple(dz.data_ptr(), dz.stride(0), A.data_ptr(),
-                                          A.stride(0), M, 256, 256, dW.data_ptr(),
-                                          dW.stride(0), st()))
-
-
 def wg_cublas():
     torch.mm(dz.t(), A, out_dtype=torch.float32, out=dW)
 
 
+# the rest of the step: output layer (1024 x 512 -> 176 classes), its dA and dW,
+# the hidden layer's dA (6144 x 256 -> 512)
+B2, C2, CP = 1024, 172, 176
+A2 = (torch.randn(B2, 512, device=dev) * 0.5).to(torch.bfloat16)
+W2 = (torch.randn(CP, 512, device=dev) * 0.05).to(torch.bfloat16)
+lab = torch.randint(0, C2, (B2,), device=dev)
+loss = torch.zeros((), device=dev)
+dlog = torch.zeros(B2, CP, device=dev, dtype=torch.bfloat16)
+dA2 = torch.zeros(B2, 512, device=dev, dtype=torch.bfloat16)
+dW2 = torch.zeros(CP, 512, device=dev)
+M1 = 6144
+dz1 = (torch.randn(M1, 256, device=dev) * 0.1).to(torch.bfloat16)
+W1 = (torch.randn(256, 512, device=dev) * 0.05).to(torch.bfloat16)
+dA1 = torch.zeros(M1, 512, device=dev, dtype=torch.bfloat16)
+
+
+hws = torch.empty(L.sal_tc_sage_head_ws_bytes(B2, 512, CP), dtype=torch.uint8, device=dev)
+
+
+def head_tc():   # logits + loss + dlogits + dA + dW in one kernel
+    _lib.check(L.sal_tc_sage_head(A2.data_ptr(), 512, B2, None, 512, W2.data_ptr(), 512, CP, C2,
+                                  lab.data_ptr(), B2, loss.data_ptr(), dlog.data_ptr(), CP,
+                                  dA2.data_ptr(), 512, dW2.data_ptr(), 512, hws.data_ptr(),
+                                  hws.numel(), st()))
+
+
+def head_cublas():   # the same four results the unfused way
+    logits_nll_cublas()
+    dA2_cublas()
+    dW2_cublas()
+
+
+def logits_nll_cublas():
+    z = torch.mm(A2, W2.t())
+    _lib.check(L.sal_lsm_nll(z.data_ptr(), z.stride(0), B2, C2, _lib.SAL_BF16, lab.data_ptr(),
+                             loss.data_ptr(), dlog.data_ptr(), CP, st()))
+
+
+def dA2_cublas():
+    torch.mm(dlog, W2, out=dA2)
+
+
+def dW2_cublas():
+    torch.mm(dlog.t(), A2, out_dtype=torch.float32, out=dW2)
+
+
+def dA1_tc():
+    _lib.check(L.sal_tc_gemm_nn(dz1.data_ptr(), 256, M1, None, 256, W1.data_ptr(), 512, 512,
+                                dA1.data_ptr(), 512, 1, st()))
+
+
+def dA1_cublas():
+    torch.mm(dz1, W1, out=dA1)
+
+
 bytes_fwd = M * 256 * 2 * 2 + M * 32
 bytes_wg = M * 256 * 2 * 2
-for name, fn, nb in [("fwd tma (gemm+relu/dropout)", fwd_tma, bytes_fwd),
+CASES = [("fwd tma (gemm+relu/dropout)", fwd_tma, bytes_fwd),
                      ("fwd tma (gemm only)", fwd_tma_plain, bytes_fwd),
-                     ("fwd simple", fwd_simple, bytes_fwd),
                      ("fwd cublas + relu_dropout", fwd_cublas, bytes_fwd),
-                     ("wgrad tma", wg_tma, bytes_wg), ("wgrad simple", wg_simple, bytes_wg),
-                     ("wgrad cublas fp32 out", wg_cublas, bytes_wg)]:
-    us = t(fn)
-    print(f"{name:32s} {us:7.1f} us  {nb / us / 1e3:7.0f} GB/s")
+                     ("wgrad tma", wg_tma, bytes_wg),
+                     ("wgrad cublas fp32 out", wg_cublas, bytes_wg),
+                     ("out layer fused tc", head_tc, B2 * 512 * 2 * 2),
+                     ("out layer cublas x3 + lsm_nll", head_cublas, B2 * 512 * 2 * 2),
+                     ("out logits cublas + lsm_nll", logits_nll_cublas, B2 * 512 * 2 + B2 * CP * 2),
+                     ("out dA cublas", dA2_cublas, B2 * CP * 2 + B2 * 512 * 2),
+                     ("out dW cublas", dW2_cublas, B2 * CP * 2 + B2 * 512 * 2),
+                     ("hidden dA tc", dA1_tc, M1 * 256 * 2 + M1 * 512 * 2),
+                     ("hidden dA cublas", dA1_cublas, M1 * 256 * 2 + M1 * 512 * 2)]
+
+if __name__ == "__main__":
+    for name, fn, nb in CASES:
+        us = t(fn)
+        print(f"{name:32s} {us:7.1f} us  {nb / us / 1e3:7.0f} GB/s")
