@@ -68,6 +68,12 @@ def parse():
     p.add_argument("--materialise", action="store_true",
                    help="train on the materialised feature gather instead of the gather-free "
                         "layer-0 path")
+    p.add_argument("--no-fuse", action="store_true",
+                   help="sample the last hop into src_glob and run the layer-0 mean and the "
+                        "row gather as separate kernels (the unfused path)")
+    p.add_argument("--fused-on-train", action="store_true",
+                   help="run the fused last hop as the first kernel of the training step "
+                        "instead of on the prep stream")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-parity", action="store_true",
@@ -177,6 +183,32 @@ def ncu_traffic(kernel_prefix: str):
     return None
 
 
+def roofline_entry(kp: dict, peak: float, peak_src: str) -> dict:
+    """The dominant kernel of the step: the fused last hop (sample + layer-0 mean + self
+    rows) when the trainer runs it, else the layer-0 mean over the sampled edges."""
+    timing = ("CUDA events around each launch on its stream, prep + kernel pass over the "
+              "epoch's first batches, in this run")
+    if "fused_GBps" in kp:
+        return {"kernel": "sample_mean_kernel (fused last hop: sample + layer-0 mean + self "
+                          "rows, rows read from the HBM feature table)",
+                "bound": "hbm", "achieved": round(kp["fused_GBps"], 1), "peak": peak,
+                "unit": "GB/s", "frac": round(kp["fused_GBps"] / peak, 4),
+                "peak_source": peak_src, "traffic": ncu_traffic("sample_mean_kernel<0"),
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)",
+                "bytes_per_launch": kp["fused_bytes_per_launch"],
+                "ms_per_launch": kp["fused_ms_per_launch"],
+                "bytes_formula": "E0*(2f + 4) + N0*(4 + 16 + 2f + 4f)", "timing": timing}
+    return {"kernel": "segment_mean_rows_pipe_kernel (layer-0 mean over the sampled edges, "
+                      "rows read from the HBM feature table)",
+            "bound": "hbm", "achieved": round(kp["l0_mean_GBps"], 1), "peak": peak,
+            "unit": "GB/s", "frac": round(kp["l0_mean_GBps"] / peak, 4),
+            "peak_source": peak_src,
+            "traffic": ncu_traffic("segment_mean_rows_pipe_kernel<__half"),
+            "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one layer-0 launch)",
+            "bytes_per_launch": kp["l0_mean_bytes_per_launch"],
+            "ms_per_launch": kp["l0_mean_ms_per_launch"], "timing": timing}
+
+
 def measured_peaks():
     try:
         return json.loads((REPO / "MEASURED_PEAKS.json").read_text())
@@ -259,9 +291,19 @@ def kernel_profile(trainer, nbatches: int):
     h0 = L - 1  # expansion hop feeding layer 0
     mean_buf = torch.empty((ws.node_cap[h0], trainer.x_table.shape[1]), dtype=torch.bfloat16,
                            device=trainer.device)
+    # the fused last hop the training step runs (sal_sample_aggregate: sample + mean +
+    # self rows in one kernel), timed on the same batches after hops 0..L-2
+    fused = bool(getattr(trainer.slots[0], "fused", False))
+    fws = fout = None
+    if fused:
+        fws = MfgWorkspace(trainer.dg.num_nodes, trainer.cfg.fanouts, trainer.cfg.batch_size,
+                           device=trainer.device, last_hop_fused=True)
+        fm = trainer.model.dims[0]
+        fout = torch.zeros((fws.node_cap[h0], 2 * fm), dtype=torch.bfloat16,
+                           device=trainer.device)
     st = torch.cuda.current_stream()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    t_mfg = t_gat = t_mean = 0.0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    t_mfg = t_gat = t_mean = t_fhops = t_fused = 0.0
     edges = nodes = e0 = d0 = 0
     mfg_bytes = 0
     x = trainer.x_table
@@ -284,12 +326,22 @@ def kernel_profile(trainer, nbatches: int):
         gather_rows(x, ws.globals, out_buf, n=ws.node_cap[L], n_dev=ws.sizes[L:L + 1],
                     stream=st)
         ev[3].record(st)
+        if fused:
+            fws.run(trainer.dg, trainer.seeds_all, trainer.desc_all[step], trainer.cfg.global_seed,
+                    trainer.policy, st)
+            ev[4].record(st)
+            fws.aggregate(trainer.dg, x, fout, trainer.model.dims[0], trainer.desc_all[step],
+                          trainer.cfg.global_seed, trainer.policy, st)
+            ev[5].record(st)
         sizes, etot = ws.read_extents()
         if b == 0:
             continue  # warm-up
         t_mfg += ev[0].elapsed_time(ev[1]) / 1e3
         t_mean += ev[1].elapsed_time(ev[2]) / 1e3
         t_gat += ev[2].elapsed_time(ev[3]) / 1e3
+        if fused:
+            t_fhops += ev[3].elapsed_time(ev[4]) / 1e3
+            t_fused += ev[4].elapsed_time(ev[5]) / 1e3
         edges += sum(etot)
         nodes += sizes[-1]
         for h in range(L):  # SURVEY §8(d) MFG-build bytes per hop
@@ -354,6 +406,15 @@ def kernel_profile(trainer, nbatches: int):
     gat_bytes = nodes * f * (elem + elem) + 4 * nodes  # read rows + write rows + ids
     # layer-0 mean: sampled rows read (fp16) + edge ids + row pointers + mean written (bf16)
     mean_bytes = e0 * (f * elem + 4) + d0 * (4 + f * 2)
+    # fused last hop: per edge the sampled row + its index; per destination its global
+    # id, row pointers (16 B), own row, and the [mean | self] bf16 output
+    fused_bytes = e0 * (f * elem + 4) + d0 * (4 + 16 + f * elem + 2 * f * 2)
+    extra = {}
+    if fused:
+        extra = {"fused_GBps": fused_bytes / t_fused / 1e9,
+                 "fused_ms_per_launch": 1e3 * t_fused / k,
+                 "fused_bytes_per_launch": fused_bytes / k,
+                 "fused_hops_ms_per_batch": 1e3 * t_fhops / k}
     return {
         "sampled_edges_per_s": edges / t_mfg,
         "mfg_ms_per_batch": 1e3 * t_mfg / k,
@@ -370,6 +431,7 @@ def kernel_profile(trainer, nbatches: int):
         "sampled_edges_per_s_graph": edges / t_mfg_graph,
         "mfg_ms_per_batch_graph": 1e3 * t_mfg_graph / k,
         "mfg_bytes_per_batch": mfg_bytes / k,
+        **extra,
     }
 
 
@@ -614,7 +676,8 @@ def run_ours(args):
     fan = FanoutSpec(tuple(int(x) for x in args.fanouts.split(",")))
     dg, train, test, gen_s = build_data(args.shape)
     cfg = TrainConfig(fanouts=fan, hidden=args.hidden, gather_free=not args.materialise,
-                      graphs=not args.no_graphs)
+                      graphs=not args.no_graphs, fuse_last_hop=not args.no_fuse,
+                      fused_on_prep=not args.fused_on_train)
     for k in ("prep_priority", "late_priority", "compute_priority"):
         if getattr(args, k) is not None:
             setattr(cfg, k, getattr(args, k))
@@ -706,18 +769,7 @@ def run_ours(args):
                 pe, what="drop-in run_epoch_prep (reference contract: full MFG, f32 features, "
                          "labels), num_workers batches on concurrent streams, first batches of "
                          "the plan extrapolated to the epoch; compare cpu_baseline"),
-            "roofline": {"kernel": "segment_mean_rows_pipe_kernel (layer-0 mean over the "
-                                   "sampled edges, rows read from the HBM feature table)",
-                         "bound": "hbm", "achieved": round(kp["l0_mean_GBps"], 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(kp["l0_mean_GBps"] / peak, 4),
-                         "peak_source": peak_src,
-                         "traffic": ncu_traffic("segment_mean_rows_pipe_kernel<__half"),
-                         "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one "
-                                           "layer-0 launch)",
-                         "bytes_per_launch": kp["l0_mean_bytes_per_launch"],
-                         "ms_per_launch": kp["l0_mean_ms_per_launch"],
-                         "timing": "CUDA events around each launch on its stream, prep + "
-                                   "kernel pass over the epoch's first batches, in this run"},
+            "roofline": roofline_entry(kp, peak, peak_src),
             "mfg_roofline": {"kernel": "MFG build chain (sal_sample_mfg: seed insert, count/"
                                        "scan, sample+insert, flag scan, resolve x 3 hops), "
                                        "CUDA graph replay of the plan's batches",
@@ -760,7 +812,7 @@ def run_infer(args):
                       graphs=not args.no_graphs)
     tr = Trainer(dg, train, cfg, rank=rank, world=world)
     ev = Evaluator(dg, tr.model, fan, cfg.batch_size, cfg.global_seed + 7, rank=rank,
-                   world=world, graphs=not args.no_graphs)
+                   world=world, graphs=not args.no_graphs, fuse_last_hop=not args.no_fuse)
     tr._evaluators = {(tuple(fan.per_hop), cfg.batch_size): ev}  # the e2e call reuses it
     n = ev.set_ids(test)
     W = max(args.warmup, 3)

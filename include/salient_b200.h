@@ -97,6 +97,12 @@ typedef struct {
  * feature table, where the last hop's local ids are never consumed; the id
  * map then only holds hops 0..L-2 (table_cap sized for node_cap[L-1]). */
 #define SAL_MFG_LAST_HOP_EDGES 1
+/* Plan flag: the last hop is not materialised at all.  sal_sample_mfg builds
+ * hops 0..L-2 (the id map holds their nodes, as with SAL_MFG_LAST_HOP_EDGES);
+ * sal_sample_aggregate then samples the last hop and reduces it into the
+ * layer-0 mean in one pass (no src_glob, no dst_indptr for hop L-1).  Also
+ * sets the SAL_MFG_LAST_HOP_EDGES sizing. */
+#define SAL_MFG_LAST_HOP_FUSED 2
 
 /* Byte offsets of the arrays inside one batch workspace. */
 typedef struct {
@@ -137,6 +143,25 @@ int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* layout);
 int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* layout,
                    void* ws_dev, const int64_t* seeds_base_dev, const sal_batch_desc* desc_dev,
                    uint64_t global_seed, int32_t rng_policy, void* stream);
+
+/* Fused last hop (plan flag SAL_MFG_LAST_HOP_FUSED), after sal_sample_mfg on the
+ * same stream: for each destination d < sizes[L-1] of hop L-1, draw its fanout
+ * sample exactly as sal_sample_mfg would (hop_kernel + _sample_positions,
+ * _kernels.py:102-185), read the sampled rows of the feature table by global id
+ * and write
+ *   out[d, 0:cols]                  = mean of the sampled rows (mpnn.py:57-65,
+ *                                     fp32 sum in edge order, then * 1/count)
+ *   out[d, self_offset:+cols]       = table[globals[d], 0:cols]   (self_offset >= 0;
+ *                                     slice_features, prep.py:153-171)
+ * converted to out_dtype.  Rows >= sizes[L-1] are not written.  table: fp16,
+ * cols * 2 a multiple of 16 and <= 256 bytes; out_dtype SAL_BF16 or SAL_F16;
+ * the last hop's fanout <= 32. */
+int sal_sample_aggregate(const sal_graph* g, const sal_mfg_plan* plan,
+                         const sal_mfg_layout* layout, void* ws_dev,
+                         const sal_batch_desc* desc_dev, uint64_t global_seed,
+                         int32_t rng_policy, const void* table_dev, int32_t table_dtype,
+                         int64_t table_stride, int32_t cols, void* out_dev, int32_t out_dtype,
+                         int64_t out_stride, int64_t self_offset, void* stream);
 
 /* ---- hop-level operators (the _kernels.py operator layer) --------------- */
 size_t sal_scan_ws_bytes(int64_t max_items);

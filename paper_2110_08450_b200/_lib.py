@@ -21,6 +21,7 @@ SAL_MAX_HOPS = 8
 SAL_RNG_SPLITMIX = 0
 SAL_RNG_PHILOX = 1
 SAL_MFG_LAST_HOP_EDGES = 1
+SAL_MFG_LAST_HOP_FUSED = 2
 SAL_SEG_NO_PAD_FILL = 1
 SAL_F16 = 1
 SAL_F32 = 2
@@ -81,6 +82,8 @@ SIGNATURES = {
     "sal_mfg_plan_init": (ctypes.c_int, [P(SalMfgPlan), i32, P(i32), i64, i64]),
     "sal_mfg_plan_init_ex": (ctypes.c_int, [P(SalMfgPlan), i32, P(i32), i64, i64, i32]),
     "sal_mfg_layout_init": (ctypes.c_int, [P(SalMfgPlan), P(SalMfgLayout)]),
+    "sal_sample_aggregate": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp,
+                                             u64, i32, vp, i32, i64, i32, vp, i32, i64, i64, vp]),
     "sal_sample_mfg": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp, vp,
                                       u64, i32, vp]),
     "sal_scan_ws_bytes": (ctypes.c_size_t, [i64]),

@@ -20,7 +20,7 @@ LIB_NAME = "libsalient_b200.so"
 LIB_PATH = PKG_DIR / LIB_NAME
 
 SOURCES = ["capi.cu", "hop.cu", "gather.cu", "segment.cu", "generate.cu", "model_ops.cu", "tc_gemm.cu",
-           "io.cu"]
+           "io.cu", "sample_mean.cu"]
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

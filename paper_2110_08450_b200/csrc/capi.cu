@@ -109,7 +109,9 @@ int sal_mfg_plan_init(sal_mfg_plan* plan, int32_t num_hops, const int32_t* per_h
 int sal_mfg_plan_init_ex(sal_mfg_plan* plan, int32_t num_hops, const int32_t* per_hop,
                          int64_t max_seeds, int64_t num_nodes, int32_t flags) {
   if (plan == nullptr || per_hop == nullptr) return fail(SAL_EINVAL, "plan: null argument");
-  if (flags & ~SAL_MFG_LAST_HOP_EDGES) return fail(SAL_EINVAL, "plan: unknown flags 0x%x", flags);
+  if (flags & ~(SAL_MFG_LAST_HOP_EDGES | SAL_MFG_LAST_HOP_FUSED))
+    return fail(SAL_EINVAL, "plan: unknown flags 0x%x", flags);
+  if (flags & SAL_MFG_LAST_HOP_FUSED) flags |= SAL_MFG_LAST_HOP_EDGES;
   if (num_hops < 1 || num_hops > SAL_MAX_HOPS)
     return fail(SAL_EINVAL, "plan: need 1..%d hops, got %d", SAL_MAX_HOPS, num_hops);
   if (max_seeds < 0 || num_nodes < 0) return fail(SAL_EINVAL, "plan: negative size");
@@ -243,6 +245,9 @@ static int sample_mfg_hops(const sal_graph* g, const sal_mfg_plan* plan, const s
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop count");
     kernels = 2;
   }
+  // a fused last hop is sampled by sal_sample_aggregate
+  const int32_t last = (plan->flags & SAL_MFG_LAST_HOP_FUSED) ? plan->num_hops - 1 : plan->num_hops;
+  if (hop_end > last) hop_end = last;
   for (int h = hop_begin; h < hop_end; ++h) {
     int32_t* dst_indptr = (int32_t*)(base + L->dst_indptr[h]);
     int32_t* src_local = (int32_t*)(base + L->src_local[h]);
@@ -268,7 +273,7 @@ static int sample_mfg_hops(const sal_graph* g, const sal_mfg_plan* plan, const s
                                plan->sample_lanes, plan->sample_blocks_per_sm);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop sample");
     sal::NextCount nc;
-    const bool has_next = h + 1 < plan->num_hops;
+    const bool has_next = h + 1 < last;
     if (has_next) {
       nc.g = gd;
       nc.fanout = plan->fanout[h + 1];
@@ -292,6 +297,50 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
   if (plan == nullptr) return fail(SAL_EINVAL, "sample_mfg: null argument");
   return sample_mfg_hops(g, plan, L, ws, seeds_base, desc, global_seed, rng_policy, 0,
                          plan->num_hops, stream);
+}
+
+int sal_sample_aggregate(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
+                         void* ws, const sal_batch_desc* desc, uint64_t global_seed,
+                         int32_t rng_policy, const void* table, int32_t table_dtype,
+                         int64_t table_stride, int32_t cols, void* out, int32_t out_dtype,
+                         int64_t out_stride, int64_t self_offset, void* stream) {
+  if (g == nullptr || plan == nullptr || L == nullptr || ws == nullptr || desc == nullptr ||
+      table == nullptr || out == nullptr)
+    return fail(SAL_EINVAL, "sample_aggregate: null argument");
+  if (!(plan->flags & SAL_MFG_LAST_HOP_FUSED))
+    return fail(SAL_EINVAL, "sample_aggregate: the plan has no fused last hop "
+                            "(SAL_MFG_LAST_HOP_FUSED)");
+  if (rng_policy != SAL_RNG_SPLITMIX && rng_policy != SAL_RNG_PHILOX)
+    return fail(SAL_EINVAL, "sample_aggregate: unknown rng policy %d", rng_policy);
+  if (table_dtype != SAL_F16) return fail(SAL_EINVAL, "sample_aggregate: the table must be fp16");
+  if (out_dtype != SAL_BF16 && out_dtype != SAL_F16)
+    return fail(SAL_EINVAL, "sample_aggregate: out dtype must be bf16 or fp16");
+  if (cols <= 0 || (cols * 2) % 16 != 0 || cols * 2 > 256)
+    return fail(SAL_EINVAL, "sample_aggregate: cols * 2 must be a multiple of 16 in [16, 256], "
+                            "got %d columns", cols);
+  if ((table_stride * 2) % 16 != 0 || (out_stride * 2) % 16 != 0 ||
+      ((uintptr_t)table % 16) != 0 || ((uintptr_t)out % 16) != 0 ||
+      (self_offset >= 0 && (self_offset * 2) % 16 != 0))
+    return fail(SAL_EINVAL, "sample_aggregate: table/out rows must be 16-byte aligned");
+  const int h = plan->num_hops - 1;
+  if (plan->fanout[h] > 32)
+    return fail(SAL_EINVAL, "sample_aggregate: last-hop fanout %d > 32", plan->fanout[h]);
+  char* base = (char*)ws;
+  int64_t* sizes = (int64_t*)(base + L->sizes);
+  sal::HopKey hk;
+  hk.prefix = 0;
+  hk.global_seed = global_seed;
+  hk.hop = (uint32_t)h;
+  hk.batch = 0;
+  hk.derive = 1;
+  return counted(
+      cuda_status(sal::launch_sample_mean(to_dev(g), (const int32_t*)(base + L->globals),
+                                          sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
+                                          rng_policy, table, table_stride, cols, out, out_dtype,
+                                          out_stride, self_offset, sizes + h + 1,
+                                          (cudaStream_t)stream),
+                  "sample_aggregate"),
+      1);
 }
 
 // ---------------------------------------------------------------------------

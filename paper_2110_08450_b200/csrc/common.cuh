@@ -216,4 +216,28 @@ SAL_DEVINL void st_stream_v4(int4* p, int4 v) {
 
 SAL_DEVINL int64_t ld_i64(const int64_t* p) { return __ldg((const long long*)p); }
 
+// Predicated loads into registers the caller already holds ("+" operands): a
+// load guarded by an `if` otherwise lands in a temporary and is copied into the
+// live register right away, and that copy waits for the load — which serialises
+// a software pipeline that means to consume the value an iteration later.
+SAL_DEVINL void ldp_v4_stream(uint4& r, const void* p, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+      : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+      : "l"(p), "r"((int)pred));
+}
+SAL_DEVINL void ldp_s32(int32_t& r, const void* p, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.s32 %0, [%1];\n\t}"
+      : "+r"(r)
+      : "l"(p), "r"((int)pred));
+}
+SAL_DEVINL void ldp_s64(int64_t& r, const void* p, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.s64 %0, [%1];\n\t}"
+      : "+l"(r)
+      : "l"(p), "r"((int)pred));
+}
+
 }  // namespace sal

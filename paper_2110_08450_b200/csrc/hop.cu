@@ -16,6 +16,7 @@
 // packed slot word {key:32 | NEWF | first_edge:31}.
 #include "common.cuh"
 #include "salient_internal.h"
+#include "sampling.cuh"
 
 namespace sal {
 
@@ -155,31 +156,6 @@ SAL_DEVINL void emit_edge(const int32_t* __restrict__ indices, int64_t slot_pos,
     slot[e] = (int32_t)table_insert_min(table, log2cap, key, (uint32_t)e);
 }
 
-// Exact z % d for d in [1, 2^32) without the u64 division routine: with the
-// per-destination reciprocal m = floor((2^64-1)/d), q = umulhi(z, m) is at most
-// 2 below floor(z/d), so r = z - q*d needs at most two corrections.
-SAL_DEVINL uint32_t mod_by_recip(uint64_t z, uint32_t d, uint64_t m) {
-  const uint64_t q = __umul64hi(z, m);
-  uint64_t r = z - q * (uint64_t)d;
-  if (r >= d) r -= d;
-  if (r >= d) r -= d;
-  return (uint32_t)r;
-}
-
-// Draw -> position for the two RNG policies.  recip = floor((2^64-1)/deg).
-template <int kPolicy>
-SAL_DEVINL uint32_t draw_position(uint64_t key, uint2 pkey, uint32_t ctr, uint32_t dst,
-                                  uint32_t hop, uint32_t batch, uint32_t deg, uint64_t recip) {
-  if (kPolicy == kRngSplitmix) {
-    // _kernels.py:37-39 + 120: mix64(key + (c+1)G) % deg  (u64 modulo)
-    const uint64_t z = mix64(key + (uint64_t)(ctr + 1) * kGolden);
-    return mod_by_recip(z, deg, recip);
-  } else {
-    const uint4 r = philox4x32_10(make_uint4(ctr, dst, hop, batch), pkey);
-    return (uint32_t)(((uint64_t)r.x * deg) >> 32);
-  }
-}
-
 // G lanes per destination (G = 32, 16 or 8; 32/G destinations per warp in
 // flight).  Rejection sampling runs G draws per round: lane l of the group
 // takes draw ctr + l; a draw is fresh if its position is not yet accepted and
@@ -231,7 +207,7 @@ sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restri
     }
     const uint64_t key = mix64(prefix ^ (uint64_t)i);  // _kernels.py:167
     const uint32_t udeg = (uint32_t)deg;
-    const uint64_t recip = kPolicy == kRngSplitmix ? ~0ull / (uint64_t)udeg : 0ull;
+    const uint64_t recip = kPolicy == kRngSplitmix ? recip_u32(udeg) : 0ull;
     // accepted positions: this group's slice of shared memory when the fanout
     // fits, else staged in this destination's own output range
     int32_t* accepted = fanout <= G ? &sh_acc[threadIdx.x >> 5][grp * G] : src_glob + out;

@@ -287,13 +287,15 @@ class FusedSAGE:
 
     # ------------------------------------------------------------- fwd
     def forward(self, a0: torch.Tensor, adjs, x_global=None, salt: torch.Tensor | None = None,
-                head: bool = False):
+                head: bool = False, mean0_ready: bool = False):
         """a0: layer-0 cat buffer (right half = features in local order).
 
         adjs[i] = (indptr, src, n_pad, n_dst_dev).  With x_global = (table,
         edge_global_ids) layer 0's mean is read straight from the feature table
         (the sampler's per-edge global ids of the last hop).
         head: stop after the output layer's mean (loss_backward runs the rest).
+        mean0_ready: a0's left half already holds layer 0's mean (the fused last hop,
+        sal_sample_aggregate).
         Returns (logits [n_pad_last, C] or None with head, saved)."""
         L = _lib.lib()
         st = _lib.stream_ptr()
@@ -304,7 +306,9 @@ class FusedSAGE:
             f = self.dims[i]
             h = a[:, f:]
             mean = a[:n_pad, :f]
-            if i == 0 and x_global is not None:
+            if i == 0 and mean0_ready:
+                pass
+            elif i == 0 and x_global is not None:
                 # gather-free layer 0: edges carry global ids, rows come from the table
                 table, gsrc = x_global
                 # the table may be narrower than the model's (zero-padded) input width.

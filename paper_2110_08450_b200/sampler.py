@@ -350,20 +350,24 @@ class MfgWorkspace:
 
     def __init__(self, num_nodes: int, fanouts: FanoutSpec, max_seeds: int, device=None,
                  last_hop_edges: bool = False, sample_lanes: int = 0, sample_bps: int = 0,
-                 table_factor: int = 1):
+                 table_factor: int = 1, last_hop_fused: bool = False):
         """last_hop_edges: SAL_MFG_LAST_HOP_EDGES — the last hop only emits global
         source ids (src_glob); its relabel is skipped (training with the
-        layer-0 mean read straight from the feature table)."""
+        layer-0 mean read straight from the feature table).
+        last_hop_fused: SAL_MFG_LAST_HOP_FUSED — run() builds hops 0..L-2 only and
+        aggregate() samples the last hop straight into the layer-0 mean."""
         _lib.require_cuda()
         L = _lib.lib()
         self.device = torch.device(device or "cuda")
         self.fanouts = fanouts
         self.num_hops = len(fanouts)
         self.max_seeds = int(max_seeds)
-        self.last_hop_edges = bool(last_hop_edges)
+        self.last_hop_fused = bool(last_hop_fused)
+        self.last_hop_edges = bool(last_hop_edges) or self.last_hop_fused
         self.plan = _lib.SalMfgPlan()
         per = (ctypes.c_int32 * self.num_hops)(*fanouts.per_hop)
-        flags = _lib.SAL_MFG_LAST_HOP_EDGES if last_hop_edges else 0
+        flags = ((_lib.SAL_MFG_LAST_HOP_EDGES if self.last_hop_edges else 0)
+                 | (_lib.SAL_MFG_LAST_HOP_FUSED if self.last_hop_fused else 0))
         _lib.check(L.sal_mfg_plan_init_ex(ctypes.byref(self.plan), self.num_hops, per,
                                           self.max_seeds, int(num_nodes), flags),
                    "mfg_plan_init")
@@ -407,6 +411,23 @@ class MfgWorkspace:
                                     seeds_base.data_ptr(), desc.data_ptr(),
                                     int(global_seed) & MASK64, int(rng_policy),
                                     _lib.stream_ptr(stream)), "sample_mfg")
+
+    def aggregate(self, g: DeviceGraph, table: torch.Tensor, out: torch.Tensor,
+                  self_offset: int, desc: torch.Tensor, global_seed: int,
+                  rng_policy: int = _lib.SAL_RNG_SPLITMIX, stream=None) -> None:
+        """Fused last hop (after run(), same stream): out[d, :cols] = mean of the
+        sampled table rows of layer-0 destination d, out[d, self_offset:+cols] =
+        its own row (self_offset < 0: not written); cols = table.shape[1]."""
+        if not self.last_hop_fused:
+            raise ValueError("aggregate: workspace built without last_hop_fused")
+        L = _lib.lib()
+        gc = g.cstruct
+        _lib.check(L.sal_sample_aggregate(
+            ctypes.byref(gc), ctypes.byref(self.plan), ctypes.byref(self.layout),
+            self.buf.data_ptr(), desc.data_ptr(), int(global_seed) & MASK64, int(rng_policy),
+            table.data_ptr(), _lib.dtype_code(table.dtype), table.stride(0), table.shape[1],
+            out.data_ptr(), _lib.dtype_code(out.dtype), out.stride(0), int(self_offset),
+            _lib.stream_ptr(stream)), "sample_aggregate")
 
     def load_seeds(self, seeds: SeedBatch, stream=None) -> None:
         n = len(seeds)

@@ -66,6 +66,10 @@ class TrainConfig:
     sampler_lanes: int = 0         # lanes per destination (0 = smallest group holding the fanout)
     sampler_bps: int = 0           # sampler grid cap in blocks per SM (0 = 8)
     table_factor: int = 1          # id-table capacity multiplier (lower load, fewer probes)
+    # gather_free: the last hop sampled straight into the layer-0 mean + self rows by one
+    # kernel (sal_sample_aggregate) instead of sample -> src_glob -> mean + row gather
+    fuse_last_hop: bool = True
+    fused_on_prep: bool = True     # ... on the prep stream (False: first kernel of the step)
 
 
 def shard_plan(plan, batch_size: int, rank: int, world: int):
@@ -116,6 +120,16 @@ def _model_width(dg: DeviceGraph) -> int:
     return fp
 
 
+def _fusable(dg: DeviceGraph, cfg: TrainConfig) -> bool:
+    """sal_sample_aggregate's shape limits: fp16 table rows of 16-byte multiples up to
+    256 bytes, last-hop fanout <= 32, 16-bit activations."""
+    x = dg.features
+    return (cfg.gather_free and cfg.fuse_last_hop and x.dtype == torch.float16
+            and (x.shape[1] * 2) % 16 == 0 and x.shape[1] * 2 <= 256
+            and (x.stride(0) * 2) % 16 == 0 and cfg.fanouts.per_hop[0] <= 32
+            and cfg.act_dtype in (torch.bfloat16, torch.float16))
+
+
 def _model_table(dg: DeviceGraph) -> torch.Tensor:
     f, fp = dg.num_features, dg.features.shape[1]
     if fp != f:
@@ -126,9 +140,11 @@ def _model_table(dg: DeviceGraph) -> torch.Tensor:
 class _Slot:
     def __init__(self, dg: DeviceGraph, cfg: TrainConfig, device, backward: bool = True):
         # gather-free: layer 0 reads rows by global id, so the last hop needs no relabel
+        self.fused = _fusable(dg, cfg)
         self.ws = MfgWorkspace(dg.num_nodes, cfg.fanouts, cfg.batch_size, device=device,
                                last_hop_edges=cfg.gather_free, sample_lanes=cfg.sampler_lanes,
-                               sample_bps=cfg.sampler_bps, table_factor=cfg.table_factor)
+                               sample_bps=cfg.sampler_bps, table_factor=cfg.table_factor,
+                               last_hop_fused=self.fused)
         ws = self.ws
         nh = ws.num_hops
         rows = ws.node_cap[-1] if not cfg.gather_free else ws.node_cap[-2]
@@ -138,6 +154,7 @@ class _Slot:
         self.labels = torch.full((cfg.batch_size,), -1, dtype=torch.int64, device=device)
         self.desc = torch.zeros(3, dtype=torch.int64, device=device)
         self.seeds = torch.zeros(max(cfg.batch_size, 1), dtype=torch.int64, device=device)
+        self.desc_used = self.desc   # the descriptor the last prep read (fused last hop)
         # reverse adjacency of layers i >= 1 (hop h = L-1-i), built on the prep stream
         L = _lib.lib()
         self.transposes = [None]
@@ -273,12 +290,18 @@ class Trainer:
                                        _lib.stream_ptr(st)), "plan_next")
             desc, seeds_base = slot.desc, self.seeds_all
         ws.run(self.dg, seeds_base, desc, self.cfg.global_seed, self.policy, st)
+        slot.desc_used = desc
         nh = self.nh
-        rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
-        n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
         f, fx = self.model.dims[0], self.x_table.shape[1]
-        gather_rows(self.x_table, ws.globals, slot.feats[:, f:f + fx], n=rows, n_dev=n_dev,
-                    stream=st)
+        if slot.fused:
+            if self.cfg.fused_on_prep:  # last hop -> layer-0 [mean | self] in one pass
+                ws.aggregate(self.dg, self.x_table, slot.feats, f, desc, self.cfg.global_seed,
+                             self.policy, st)
+        else:
+            rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
+            n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
+            gather_rows(self.x_table, ws.globals, slot.feats[:, f:f + fx], n=rows, n_dev=n_dev,
+                        stream=st)
         if late:
             self._prep_late(slot, stage)
 
@@ -332,9 +355,15 @@ class Trainer:
         m = self.model
         if part in ("all", "pre"):
             xg = (self.x_table, slot.ws.src_glob) if self.cfg.gather_free else None
+            if slot.fused:
+                xg = None
+                if not self.cfg.fused_on_prep:
+                    slot.ws.aggregate(self.dg, self.x_table, slot.feats, m.dims[0],
+                                      slot.desc_used, self.cfg.global_seed, self.policy,
+                                      torch.cuda.current_stream())
             head = m.head_ok()
             logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg,
-                                      salt=self.step_ctr, head=head)
+                                      salt=self.step_ctr, head=head, mean0_ready=slot.fused)
             if late is not None:
                 torch.cuda.current_stream().wait_stream(late)
             if head:  # output layer + loss on tcgen05, then the backward of every layer
@@ -547,7 +576,8 @@ class Trainer:
             self._evaluators = getattr(self, "_evaluators", {})
             ev = Evaluator(self.dg, self.model, fan, bs, self.cfg.global_seed + 7,
                            rank=self.rank, world=self.world, rng_policy=self.cfg.rng_policy,
-                           graphs=self.cfg.graphs, act_dtype=self.cfg.act_dtype)
+                           graphs=self.cfg.graphs, act_dtype=self.cfg.act_dtype,
+                           fuse_last_hop=self.cfg.fuse_last_hop)
             self._evaluators[key] = ev
         return ev.run(ids)
 
@@ -592,7 +622,7 @@ class Evaluator:
     def __init__(self, dg: DeviceGraph, model: FusedSAGE, fanouts: FanoutSpec, batch_size: int,
                  global_seed: int, rank: int = 0, world: int = 1, rng_policy: str = "splitmix",
                  graphs: bool = True, act_dtype: torch.dtype = torch.bfloat16,
-                 prep_priority: int = -1):
+                 prep_priority: int = -1, fuse_last_hop: bool = True):
         _lib.require_cuda()
         self.dg, self.model = dg, model
         self.fanouts, self.batch_size, self.global_seed = fanouts, int(batch_size), int(global_seed)
@@ -602,7 +632,7 @@ class Evaluator:
         self.policy = RNG_POLICIES[rng_policy]
         self.use_graphs = graphs
         cfg = TrainConfig(fanouts=fanouts, batch_size=self.batch_size, gather_free=True,
-                          act_dtype=act_dtype)
+                          act_dtype=act_dtype, fuse_last_hop=fuse_last_hop)
         self.slots = [_Slot(dg, cfg, self.device, backward=False) for _ in range(2)]
         # high priority here (measured 0.0728 vs 0.0736 s per pass at equal priority);
         # training measured the other way (TrainConfig.prep_priority = 0)
@@ -649,8 +679,12 @@ class Evaluator:
         ws.run(self.dg, self.seeds_all, slot.desc, self.global_seed, self.policy, st)
         nh = self.nh
         f, fx = self.model.dims[0], self.x_table.shape[1]
-        gather_rows(self.x_table, ws.globals, slot.feats[:, f:f + fx], n=ws.node_cap[nh - 1],
-                    n_dev=ws.sizes[nh - 1:nh], stream=st)
+        if slot.fused:
+            ws.aggregate(self.dg, self.x_table, slot.feats, f, slot.desc, self.global_seed,
+                         self.policy, st)
+        else:
+            gather_rows(self.x_table, ws.globals, slot.feats[:, f:f + fx],
+                        n=ws.node_cap[nh - 1], n_dev=ws.sizes[nh - 1:nh], stream=st)
         _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), self.seeds_all.data_ptr(),
                                        slot.desc.data_ptr(), self.batch_size,
                                        slot.labels.data_ptr(), _lib.stream_ptr(st)),
@@ -667,8 +701,9 @@ class Evaluator:
         m.training = False
         head = m.head_ok()
         try:
-            logits, saved = m.forward(slot.feats, adjs, x_global=(self.x_table, ws.src_glob),
-                                      head=head)
+            xg = None if slot.fused else (self.x_table, ws.src_glob)
+            logits, saved = m.forward(slot.feats, adjs, x_global=xg, head=head,
+                                      mean0_ready=slot.fused)
         finally:
             m.training = was
         if head:   # logits stay in TMEM: argmax + correct count in the GEMM's epilogue
