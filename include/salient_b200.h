@@ -312,6 +312,17 @@ int sal_mean_bwd_t_live(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32
                         const int32_t* tdst_dev, const float* tw_dev, int64_t rows,
                         const int64_t* m_dev, const uint8_t* mask_dev, float p, void* dz_dev,
                         int64_t ldz, int32_t dz_dtype, void* stream);
+/* the same input gradient (bit-identical to sal_mean_bwd_t) in two disjoint passes of
+ * one launch: destination-major over the forward adjacency (indptr/src, n_dst_dev
+ * destinations) for the rows with exactly one in-edge and no self term
+ * (s >= n_pad), reading each dA[d] once for all its sources; source-major over
+ * the reverse adjacency for the rest.  m_dev != NULL: live rows only, as
+ * sal_mean_bwd_t_live. */
+int sal_mean_bwd(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
+                 const int64_t* n_dst_dev, const int32_t* indptr_dev, const int32_t* src_dev,
+                 const int32_t* tindptr_dev, const int32_t* tdst_dev, const float* tw_dev,
+                 int64_t rows, const int64_t* m_dev, const uint8_t* mask_dev, float p,
+                 void* dz_dev, int64_t ldz, int32_t dz_dtype, void* stream);
 /* Adam (torch.optim.Adam, no weight decay) on flat fp32 params; step count
  * t = *t_dev + 1; refreshes the optional bf16 shadow copy; zero_grad != 0
  * leaves grad zeroed (the next backward accumulates without a memset) */

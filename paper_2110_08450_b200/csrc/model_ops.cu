@@ -461,6 +461,175 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
 }
 
 // ---------------------------------------------------------------------------
+// The same input gradient in two disjoint passes (sal_mean_bwd):
+//   * destination-major, warp per destination d: the source rows s of d with one
+//     in-edge and no self term (s >= n_pad) — most rows of a sampled MFG — get
+//     dz[s] = mask(s) * scale * (0 + dA[d, 0:f] * (1/deg d)): dA[d] is read once
+//     for its ~fanout sources, and no reverse-adjacency chain is walked;
+//   * source-major, warp per 32 source rows: every other row (self term, several
+//     or no in-edges) as mean_bwd_t_kernel does it.
+// Same arithmetic as mean_bwd_t_kernel row for row, so the output is bit-identical.
+template <typename TG, typename TO>
+__global__ void __launch_bounds__(256, 3)
+mean_bwd_split_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_pad,
+                      const int64_t* __restrict__ n_dst_dev, const int32_t* __restrict__ indptr,
+                      const int32_t* __restrict__ src, const int32_t* __restrict__ tindptr,
+                      const int32_t* __restrict__ tdst, const float* __restrict__ tw,
+                      int64_t rows, const int64_t* __restrict__ m_dev, int live,
+                      const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz,
+                      int64_t ldz, int dst_blocks) {
+  const int lane = threadIdx.x & 31;
+  const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
+  int nrows = (int)rows;
+  if (live && m_dev) {
+    const int64_t cap = (*m_dev + 63) / 64 * 64;
+    if (cap < nrows) nrows = (int)cap;
+  }
+  const int npad = (int)n_pad;
+  if ((int)blockIdx.x < dst_blocks) {
+    // ---- destination-major: single-in-edge rows without a self term
+    const int n_dst = (int)(n_dst_dev ? *n_dst_dev : n_pad);
+    const int nw = dst_blocks * (int)(blockDim.x >> 5);
+    for (int d = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); d < n_dst; d += nw) {
+      const int beg = __ldg(indptr + d), end = __ldg(indptr + d + 1);
+      const float w = 1.f / (float)(end - beg);
+      for (int e0 = beg; e0 < end; e0 += 32) {
+        const int e = e0 + lane;
+        int sj = -1;
+        bool simple = false;
+        if (e < end) {
+          sj = __ldg(src + e);
+          simple = sj >= npad && sj < nrows && __ldg(tindptr + sj + 1) - __ldg(tindptr + sj) == 1;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, simple);
+        if (!m) continue;
+        for (int c0 = 0; c0 < f; c0 += 256) {
+          const int c = c0 + lane * 8;
+          const bool active = c < f;
+          float v[8];
+          if (active) {
+            ld8<TG>(dA + (int64_t)d * lda + c, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = 0.f + v[j] * w;
+          }
+          // the mask bytes of up to 8 sources in flight, then their rows written
+          unsigned mm = m;
+          while (mm) {
+            int sk[8];
+            uint8_t bk[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int j = mm ? __ffs(mm) - 1 : -1;
+              if (mm) mm &= mm - 1;
+              sk[k] = __shfl_sync(0xffffffffu, sj, j < 0 ? 0 : j);
+              if (j < 0) sk[k] = -1;
+              bk[k] = (active && sk[k] >= 0) ? mask[((int64_t)sk[k] * f + c) >> 3] : (uint8_t)0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              if (active && sk[k] >= 0) {
+                float acc[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[q] = ((bk[k] >> q) & 1) ? v[q] * scale : 0.f;
+                st8<TO>(dz + (int64_t)sk[k] * ldz + c, acc);
+              }
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+  // ---- source-major: the remaining rows (self term, several or no in-edges), 8
+  // rows per warp task (rows below n_pad are all of this kind)
+  constexpr int kChunk = 8;
+  const int nw = (int)((gridDim.x - dst_blocks) * (blockDim.x >> 5));
+  for (int base = (int)(((blockIdx.x - dst_blocks) * blockDim.x + threadIdx.x) >> 5) * kChunk;
+       base < nrows; base += nw * kChunk) {
+    const int s_l = base + lane;
+    int tb = 0, te = 0, d0 = -1;
+    float w0 = 0.f;
+    bool complex_row = false;
+    if (lane < kChunk && s_l < nrows) {
+      tb = __ldg(tindptr + s_l);
+      te = __ldg(tindptr + s_l + 1);
+      complex_row = !(te - tb == 1 && s_l >= npad);
+      if (complex_row && te > tb) {
+        d0 = __ldg(tdst + tb);
+        w0 = tw ? __ldg(tw + tb) : 1.f / (float)(__ldg(indptr + d0 + 1) - __ldg(indptr + d0));
+      }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, complex_row);
+    // complex rows four at a time: self and first-edge rows loaded back to back
+    while (m) {
+      int rk[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        rk[k] = m ? __ffs(m) - 1 : -1;
+        if (m) m &= m - 1;
+      }
+      for (int c0 = 0; c0 < f; c0 += 256) {
+        const int c = c0 + lane * 8;
+        const bool active = c < f;
+        constexpr int V = (int)sizeof(TG) / 2;   // 16-byte vectors per 8 columns
+        uint4 sraw[4][V], nraw[4][V];              // raw rows: converted after all loads
+        float wk[4];
+        uint8_t mk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = rk[k] < 0 ? 0 : rk[k];
+          const int dd = __shfl_sync(0xffffffffu, d0, r);
+          wk[k] = __shfl_sync(0xffffffffu, w0, r);
+          const int s = base + r;
+#pragma unroll
+          for (int q = 0; q < V; ++q) sraw[k][q] = nraw[k][q] = make_uint4(0, 0, 0, 0);
+          mk[k] = 0;
+          if (active && rk[k] >= 0) {
+            if (s < npad) {
+              const uint4* ps = reinterpret_cast<const uint4*>(dA + (int64_t)s * lda + f + c);
+#pragma unroll
+              for (int q = 0; q < V; ++q) sraw[k][q] = __ldg(ps + q);
+            }
+            if (dd >= 0) {
+              const uint4* pn = reinterpret_cast<const uint4*>(dA + (int64_t)dd * lda + c);
+#pragma unroll
+              for (int q = 0; q < V; ++q) nraw[k][q] = __ldg(pn + q);
+            }
+            mk[k] = mask[((int64_t)s * f + c) >> 3];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (rk[k] < 0) break;
+          const int r = rk[k];
+          const int s = base + r;
+          const int rtb = __shfl_sync(0xffffffffu, tb, r);
+          const int rte = __shfl_sync(0xffffffffu, te, r);
+          if (!active) continue;
+          const TG* sv = reinterpret_cast<const TG*>(sraw[k]);
+          const TG* nv = reinterpret_cast<const TG*>(nraw[k]);
+          float acc[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = F<TG>::in(sv[j]) + F<TG>::in(nv[j]) * wk[k];
+          for (int q = rtb + 1; q < rte; ++q) {
+            const int d = __ldg(tdst + q);
+            const float w = tw ? __ldg(tw + q)
+                               : 1.f / (float)(__ldg(indptr + d + 1) - __ldg(indptr + d));
+            float v[8];
+            ld8<TG>(dA + (int64_t)d * lda + c, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += v[j] * w;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = ((mk[k] >> j) & 1) ? acc[j] * scale : 0.f;
+          st8<TO>(dz + (int64_t)s * ldz + c, acc);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Adam (torch.optim.Adam semantics, no weight decay) over flat fp32 params,
 // bias correction from the device step counter; refreshes the bf16 shadow.
 __global__ void adam_kernel(float* __restrict__ p, float* __restrict__ g,
@@ -716,6 +885,42 @@ int sal_mean_bwd_t_live(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f
   if (m_dev == nullptr) return SAL_EINVAL;
   return mean_bwd_t_launch(dA, lda, dA_dtype, f, n_pad, indptr, tindptr, tdst, tw, rows, m_dev,
                            0, 1, mask, p, dz, ldz, dz_dtype, stream, 1);
+}
+
+int sal_mean_bwd(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
+                 const int64_t* n_dst_dev, const int32_t* indptr, const int32_t* src,
+                 const int32_t* tindptr, const int32_t* tdst, const float* tw, int64_t rows,
+                 const int64_t* m_dev, const uint8_t* mask, float p, void* dz, int64_t ldz,
+                 int32_t dz_dtype, void* stream) {
+  if (dA == nullptr || indptr == nullptr || src == nullptr || tindptr == nullptr ||
+      tdst == nullptr || mask == nullptr || dz == nullptr)
+    return sal::set_error(SAL_EINVAL, "mean_bwd: null argument");
+  if (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0 || f <= 0)
+    return sal::set_error(SAL_EINVAL, "mean_bwd: f, lda and ldz must be multiples of 8");
+  if (rows < 0 || n_pad < 0 || n_pad > rows)
+    return sal::set_error(SAL_EINVAL, "mean_bwd: bad row counts");
+  if (rows == 0) return SAL_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int dst_blocks = (int)((n_pad + 7) / 8);
+  const int cap = sal::num_sms() * 8;
+  if (dst_blocks > cap) dst_blocks = cap;
+  if (dst_blocks < 1) dst_blocks = 1;
+  int src_blocks = (int)((rows + 63) / 64);   // 8 warps x 8-row tasks per block
+  if (src_blocks > cap) src_blocks = cap;
+  if (src_blocks < 1) src_blocks = 1;
+  const int g = dst_blocks + src_blocks;
+  const int live = m_dev != nullptr;
+  if (dA_dtype == SAL_BF16 && dz_dtype == SAL_BF16)
+    sal::mean_bwd_split_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(
+        (const __nv_bfloat16*)dA, lda, f, n_pad, n_dst_dev, indptr, src, tindptr, tdst, tw,
+        rows, m_dev, live, mask, p, (__nv_bfloat16*)dz, ldz, dst_blocks);
+  else if (dA_dtype == SAL_F32 && dz_dtype == SAL_F32)
+    sal::mean_bwd_split_kernel<float, float><<<g, 256, 0, st>>>(
+        (const float*)dA, lda, f, n_pad, n_dst_dev, indptr, src, tindptr, tdst, tw, rows, m_dev,
+        live, mask, p, (float*)dz, ldz, dst_blocks);
+  else
+    return sal::set_error(SAL_EINVAL, "mean_bwd: dtypes must be bf16/bf16 or f32/f32");
+  return sal::done(1);
 }
 
 int sal_adam_step(float* param, float* grad, float* m, float* v, void* shadow_bf16,

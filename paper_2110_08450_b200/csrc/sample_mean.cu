@@ -21,6 +21,7 @@
 // mpnn.py:57-65 (_mean_neighbors), prep.py:153-171 (slice_features).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 
@@ -74,6 +75,11 @@ SAL_DEVINL uint4 pack8(const float* f) {
 }
 
 constexpr int kSmThreads = 256;
+
+// 1/c for c = 0..32, the correctly rounded fp32 values 1.f / (float)c gives
+// (generated with numpy float32 division; hex literals are exact)
+__constant__ float c_inv[33] = {
+    0.0f, 0x1.0000000000000p+0f, 0x1.0000000000000p-1f, 0x1.5555560000000p-2f, 0x1.0000000000000p-2f, 0x1.99999a0000000p-3f, 0x1.5555560000000p-3f, 0x1.24924a0000000p-3f, 0x1.0000000000000p-3f, 0x1.c71c720000000p-4f, 0x1.99999a0000000p-4f, 0x1.745d180000000p-4f, 0x1.5555560000000p-4f, 0x1.3b13b20000000p-4f, 0x1.24924a0000000p-4f, 0x1.1111120000000p-4f, 0x1.0000000000000p-4f, 0x1.e1e1e20000000p-5f, 0x1.c71c720000000p-5f, 0x1.af286c0000000p-5f, 0x1.99999a0000000p-5f, 0x1.8618620000000p-5f, 0x1.745d180000000p-5f, 0x1.642c860000000p-5f, 0x1.5555560000000p-5f, 0x1.47ae140000000p-5f, 0x1.3b13b20000000p-5f, 0x1.2f684c0000000p-5f, 0x1.24924a0000000p-5f, 0x1.1a7b960000000p-5f, 0x1.1111120000000p-5f, 0x1.0842100000000p-5f, 0x1.0000000000000p-5f};
 
 // One destination's sample: lane j < cnt receives the global id of accepted
 // edge j in `sid` (a predicated load: the value is consumed an iteration later).
@@ -135,7 +141,7 @@ __host__ __device__ constexpr int stage_bytes() { return (kRows + 1) * 256; }
 // No register holds a row, so the warp carries one destination's rows in flight
 // while it accumulates the previous one, and every load result is consumed an
 // iteration after it was issued.
-template <int kPolicy, typename TIn, typename TOut, int kRows>
+template <int kPolicy, typename TIn, typename TOut, int kRows, bool kFull>
 __global__ void __launch_bounds__(kSmThreads)
 sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                    const int32_t* __restrict__ globals, const int64_t* __restrict__ n_dst_ptr,
@@ -159,7 +165,7 @@ sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
   __shared__ int32_t sh_acc[kSmThreads / 32][32];
   int32_t* accepted = sh_acc[warp];
   if (size_unknown != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *size_unknown = -1;
-  const bool vlane = sub < vpr;
+  const bool vlane = kFull || sub < vpr;   // kFull: 256-byte rows, every lane busy
   const bool do_self = grp == 1 && vlane && self_off >= 0;
   const char* tbase = reinterpret_cast<const char*>(table) + sub * 16;
   const int64_t tbytes = t_stride * (int64_t)sizeof(TIn);
@@ -242,15 +248,23 @@ sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
     float acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    // branch-free: rows past the count add +0 (acc starts at +0 and so is never -0,
+    // which makes the add exact no-op)
 #pragma unroll
     for (int u = 0; u < kRows / 2; ++u) {
       const int e = u * 2 + grp;
-      if (e < cnt && vlane) acc8<TIn>(acc, *reinterpret_cast<const uint4*>(ls + e * 256));
+      uint4 v = *reinterpret_cast<const uint4*>(ls + e * 256);
+      const bool on = e < cnt && vlane;
+      v.x = on ? v.x : 0u;
+      v.y = on ? v.y : 0u;
+      v.z = on ? v.z : 0u;
+      v.w = on ? v.w : 0u;
+      acc8<TIn>(acc, v);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
     if (cnt > 0) {
-      const float inv = 1.f / (float)cnt;
+      const float inv = c_inv[cnt];   // == 1.f / (float)cnt
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] *= inv;
     }
@@ -300,11 +314,23 @@ static cudaError_t launch_sm(const GraphDev& g, const int32_t* globals, const in
                              int64_t out_stride, int64_t self_off, int64_t* size_unknown,
                              cudaStream_t st) {
   const int smem = (kSmThreads / 32) * 2 * stage_bytes<kRows>();
-  auto k = sample_mean_kernel<kPolicy, __half, TO, kRows>;
+  auto k = vpr == 16 ? sample_mean_kernel<kPolicy, __half, TO, kRows, true>
+                     : sample_mean_kernel<kPolicy, __half, TO, kRows, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int64_t grid = (max_dst + kSmThreads / 32 - 1) / (kSmThreads / 32);
-  const int64_t cap = (int64_t)num_sms() * sample_mean_bps<kRows>();
+  int bps = sample_mean_bps<kRows>();
+  if (const char* e = getenv("SAL_SAMPLE_MEAN_BPS")) {   // A/B knob (tools/)
+    const int b = atoi(e);
+    if (b >= 1 && b < bps) bps = b;
+  }
+  int64_t cap = (int64_t)num_sms() * bps;
+  // A/B knob (tools/): SAL_SAMPLE_MEAN_DPW = destinations per warp (a non-persistent
+  // grid of short-lived blocks the scheduler can interleave with other kernels)
+  if (const char* e = getenv("SAL_SAMPLE_MEAN_DPW")) {
+    const int dpw = atoi(e);
+    if (dpw > 0) cap = (max_dst + (int64_t)dpw * (kSmThreads / 32) - 1) / ((int64_t)dpw * (kSmThreads / 32));
+  }
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   k<<<(int)grid, kSmThreads, smem, st>>>(g.indptr, g.indices, globals, n_dst, fanout, hk, desc,

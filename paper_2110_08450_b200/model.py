@@ -222,6 +222,10 @@ class FusedSAGE:
         self.wgrad_fork_late = True
         # the last input gradient writes only the rows layer 0's weight gradient reads
         self.mbt_live = True
+        # input gradients as sal_mean_bwd: single-in-edge rows destination-major (each
+        # dA row read once for all its sources), the rest source-major (bit-identical
+        # to sal_mean_bwd_t)
+        self.mbt_split = True
         # zero-fill the padding rows of the tcgen05 forward's output and mask in training
         self.pad_fill = False
         self._wgrad_stream = torch.cuda.Stream(device=dev)
@@ -484,7 +488,16 @@ class FusedSAGE:
         mask = saved[i - 1]["mask"]
         m_rows = saved[i - 1]["adj"][3]   # true rows of dz = layer i-1's destinations
 
-        if i == 1 and self.mbt_live and m_rows is not None and self._tc_wgrad_layer(0):
+        live = i == 1 and self.mbt_live and m_rows is not None and self._tc_wgrad_layer(0)
+        if self.mbt_split:
+            _lib.check(L.sal_mean_bwd(
+                dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
+                _lib.ptr(n_dev), indptr.data_ptr(), src.data_ptr(), tindptr.data_ptr(),
+                tdst.data_ptr(), tw.data_ptr(), rows, m_rows.data_ptr() if live else None,
+                mask.data_ptr(), p, dzp.data_ptr(), dzp.stride(0), _lib.dtype_code(self.act),
+                _lib.stream_ptr()), "mean_bwd")
+            return dzp
+        if live:
             # dz_0's only reader is layer 0's split-K weight gradient, which reads
             # whole 64-row chunks up to its true row count: skip the padding rows
             _lib.check(L.sal_mean_bwd_t_live(

@@ -385,3 +385,50 @@ def test_adam_step_matches_torch_adam(n):
         assert (grad == 0).all()
         assert torch.allclose(p, ref.detach(), rtol=1e-5, atol=1e-6)
         assert torch.equal(shadow, p.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("dtype,f,live", [(torch.bfloat16, 256, None), (torch.bfloat16, 256, 1300),
+                                          (torch.bfloat16, 512, None), (torch.bfloat16, 104, None),
+                                          (torch.bfloat16, 32, 640), (torch.float32, 64, None)])
+def test_mean_bwd_split_equals_mean_bwd_t(dtype, f, live):
+    """sal_mean_bwd (destination-major pass for single-in-edge rows + source-major pass
+    for the rest) is bit-identical to sal_mean_bwd_t(_live): rows with no, one and
+    several in-edges (duplicate sources), self rows, destinations past the device
+    count, and the live-rows cut."""
+    from paper_2110_08450_b200 import _lib
+    from paper_2110_08450_b200.model import build_transpose
+    rng = np.random.default_rng(f + (live or 0))
+    n_pad, n_dst, rows, p = 300, 280, 2000, 0.5
+    deg = rng.integers(0, 12, size=n_pad)
+    indptr = np.zeros(n_pad + 1, dtype=np.int32)
+    indptr[1:] = np.cumsum(deg)
+    src = rng.integers(0, rows - 100, size=int(indptr[-1])).astype(np.int32)
+    ip, sr = torch.from_numpy(indptr).cuda(), torch.from_numpy(src).cuda()
+    nd = torch.tensor([n_dst], dtype=torch.int64, device="cuda")
+    tind, tdst, tw = build_transpose(ip, sr, nd, n_pad, rows)
+    dA = (torch.randn(n_pad, 2 * f, device="cuda") * 0.1).to(dtype)
+    mask = torch.from_numpy(rng.integers(0, 256, size=rows * f // 8, dtype=np.uint8)).cuda()
+    want = torch.full((rows, f), float("nan"), device="cuda", dtype=dtype)
+    got = torch.full((rows, f), float("nan"), device="cuda", dtype=dtype)
+    L = _lib.lib()
+    dc = _lib.dtype_code(dtype)
+    md = torch.tensor([live or 0], dtype=torch.int64, device="cuda")
+    if live is None:
+        _lib.check(L.sal_mean_bwd_t(dA.data_ptr(), dA.stride(0), dc, f, n_pad, ip.data_ptr(),
+                                    tind.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows,
+                                    mask.data_ptr(), p, want.data_ptr(), want.stride(0), dc,
+                                    _lib.stream_ptr()), "mbt")
+    else:
+        _lib.check(L.sal_mean_bwd_t_live(dA.data_ptr(), dA.stride(0), dc, f, n_pad,
+                                         ip.data_ptr(), tind.data_ptr(), tdst.data_ptr(),
+                                         tw.data_ptr(), rows, md.data_ptr(), mask.data_ptr(), p,
+                                         want.data_ptr(), want.stride(0), dc,
+                                         _lib.stream_ptr()), "mbt_live")
+    _lib.check(L.sal_mean_bwd(dA.data_ptr(), dA.stride(0), dc, f, n_pad, nd.data_ptr(),
+                              ip.data_ptr(), sr.data_ptr(), tind.data_ptr(), tdst.data_ptr(),
+                              tw.data_ptr(), rows, md.data_ptr() if live is not None else None,
+                              mask.data_ptr(), p, got.data_ptr(), got.stride(0), dc,
+                              _lib.stream_ptr()), "mean_bwd")
+    torch.cuda.synchronize()
+    iv = torch.int16 if dtype == torch.bfloat16 else torch.int32
+    assert torch.equal(got.view(iv), want.view(iv))

@@ -2,7 +2,7 @@
 destination rows) alone on the papers-shape layer: 6144 destinations x 10
 sampled edges over 67584 source rows, f = 256, bf16, p = 0.5.
 
-python tools/mbt_bench.py   (under gpurun)
+python tools/mbt_bench.py [--split]   (under gpurun)
 """
 import sys
 from pathlib import Path
@@ -31,7 +31,17 @@ mask = torch.from_numpy(rng.integers(0, 256, size=rows * f // 8, dtype=np.uint8)
 dz = torch.empty(rows, f, device=dev, dtype=torch.bfloat16)
 
 
+SPLIT = "--split" in sys.argv
+
+
 def run():
+    if SPLIT:
+        _lib.check(L.sal_mean_bwd(dA.data_ptr(), dA.stride(0), _lib.SAL_BF16, f, n_dst,
+                                  n_dev.data_ptr(), indptr.data_ptr(), src.data_ptr(),
+                                  tind.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows, None,
+                                  mask.data_ptr(), 0.5, dz.data_ptr(), dz.stride(0),
+                                  _lib.SAL_BF16, _lib.stream_ptr()), "mean_bwd")
+        return
     _lib.check(L.sal_mean_bwd_t(dA.data_ptr(), dA.stride(0), _lib.SAL_BF16, f, n_dst,
                                 indptr.data_ptr(), tind.data_ptr(), tdst.data_ptr(),
                                 tw.data_ptr(), rows, mask.data_ptr(), 0.5, dz.data_ptr(),
@@ -53,7 +63,7 @@ for _ in range(20):
     ts.append(a.elapsed_time(b) * 1e3)
 byts = rows * f * 2 + rows * f // 8 + n_dst * fan * (2 * f + 12) + (rows + 1) * 4
 t = float(np.median(ts))
-print(f"mean_bwd_t  rows {rows}  edges {n_dst * fan}  {t:.1f} us  {byts / t / 1e3:.0f} GB/s "
+print(f"{'mean_bwd(split)' if SPLIT else 'mean_bwd_t'}  rows {rows}  edges {n_dst * fan}  {t:.1f} us  {byts / t / 1e3:.0f} GB/s "
       f"(algorithmic {byts / 1e6:.1f} MB)")
 # checksum for A/B of kernel variants
 bits = dz.view(torch.int16).to(torch.int64)
