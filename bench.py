@@ -104,6 +104,11 @@ def dist_setup(args):
     if world > 1:
         torch.cuda.set_device(dev)
         if backend == "nccl":
+            # communicator setup (ranks, NVLS/NVLink transport) logged to stderr; stdout
+            # carries only the JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             torch.distributed.init_process_group(backend)
