@@ -157,7 +157,8 @@ extern "C" {
 
 int sal_gen_degrees(int64_t n, uint64_t seed, double scale, double a, int64_t* degs,
                     void* stream) {
-  if (n < 0 || !(a > 1.0) || !(scale >= 0.0)) return SAL_EINVAL;
+  if (n < 0 || !(a > 1.0) || !(scale >= 0.0))
+    return sal::set_error(SAL_EINVAL, "gen_degrees: invalid argument (n < 0 || !(a > 1.0) || !(scale >= 0.0))");
   if (n == 0) return SAL_OK;
   sal::degrees_kernel<<<sal::gen_grid(n), 256, 0, (cudaStream_t)stream>>>(n, seed, scale, a,
                                                                            degs);
@@ -171,7 +172,8 @@ int sal_gen_owner(const int64_t* indptr, int64_t n, int32_t* owner, void* stream
 
 int sal_gen_pairing(const int32_t* owner, int64_t n_stubs, uint64_t seed, int32_t* indices,
                     void* stream) {
-  if (n_stubs % 2 != 0) return SAL_EINVAL;
+  if (n_stubs % 2 != 0)
+    return sal::set_error(SAL_EINVAL, "gen_pairing: invalid argument (n_stubs % 2 != 0)");
   sal::Feistel F;
   int bits = 2;
   while ((1ull << bits) < (uint64_t)n_stubs) ++bits;

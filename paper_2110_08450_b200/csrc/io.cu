@@ -360,7 +360,8 @@ int sal_load_labels(const char* path, const sal_file_header* h, int64_t* out_dev
 
 int sal_validate_csr(const int64_t* indptr_dev, const int32_t* indices_dev, int64_t n, int64_t e,
                      int32_t* flags_dev, void* stream) {
-  if (!indptr_dev || !flags_dev || n < 0 || e < 0) return SAL_EINVAL;
+  if (!indptr_dev || !flags_dev || n < 0 || e < 0)
+    return sal::set_error(SAL_EINVAL, "validate_csr: invalid argument (!indptr_dev || !flags_dev || n < 0 || e < 0)");
   const int64_t m = n > e ? n : e;
   sal::validate_csr_kernel<<<sal::grid_for(m), 256, 0, (cudaStream_t)stream>>>(
       indptr_dev, indices_dev, n, e, flags_dev);
@@ -371,7 +372,8 @@ int sal_validate_csr(const int64_t* indptr_dev, const int32_t* indices_dev, int6
 
 int sal_validate_labels(const int64_t* y_dev, int64_t n, int64_t num_classes, int32_t* flags_dev,
                         void* stream) {
-  if (!flags_dev || n < 0) return SAL_EINVAL;
+  if (!flags_dev || n < 0)
+    return sal::set_error(SAL_EINVAL, "validate_labels: invalid argument (!flags_dev || n < 0)");
   if (n == 0) return SAL_OK;
   sal::validate_labels_kernel<<<sal::grid_for(n), 256, 0, (cudaStream_t)stream>>>(
       y_dev, n, num_classes, flags_dev);

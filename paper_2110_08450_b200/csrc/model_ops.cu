@@ -741,7 +741,8 @@ int sal_plan_next(const int64_t* desc_all, int64_t n_steps, int64_t* cursor, sal
 int sal_relu_dropout_fwd(const void* x, int64_t sx, void* y, int64_t sy, int64_t rows,
                          int32_t cols, int32_t dtype, uint8_t* mask, float p, uint64_t seed,
                          const int64_t* salt_dev, void* stream) {
-  if (cols % 8 != 0 || sx % 8 != 0 || sy % 8 != 0) return SAL_EINVAL;
+  if (cols % 8 != 0 || sx % 8 != 0 || sy % 8 != 0)
+    return sal::set_error(SAL_EINVAL, "relu_dropout_fwd: invalid argument (cols % 8 != 0 || sx % 8 != 0 || sy % 8 != 0)");
   cudaStream_t st = (cudaStream_t)stream;
   const int g = sal::ew_grid(rows * (cols / 8));
   if (dtype == SAL_BF16)
@@ -751,14 +752,15 @@ int sal_relu_dropout_fwd(const void* x, int64_t sx, void* y, int64_t sy, int64_t
     sal::relu_dropout_fwd_kernel<float><<<g, 256, 0, st>>>((const float*)x, sx, (float*)y, sy,
                                                           rows, cols, mask, p, seed, salt_dev);
   else
-    return SAL_EINVAL;
+    return sal::set_error(SAL_EINVAL, "relu_dropout_fwd: unsupported dtype or shape");
   return sal::done(1);
 }
 
 int sal_relu_dropout_bwd(const void* dy, int64_t sdy, int32_t dy_dtype, const uint8_t* mask,
                          void* dx, int64_t sdx, int32_t dx_dtype, int64_t rows, int32_t cols,
                          float p, void* stream) {
-  if (cols % 8 != 0) return SAL_EINVAL;
+  if (cols % 8 != 0)
+    return sal::set_error(SAL_EINVAL, "relu_dropout_bwd: invalid argument (cols % 8 != 0)");
   cudaStream_t st = (cudaStream_t)stream;
   const int g = sal::ew_grid(rows * (cols / 8));
   if (dy_dtype == SAL_F32 && dx_dtype == SAL_BF16)
@@ -771,7 +773,7 @@ int sal_relu_dropout_bwd(const void* dy, int64_t sdy, int32_t dy_dtype, const ui
     sal::relu_dropout_bwd_kernel<float, float><<<g, 256, 0, st>>>((const float*)dy, sdy, mask,
                                                                  (float*)dx, sdx, rows, cols, p);
   else
-    return SAL_EINVAL;
+    return sal::set_error(SAL_EINVAL, "relu_dropout_bwd: unsupported dtype or shape");
   return sal::done(1);
 }
 
@@ -788,13 +790,14 @@ int sal_lsm_nll(const void* logits, int64_t ld, int64_t rows, int32_t C, int32_t
     sal::lsm_nll_kernel<float><<<grid, 32 * warps, 0, st>>>((const float*)logits, ld, rows, C,
                                                            labels, loss, (float*)grad, ldg);
   else
-    return SAL_EINVAL;
+    return sal::set_error(SAL_EINVAL, "lsm_nll: unsupported dtype or shape");
   return sal::done(1);
 }
 
 int sal_argmax_correct(const void* logits, int64_t ld, int64_t rows, int32_t C, int32_t dtype,
                        const int64_t* labels, int64_t* counts, int64_t* pred, void* stream) {
-  if (rows < 0 || C <= 0 || !counts || !labels) return SAL_EINVAL;
+  if (rows < 0 || C <= 0 || !counts || !labels)
+    return sal::set_error(SAL_EINVAL, "argmax_correct: invalid argument (rows < 0 || C <= 0 || !counts || !labels)");
   if (rows == 0) return SAL_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int warps = 8;
@@ -807,7 +810,7 @@ int sal_argmax_correct(const void* logits, int64_t ld, int64_t rows, int32_t C, 
     sal::argmax_correct_kernel<float><<<grid, 32 * warps, 0, st>>>((const float*)logits, ld,
                                                                   rows, C, labels, c, pred);
   else
-    return SAL_EINVAL;
+    return sal::set_error(SAL_EINVAL, "argmax_correct: unsupported dtype or shape");
   return sal::done(1);
 }
 
@@ -821,7 +824,7 @@ int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t
                         int32_t* tdst, float* tw, void* ws, int32_t ws_zeroed, void* stream) {
   (void)max_edges;
   if (indptr == nullptr || src == nullptr || tindptr == nullptr || tdst == nullptr || ws == nullptr)
-    return SAL_EINVAL;
+    return sal::set_error(SAL_EINVAL, "transpose_build: unsupported dtype or shape");
   cudaStream_t st = (cudaStream_t)stream;
   int32_t* tcount = (int32_t*)ws;
   int32_t* tfill = tcount + (n_src_rows + 1);
@@ -853,8 +856,10 @@ static int mean_bwd_t_launch(const void* dA, int64_t lda, int32_t dA_dtype, int3
                              const int64_t* m_dev, int32_t part, int32_t nparts,
                              const uint8_t* mask, float p, void* dz, int64_t ldz,
                              int32_t dz_dtype, void* stream, int live) {
-  if (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0) return SAL_EINVAL;
-  if (nparts < 1 || part < 0 || part >= nparts) return SAL_EINVAL;
+  if (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0)
+    return sal::set_error(SAL_EINVAL, "mean_bwd_t_launch: invalid argument (f % 8 != 0 || lda % 8 != 0 || ldz % 8 != 0)");
+  if (nparts < 1 || part < 0 || part >= nparts)
+    return sal::set_error(SAL_EINVAL, "mean_bwd_t_launch: invalid argument (nparts < 1 || part < 0 || part >= nparts)");
   cudaStream_t st = (cudaStream_t)stream;
   const int g = sal::warp_grid((rows / nparts + 7) / 8);
   if (dA_dtype == SAL_BF16 && dz_dtype == SAL_BF16)
@@ -866,7 +871,7 @@ static int mean_bwd_t_launch(const void* dA, int64_t lda, int32_t dA_dtype, int3
         (const float*)dA, lda, f, n_pad, indptr, tindptr, tdst, tw, rows, m_dev, part, nparts,
         mask, p, (float*)dz, ldz, live);
   else
-    return SAL_EINVAL;
+    return sal::set_error(SAL_EINVAL, "mean_bwd_t_launch: unsupported dtype or shape");
   return sal::done(1);
 }
 
@@ -882,7 +887,8 @@ int sal_mean_bwd_t_live(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f
                         const int32_t* indptr, const int32_t* tindptr, const int32_t* tdst,
                         const float* tw, int64_t rows, const int64_t* m_dev, const uint8_t* mask,
                         float p, void* dz, int64_t ldz, int32_t dz_dtype, void* stream) {
-  if (m_dev == nullptr) return SAL_EINVAL;
+  if (m_dev == nullptr)
+    return sal::set_error(SAL_EINVAL, "mean_bwd_t_live: invalid argument (m_dev == nullptr)");
   return mean_bwd_t_launch(dA, lda, dA_dtype, f, n_pad, indptr, tindptr, tdst, tw, rows, m_dev,
                            0, 1, mask, p, dz, ldz, dz_dtype, stream, 1);
 }
@@ -927,7 +933,7 @@ int sal_adam_step(float* param, float* grad, float* m, float* v, void* shadow_bf
                   int64_t n, float lr, float beta1, float beta2, float eps,
                   const int64_t* t_dev, int32_t zero_grad, void* stream) {
   if (param == nullptr || grad == nullptr || m == nullptr || v == nullptr || t_dev == nullptr)
-    return SAL_EINVAL;
+    return sal::set_error(SAL_EINVAL, "adam_step: unsupported dtype or shape");
   const bool vec = n % 4 == 0 &&
                    ((uintptr_t)param | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) % 16 == 0 &&
                    (uintptr_t)shadow_bf16 % 8 == 0;
@@ -955,12 +961,14 @@ __global__ void zero_spans_kernel(ZeroSpans z) {
 }
 
 int sal_zero_spans(void* const* ptrs, const int64_t* bytes, int32_t n, void* stream) {
-  if (n < 0 || n > 8 || (n && (!ptrs || !bytes))) return SAL_EINVAL;
+  if (n < 0 || n > 8 || (n && (!ptrs || !bytes)))
+    return sal::set_error(SAL_EINVAL, "zero_spans: invalid argument (n < 0 || n > 8 || (n && (!ptrs || !bytes)))");
   ZeroSpans z;
   z.n = n;
   int64_t most = 0;
   for (int k = 0; k < n; ++k) {
-    if (((uintptr_t)ptrs[k] & 15) || (bytes[k] & 15)) return SAL_EINVAL;
+    if (((uintptr_t)ptrs[k] & 15) || (bytes[k] & 15))
+      return sal::set_error(SAL_EINVAL, "zero_spans: invalid argument (((uintptr_t)ptrs[k] & 15) || (bytes[k] & 15))");
     z.p[k] = (uint4*)ptrs[k];
     z.n16[k] = bytes[k] / 16;
     if (z.n16[k] > most) most = z.n16[k];

@@ -1322,9 +1322,10 @@ int sal_tc_sage_fwd(const void* A, int64_t lda, int64_t M, const int64_t* m_dev,
                     uint64_t seed, const int64_t* salt_dev, int32_t relu_dropout, void* stream) {
   // two column blocks of 128 (grid.y); each CTA holds its [128 x K] W block
   // (K = 256: layer 0; K = 512: the hidden layer)
-  if (N != sal::tc::kFN || (K != 256 && K != 512)) return SAL_EINVAL;
+  if (N != sal::tc::kFN || (K != 256 && K != 512))
+    return sal::set_error(SAL_EINVAL, "tc_sage_fwd: invalid argument (N != sal::tc::kFN || (K != 256 && K != 512))");
   if (lda % 8 || ldy % 8 || ((uintptr_t)A & 15) || ((uintptr_t)W & 15) || ((uintptr_t)Y & 15))
-    return SAL_EINVAL;
+    return sal::set_error(SAL_EINVAL, "tc_sage_fwd: unsupported dtype or shape");
   if (M <= 0) return SAL_OK;
   const int bn = 128;
   const int nblk = N / bn;

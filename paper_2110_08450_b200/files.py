@@ -211,3 +211,11 @@ def save_labels(y: LabelVector, path) -> None:
         f.write(LABL_MAGIC)
         f.write(struct.pack("<IQI", FORMAT_VERSION, len(y.values), y.num_classes))
         f.write(np.asarray(y.values).astype("<u4").tobytes())
+
+
+# The reference's loader names (graph.py:202-260).  They return the HBM-resident
+# objects every entry point of this package accepts (DeviceGraph, device feature
+# rows, (labels, num_classes)), with the reference's header checks and errors.
+load_csr = load_csr_device
+load_features = load_features_device
+load_labels = load_labels_device

@@ -89,6 +89,48 @@ def mfg_forward(mfg: Mfg, features, weights) -> torch.Tensor:
     return h
 
 
+def sampled_reference_forward(mfg: Mfg, features_global, weights) -> torch.Tensor:
+    """Same math as mfg_forward, indexing the GLOBAL feature matrix (mpnn.py:86-111).
+
+    Layer 0 never touches a sliced local buffer: every edge is resolved to its global
+    endpoint through the id map and the row is read from the global table on the
+    device (sal_segment_mean_fwd_global), the destinations' own rows likewise; the
+    layers above index hidden rows by local id (the reference's dict keyed by global
+    id is the same bijection).  A disagreement with mfg_forward pinpoints a local-id
+    or slicing defect.  Returns |seeds| rows on device."""
+    if len(weights) != len(mfg.layers):
+        raise ValueError("one weight set per MFG layer required")
+    dev = mfg.id_map.device
+    X = torch.as_tensor(features_global).to(dev)
+    if X.dtype != torch.float32:
+        X = X.float()
+    X = X.contiguous()
+    _check_dims(X.shape[1], weights)
+    gids = mfg.id_map.global_ids
+    L = _lib.lib()
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        h = None
+        for i, (layer, w) in enumerate(zip(mfg.layers, weights)):
+            if i == 0:
+                neigh = torch.empty((layer.num_dst, X.shape[1]), dtype=torch.float32, device=dev)
+                if layer.num_dst:
+                    _lib.check(L.sal_segment_mean_fwd_global(
+                        layer.indptr.data_ptr(), layer.src_local.data_ptr(), gids.data_ptr(),
+                        None, layer.num_dst, X.data_ptr(), _lib.SAL_F32, X.stride(0),
+                        X.shape[1], neigh.data_ptr(), _lib.SAL_F32, neigh.stride(0),
+                        _lib.stream_ptr()), "segment_mean_fwd_global")
+                h_dst = X[gids[:layer.num_dst].long()]
+            else:
+                neigh = segment_mean(layer.indptr, layer.src_local, h, layer.num_dst)
+                h_dst = h[:layer.num_dst]
+            h = h_dst @ _as_dev(w.w_self, dev).T + neigh @ _as_dev(w.w_neigh, dev).T
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return h
+
+
 def full_forward(g, X, weights, dst_ids, num_layers: int | None = None) -> torch.Tensor:
     """Exact full-neighbourhood evaluation (mpnn.py:114-135) on the device graph."""
     from .graph import as_device_graph

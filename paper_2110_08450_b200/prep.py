@@ -260,13 +260,10 @@ def _prep_into_slot(dg, x, yv, slot: _Slot, seeds: SeedBatch, seeds_base: torch.
     slot.seeds = seeds
 
 
-def _finish_slot(slot: _Slot, cols: int, variant: SamplerVariant, run=None) -> PreparedBatch:
-    slot.done.synchronize()
-    ws = slot.ws
-    ext = slot.extents.tolist()
-    nh = ws.num_hops
-    sizes, etot = ext[:nh + 1], ext[nh + 1:]
+def _mfg_from_ws(ws: MfgWorkspace, sizes, etot, seeds: SeedBatch, variant: SamplerVariant) -> Mfg:
+    """The Mfg view of a sampled workspace, given its host-known extents."""
     from .sampler import MfgLayer
+    nh = ws.num_hops
     layers = []
     for h in range(nh):
         nd = sizes[h]
@@ -275,7 +272,16 @@ def _finish_slot(slot: _Slot, cols: int, variant: SamplerVariant, run=None) -> P
                                src_local=ws.src_local[h][:etot[h]]))
     idm = IdMap(variant, device=ws.device, _table=ws.table, _globals=ws.globals,
                 _size=sizes[-1])
-    mfg = Mfg(layers=tuple(reversed(layers)), id_map=idm, seeds=slot.seeds, workspace=ws)
+    return Mfg(layers=tuple(reversed(layers)), id_map=idm, seeds=seeds, workspace=ws)
+
+
+def _finish_slot(slot: _Slot, cols: int, variant: SamplerVariant, run=None) -> PreparedBatch:
+    slot.done.synchronize()
+    ws = slot.ws
+    ext = slot.extents.tolist()
+    nh = ws.num_hops
+    sizes, etot = ext[:nh + 1], ext[nh + 1:]
+    mfg = _mfg_from_ws(ws, sizes, etot, slot.seeds, variant)
     feats = slot.features[:sizes[-1], :cols]
     labels = slot.labels[:len(slot.seeds)]
     stats = tuple((l.num_dst, l.num_src, l.num_edges) for l in mfg.layers)
@@ -287,19 +293,44 @@ def _finish_slot(slot: _Slot, cols: int, variant: SamplerVariant, run=None) -> P
 def prepare_batch(g, fm, y, seeds: SeedBatch, fanouts: FanoutSpec, variant: SamplerVariant,
                   global_seed: int, slot=None, pool=None, *, feature_dtype: str = "f32",
                   rng_policy: str = "splitmix") -> PreparedBatch:
-    """Sample the MFG then slice features and labels for one batch (prep.py:192-206)."""
+    """Sample the MFG then slice features and labels for one batch (prep.py:192-206).
+
+    Like the reference, the MFG is built first and the feature/label buffers are then
+    sized to it (its _Slot.reserve): one MFG workspace plus exactly num_nodes x cols
+    feature rows, not a worst-case node_cap buffer.  A `slot` from this module (the
+    buffers of an epoch run, or one the caller keeps) is reused instead; `pool` is
+    accepted for signature compatibility (slots are recycled by run_epoch_prep)."""
     dg = as_device_graph(g)
     x = _feature_source(fm) if fm is not None else None
     yv = _label_source(y) if y is not None else None
-    cfg = PrepConfig(fanouts=fanouts, variant=variant, feature_dtype=feature_dtype,
-                     rng_policy=rng_policy)
     cols = x.shape[1] if x is not None else 0
-    s = _Slot(dg, cfg, len(seeds), cols, dg.device)
     stream = torch.cuda.current_stream()
-    s.ws.load_seeds(seeds, stream)
-    _prep_into_slot(dg, x, yv, s, seeds, s.ws.seeds, s.ws.desc, global_seed,
-                    RNG_POLICIES[rng_policy], stream)
-    return _finish_slot(s, cols, variant)
+    policy = RNG_POLICIES[rng_policy]
+    if isinstance(slot, _Slot):
+        if slot.ws.fanouts != fanouts or slot.ws.max_seeds < len(seeds):
+            raise ValueError("slot was built for other fanouts or a smaller batch")
+        slot.ws.load_seeds(seeds, stream)
+        _prep_into_slot(dg, x, yv, slot, seeds, slot.ws.seeds, slot.ws.desc, global_seed,
+                        policy, stream)
+        return _finish_slot(slot, cols, variant)
+    ws = MfgWorkspace(dg.num_nodes, fanouts, len(seeds), device=dg.device)
+    ws.load_seeds(seeds, stream)
+    ws.run(dg, ws.seeds, ws.desc, global_seed, policy, stream)
+    sizes, etot = ws.read_extents()
+    n = sizes[-1]
+    feats = torch.empty((n, cols), dtype=_TORCH_DT[feature_dtype], device=dg.device)
+    if x is not None and n:
+        gather_rows(x, ws.globals, feats, n=n, stream=stream)
+    labels = torch.empty(len(seeds), dtype=torch.int64, device=dg.device)
+    if yv is not None and len(seeds):
+        _lib.check(_lib.lib().sal_gather_labels(yv.data_ptr(), ws.seeds.data_ptr(),
+                                                ws.desc.data_ptr(), len(seeds),
+                                                labels.data_ptr(), _lib.stream_ptr(stream)),
+                   "gather_labels")
+    mfg = _mfg_from_ws(ws, sizes, etot, seeds, variant)
+    stats = tuple((l.num_dst, l.num_src, l.num_edges) for l in mfg.layers)
+    return PreparedBatch(mfg=mfg, features=feats, labels=labels,
+                         byte_size=_batch_bytes(mfg, cols, len(seeds)), stats=stats)
 
 
 @dataclass
@@ -386,8 +417,14 @@ class EpochPrepRun:
         try:
             while nxt < nb and len(pending) < depth:
                 launch()
+            in_order = cfg.delivery == "in_order"
             while pending:
-                slot = pending.pop(0)
+                # in_order: plan order (prep.py:289-297); completion_order: the first
+                # in-flight batch whose stream has finished it, else the oldest
+                j = 0
+                if not in_order:
+                    j = next((i for i, sl in enumerate(pending) if sl.done.query()), 0)
+                slot = pending.pop(j)
                 batch = _finish_slot(slot, cols, cfg.variant, run=self)
                 ts = slot.ev[0].elapsed_time(slot.ev[1]) / 1e3
                 tsl = slot.ev[1].elapsed_time(slot.ev[2]) / 1e3

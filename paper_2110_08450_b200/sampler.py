@@ -541,20 +541,21 @@ def sample_neighbors(g, v: int, d: int, rng: CounterRng) -> np.ndarray:
     """Edge-slot positions of node v sampled without replacement (sampler.py:253-273).
 
     Runs the device sampler on a one-destination hop whose neighbour list is
-    replaced by slot positions; advances rng.counter by the draws consumed.
+    replaced by slot positions; advances rng.counter by the draws consumed.  A
+    stream already advanced to counter c continues exactly: draw k of the stream
+    (key, c) is draw k of the fresh stream key + c * G (rng.py:38-51).
     """
     dg = as_device_graph(g)
     deg = dg.degree(int(v))
     dev = dg.device
-    if rng.counter != 0:
-        raise NotImplementedError("device sample_neighbors needs a fresh CounterRng")
     slots = DeviceGraph(1, torch.tensor([0, deg], dtype=torch.int64, device=dev),
                         torch.arange(max(deg, 1), dtype=torch.int32, device=dev)[:deg])
     idm = IdMap(device=dev, size_hint=1)
     idm.insert([0])
     draws = torch.zeros(1, dtype=torch.int32, device=dev)
-    # key_0 = fmix(prefix ^ 0) must equal rng.key -> prefix = fmix^-1(key)
-    layer = _hop(slots, idm, 1, int(d), _fmix_inverse(rng.key), draws=draws)
+    # key_0 = fmix(prefix ^ 0) must equal the continued key -> prefix = fmix^-1(key)
+    key = (rng.key + rng.counter * _G) & MASK64
+    layer = _hop(slots, idm, 1, int(d), _fmix_inverse(key), draws=draws)
     gids = idm.global_ids.cpu().numpy().astype(np.int64)
     rng.counter += int(draws.item())
     return gids[layer.src_local.cpu().numpy()]

@@ -120,6 +120,12 @@ def _model_width(dg: DeviceGraph) -> int:
     return fp
 
 
+def philox_epoch_seed(global_seed: int, epoch: int) -> int:
+    """The Philox key of one training epoch: splitmix64 of (global_seed, epoch)."""
+    from .sampler import MASK64, _fmix
+    return _fmix((global_seed ^ _fmix((epoch + 0x9E3779B97F4A7C15) & MASK64)) & MASK64)
+
+
 def _fusable(dg: DeviceGraph, cfg: TrainConfig) -> bool:
     """sal_sample_aggregate's shape limits: fp16 table rows of 16-byte multiples up to
     256 bytes, last-hop fanout <= 32, 16-bit activations."""
@@ -229,6 +235,7 @@ class Trainer:
         self.compute_stream = (torch.cuda.Stream(device=self.device, priority=cfg.compute_priority)
                                if cfg.compute_priority != 0 else None)
         self.policy = RNG_POLICIES[cfg.rng_policy]
+        self.sample_seed = cfg.global_seed
         self.x_table = _model_table(dg)
         self.cursor = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.step_ctr = torch.zeros(1, dtype=torch.int64, device=self.device)
@@ -271,6 +278,14 @@ class Trainer:
         self.perm_host = perm
         self.epoch = epoch
         self.plan = plan
+        if self.cfg.rng_policy == "philox":
+            # Philox streams are keyed on (seed, epoch) x (draw, node, hop, batch): a new
+            # key each epoch (the graphs hold it by value, so they are re-captured);
+            # splitmix keeps the reference's (global_seed, batch_id, hop) keying
+            seed = philox_epoch_seed(self.cfg.global_seed, epoch)
+            if seed != self.sample_seed:
+                self.sample_seed = seed
+                self.graphs.clear()
         self.cursor.zero_()
         self.step_ctr.zero_()
         return self.steps_per_epoch
@@ -289,13 +304,13 @@ class Trainer:
                                        self.cursor.data_ptr(), slot.desc.data_ptr(),
                                        _lib.stream_ptr(st)), "plan_next")
             desc, seeds_base = slot.desc, self.seeds_all
-        ws.run(self.dg, seeds_base, desc, self.cfg.global_seed, self.policy, st)
+        ws.run(self.dg, seeds_base, desc, self.sample_seed, self.policy, st)
         slot.desc_used = desc
         nh = self.nh
         f, fx = self.model.dims[0], self.x_table.shape[1]
         if slot.fused:
             if self.cfg.fused_on_prep:  # last hop -> layer-0 [mean | self] in one pass
-                ws.aggregate(self.dg, self.x_table, slot.feats, f, desc, self.cfg.global_seed,
+                ws.aggregate(self.dg, self.x_table, slot.feats, f, desc, self.sample_seed,
                              self.policy, st)
         else:
             rows = ws.node_cap[nh] if not self.cfg.gather_free else ws.node_cap[nh - 1]
@@ -359,11 +374,11 @@ class Trainer:
                 xg = None
                 if not self.cfg.fused_on_prep:
                     slot.ws.aggregate(self.dg, self.x_table, slot.feats, m.dims[0],
-                                      slot.desc_used, self.cfg.global_seed, self.policy,
+                                      slot.desc_used, self.sample_seed, self.policy,
                                       torch.cuda.current_stream())
             head = m.head_ok()
             logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg,
-                                      salt=self.step_ctr, head=head, mean0_ready=slot.fused)
+                                      salt=m.t, head=head, mean0_ready=slot.fused)
             if late is not None:
                 torch.cuda.current_stream().wait_stream(late)
             if head:  # output layer + loss on tcgen05, then the backward of every layer

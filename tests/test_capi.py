@@ -65,3 +65,22 @@ def test_plan_small_graph_caps_clip():
     assert list(plan.node_cap)[:3] == [64, 100, 100]
     rc = L.sal_mfg_plan_init(ctypes.byref(plan), 1, (ctypes.c_int32 * 1)(-1), 8, 100)
     assert rc == -1
+
+
+def test_invalid_arguments_set_the_error_message():
+    """Every SAL_EINVAL comes with its own sal_last_error() message (checked on entry
+    points that validate before touching the device)."""
+    L = _lib.lib()
+    cases = [
+        (lambda: L.sal_zero_spans(None, None, 9, None), "zero_spans"),
+        (lambda: L.sal_argmax_correct(None, 0, 1, 10, _lib.SAL_BF16, None, None, None, None),
+         "argmax_correct"),
+        (lambda: L.sal_mean_bwd(None, 8, _lib.SAL_BF16, 8, 0, None, None, None, None, None, None,
+                                0, None, None, 0.0, None, 8, _lib.SAL_BF16, None), "mean_bwd"),
+        (lambda: L.sal_sample_aggregate(None, None, None, None, None, 0, 0, None, 0, 0, 0, None,
+                                        0, 0, 0, None), "sample_aggregate"),
+    ]
+    for call, name in cases:
+        L.sal_zero_spans(None, None, 0, None)   # a successful call in between
+        assert call() == -1                     # SAL_EINVAL
+        assert name in L.sal_last_error().decode(), name

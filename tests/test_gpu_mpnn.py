@@ -79,6 +79,11 @@ def test_mfg_forward_matches_reference(prep_small):
     assert np.array_equal(ws[0].w_self, z["fwd_w0"][0])
     got = mfg_forward(pb.mfg, pb.features, ws).cpu().numpy()
     assert np.max(np.abs(got - z["fwd"])) <= 1e-6
+    # the global-index path (reference mpnn.py:86-111) agrees with the golden too
+    from paper_2110_08450_b200 import sampled_reference_forward
+    glob = sampled_reference_forward(pb.mfg, fm.data.astype(np.float32), ws).cpu().numpy()
+    assert np.max(np.abs(glob - z["fwd"])) <= 1e-6
+    assert np.max(np.abs(glob - got)) <= 1e-6
 
 
 def test_unbounded_fanout_matches_full_forward():

@@ -94,6 +94,38 @@ def test_prepare_batch_digest_and_bytes_vs_reference(data13, prep_small):
     assert pb.stats == tuple((l.num_dst, l.num_src, l.num_edges) for l in pb.mfg.layers)
 
 
+def test_prepare_batch_sized_buffers_and_caller_slot(data13, prep_small):
+    """prepare_batch sizes its feature rows to the MFG (reference _Slot.reserve), and a
+    caller-kept slot gives the same batch; a slot built for other fanouts is refused."""
+    g, dg, _, fm16, y = data13
+    z = prep_small
+    plan = make_epoch_plan(np.arange(1000), 128, 5)
+    fan = FanoutSpec((15, 10, 5))
+    pb = prepare_batch(dg, fm16, y, plan.batches[0], fan, SamplerVariant(), 42)
+    assert pb.features.shape[0] == pb.num_nodes    # exact, not the worst-case capacity
+    slot = prep_mod._Slot(dg, PrepConfig(fanouts=fan), 128, fm16.cols, dg.device)
+    for _ in range(2):   # reusable
+        pb2 = prepare_batch(dg, fm16, y, plan.batches[0], fan, SamplerVariant(), 42, slot=slot)
+        assert pb2.digest() == str(z["pb_digest"])
+    with pytest.raises(ValueError):
+        prepare_batch(dg, fm16, y, plan.batches[0], FanoutSpec((3, 3)), SamplerVariant(), 42,
+                      slot=slot)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_completion_order_delivery(data13, prep_small, P):
+    """delivery='completion_order' (reference prep.py:289-305): every batch exactly once,
+    each with the digest it has in plan order."""
+    g, dg, fm32, fm16, y = data13
+    z = prep_small
+    plan = make_epoch_plan(np.arange(1000), 128, 5)
+    run = run_epoch_prep(dg, fm16, y, plan, PrepConfig(num_workers=P, delivery="completion_order",
+                                                       fanouts=FanoutSpec((15, 10, 5))), 42)
+    got = {b.mfg.seeds.batch_id: b.digest() for b in run}
+    assert sorted(got) == list(range(8))
+    assert [got[i] for i in range(8)] == [str(d) for d in z["digests16"]]
+
+
 @pytest.mark.parametrize("P", [1, 2, 4])
 def test_epoch_digests_match_reference_any_depth(data13, prep_small, P):
     g, dg, fm32, fm16, y = data13

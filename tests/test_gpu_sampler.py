@@ -141,6 +141,29 @@ def test_sample_neighbors_vs_reference_oracle(small_graph, dg_small):
             assert set(draws) == set(want) and draws[-1] == want[-1]
 
 
+def test_sample_neighbors_continues_an_advanced_stream(small_graph, dg_small):
+    """Several calls on one CounterRng (reference sampler.py:253-273): each call picks
+    up the stream where the previous one left it, exactly like the host loop."""
+    def host_sample(deg, d, rng):   # the reference's sequential rejection sampler
+        if deg <= d:
+            return list(range(deg))
+        seen, out = set(), []
+        while len(out) < d:
+            pos = rng.next_below(deg)
+            if pos not in seen:
+                seen.add(pos)
+                out.append(pos)
+        return out
+
+    for v in (v for v in range(0, 400, 3) if small_graph.degree(v) > 3):
+        key = stream_key(7, 1, 2, v)
+        dev, host = CounterRng(key), CounterRng(key)
+        for _ in range(3):
+            got = sample_neighbors(dg_small, v, 3, dev)
+            assert got.tolist() == host_sample(small_graph.degree(v), 3, host)
+            assert dev.counter == host.counter
+
+
 def test_large_fanout_path(dg_small, small_graph):
     """fanout > 32 (global-memory accepted set) vs oracle."""
     seeds = SeedBatch(4, np.arange(0, 1000, 9))
@@ -258,3 +281,69 @@ def test_last_hop_edges_only_matches_full_sample(fan):
         assert torch.equal(edg.src_glob[:ef[L - 1]], want)
         with pytest.raises(ValueError):
             edg.to_mfg(b)
+
+
+def _star_forest(k: int, degs: np.ndarray):
+    """k hubs (ids 0..k-1), hub i linked to degs[i] private leaves, as a device CSR."""
+    n = k + int(degs.sum())
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:k + 1] = np.cumsum(degs)
+    indptr[k + 1:] = indptr[k]
+    indices = (k + np.arange(int(degs.sum()))).astype(np.int32)
+    return DeviceGraph(n, torch.from_numpy(indptr).cuda(), torch.from_numpy(indices).cuda()), indptr
+
+
+def _sampled_positions(dg, indptr, k, f, policy, batch_id=0, seed=5):
+    """Slot positions sampled for hubs 0..k-1 in one hop (one batch of k seeds)."""
+    m = multihop_mfg(dg, SeedBatch(batch_id, np.arange(k)), FanoutSpec((f,)), seed,
+                     rng_policy=policy)
+    gids, layers = m.to_host()
+    ip, src = layers[0]["indptr"], gids[layers[0]["src_local"]]
+    pos = src - k - indptr[np.repeat(np.arange(k), np.diff(ip))]
+    return [pos[ip[i]:ip[i + 1]] for i in range(k)]
+
+
+@pytest.mark.parametrize("policy", ["philox", "splitmix"])
+def test_subset_frequencies_chi2(policy):
+    """Joint uniformity, not just marginals: 20,000 nodes of degree 6 at fanout 3 —
+    each of the C(6,3) = 20 subsets must come up equally often (chi-square, 19 dof,
+    p > 1e-4), and each node's sample is 3 distinct positions.  A sampler drawing a
+    random contiguous window (uniform marginals) fails this."""
+    from itertools import combinations
+    from scipy import stats
+    k, d, f = 20_000, 6, 3
+    dg, indptr = _star_forest(k, np.full(k, d))
+    idx = {c: i for i, c in enumerate(combinations(range(d), f))}
+    counts = np.zeros(len(idx), dtype=np.int64)
+    for p in _sampled_positions(dg, indptr, k, f, policy):
+        assert len(set(p.tolist())) == f
+        counts[idx[tuple(sorted(p.tolist()))]] += 1
+    assert stats.chisquare(counts).pvalue > 1e-4, counts
+
+
+@pytest.mark.parametrize("policy", ["philox", "splitmix"])
+def test_pairwise_inclusion_by_degree(policy):
+    """Pairwise inclusion over nodes of degree 4..12 at fanout 3: P(i and j both
+    sampled) = f(f-1) / (d(d-1)) for every pair of slots (uniform sampling without
+    replacement); chi-square per degree over the C(d,2) pair counts, plus the
+    first-order rate f/d per slot."""
+    from scipy import stats
+    f, per = 3, 3000
+    degs = np.repeat(np.arange(4, 13), per)
+    k = len(degs)
+    dg, indptr = _star_forest(k, degs)
+    samples = _sampled_positions(dg, indptr, k, f, policy, batch_id=3, seed=9)
+    for d in range(4, 13):
+        pair = np.zeros((d, d), dtype=np.int64)
+        single = np.zeros(d, dtype=np.int64)
+        for i in np.nonzero(degs == d)[0]:
+            p = np.sort(samples[i])
+            single[p] += 1
+            for a in range(f):
+                for b in range(a + 1, f):
+                    pair[p[a], p[b]] += 1
+        iu = np.triu_indices(d, 1)
+        obs = pair[iu]
+        assert obs.sum() == per * f * (f - 1) // 2
+        assert stats.chisquare(obs).pvalue > 1e-4, (d, obs)
+        assert stats.chisquare(single).pvalue > 1e-4, (d, single)

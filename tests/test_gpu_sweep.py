@@ -7,7 +7,7 @@ import pytest
 from conftest import GOLDEN, golden
 from paper_2110_08450_b200 import DeviceGraph, FanoutSpec, SeedBatch
 from paper_2110_08450_b200.graph import CsrGraph
-from paper_2110_08450_b200 import sweep as S
+from paper_2110_08450_b200 import harness as S
 
 pytestmark = pytest.mark.gpu
 TRACE = GOLDEN / "files" / "trace.trce"

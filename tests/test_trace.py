@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from conftest import GOLDEN, golden
-from paper_2110_08450_b200 import sweep as S
+from paper_2110_08450_b200 import harness as S
 from paper_2110_08450_b200 import files as F
 
 TRACE = GOLDEN / "files" / "trace.trce"

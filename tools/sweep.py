@@ -19,7 +19,7 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 from paper_2110_08450_b200 import FanoutSpec, make_epoch_plan  # noqa: E402
-from paper_2110_08450_b200 import sweep as S  # noqa: E402
+from paper_2110_08450_b200 import harness as S  # noqa: E402
 
 
 def main():
