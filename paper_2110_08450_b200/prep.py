@@ -70,6 +70,9 @@ class PrepConfig:
     delivery: str = "in_order"
     feature_dtype: str = "f32"      # output dtype of the sliced features
     rng_policy: str = "splitmix"
+    # each batch as two CUDA-graph replays (sample | slice) instead of ~15 host launches;
+    # the slots, streams and graphs of a run are kept for the next run of the same shape
+    graphs: bool = True
 
     def __post_init__(self):
         if self.num_workers < 1:
@@ -352,6 +355,87 @@ class PrepReport:
         return "threads,sampling_s,slicing_s,both_s"
 
 
+class _EpochResources:
+    """Slots, streams, plan buffers and per-slot CUDA graphs of one run shape, kept
+    across runs of the same (graph, features, labels, config, seed): a second epoch
+    allocates nothing and captures nothing."""
+
+    def __init__(self, dg, x, yv, cfg: PrepConfig, max_seeds: int, cols: int, n_ids: int,
+                 nb: int, global_seed: int):
+        dev = dg.device
+        self.depth = cfg.depth
+        self.slots = [_Slot(dg, cfg, max_seeds, cols, dev) for _ in range(self.depth + 1)]
+        self.streams = [torch.cuda.Stream(device=dev)
+                        for _ in range(max(1, min(cfg.num_workers, self.depth)))]
+        # plan buffers with headroom (the graphs hold their addresses): any epoch of up
+        # to 2048 batches reuses them
+        nb_cap = max(nb, 2048)
+        ids_cap = max(n_ids, min(nb_cap * max_seeds, 1 << 24))
+        self.seeds_all = torch.zeros(max(ids_cap, 1), dtype=torch.int64, device=dev)
+        self.desc_all = torch.zeros((nb_cap, 3), dtype=torch.int64, device=dev)
+        self.max_seeds = max_seeds
+        self.graphed = False
+
+    def fits(self, max_seeds: int, n_ids: int, nb: int) -> bool:
+        return (max_seeds <= self.max_seeds and n_ids <= self.seeds_all.numel()
+                and nb <= self.desc_all.shape[0])
+
+    def capture(self, dg, x, yv, global_seed: int, policy: int) -> None:
+        """Per slot: g_sample = {plan cursor -> slot desc, MFG build}, g_slice = {row
+        gather, labels, extents D2H}.  The cursor (one int64) is the only per-batch input."""
+        n_cap = self.desc_all.shape[0]
+        L = _lib.lib()
+        torch.cuda.synchronize()
+        for slot in self.slots:
+            ws = slot.ws
+            slot.cursor = torch.zeros(1, dtype=torch.int64, device=ws.device)
+            slot.cursor_host = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+            slot.gdesc = torch.zeros(3, dtype=torch.int64, device=ws.device)
+            nh = ws.num_hops
+            gs, gl = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gs):
+                _lib.check(L.sal_plan_next(self.desc_all.data_ptr(), n_cap,
+                                           slot.cursor.data_ptr(), slot.gdesc.data_ptr(),
+                                           _lib.stream_ptr()), "plan_next")
+                ws.run(dg, self.seeds_all, slot.gdesc, global_seed, policy)
+            with torch.cuda.graph(gl):
+                if x is not None:
+                    gather_rows(x, ws.globals, slot.features[:, :x.shape[1]], n=ws.node_cap[-1],
+                                n_dev=ws.sizes[nh:nh + 1])
+                if yv is not None and self.max_seeds:
+                    _lib.check(L.sal_gather_labels(yv.data_ptr(), self.seeds_all.data_ptr(),
+                                                   slot.gdesc.data_ptr(), self.max_seeds,
+                                                   slot.labels.data_ptr(), _lib.stream_ptr()),
+                               "gather_labels")
+                slot.extents[:nh + 1].copy_(ws.sizes, non_blocking=True)
+                slot.extents[nh + 1:].copy_(ws.etot, non_blocking=True)
+            slot.g_sample, slot.g_slice = gs, gl
+        torch.cuda.synchronize()
+        self.graphed = True
+
+
+_RES_CACHE: dict = {}
+
+
+def release_prep_cache() -> None:
+    """Free the slots and graphs run_epoch_prep keeps for the next run."""
+    _RES_CACHE.clear()
+
+
+def _resources(dg, x, yv, cfg: PrepConfig, max_seeds: int, cols: int, n_ids: int, nb: int,
+               global_seed: int) -> _EpochResources:
+    key = (id(dg), None if x is None else (x.data_ptr(), tuple(x.shape), x.stride(0), x.dtype),
+           None if yv is None else yv.data_ptr(), tuple(cfg.fanouts.per_hop), cfg.feature_dtype,
+           cfg.rng_policy, cfg.depth, cfg.num_workers, global_seed)
+    res = _RES_CACHE.get(key)
+    if res is None or not res.fits(max_seeds, n_ids, nb):
+        _RES_CACHE.clear()   # one shape at a time: slots hold worst-case buffers
+        res = _EpochResources(dg, x, yv, cfg, max_seeds, cols, n_ids, nb, global_seed)
+        res.refs = (dg, x, yv)   # keep the captured pointers alive
+        _RES_CACHE[key] = res
+    return res
+
+
 class EpochPrepRun:
     """Iterable over an epoch's PreparedBatches (prep.py:226-334)."""
 
@@ -380,23 +464,37 @@ class EpochPrepRun:
             return
         max_seeds = max(len(b) for b in plan.batches)
         depth = cfg.depth
-        slots = [_Slot(dg, cfg, max_seeds, cols, dg.device) for _ in range(depth + 1)]
-        self._free = list(slots)
-        # num_workers batches are prepared concurrently, one CUDA stream each (the
-        # reference's P worker threads, prep.py:255-287)
-        streams = [torch.cuda.Stream(device=dg.device)
-                   for _ in range(max(1, min(cfg.num_workers, depth)))]
+        policy = RNG_POLICIES[cfg.rng_policy]
         # the whole plan goes to HBM once: seeds + one sal_batch_desc per batch
         lens = np.array([len(b) for b in plan.batches], dtype=np.int64)
         offs = np.zeros(nb, dtype=np.int64)
         offs[1:] = np.cumsum(lens)[:-1]
         descs = np.stack([np.array([b.batch_id for b in plan.batches], dtype=np.int64), offs,
                           lens], axis=1)
-        seeds_all = torch.from_numpy(np.concatenate([b.dst_ids for b in plan.batches])
-                                     if lens.sum() else np.zeros(1, np.int64)).to(dg.device)
-        desc_all = torch.from_numpy(np.ascontiguousarray(descs)).to(dg.device)
+        n_ids = int(lens.sum())
+        if cfg.graphs:
+            res = _resources(dg, x, yv, cfg, max_seeds, cols, n_ids, nb, self._seed)
+            slots, streams = res.slots, res.streams
+            seeds_all, desc_all = res.seeds_all, res.desc_all
+        else:
+            res = None
+            slots = [_Slot(dg, cfg, max_seeds, cols, dg.device) for _ in range(depth + 1)]
+            # num_workers batches are prepared concurrently, one CUDA stream each (the
+            # reference's P worker threads, prep.py:255-287)
+            streams = [torch.cuda.Stream(device=dg.device)
+                       for _ in range(max(1, min(cfg.num_workers, depth)))]
+            seeds_all = torch.zeros(max(n_ids, 1), dtype=torch.int64, device=dg.device)
+            desc_all = torch.zeros((nb, 3), dtype=torch.int64, device=dg.device)
+        if n_ids:
+            seeds_all[:n_ids].copy_(torch.from_numpy(np.concatenate([b.dst_ids
+                                                                     for b in plan.batches])))
+        desc_all[:nb].copy_(torch.from_numpy(np.ascontiguousarray(descs)))
+        if res is not None and not res.graphed:
+            res.capture(dg, x, yv, self._seed, policy)
+        for st in streams:   # plan uploads (current stream) before any replay reads them
+            st.wait_stream(torch.cuda.current_stream())
+        self._free = list(slots)
         pending = []
-        policy = RNG_POLICIES[cfg.rng_policy]
         nxt = 0
 
         def launch():
@@ -405,7 +503,8 @@ class EpochPrepRun:
             slot.index = nxt
             try:
                 _prep_one(dg, x, yv, slot, plan.batches[nxt], seeds_all, desc_all[nxt],
-                          self._seed, policy, streams[nxt % len(streams)])
+                          self._seed, policy, streams[nxt % len(streams)],
+                          cursor=nxt if res is not None else None)
             except Exception as exc:
                 raise RuntimeError("batch preparation worker failed") from exc
             pending.append(slot)
@@ -446,9 +545,24 @@ class EpochPrepRun:
             self.report.both_s = time.perf_counter() - t0
 
 
-def _prep_one(dg, x, yv, slot, seeds, seeds_base, desc, global_seed, policy, stream):
-    """Per-batch work item (module-level so tests can inject failures)."""
-    _prep_into_slot(dg, x, yv, slot, seeds, seeds_base, desc, global_seed, policy, stream)
+def _prep_one(dg, x, yv, slot, seeds, seeds_base, desc, global_seed, policy, stream,
+              cursor=None):
+    """Per-batch work item (module-level so tests can inject failures): the slot's two
+    graph replays behind a one-word cursor upload, or (cursor None) the direct launches."""
+    if cursor is None:
+        _prep_into_slot(dg, x, yv, slot, seeds, seeds_base, desc, global_seed, policy, stream)
+        return
+    with torch.cuda.stream(stream):
+        stream.wait_event(slot.free)
+        slot.cursor_host[0] = cursor
+        slot.cursor.copy_(slot.cursor_host, non_blocking=True)
+        slot.ev[0].record(stream)
+        slot.g_sample.replay()
+        slot.ev[1].record(stream)
+        slot.g_slice.replay()
+        slot.ev[2].record(stream)
+        slot.done.record(stream)
+    slot.seeds = seeds
 
 
 def run_epoch_prep(g, fm, y, plan: EpochPlan, cfg: PrepConfig, global_seed: int) -> EpochPrepRun:
