@@ -331,6 +331,14 @@ int sal_adam_step(float* param_dev, float* grad_dev, float* m_dev, float* v_dev,
                   const int64_t* t_dev, int32_t zero_grad, void* stream);
 /* per-step bookkeeping: *last = *loss; log[*step] = *loss; *loss = 0 (ready
  * for the next step's accumulation); ++*step; ++*adam_t */
+/* sal_adam_step (vectorised: n % 4 == 0, 16-byte aligned) and sal_step_tail in one
+ * launch: the last block to finish does the bookkeeping (ticket_dev: one zeroed
+ * uint32 the kernel leaves zeroed) */
+int sal_adam_step_tail(float* param_dev, float* grad_dev, float* m_dev, float* v_dev,
+                       void* shadow_bf16_dev, int64_t n, float lr, float beta1, float beta2,
+                       float eps, int64_t* t_dev, int32_t zero_grad, float* loss_dev,
+                       float* last_dev, float* log_dev, int64_t log_len, int64_t* step_dev,
+                       unsigned int* ticket_dev, void* stream);
 int sal_step_tail(float* loss_dev, float* last_dev, float* log_dev, int64_t log_len,
                   int64_t* step_dev, int64_t* adam_t_dev, void* stream);
 

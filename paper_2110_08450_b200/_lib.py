@@ -123,6 +123,9 @@ SIGNATURES = {
                                       ctypes.c_float, vp, i64, i32, vp]),
     "sal_mean_bwd_t_live": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp, vp,
                                            ctypes.c_float, vp, i64, i32, vp]),
+    "sal_adam_step_tail": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, ctypes.c_float, ctypes.c_float,
+                                          ctypes.c_float, ctypes.c_float, vp, i32, vp, vp, vp,
+                                          i64, vp, vp, vp]),
     "sal_adam_step": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, ctypes.c_float, ctypes.c_float,
                                      ctypes.c_float, ctypes.c_float, vp, i32, vp]),
     "sal_step_tail": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),

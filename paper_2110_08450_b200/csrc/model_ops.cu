@@ -696,6 +696,52 @@ __global__ void adam4_kernel(float4* __restrict__ p, float4* __restrict__ g,
   }
 }
 
+// adam4_kernel + step_tail_kernel in one launch: the block that finishes last (a
+// ticket counter, reset by that block) does the per-step bookkeeping, after every
+// block has read the step count it increments
+__global__ void adam4_tail_kernel(float4* __restrict__ p, float4* __restrict__ g,
+                                  float4* __restrict__ m, float4* __restrict__ v,
+                                  uint2* __restrict__ shadow, int64_t n4, float lr, float b1,
+                                  float b2, float eps, int64_t* __restrict__ t_dev, int zero_grad,
+                                  float* __restrict__ loss, float* __restrict__ last,
+                                  float* __restrict__ log, int64_t log_len,
+                                  int64_t* __restrict__ step, unsigned int* __restrict__ ticket) {
+  const float t = (float)(*t_dev + 1);
+  const float stp = lr / (1.f - __powf(b1, t));
+  const float rbc2 = rsqrtf(1.f - __powf(b2, t));
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 pi = p[i], gi = g[i], mi = m[i], vi = v[i];
+    adam_elem(pi.x, gi.x, mi.x, vi.x, b1, b2, stp, rbc2, eps, zero_grad);
+    adam_elem(pi.y, gi.y, mi.y, vi.y, b1, b2, stp, rbc2, eps, zero_grad);
+    adam_elem(pi.z, gi.z, mi.z, vi.z, b1, b2, stp, rbc2, eps, zero_grad);
+    adam_elem(pi.w, gi.w, mi.w, vi.w, b1, b2, stp, rbc2, eps, zero_grad);
+    p[i] = pi;
+    m[i] = mi;
+    v[i] = vi;
+    if (zero_grad) g[i] = gi;
+    if (shadow) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(pi.x, pi.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(pi.z, pi.w);
+      shadow[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ticket, 1u) == gridDim.x - 1) {   // every block has read *t_dev
+      *ticket = 0;
+      const int64_t s = *step;
+      const float l = *loss;
+      *loss = 0.f;
+      *last = l;
+      if (s >= 0 && s < log_len) log[s] = l;
+      *step = s + 1;
+      *t_dev += 1;
+    }
+  }
+}
+
 __global__ void step_tail_kernel(float* __restrict__ loss, float* __restrict__ last,
                                  float* __restrict__ log, int64_t log_len,
                                  int64_t* __restrict__ step, int64_t* __restrict__ adam_t) {
@@ -975,6 +1021,23 @@ int sal_zero_spans(void* const* ptrs, const int64_t* bytes, int32_t n, void* str
   }
   if (n == 0 || most == 0) return SAL_OK;
   zero_spans_kernel<<<sal::ew_grid(most), 256, 0, (cudaStream_t)stream>>>(z);
+  return sal::done(1);
+}
+
+int sal_adam_step_tail(float* param, float* grad, float* m, float* v, void* shadow_bf16,
+                       int64_t n, float lr, float beta1, float beta2, float eps, int64_t* t_dev,
+                       int32_t zero_grad, float* loss, float* last, float* log, int64_t log_len,
+                       int64_t* step, unsigned int* ticket_dev, void* stream) {
+  if (param == nullptr || grad == nullptr || m == nullptr || v == nullptr || t_dev == nullptr ||
+      loss == nullptr || last == nullptr || step == nullptr || ticket_dev == nullptr)
+    return sal::set_error(SAL_EINVAL, "adam_step_tail: null argument");
+  if (n % 4 != 0 ||
+      ((uintptr_t)param | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) % 16 != 0 ||
+      (uintptr_t)shadow_bf16 % 8 != 0)
+    return sal::set_error(SAL_EINVAL, "adam_step_tail: n %% 4 and 16-byte aligned buffers needed");
+  sal::adam4_tail_kernel<<<sal::ew_grid(n / 4), 256, 0, (cudaStream_t)stream>>>(
+      (float4*)param, (float4*)grad, (float4*)m, (float4*)v, (uint2*)shadow_bf16, n / 4, lr,
+      beta1, beta2, eps, t_dev, zero_grad, loss, last, log, log_len, step, ticket_dev);
   return sal::done(1);
 }
 

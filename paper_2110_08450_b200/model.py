@@ -396,16 +396,18 @@ class FusedSAGE:
                 if self._tc_wgrad_layer(i) or (i == self.L - 1 and self.head_ok())]
 
     def backward(self, dlogits: torch.Tensor, saved, transposes=None,
-                 grads_zeroed: bool = False) -> None:
+                 grads_zeroed: bool = False, t_events=None) -> None:
         """Writes every weight gradient into self.grad (overwrite semantics; with
         grads_zeroed the tcgen05 layers accumulate into blocks the caller zeroed).
 
         transposes[i] = (tindptr, tdst) reverse adjacency of layer i (i >= 1);
         built here when not supplied (the trainer builds them on the prep
-        stream)."""
-        self._backward_below(self.L - 1, dlogits, saved, transposes, grads_zeroed)
+        stream).  t_events[i]: an event the current stream waits on before it reads
+        transposes[i]."""
+        self._backward_below(self.L - 1, dlogits, saved, transposes, grads_zeroed, t_events)
 
-    def _backward_below(self, top: int, dz, saved, transposes, grads_zeroed: bool):
+    def _backward_below(self, top: int, dz, saved, transposes, grads_zeroed: bool,
+                        t_events=None):
         """Weight gradients of layers top..0 from dz of layer top, and the input
         gradients between them."""
         cs = torch.cuda.current_stream()
@@ -436,6 +438,8 @@ class FusedSAGE:
             if late:
                 fork_wgrad(i, dz)
                 forked = True
+            if t_events is not None:
+                cs.wait_event(t_events[i])
             dz = self._input_grad(i, dA, saved, transposes)
         if forked:
             cs.wait_stream(ws)
@@ -535,7 +539,8 @@ class FusedSAGE:
         return hb[0][:rows], hb[1]
 
     def loss_backward(self, saved, labels: torch.Tensor, out: torch.Tensor, transposes=None,
-                      grads_zeroed: bool = False, loss_zeroed: bool = False) -> torch.Tensor:
+                      grads_zeroed: bool = False, loss_zeroed: bool = False,
+                      t_events=None) -> torch.Tensor:
         """After forward(..., head=True): the output layer (logits in TMEM only, the loss
         *out += mean NLL, dlogits, its dA and dW) in one tcgen05 kernel, then the
         backward of the layers below.  grads_zeroed: the caller zeroed the tcgen05
@@ -560,8 +565,10 @@ class FusedSAGE:
             "tc_sage_head")
         if i == 0:
             return out
+        if t_events is not None:
+            torch.cuda.current_stream().wait_event(t_events[i])
         dz = self._input_grad(i, dA, saved, transposes)
-        self._backward_below(i - 1, dz, saved, transposes, grads_zeroed)
+        self._backward_below(i - 1, dz, saved, transposes, grads_zeroed, t_events)
         return out
 
     def score(self, saved, labels: torch.Tensor, counts: torch.Tensor) -> None:

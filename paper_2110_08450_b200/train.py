@@ -161,6 +161,9 @@ class _Slot:
         self.desc = torch.zeros(3, dtype=torch.int64, device=device)
         self.seeds = torch.zeros(max(cfg.batch_size, 1), dtype=torch.int64, device=device)
         self.desc_used = self.desc   # the descriptor the last prep read (fused last hop)
+        # late-stream milestones: labels + zeroed gradient blocks, reverse adjacency of layer i
+        self.ev_head = torch.cuda.Event()
+        self.ev_t = [torch.cuda.Event() for _ in range(ws.num_hops)]
         # reverse adjacency of layers i >= 1 (hop h = L-1-i), built on the prep stream
         L = _lib.lib()
         self.transposes = [None]
@@ -241,6 +244,7 @@ class Trainer:
         self.step_ctr = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.losses = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.last_loss = torch.zeros((), dtype=torch.float32, device=self.device)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=self.device)   # adam_step_tail
         self.graphs = {}
         self.graph_kernels = {}
         self.graph_allreduce = True    # NCCL all-reduce captured inside the step graph
@@ -330,12 +334,8 @@ class Trainer:
         nh = self.nh
         seeds_base = stage.dseeds if stage is not None else self.seeds_all
         desc = stage.ddesc if stage is not None else slot.desc
-        _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), seeds_base.data_ptr(),
-                                       desc.data_ptr(), self.cfg.batch_size,
-                                       slot.labels.data_ptr(), _lib.stream_ptr(st)),
-                   "gather_labels")
-        # reverse adjacency for the backward pass; every layer's count/scan workspace is
-        # zeroed by one kernel (no memset nodes in the captured chain)
+        # every layer's count/scan workspace and (zero_grads) the tcgen05 gradient blocks
+        # are zeroed by one kernel (no memset nodes in the captured chain)
         spans = [(t.data_ptr(), t.numel()) for t in slot.t_ws[1:]]
         if zero_grads:
             spans += self.model.tc_grad_spans()
@@ -345,11 +345,20 @@ class Trainer:
             nbytes = (ctypes.c_int64 * len(chunk))(*[b for _, b in chunk])
             _lib.check(L.sal_zero_spans(ptrs, nbytes, len(chunk), _lib.stream_ptr(st)),
                        "zero_spans")
-        for i in range(1, nh):
+        _lib.check(L.sal_gather_labels(self.dg.labels.data_ptr(), seeds_base.data_ptr(),
+                                       desc.data_ptr(), self.cfg.batch_size,
+                                       slot.labels.data_ptr(), _lib.stream_ptr(st)),
+                   "gather_labels")
+        # the output layer waits only for its labels and zeroed gradient block; each
+        # layer's input gradient waits only for its own reverse adjacency, built in the
+        # order the backward consumes them
+        slot.ev_head.record(st)
+        for i in reversed(range(1, nh)):
             h = nh - 1 - i
             build_transpose(ws.dst_indptr[h], ws.src_local[h], ws.sizes[h:h + 1], ws.node_cap[h],
                             ws.node_cap[h + 1], out=slot.transposes[i], ws=slot.t_ws[i],
                             ws_zeroed=True)
+            slot.ev_t[i].record(st)
 
     def _adjs(self, slot: _Slot):
         ws = slot.ws
@@ -379,17 +388,32 @@ class Trainer:
             head = m.head_ok()
             logits, saved = m.forward(slot.feats, self._adjs(slot), x_global=xg,
                                       salt=m.t, head=head, mean0_ready=slot.fused)
-            if late is not None:
-                torch.cuda.current_stream().wait_stream(late)
+            t_events = None
+            if late is not None:   # wait for each late-stream input where it is consumed
+                torch.cuda.current_stream().wait_event(slot.ev_head)
+                t_events = slot.ev_t
             if head:  # output layer + loss on tcgen05, then the backward of every layer
                 m.loss_backward(saved, slot.labels, self.loss_buf, slot.transposes,
-                                grads_zeroed=late is not None, loss_zeroed=True)
+                                grads_zeroed=late is not None, loss_zeroed=True,
+                                t_events=t_events)
             else:
                 loss, dlog = m.loss(logits, slot.labels, out=self.loss_buf, zeroed=True)
-                m.backward(dlog, saved, slot.transposes, grads_zeroed=late is not None)
+                m.backward(dlog, saved, slot.transposes, grads_zeroed=late is not None,
+                           t_events=t_events)
+            if late is not None:
+                torch.cuda.current_stream().wait_stream(late)
         if part == "all" and self.world > 1:
             allreduce_mean(m.grad, self.world)
         if part in ("all", "post"):
+            if m.act == torch.bfloat16 and m.flat.numel() % 4 == 0:
+                # Adam + the per-step bookkeeping in one launch
+                _lib.check(_lib.lib().sal_adam_step_tail(
+                    m.flat.data_ptr(), m.grad.data_ptr(), m.m.data_ptr(), m.v.data_ptr(),
+                    m.shadow.data_ptr(), m.flat.numel(), m.lr, m.betas[0], m.betas[1], m.eps,
+                    m.t.data_ptr(), 0, self.loss_buf.data_ptr(), self.last_loss.data_ptr(),
+                    self.losses.data_ptr(), self.losses.numel(), self.step_ctr.data_ptr(),
+                    self.ticket.data_ptr(), _lib.stream_ptr()), "adam_step_tail")
+                return
             m.adam_step()
             _lib.check(_lib.lib().sal_step_tail(self.loss_buf.data_ptr(),
                                                 self.last_loss.data_ptr(),
