@@ -74,7 +74,7 @@ SAL_DEVINL uint4 pack8(const float* f) {
   return *reinterpret_cast<const uint4*>(t);
 }
 
-constexpr int kSmThreads = 256;
+constexpr int kSmThreads = 128;   // 4 warps: finer shared-memory granularity per SM
 
 // 1/c for c = 0..32, the correctly rounded fp32 values 1.f / (float)c gives
 // (generated with numpy float32 division; hex literals are exact)
@@ -304,7 +304,7 @@ static int sample_mean_bps() {
   // resident blocks per SM: the shared-memory stages (8 warps x 2 stages) bound it
   const int per_block = (kSmThreads / 32) * 2 * stage_bytes<kRows>();
   const int b = (227 * 1024) / (per_block + 1024);
-  return b < 1 ? 1 : (b > 4 ? 4 : b);
+  return b < 1 ? 1 : (b > 8 ? 8 : b);
 }
 
 template <int kPolicy, typename TO, int kRows>
@@ -348,8 +348,16 @@ cudaError_t launch_sample_mean(const GraphDev& g, const int32_t* globals, const 
 #define SAL_SM(P, TO, R)                                                                   \
   return launch_sm<P, TO, R>(g, globals, n_dst, max_dst, fanout, hk, desc, table, t_stride, \
                              vpr, out, out_stride, self_off, size_unknown, st)
-#define SAL_SM_R(P, TO) \
-  if (fanout <= 16) { SAL_SM(P, TO, 16); } else { SAL_SM(P, TO, 32); }
+// stage rows: the smallest of 16 / 20 / 32 that holds the fanout (shared memory per
+// warp bounds the resident warps, and with them the rows in flight per SM)
+#define SAL_SM_R(P, TO)                 \
+  if (fanout <= 16) {                   \
+    SAL_SM(P, TO, 16);                  \
+  } else if (fanout <= 20) {            \
+    SAL_SM(P, TO, 20);                  \
+  } else {                              \
+    SAL_SM(P, TO, 32);                  \
+  }
   if (out_dtype == SAL_BF16) {
     if (policy == kRngSplitmix) { SAL_SM_R(kRngSplitmix, __nv_bfloat16); }
     else { SAL_SM_R(kRngPhilox, __nv_bfloat16); }
