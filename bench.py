@@ -309,6 +309,7 @@ def kernel_profile(trainer, nbatches: int):
     st = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     t_mfg = t_gat = t_mean = t_fhops = t_fused = 0.0
+    fused_checked = fused_equal = 0
     edges = nodes = e0 = d0 = 0
     mfg_bytes = 0
     x = trainer.x_table
@@ -347,6 +348,17 @@ def kernel_profile(trainer, nbatches: int):
         if fused:
             t_fhops += ev[3].elapsed_time(ev[4]) / 1e3
             t_fused += ev[4].elapsed_time(ev[5]) / 1e3
+            # the fused kernel against the two-kernel path on this batch: the same sample
+            # (the full MFG's last hop), the same summation order -> identical bf16 means;
+            # self rows = the table rows of the layer-0 destinations, converted
+            nd = sizes[h0]
+            fm = trainer.model.dims[0]
+            same = torch.equal(fout[:nd, :f].view(torch.int16), mean_buf[:nd].view(torch.int16))
+            want_self = x[ws.globals[:nd].long()].to(torch.bfloat16)
+            same = same and torch.equal(fout[:nd, fm:fm + f].view(torch.int16),
+                                        want_self.view(torch.int16))
+            fused_checked += 1
+            fused_equal += int(same)
         edges += sum(etot)
         nodes += sizes[-1]
         for h in range(L):  # SURVEY §8(d) MFG-build bytes per hop
@@ -419,7 +431,11 @@ def kernel_profile(trainer, nbatches: int):
         extra = {"fused_GBps": fused_bytes / t_fused / 1e9,
                  "fused_ms_per_launch": 1e3 * t_fused / k,
                  "fused_bytes_per_launch": fused_bytes / k,
-                 "fused_hops_ms_per_batch": 1e3 * t_fhops / k}
+                 "fused_hops_ms_per_batch": 1e3 * t_fhops / k,
+                 "fused_parity": {"batches": fused_checked, "equal": fused_equal,
+                                  "what": "sal_sample_aggregate output vs the layer-0 mean over "
+                                          "the full (reference-exact) MFG's last hop + the "
+                                          "destination rows, bit for bit"}}
     return {
         "sampled_edges_per_s": edges / t_mfg,
         "mfg_ms_per_batch": 1e3 * t_mfg / k,

@@ -2,7 +2,8 @@
 start offset, duration, stream, name — shows which chain is critical and where
 the gaps are.
 
-python tools/step_timeline.py [steps]   (under gpurun)
+python tools/step_timeline.py [steps] [--no-prep]   (under gpurun; --no-prep replays the
+step with the batch preparation removed: the training chain alone, stale inputs)
 """
 import sys
 from pathlib import Path
@@ -14,13 +15,21 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 from paper_2110_08450_b200.train import TrainConfig, Trainer  # noqa: E402
 
-steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+steps = int(args[0]) if args else 3
 dg, train, _, _ = bench.build_data("papers")
 tr = Trainer(dg, train, TrainConfig(gather_free=True))
 tr.set_epoch(0)
 tr.begin_epoch(False)
 tr.run_steps(0, 12)
 torch.cuda.synchronize()
+if "--no-prep" in sys.argv:
+    from paper_2110_08450_b200 import sampler
+    sampler.MfgWorkspace.run = lambda self, *a, **k: None
+    sampler.MfgWorkspace.aggregate = lambda self, *a, **k: None
+    tr.graphs.clear()
+    tr.run_steps(12, 4)
+    torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     tr.run_steps(12, steps)
     torch.cuda.synchronize()
