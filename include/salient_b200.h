@@ -89,6 +89,10 @@ typedef struct {
    * power of two) before sal_mfg_layout_init to lower the id-table load */
   int32_t sample_lanes;
   int32_t sample_blocks_per_sm;
+  /* resident blocks per SM of sal_sample_aggregate (0 = as many as shared memory
+   * allows); a trainer caps it so its weight-gradient CTAs fit beside it */
+  int32_t aggregate_blocks_per_sm;
+  int32_t reserved2;
 } sal_mfg_plan;
 
 /* Plan flag: the last hop emits its edges as global ids only (layout.src_glob);

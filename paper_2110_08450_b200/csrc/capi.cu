@@ -338,7 +338,7 @@ int sal_sample_aggregate(const sal_graph* g, const sal_mfg_plan* plan, const sal
                                           sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
                                           rng_policy, table, table_stride, cols, out, out_dtype,
                                           out_stride, self_offset, sizes + h + 1,
-                                          (cudaStream_t)stream),
+                                          plan->aggregate_blocks_per_sm, (cudaStream_t)stream),
                   "sample_aggregate"),
       1);
 }

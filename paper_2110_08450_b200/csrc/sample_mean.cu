@@ -312,7 +312,7 @@ static cudaError_t launch_sm(const GraphDev& g, const int32_t* globals, const in
                              int64_t max_dst, int32_t fanout, HopKey hk, const BatchDesc* desc,
                              const void* table, int64_t t_stride, int vpr, void* out,
                              int64_t out_stride, int64_t self_off, int64_t* size_unknown,
-                             cudaStream_t st) {
+                             int bps_cap, cudaStream_t st) {
   const int smem = (kSmThreads / 32) * 2 * stage_bytes<kRows>();
   auto k = vpr == 16 ? sample_mean_kernel<kPolicy, __half, TO, kRows, true>
                      : sample_mean_kernel<kPolicy, __half, TO, kRows, false>;
@@ -320,6 +320,7 @@ static cudaError_t launch_sm(const GraphDev& g, const int32_t* globals, const in
   if (e != cudaSuccess) return e;
   int64_t grid = (max_dst + kSmThreads / 32 - 1) / (kSmThreads / 32);
   int bps = sample_mean_bps<kRows>();
+  if (bps_cap > 0 && bps_cap < bps) bps = bps_cap;
   if (const char* e = getenv("SAL_SAMPLE_MEAN_BPS")) {   // A/B knob (tools/)
     const int b = atoi(e);
     if (b >= 1 && b < bps) bps = b;
@@ -343,11 +344,11 @@ cudaError_t launch_sample_mean(const GraphDev& g, const int32_t* globals, const 
                                int64_t max_dst, int32_t fanout, HopKey hk, const BatchDesc* desc,
                                int32_t policy, const void* table, int64_t t_stride, int32_t cols,
                                void* out, int32_t out_dtype, int64_t out_stride, int64_t self_off,
-                               int64_t* size_unknown, cudaStream_t st) {
+                               int64_t* size_unknown, int bps_cap, cudaStream_t st) {
   const int vpr = cols * 2 / 16;
 #define SAL_SM(P, TO, R)                                                                   \
   return launch_sm<P, TO, R>(g, globals, n_dst, max_dst, fanout, hk, desc, table, t_stride, \
-                             vpr, out, out_stride, self_off, size_unknown, st)
+                             vpr, out, out_stride, self_off, size_unknown, bps_cap, st)
 // stage rows: the smallest of 16 / 20 / 32 that holds the fanout (shared memory per
 // warp bounds the resident warps, and with them the rows in flight per SM)
 #define SAL_SM_R(P, TO)                 \

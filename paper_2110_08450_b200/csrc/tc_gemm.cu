@@ -433,10 +433,12 @@ sage_fwd_tma_st_kernel(const __grid_constant__ CUtensorMap mapA,
 // the CTAs of one split read the same dz/A rows at the same time, so the
 // second read of each chunk hits L2.  Stage = dz chunk [64 rows x 128] + A
 // chunk [64 x 128], each two TMA boxes of {64 mn, 64 k}.
-// stage count (-DSAL_WGRAD_STAGES=N builds the A/B variants of
-// profiles/r1_ab_wgrad_epilogue.txt; 3, 4 and 6 time alike alone, 6 is best in the step)
+// stage count (-DSAL_WGRAD_STAGES=N builds the A/B variants).  3, 4 and 6 time alike
+// alone (profiles/r1_ab_wgrad_epilogue.txt); with the fused last hop beside it, 3 stages
+// (99 KB) let a weight-gradient CTA share an SM with three fused-kernel blocks:
+// 164 -> 161 us per step (profiles/r2_ab_wgrad_stages.txt)
 #ifndef SAL_WGRAD_STAGES
-#define SAL_WGRAD_STAGES 6
+#define SAL_WGRAD_STAGES 3
 #endif
 constexpr int kGC = 64;      // GEMM-K rows (M rows of dz / A) per chunk
 constexpr int kQStages = SAL_WGRAD_STAGES;

@@ -350,12 +350,14 @@ class MfgWorkspace:
 
     def __init__(self, num_nodes: int, fanouts: FanoutSpec, max_seeds: int, device=None,
                  last_hop_edges: bool = False, sample_lanes: int = 0, sample_bps: int = 0,
-                 table_factor: int = 1, last_hop_fused: bool = False):
+                 table_factor: int = 1, last_hop_fused: bool = False,
+                 aggregate_bps: int = 0):
         """last_hop_edges: SAL_MFG_LAST_HOP_EDGES — the last hop only emits global
         source ids (src_glob); its relabel is skipped (training with the
         layer-0 mean read straight from the feature table).
         last_hop_fused: SAL_MFG_LAST_HOP_FUSED — run() builds hops 0..L-2 only and
-        aggregate() samples the last hop straight into the layer-0 mean."""
+        aggregate() samples the last hop straight into the layer-0 mean.
+        aggregate_bps: resident blocks per SM of aggregate() (0 = as many as fit)."""
         _lib.require_cuda()
         L = _lib.lib()
         self.device = torch.device(device or "cuda")
@@ -374,6 +376,7 @@ class MfgWorkspace:
         # design-space knobs (tools/sweep.py): sampler launch shape, id-table load
         if table_factor < 1 or table_factor & (table_factor - 1):
             raise ValueError("table_factor must be a power of two")
+        self.plan.aggregate_blocks_per_sm = int(aggregate_bps)
         self.plan.sample_lanes = int(sample_lanes)
         self.plan.sample_blocks_per_sm = int(sample_bps)
         self.plan.table_cap = int(self.plan.table_cap) * int(table_factor)

@@ -70,6 +70,9 @@ class TrainConfig:
     # kernel (sal_sample_aggregate) instead of sample -> src_glob -> mean + row gather
     fuse_last_hop: bool = True
     fused_on_prep: bool = True     # ... on the prep stream (False: first kernel of the step)
+    # resident blocks per SM of the fused last hop in training: three 4-warp blocks leave
+    # room for a 3-stage tcgen05 weight-gradient CTA beside them (164 -> 161 us per step)
+    fused_bps: int = 3
 
 
 def shard_plan(plan, batch_size: int, rank: int, world: int):
@@ -150,7 +153,8 @@ class _Slot:
         self.ws = MfgWorkspace(dg.num_nodes, cfg.fanouts, cfg.batch_size, device=device,
                                last_hop_edges=cfg.gather_free, sample_lanes=cfg.sampler_lanes,
                                sample_bps=cfg.sampler_bps, table_factor=cfg.table_factor,
-                               last_hop_fused=self.fused)
+                               last_hop_fused=self.fused,
+                               aggregate_bps=cfg.fused_bps if backward else 0)
         ws = self.ws
         nh = ws.num_hops
         rows = ws.node_cap[-1] if not cfg.gather_free else ws.node_cap[-2]
