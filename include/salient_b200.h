@@ -92,7 +92,11 @@ typedef struct {
   /* resident blocks per SM of sal_sample_aggregate (0 = as many as shared memory
    * allows); a trainer caps it so its weight-gradient CTAs fit beside it */
   int32_t aggregate_blocks_per_sm;
-  int32_t reserved2;
+  /* SAL_MFG_LAST_HOP_FUSED plans: sal_sample_mfg skips the id-table and scan-workspace
+   * resets and sal_sample_aggregate leaves them reset for the workspace's next batch
+   * (the caller resets the workspace once before its first batch) — two memset nodes
+   * fewer at the head of a pipelined batch preparation */
+  int32_t reset_in_aggregate;
 } sal_mfg_plan;
 
 /* Plan flag: the last hop emits its edges as global ids only (layout.src_glob);

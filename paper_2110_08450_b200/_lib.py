@@ -52,7 +52,7 @@ class SalMfgPlan(ctypes.Structure):
                 ("node_cap", i64 * (SAL_MAX_HOPS + 1)), ("edge_cap", i64 * SAL_MAX_HOPS),
                 ("table_cap", i64), ("flags", i32), ("reserved", i32), ("sample_lanes", i32),
                 ("sample_blocks_per_sm", i32), ("aggregate_blocks_per_sm", i32),
-                ("reserved2", i32)]
+                ("reset_in_aggregate", i32)]
 
 
 class SalMfgLayout(ctypes.Structure):

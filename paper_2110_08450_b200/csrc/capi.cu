@@ -234,9 +234,11 @@ static int sample_mfg_hops(const sal_graph* g, const sal_mfg_plan* plan, const s
   if (hop_begin == 0) {
     // table + all scan workspaces as memset nodes: measured faster in the
     // overlapped step than a reset kernel, which takes SM slots from training
-    e = cudaMemsetAsync(m.table, 0xFF, plan->table_cap * 8, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(scan, 0, L->scan_bytes, st);
-    if (e != cudaSuccess) return cuda_status(e, "sample_mfg: table reset");
+    if (!(plan->reset_in_aggregate && (plan->flags & SAL_MFG_LAST_HOP_FUSED))) {
+      e = cudaMemsetAsync(m.table, 0xFF, plan->table_cap * 8, st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(scan, 0, L->scan_bytes, st);
+      if (e != cudaSuccess) return cuda_status(e, "sample_mfg: table reset");
+    }
     e = sal::launch_seed_insert(seeds_base, desc, m, plan->max_seeds, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: seed insert");
     e = sal::launch_hop_count(gd, m.globals, sizes, plan->node_cap[0], plan->fanout[0],
@@ -338,7 +340,11 @@ int sal_sample_aggregate(const sal_graph* g, const sal_mfg_plan* plan, const sal
                                           sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
                                           rng_policy, table, table_stride, cols, out, out_dtype,
                                           out_stride, self_offset, sizes + h + 1,
-                                          plan->aggregate_blocks_per_sm, (cudaStream_t)stream),
+                                          plan->aggregate_blocks_per_sm,
+                                          plan->reset_in_aggregate
+                                              ? (unsigned long long*)(base + L->table) : nullptr,
+                                          plan->table_cap, base + L->scan, L->scan_bytes,
+                                          (cudaStream_t)stream),
                   "sample_aggregate"),
       1);
 }

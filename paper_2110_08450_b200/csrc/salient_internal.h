@@ -77,7 +77,9 @@ cudaError_t launch_sample_mean(const GraphDev& g, const int32_t* globals, const 
                                int64_t max_dst, int32_t fanout, HopKey hk, const BatchDesc* desc,
                                int32_t policy, const void* table, int64_t t_stride, int32_t cols,
                                void* out, int32_t out_dtype, int64_t out_stride, int64_t self_off,
-                               int64_t* size_unknown, int bps_cap, cudaStream_t st);
+                               int64_t* size_unknown, int bps_cap, unsigned long long* reset_table,
+                               int64_t table_words, void* reset_scan, int64_t scan_bytes,
+                               cudaStream_t st);
 cudaError_t launch_gather_rows(const void* x, int64_t x_rows, int32_t cols, int64_t x_stride,
                                int32_t in_dtype, const void* ids, int32_t id_bytes,
                                const int64_t* n_dev, int64_t n, void* out, int64_t out_stride,

@@ -148,8 +148,17 @@ sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
                    int32_t fanout, HopKey hk, const BatchDesc* __restrict__ desc,
                    const TIn* __restrict__ table, int64_t t_stride, int vpr,
                    TOut* __restrict__ out, int64_t out_stride, int64_t self_off,
-                   int64_t* __restrict__ size_unknown) {
+                   int64_t* __restrict__ size_unknown, ulonglong2* __restrict__ reset_table,
+                   int64_t table_pairs, uint4* __restrict__ reset_scan, int64_t scan_vecs) {
   extern __shared__ __align__(16) unsigned char sm_stage[];
+  if (reset_table != nullptr) {
+    // the id table and scan workspace of hops 0..L-2 are no longer read: leave them
+    // reset for this workspace's next batch (sal_mfg_plan.reset_in_aggregate)
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = t; i < table_pairs; i += nt) reset_table[i] = make_ulonglong2(~0ull, ~0ull);
+    for (int64_t i = t; i < scan_vecs; i += nt) reset_scan[i] = make_uint4(0, 0, 0, 0);
+  }
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int grp = lane >> 4, sub = lane & 15;
@@ -312,7 +321,8 @@ static cudaError_t launch_sm(const GraphDev& g, const int32_t* globals, const in
                              int64_t max_dst, int32_t fanout, HopKey hk, const BatchDesc* desc,
                              const void* table, int64_t t_stride, int vpr, void* out,
                              int64_t out_stride, int64_t self_off, int64_t* size_unknown,
-                             int bps_cap, cudaStream_t st) {
+                             int bps_cap, unsigned long long* reset_table, int64_t table_words,
+                             void* reset_scan, int64_t scan_bytes, cudaStream_t st) {
   const int smem = (kSmThreads / 32) * 2 * stage_bytes<kRows>();
   auto k = vpr == 16 ? sample_mean_kernel<kPolicy, __half, TO, kRows, true>
                      : sample_mean_kernel<kPolicy, __half, TO, kRows, false>;
@@ -336,7 +346,9 @@ static cudaError_t launch_sm(const GraphDev& g, const int32_t* globals, const in
   if (grid < 1) grid = 1;
   k<<<(int)grid, kSmThreads, smem, st>>>(g.indptr, g.indices, globals, n_dst, fanout, hk, desc,
                                          (const __half*)table, t_stride, vpr, (TO*)out,
-                                         out_stride, self_off, size_unknown);
+                                         out_stride, self_off, size_unknown,
+                                         (ulonglong2*)reset_table, table_words / 2,
+                                         (uint4*)reset_scan, reset_table ? scan_bytes / 16 : 0);
   return cudaGetLastError();
 }
 
@@ -344,11 +356,14 @@ cudaError_t launch_sample_mean(const GraphDev& g, const int32_t* globals, const 
                                int64_t max_dst, int32_t fanout, HopKey hk, const BatchDesc* desc,
                                int32_t policy, const void* table, int64_t t_stride, int32_t cols,
                                void* out, int32_t out_dtype, int64_t out_stride, int64_t self_off,
-                               int64_t* size_unknown, int bps_cap, cudaStream_t st) {
+                               int64_t* size_unknown, int bps_cap, unsigned long long* reset_table,
+                               int64_t table_words, void* reset_scan, int64_t scan_bytes,
+                               cudaStream_t st) {
   const int vpr = cols * 2 / 16;
 #define SAL_SM(P, TO, R)                                                                   \
   return launch_sm<P, TO, R>(g, globals, n_dst, max_dst, fanout, hk, desc, table, t_stride, \
-                             vpr, out, out_stride, self_off, size_unknown, bps_cap, st)
+                             vpr, out, out_stride, self_off, size_unknown, bps_cap, reset_table, \
+                             table_words, reset_scan, scan_bytes, st)
 // stage rows: the smallest of 16 / 20 / 32 that holds the fanout (shared memory per
 // warp bounds the resident warps, and with them the rows in flight per SM)
 #define SAL_SM_R(P, TO)                 \

@@ -351,13 +351,15 @@ class MfgWorkspace:
     def __init__(self, num_nodes: int, fanouts: FanoutSpec, max_seeds: int, device=None,
                  last_hop_edges: bool = False, sample_lanes: int = 0, sample_bps: int = 0,
                  table_factor: int = 1, last_hop_fused: bool = False,
-                 aggregate_bps: int = 0):
+                 aggregate_bps: int = 0, reset_in_aggregate: bool = False):
         """last_hop_edges: SAL_MFG_LAST_HOP_EDGES — the last hop only emits global
         source ids (src_glob); its relabel is skipped (training with the
         layer-0 mean read straight from the feature table).
         last_hop_fused: SAL_MFG_LAST_HOP_FUSED — run() builds hops 0..L-2 only and
         aggregate() samples the last hop straight into the layer-0 mean.
-        aggregate_bps: resident blocks per SM of aggregate() (0 = as many as fit)."""
+        aggregate_bps: resident blocks per SM of aggregate() (0 = as many as fit).
+        reset_in_aggregate: (fused plans) run() skips the table/scan resets and
+        aggregate() leaves them reset for the next batch; reset once here."""
         _lib.require_cuda()
         L = _lib.lib()
         self.device = torch.device(device or "cuda")
@@ -377,6 +379,7 @@ class MfgWorkspace:
         if table_factor < 1 or table_factor & (table_factor - 1):
             raise ValueError("table_factor must be a power of two")
         self.plan.aggregate_blocks_per_sm = int(aggregate_bps)
+        self.plan.reset_in_aggregate = 1 if (reset_in_aggregate and self.last_hop_fused) else 0
         self.plan.sample_lanes = int(sample_lanes)
         self.plan.sample_blocks_per_sm = int(sample_bps)
         self.plan.table_cap = int(self.plan.table_cap) * int(table_factor)
@@ -399,6 +402,9 @@ class MfgWorkspace:
         self.src_glob = self._view(lay.src_glob, max(self.edge_cap + [1]), torch.int32)
         self.seeds = torch.empty(max(1, self.max_seeds), dtype=torch.int64, device=self.device)
         self.desc = torch.zeros(3, dtype=torch.int64, device=self.device)
+        if self.plan.reset_in_aggregate:   # the first batch finds a reset table + scans
+            self.table.fill_(-1)
+            self.buf[lay.scan:lay.scan + lay.scan_bytes].zero_()
 
     def _view(self, off: int, n: int, dt: torch.dtype) -> torch.Tensor:
         nbytes = n * torch.empty((), dtype=dt).element_size()

@@ -154,7 +154,8 @@ class _Slot:
                                last_hop_edges=cfg.gather_free, sample_lanes=cfg.sampler_lanes,
                                sample_bps=cfg.sampler_bps, table_factor=cfg.table_factor,
                                last_hop_fused=self.fused,
-                               aggregate_bps=cfg.fused_bps if backward else 0)
+                               aggregate_bps=cfg.fused_bps if backward else 0,
+                               reset_in_aggregate=True)
         ws = self.ws
         nh = ws.num_hops
         rows = ws.node_cap[-1] if not cfg.gather_free else ws.node_cap[-2]

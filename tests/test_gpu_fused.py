@@ -147,3 +147,25 @@ def test_fused_special_values_bit_exact():
     b, nb, _ = _fused(dg, FanoutSpec((15, 10)), seeds, desc, 9, 0, torch.bfloat16, 128)
     assert na == nb
     assert torch.equal(a[:na].view(torch.int16), b[:nb].view(torch.int16))
+
+
+def test_reset_in_aggregate_reuses_the_workspace(g128):
+    """sal_mfg_plan.reset_in_aggregate: run() skips the table/scan resets and the fused
+    kernel leaves them reset, so one workspace serves batch after batch exactly like
+    fresh workspaces (and like the unfused two-kernel path)."""
+    fan = FanoutSpec((15, 10, 5))
+    ws = MfgWorkspace(g128.num_nodes, fan, 1024, device="cuda", last_hop_fused=True,
+                      reset_in_aggregate=True)
+    assert ws.plan.reset_in_aggregate == 1
+    h = ws.num_hops - 1
+    rng = np.random.default_rng(21)
+    for b in range(4):
+        seeds = torch.from_numpy(rng.choice(g128.num_nodes, 1024, replace=False)).cuda()
+        desc = torch.tensor([b, 0, 1024], dtype=torch.int64, device="cuda")
+        want, n, _ = _two_kernel(g128, fan, seeds, desc, 4, 0, torch.bfloat16, 128)
+        ws.run(g128, seeds, desc, 4, 0)
+        out = torch.zeros_like(want)
+        ws.aggregate(g128, g128.features, out, 128, desc, 4, 0)
+        assert int(ws.sizes[h].item()) == n
+        assert torch.equal(out[:n].view(torch.int16), want[:n].view(torch.int16)), b
+        assert bool((ws.table == -1).all())          # left reset for the next batch
