@@ -119,12 +119,30 @@ SAL_DEVINL int sample_dst(const int32_t* __restrict__ indices, int d, int64_t lo
   return fanout;
 }
 
-SAL_DEVINL void cp_async16(uint32_t smem, const void* gmem, bool pred) {
+// 16 bytes global -> shared, L2 policy evict_first: every feature row is read once per
+// batch, so it should not push the step's reused tensors (the layer-0 input this
+// kernel writes, the backward's gradients) out of L2
+SAL_DEVINL void cp_async16(uint32_t smem, const void* gmem, bool pred, uint64_t policy) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
-      "@q cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(smem),
-      "l"(gmem), "r"((int)pred)
+      "@q cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %3;\n\t}" ::"r"(smem),
+      "l"(gmem), "r"((int)pred), "l"(policy)
       : "memory");
+}
+SAL_DEVINL void st_v4_policy(void* p, uint4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(policy)
+               : "memory");
+}
+SAL_DEVINL uint64_t l2_evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+SAL_DEVINL uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 SAL_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 SAL_DEVINL void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
@@ -187,15 +205,18 @@ sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
   int d = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (d >= n) return;
 
+  const uint64_t pol = l2_evict_first_policy();
+  // the [mean | self] rows are read again by the next step's layer-0 GEMM
+  const uint64_t pol_out = l2_evict_last_policy();
   auto issue_rows = [&](int stage, int32_t sid, int cnt, int32_t v) {
     const uint32_t sb = st0 + stage * stage_bytes<kRows>();
 #pragma unroll
     for (int u = 0; u < kRows / 2; ++u) {
       const int e = u * 2 + grp;
       const int id = __shfl_sync(0xffffffffu, sid, e);
-      cp_async16(sb + e * 256, tbase + (int64_t)id * tbytes, e < cnt && vlane);
+      cp_async16(sb + e * 256, tbase + (int64_t)id * tbytes, e < cnt && vlane, pol);
     }
-    cp_async16(sb + kRows * 256, tbase + (int64_t)v * tbytes, do_self);
+    cp_async16(sb + kRows * 256, tbase + (int64_t)v * tbytes, do_self, pol);
     cp_async_commit();
   };
   auto recip_of = [&](int64_t lo, int64_t hi) -> uint64_t {
@@ -280,7 +301,7 @@ sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
     TOut* orow = out + (int64_t)d * out_stride;
     if (vlane) {
       if (grp == 0) {
-        *reinterpret_cast<uint4*>(orow + sub * 8) = pack8<TOut>(acc);
+        st_v4_policy(orow + sub * 8, pack8<TOut>(acc), pol_out);
       } else if (self_off >= 0) {
         // converted, not added to 0 (that would turn -0 into +0)
         const uint4 raw = *reinterpret_cast<const uint4*>(ls + kRows * 256);
@@ -288,7 +309,7 @@ sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
         float sv[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) sv[j] = CvtS<TIn>::in(t[j]);
-        *reinterpret_cast<uint4*>(orow + self_off + sub * 8) = pack8<TOut>(sv);
+        st_v4_policy(orow + self_off + sub * 8, pack8<TOut>(sv), pol_out);
       }
     }
     if (d1 >= n) break;
