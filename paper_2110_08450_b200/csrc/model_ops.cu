@@ -469,8 +469,11 @@ mean_bwd_t_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_p
 //   * source-major, warp per 32 source rows: every other row (self term, several
 //     or no in-edges) as mean_bwd_t_kernel does it.
 // Same arithmetic as mean_bwd_t_kernel row for row, so the output is bit-identical.
+#ifndef SAL_MBS_MINB
+#define SAL_MBS_MINB 3
+#endif
 template <typename TG, typename TO>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, SAL_MBS_MINB)
 mean_bwd_split_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t n_pad,
                       const int64_t* __restrict__ n_dst_dev, const int32_t* __restrict__ indptr,
                       const int32_t* __restrict__ src, const int32_t* __restrict__ tindptr,
@@ -486,11 +489,22 @@ mean_bwd_split_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t
     if (cap < nrows) nrows = (int)cap;
   }
   const int npad = (int)n_pad;
-  if ((int)blockIdx.x < dst_blocks) {
+  // the two passes' blocks interleaved in launch order, so both progress from the start
+  const int src_blocks = (int)gridDim.x - dst_blocks;
+  const int mpair = min(dst_blocks, src_blocks);
+  int role, bidx;
+  if ((int)blockIdx.x < 2 * mpair) {
+    role = blockIdx.x & 1;
+    bidx = blockIdx.x >> 1;
+  } else {
+    role = dst_blocks > src_blocks ? 0 : 1;
+    bidx = mpair + ((int)blockIdx.x - 2 * mpair);
+  }
+  if (role == 0) {
     // ---- destination-major: single-in-edge rows without a self term
     const int n_dst = (int)(n_dst_dev ? *n_dst_dev : n_pad);
     const int nw = dst_blocks * (int)(blockDim.x >> 5);
-    for (int d = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); d < n_dst; d += nw) {
+    for (int d = (int)((bidx * blockDim.x + threadIdx.x) >> 5); d < n_dst; d += nw) {
       const int beg = __ldg(indptr + d), end = __ldg(indptr + d + 1);
       const float w = 1.f / (float)(end - beg);
       for (int e0 = beg; e0 < end; e0 += 32) {
@@ -543,8 +557,8 @@ mean_bwd_split_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t
   // ---- source-major: the remaining rows (self term, several or no in-edges), 8
   // rows per warp task (rows below n_pad are all of this kind)
   constexpr int kChunk = 8;
-  const int nw = (int)((gridDim.x - dst_blocks) * (blockDim.x >> 5));
-  for (int base = (int)(((blockIdx.x - dst_blocks) * blockDim.x + threadIdx.x) >> 5) * kChunk;
+  const int nw = src_blocks * (int)(blockDim.x >> 5);
+  for (int base = (int)((bidx * blockDim.x + threadIdx.x) >> 5) * kChunk;
        base < nrows; base += nw * kChunk) {
     const int s_l = base + lane;
     int tb = 0, te = 0, d0 = -1;
