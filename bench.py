@@ -75,6 +75,8 @@ def parse():
                    help="run the fused last hop as the first kernel of the training step "
                         "instead of on the prep stream")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-fp32", action="store_true",
+                   help="skip the fp32-activation epoch measured beside the bf16 one")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-parity", action="store_true",
                    help="skip the parity gate (device MFGs / batches vs the oracle)")
@@ -489,6 +491,42 @@ def prep_epoch_profile(trainer, nbatches: int, workers=(1, 8)):
     return out
 
 
+def fp32_epoch(dg, train, fan, args, spe, steps: int = 200):
+    """The same training epoch with fp32 activations and fp32 GEMMs (the reference's
+    precision: features fp16 -> fp32 exactly, no bf16 rounding; cuBLAS with TF32 off
+    instead of the bf16 tcgen05 kernels), timed on the first `steps` steps and
+    extrapolated: the price of the headline's bf16 activations."""
+    from paper_2110_08450_b200.train import TrainConfig, Trainer
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        cfg = TrainConfig(fanouts=fan, hidden=args.hidden, gather_free=True,
+                          act_dtype=torch.float32, graphs=not args.no_graphs)
+        tr = Trainer(dg, train, cfg)
+        tr.set_epoch(0)
+        tr.begin_epoch(False)
+        tr.run_steps(0, 5)
+        torch.cuda.synchronize()
+        tr.set_epoch(1)
+        tr.begin_epoch(False)
+        k = min(steps, spe)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        tr.run_steps(0, k)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / k
+        out = {"value": round(ms * spe / 1e3, 4), "unit": "s", "ms_per_step": round(ms, 4),
+               "steps_timed": k, "final_loss": float(tr.last_loss.item()),
+               "what": "fp32 activations + fp32 cuBLAS GEMMs (TF32 off), unfused last hop; "
+                       "first steps of an epoch, extrapolated"}
+        del tr
+        torch.cuda.empty_cache()
+        return out
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 def _oracle():
     sys.path.insert(0, str(REPO / "oracle"))
     import oracle as O
@@ -757,6 +795,9 @@ def run_ours(args):
                "final_loss": float(loss_host[-1]),
                "path": "Trainer.run_steps(host_inputs=True): each step's seeds + batch "
                        "descriptor H2D from pinned host memory, loss D2H to pinned memory"}
+    fp32 = None
+    if rank == 0 and world == 1 and not args.no_fp32:
+        fp32 = fp32_epoch(dg, train, fan, args, spe)
     kp = kernel_profile(tr, args.kernel_batches) if rank == 0 else None
     pe = prep_epoch_profile(tr, args.prep_batches) if rank == 0 and args.prep_batches else None
     line = None
@@ -785,6 +826,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "e2e": e2e,
+            "fp32_epoch": fp32,
             "sampled_edges_per_s": kp["sampled_edges_per_s_graph"],
             "gather_GBps": kp["gather_GBps"],
             "kernels": kp,
