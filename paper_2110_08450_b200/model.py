@@ -211,9 +211,10 @@ class FusedSAGE:
         # lsm_nll, three launches fewer
         self.tc_head = True
         # the hidden layers' input-gradient GEMM dA = dz @ W_cat on tcgen05
-        # (sal_tc_gemm_nn): 6.8 against 4.5 us for cuBLAS at [6144 x 256] @ [256 x 512],
-        # +3 us per step (tools/step_ab.py), so off by default
-        self.tc_dA = False
+        # (sal_tc_gemm_nn): alone 6.8 against 4.5 us for cuBLAS at [6144 x 256] @
+        # [256 x 512], but in the overlapped step (fused last hop beside the backward)
+        # 149 against 156.5 us per step (tools/step_ab.py): no library GEMM in the step
+        self.tc_dA = True
         # weight gradients of the layers above 0 on a second stream, beside the
         # input-gradient chain
         self.overlap_wgrad = True   # measured 0.233 -> 0.228 s per papers epoch
