@@ -329,8 +329,14 @@ int sal_mean_bwd_t_live(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32
 int sal_mean_bwd(const void* dA_dev, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
                  const int64_t* n_dst_dev, const int32_t* indptr_dev, const int32_t* src_dev,
                  const int32_t* tindptr_dev, const int32_t* tdst_dev, const float* tw_dev,
-                 int64_t rows, const int64_t* m_dev, const uint8_t* mask_dev, float p,
-                 void* dz_dev, int64_t ldz, int32_t dz_dtype, void* stream);
+                 const int32_t* cplx_dev, const int32_t* n_cplx_dev, int64_t rows,
+                 const int64_t* m_dev, const uint8_t* mask_dev, float p, void* dz_dev,
+                 int64_t ldz, int32_t dz_dtype, void* stream);
+/* byte offsets, inside a sal_transpose_build workspace, of the list (int32) of the rows
+ * sal_mean_bwd handles source-major (self term, or not exactly one in-edge; any order)
+ * and of its length (int32); sal_transpose_build fills both (pass them as cplx_dev /
+ * n_cplx_dev, or NULL to scan every row) */
+int sal_transpose_complex_list(int64_t n_src_rows, int64_t* list_offset, int64_t* count_offset);
 /* Adam (torch.optim.Adam, no weight decay) on flat fp32 params; step count
  * t = *t_dev + 1; refreshes the optional bf16 shadow copy; zero_grad != 0
  * leaves grad zeroed (the next backward accumulates without a memset) */

@@ -118,8 +118,9 @@ SIGNATURES = {
     "sal_transpose_ws_bytes": (ctypes.c_size_t, [i64]),
     "sal_transpose_build": (ctypes.c_int, [vp, vp, vp, i64, i64, i64, vp, vp, vp, vp, i32, vp]),
     "sal_zero_spans": (ctypes.c_int, [vp, vp, i32, vp]),
-    "sal_mean_bwd": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, vp, vp, i64, vp,
-                                     vp, ctypes.c_float, vp, i64, i32, vp]),
+    "sal_mean_bwd": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp,
+                                     i64, vp, vp, ctypes.c_float, vp, i64, i32, vp]),
+    "sal_transpose_complex_list": (ctypes.c_int, [i64, P(i64), P(i64)]),
     "sal_mean_bwd_t": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp,
                                       ctypes.c_float, vp, i64, i32, vp]),
     "sal_mean_bwd_t_live": (ctypes.c_int, [vp, i64, i32, i32, i64, vp, vp, vp, vp, i64, vp, vp,

@@ -350,6 +350,24 @@ __global__ void transpose_fill_kernel(const int32_t* __restrict__ indptr,
   }
 }
 
+// rows s < n whose input gradient is not a single scaled dA row: a self term
+// (s < n_pad) or a number of in-edges other than one; appended in any order
+__global__ void complex_rows_kernel(const int32_t* __restrict__ tindptr, int64_t n, int64_t n_pad,
+                                    int32_t* __restrict__ list, int32_t* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t s0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; s0 < n;
+       s0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = s0 + lane;
+    bool c = false;
+    if (s < n) c = s < n_pad || tindptr[s + 1] - tindptr[s] != 1;
+    const unsigned m = __ballot_sync(0xffffffffu, c);
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (c) list[base + __popc(m & ((1u << lane) - 1u))] = (int32_t)s;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // dz_prev[s, :] = mask_prev(s) * scale * (dA[s, f:2f] (s < n_pad) +
 //                 sum_{d in T(s)} dA[d, 0:f] / deg(d));  warp per source row,
@@ -480,7 +498,8 @@ mean_bwd_split_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t
                       const int32_t* __restrict__ tdst, const float* __restrict__ tw,
                       int64_t rows, const int64_t* __restrict__ m_dev, int live,
                       const uint8_t* __restrict__ mask, float p, TO* __restrict__ dz,
-                      int64_t ldz, int dst_blocks) {
+                      int64_t ldz, int dst_blocks, const int32_t* __restrict__ cplx,
+                      const int32_t* __restrict__ n_cplx) {
   const int lane = threadIdx.x & 31;
   const float scale = p > 0.f ? (p < 1.f ? 1.f / (1.f - p) : 0.f) : 1.f;
   int nrows = (int)rows;
@@ -558,13 +577,17 @@ mean_bwd_split_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t
   // rows per warp task (rows below n_pad are all of this kind)
   constexpr int kChunk = 8;
   const int nw = src_blocks * (int)(blockDim.x >> 5);
+  // with a prebuilt list of those rows (cplx, built beside the forward pass) the
+  // tasks walk the list; else they scan every row
+  const int nitems = cplx ? *n_cplx : nrows;
   for (int base = (int)((bidx * blockDim.x + threadIdx.x) >> 5) * kChunk;
-       base < nrows; base += nw * kChunk) {
-    const int s_l = base + lane;
+       base < nitems; base += nw * kChunk) {
+    int s_l = -1;
     int tb = 0, te = 0, d0 = -1;
     float w0 = 0.f;
     bool complex_row = false;
-    if (lane < kChunk && s_l < nrows) {
+    if (lane < kChunk && base + lane < nitems) s_l = cplx ? __ldg(cplx + base + lane) : base + lane;
+    if (s_l >= 0 && s_l < nrows) {
       tb = __ldg(tindptr + s_l);
       te = __ldg(tindptr + s_l + 1);
       complex_row = !(te - tb == 1 && s_l >= npad);
@@ -594,7 +617,7 @@ mean_bwd_split_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t
           const int r = rk[k] < 0 ? 0 : rk[k];
           const int dd = __shfl_sync(0xffffffffu, d0, r);
           wk[k] = __shfl_sync(0xffffffffu, w0, r);
-          const int s = base + r;
+          const int s = __shfl_sync(0xffffffffu, s_l, r);
 #pragma unroll
           for (int q = 0; q < V; ++q) sraw[k][q] = nraw[k][q] = make_uint4(0, 0, 0, 0);
           mk[k] = 0;
@@ -616,7 +639,7 @@ mean_bwd_split_kernel(const TG* __restrict__ dA, int64_t lda, int32_t f, int64_t
         for (int k = 0; k < 4; ++k) {
           if (rk[k] < 0) break;
           const int r = rk[k];
-          const int s = base + r;
+          const int s = __shfl_sync(0xffffffffu, s_l, r);
           const int rtb = __shfl_sync(0xffffffffu, tb, r);
           const int rte = __shfl_sync(0xffffffffu, te, r);
           if (!active) continue;
@@ -874,9 +897,22 @@ int sal_argmax_correct(const void* logits, int64_t ld, int64_t rows, int32_t C, 
   return sal::done(1);
 }
 
+// transpose workspace: tcount, tfill (int32 [n+1] each), the complex-row count (int32,
+// 16 B slot) and list (int32 [n]), then the scan workspace (16-byte aligned)
+static int64_t tws_list_count_off(int64_t n) { return 8 * (n + 1); }
+static int64_t tws_list_off(int64_t n) { return 8 * (n + 1) + 16; }
+static int64_t tws_scan_off(int64_t n) { return (tws_list_off(n) + 4 * n + 15) / 16 * 16; }
+
 size_t sal_transpose_ws_bytes(int64_t n_src_rows) {
-  // tcount + tfill (int32 each) + scan workspace
-  return (size_t)(8 * (n_src_rows + 1)) + sal::scan_ws_bytes(n_src_rows) + 64;
+  return (size_t)tws_scan_off(n_src_rows) + sal::scan_ws_bytes(n_src_rows) + 64;
+}
+
+int sal_transpose_complex_list(int64_t n_src_rows, int64_t* list_offset, int64_t* count_offset) {
+  if (n_src_rows < 0 || list_offset == nullptr || count_offset == nullptr)
+    return sal::set_error(SAL_EINVAL, "transpose_complex_list: bad arguments");
+  *list_offset = tws_list_off(n_src_rows);
+  *count_offset = tws_list_count_off(n_src_rows);
+  return SAL_OK;
 }
 
 int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t* n_dst_dev,
@@ -888,11 +924,12 @@ int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t
   cudaStream_t st = (cudaStream_t)stream;
   int32_t* tcount = (int32_t*)ws;
   int32_t* tfill = tcount + (n_src_rows + 1);
-  char* scan = (char*)(tfill + (n_src_rows + 1));
-  scan = (char*)(((uintptr_t)scan + 15) & ~(uintptr_t)15);
+  int32_t* ncplx = (int32_t*)((char*)ws + tws_list_count_off(n_src_rows));
+  int32_t* cplx = (int32_t*)((char*)ws + tws_list_off(n_src_rows));
+  char* scan = (char*)ws + tws_scan_off(n_src_rows);
   if (!ws_zeroed) {  // else the caller zeroed the whole ws (sal_zero_spans)
-    const size_t zero_bytes = (size_t)(8 * (n_src_rows + 1));
-    if (cudaMemsetAsync(ws, 0, zero_bytes, st) != cudaSuccess) return SAL_ECUDA;
+    if (cudaMemsetAsync(ws, 0, (size_t)tws_list_off(n_src_rows), st) != cudaSuccess)
+      return SAL_ECUDA;
     const size_t sb = sal::scan_ws_bytes(n_src_rows);
     if (cudaMemsetAsync(scan, 0, sb, st) != cudaSuccess) return SAL_ECUDA;
   }
@@ -907,7 +944,10 @@ int sal_transpose_build(const int32_t* indptr, const int32_t* src, const int64_t
                                                                            tindptr, sw);
   sal::transpose_fill_kernel<<<sal::warp_grid(n_pad), 256, 0, st>>>(indptr, src, n_dst_dev, n_pad,
                                                                     tindptr, tfill, tdst, tw);
-  return sal::done(3);
+  // the rows sal_mean_bwd's source-major pass handles (self term, 0 or >= 2 in-edges)
+  sal::complex_rows_kernel<<<sal::ew_grid(n_src_rows), 256, 0, st>>>(tindptr, n_src_rows, n_pad,
+                                                                     cplx, ncplx);
+  return sal::done(4);
 }
 
 static int mean_bwd_t_launch(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f,
@@ -955,9 +995,12 @@ int sal_mean_bwd_t_live(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f
 
 int sal_mean_bwd(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64_t n_pad,
                  const int64_t* n_dst_dev, const int32_t* indptr, const int32_t* src,
-                 const int32_t* tindptr, const int32_t* tdst, const float* tw, int64_t rows,
+                 const int32_t* tindptr, const int32_t* tdst, const float* tw,
+                 const int32_t* cplx, const int32_t* n_cplx, int64_t rows,
                  const int64_t* m_dev, const uint8_t* mask, float p, void* dz, int64_t ldz,
                  int32_t dz_dtype, void* stream) {
+  if ((cplx == nullptr) != (n_cplx == nullptr))
+    return sal::set_error(SAL_EINVAL, "mean_bwd: cplx and n_cplx go together");
   if (dA == nullptr || indptr == nullptr || src == nullptr || tindptr == nullptr ||
       tdst == nullptr || mask == nullptr || dz == nullptr)
     return sal::set_error(SAL_EINVAL, "mean_bwd: null argument");
@@ -973,17 +1016,19 @@ int sal_mean_bwd(const void* dA, int64_t lda, int32_t dA_dtype, int32_t f, int64
   if (dst_blocks < 1) dst_blocks = 1;
   int src_blocks = (int)((rows + 63) / 64);   // 8 warps x 8-row tasks per block
   if (src_blocks > cap) src_blocks = cap;
+  // walking a prebuilt list: a grid-stride pass over a fraction of the rows
+  if (cplx != nullptr && src_blocks > sal::num_sms() * 2) src_blocks = sal::num_sms() * 2;
   if (src_blocks < 1) src_blocks = 1;
   const int g = dst_blocks + src_blocks;
   const int live = m_dev != nullptr;
   if (dA_dtype == SAL_BF16 && dz_dtype == SAL_BF16)
     sal::mean_bwd_split_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(
         (const __nv_bfloat16*)dA, lda, f, n_pad, n_dst_dev, indptr, src, tindptr, tdst, tw,
-        rows, m_dev, live, mask, p, (__nv_bfloat16*)dz, ldz, dst_blocks);
+        rows, m_dev, live, mask, p, (__nv_bfloat16*)dz, ldz, dst_blocks, cplx, n_cplx);
   else if (dA_dtype == SAL_F32 && dz_dtype == SAL_F32)
     sal::mean_bwd_split_kernel<float, float><<<g, 256, 0, st>>>(
         (const float*)dA, lda, f, n_pad, n_dst_dev, indptr, src, tindptr, tdst, tw, rows, m_dev,
-        live, mask, p, (float*)dz, ldz, dst_blocks);
+        live, mask, p, (float*)dz, ldz, dst_blocks, cplx, n_cplx);
   else
     return sal::set_error(SAL_EINVAL, "mean_bwd: dtypes must be bf16/bf16 or f32/f32");
   return sal::done(1);

@@ -484,8 +484,11 @@ class FusedSAGE:
         f = self.dims[i]
         indptr, src, _, n_dev = rec["adj"]
         rows = a.shape[0]
+        cplx = ncplx = None
         if transposes is not None and transposes[i] is not None:
-            tindptr, tdst, tw = transposes[i]
+            tindptr, tdst, tw = transposes[i][:3]
+            if len(transposes[i]) == 5:   # the workspace's list of source-major rows
+                cplx, ncplx = transposes[i][3:]
         else:
             tindptr, tdst, tw = build_transpose(indptr, src, n_dev, n_pad, rows)
         dzp = torch.empty((rows, f), dtype=self.act, device=a.device)
@@ -498,7 +501,8 @@ class FusedSAGE:
             _lib.check(L.sal_mean_bwd(
                 dA.data_ptr(), dA.stride(0), _lib.dtype_code(dA.dtype), f, n_pad,
                 _lib.ptr(n_dev), indptr.data_ptr(), src.data_ptr(), tindptr.data_ptr(),
-                tdst.data_ptr(), tw.data_ptr(), rows, m_rows.data_ptr() if live else None,
+                tdst.data_ptr(), tw.data_ptr(), _lib.ptr(cplx), _lib.ptr(ncplx), rows,
+                m_rows.data_ptr() if live else None,
                 mask.data_ptr(), p, dzp.data_ptr(), dzp.stride(0), _lib.dtype_code(self.act),
                 _lib.stream_ptr()), "mean_bwd")
             return dzp
@@ -608,7 +612,7 @@ def build_transpose(indptr, src, n_dst_dev, n_pad: int, n_src_rows: int, out=Non
         tdst = torch.empty(max(src.numel(), 1), dtype=torch.int32, device=dev)
         tw = torch.empty(max(src.numel(), 1), dtype=torch.float32, device=dev)
     else:
-        tindptr, tdst, tw = out
+        tindptr, tdst, tw = out[:3]
     if ws is None:
         ws = torch.empty(L.sal_transpose_ws_bytes(n_src_rows), dtype=torch.uint8, device=dev)
     _lib.check(L.sal_transpose_build(indptr.data_ptr(), src.data_ptr(), _lib.ptr(n_dst_dev),

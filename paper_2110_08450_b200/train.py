@@ -181,7 +181,15 @@ class _Slot:
                 torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.int32, device=device),
                 torch.zeros(max(ws.edge_cap[h], 1), dtype=torch.float32, device=device)))
             nb = -(-L.sal_transpose_ws_bytes(n_src) // 16) * 16   # 16 B multiple (zero_spans)
-            self.t_ws.append(torch.empty(nb, dtype=torch.uint8, device=device))
+            tws = torch.empty(nb, dtype=torch.uint8, device=device)
+            self.t_ws.append(tws)
+            # the build also lists the rows the input gradient handles source-major
+            lo, co = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(L.sal_transpose_complex_list(n_src, ctypes.byref(lo), ctypes.byref(co)),
+                       "transpose_complex_list")
+            self.transposes[-1] = self.transposes[-1] + (
+                tws[lo.value:lo.value + 4 * max(n_src, 1)].view(torch.int32),
+                tws[co.value:co.value + 4].view(torch.int32))
 
 
 class _Staging:

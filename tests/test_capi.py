@@ -76,7 +76,8 @@ def test_invalid_arguments_set_the_error_message():
         (lambda: L.sal_argmax_correct(None, 0, 1, 10, _lib.SAL_BF16, None, None, None, None),
          "argmax_correct"),
         (lambda: L.sal_mean_bwd(None, 8, _lib.SAL_BF16, 8, 0, None, None, None, None, None, None,
-                                0, None, None, 0.0, None, 8, _lib.SAL_BF16, None), "mean_bwd"),
+                                None, None, 0, None, None, 0.0, None, 8, _lib.SAL_BF16, None),
+         "mean_bwd"),
         (lambda: L.sal_sample_aggregate(None, None, None, None, None, 0, 0, None, 0, 0, 0, None,
                                         0, 0, 0, None), "sample_aggregate"),
     ]

@@ -1,5 +1,7 @@
 """GraphSAGE training path: fused model vs a torch-autograd fp32 reference,
 CUDA-graph replay vs eager, and learning on a labelled synthetic graph."""
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -424,11 +426,22 @@ def test_mean_bwd_split_equals_mean_bwd_t(dtype, f, live):
                                          tw.data_ptr(), rows, md.data_ptr(), mask.data_ptr(), p,
                                          want.data_ptr(), want.stride(0), dc,
                                          _lib.stream_ptr()), "mbt_live")
-    _lib.check(L.sal_mean_bwd(dA.data_ptr(), dA.stride(0), dc, f, n_pad, nd.data_ptr(),
-                              ip.data_ptr(), sr.data_ptr(), tind.data_ptr(), tdst.data_ptr(),
-                              tw.data_ptr(), rows, md.data_ptr() if live is not None else None,
-                              mask.data_ptr(), p, got.data_ptr(), got.stride(0), dc,
-                              _lib.stream_ptr()), "mean_bwd")
-    torch.cuda.synchronize()
     iv = torch.int16 if dtype == torch.bfloat16 else torch.int32
-    assert torch.equal(got.view(iv), want.view(iv))
+    # scanning every row, and walking the workspace's list of source-major rows
+    ws = torch.zeros(L.sal_transpose_ws_bytes(rows), dtype=torch.uint8, device="cuda")
+    build_transpose(ip, sr, nd, n_pad, rows, ws=ws, ws_zeroed=True)
+    lo, co = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(L.sal_transpose_complex_list(rows, ctypes.byref(lo), ctypes.byref(co)), "list")
+    cplx = ws[lo.value:lo.value + 4 * rows].view(torch.int32)
+    ncplx = ws[co.value:co.value + 4].view(torch.int32)
+    for lst in (None, (cplx, ncplx)):
+        got.fill_(float("nan"))
+        _lib.check(L.sal_mean_bwd(dA.data_ptr(), dA.stride(0), dc, f, n_pad, nd.data_ptr(),
+                                  ip.data_ptr(), sr.data_ptr(), tind.data_ptr(), tdst.data_ptr(),
+                                  tw.data_ptr(), lst[0].data_ptr() if lst else None,
+                                  lst[1].data_ptr() if lst else None, rows,
+                                  md.data_ptr() if live is not None else None,
+                                  mask.data_ptr(), p, got.data_ptr(), got.stride(0), dc,
+                                  _lib.stream_ptr()), "mean_bwd")
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(iv), want.view(iv)), lst is not None

@@ -4,6 +4,7 @@ sampled edges over 67584 source rows, f = 256, bf16, p = 0.5.
 
 python tools/mbt_bench.py [--split]   (under gpurun)
 """
+import ctypes
 import sys
 from pathlib import Path
 
@@ -25,7 +26,12 @@ src_np = rng.permutation(np.arange(n_dst, rows))[:n_dst * fan].astype(np.int32)
 src_np[::7] = rng.integers(0, rows, size=src_np[::7].shape[0])
 src = torch.from_numpy(src_np).to(dev)
 n_dev = torch.tensor([n_dst], dtype=torch.int64, device=dev)
-tind, tdst, tw = build_transpose(indptr, src, n_dev, n_dst, rows)
+tws = torch.zeros(L.sal_transpose_ws_bytes(rows), dtype=torch.uint8, device=dev)
+tind, tdst, tw = build_transpose(indptr, src, n_dev, n_dst, rows, ws=tws, ws_zeroed=True)
+_lo, _co = ctypes.c_int64(), ctypes.c_int64()
+L.sal_transpose_complex_list(rows, ctypes.byref(_lo), ctypes.byref(_co))
+cplx = tws[_lo.value:_lo.value + 4 * rows].view(torch.int32)
+ncplx = tws[_co.value:_co.value + 4].view(torch.int32)
 dA = (torch.randn(n_dst, 2 * f, device=dev) * 0.1).to(torch.bfloat16)
 mask = torch.from_numpy(rng.integers(0, 256, size=rows * f // 8, dtype=np.uint8)).to(dev)
 dz = torch.empty(rows, f, device=dev, dtype=torch.bfloat16)
@@ -38,7 +44,8 @@ def run():
     if SPLIT:
         _lib.check(L.sal_mean_bwd(dA.data_ptr(), dA.stride(0), _lib.SAL_BF16, f, n_dst,
                                   n_dev.data_ptr(), indptr.data_ptr(), src.data_ptr(),
-                                  tind.data_ptr(), tdst.data_ptr(), tw.data_ptr(), rows, None,
+                                  tind.data_ptr(), tdst.data_ptr(), tw.data_ptr(),
+                                  cplx.data_ptr(), ncplx.data_ptr(), rows, None,
                                   mask.data_ptr(), 0.5, dz.data_ptr(), dz.stride(0),
                                   _lib.SAL_BF16, _lib.stream_ptr()), "mean_bwd")
         return
