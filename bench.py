@@ -888,9 +888,7 @@ def run_infer(args):
     n = ev.set_ids(test)
     W = max(args.warmup, 3)
     K = args.steps if 0 < args.steps <= n else n
-    for p in range(min(2, n)):
-        if ev.use_graphs:
-            ev._capture(p)
+    ev.capture_all()
     ev.begin()
     ev.steps(0, min(W, n))
     torch.cuda.synchronize()

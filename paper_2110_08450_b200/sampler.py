@@ -403,8 +403,14 @@ class MfgWorkspace:
         self.seeds = torch.empty(max(1, self.max_seeds), dtype=torch.int64, device=self.device)
         self.desc = torch.zeros(3, dtype=torch.int64, device=self.device)
         if self.plan.reset_in_aggregate:   # the first batch finds a reset table + scans
-            self.table.fill_(-1)
-            self.buf[lay.scan:lay.scan + lay.scan_bytes].zero_()
+            self.reset_tables()
+
+    def reset_tables(self) -> None:
+        """Reset the id table and scan workspace (current stream): what a fused plan's
+        aggregate() leaves behind, for a caller that ran run() without it."""
+        lay = self.layout
+        self.table.fill_(-1)
+        self.buf[lay.scan:lay.scan + lay.scan_bytes].zero_()
 
     def _view(self, off: int, n: int, dt: torch.dtype) -> torch.Tensor:
         nbytes = n * torch.empty((), dtype=dt).element_size()

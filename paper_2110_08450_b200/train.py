@@ -663,12 +663,14 @@ class Evaluator:
     PAPER.md:1428-1439, inference fanout (20,20,20) in the paper).
 
     Batches are `ids` chunked in order (batch_id = chunk index, no shuffle),
-    sampled with `global_seed`; chunk b runs on rank b % world.  Each step is
-    {prep(k+1) on the prep stream: plan cursor -> MFG (last hop edges only) ->
-    destination rows -> labels  ||  forward(k) without dropout: layer-0 mean
-    straight from the fp16 table, SAGE layers, argmax + correct count}, captured
-    as one CUDA graph per slot parity.  The (correct, total) pair stays on the
-    device until the end of the pass (one D2H; one all-reduce when world > 1).
+    sampled with `global_seed`; chunk b runs on rank b % world.  Three slots, each
+    step one captured graph of three independent chains:
+      hops(k+2):   plan cursor -> MFG hops 0..L-2      (latency-bound; hop stream)
+      fill(k+1):   fused last hop -> [mean | self], labels  (HBM-bound; fill stream)
+      forward(k):  SAGE layers without dropout, argmax + correct count
+    so batch k+2's dependent hop kernels run under batch k+1's row traffic instead
+    of before it.  The (correct, total) pair stays on the device until the end of
+    the pass (one D2H; one all-reduce when world > 1).
     """
 
     def __init__(self, dg: DeviceGraph, model: FusedSAGE, fanouts: FanoutSpec, batch_size: int,
@@ -685,10 +687,12 @@ class Evaluator:
         self.use_graphs = graphs
         cfg = TrainConfig(fanouts=fanouts, batch_size=self.batch_size, gather_free=True,
                           act_dtype=act_dtype, fuse_last_hop=fuse_last_hop)
-        self.slots = [_Slot(dg, cfg, self.device, backward=False) for _ in range(2)]
-        # high priority here (measured 0.0728 vs 0.0736 s per pass at equal priority);
-        # training measured the other way (TrainConfig.prep_priority = 0)
-        self.prep_stream = torch.cuda.Stream(device=self.device, priority=prep_priority)
+        self.D = 3
+        self.slots = [_Slot(dg, cfg, self.device, backward=False) for _ in range(self.D)]
+        # the hop chain at high priority (latency-bound: its blocks go first as the row
+        # traffic's blocks drain); the fill at the default
+        self.hop_stream = torch.cuda.Stream(device=self.device, priority=prep_priority)
+        self.fill_stream = torch.cuda.Stream(device=self.device)
         self.x_table = _model_table(dg)
         self.cursor = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.counts = torch.zeros(2, dtype=torch.int64, device=self.device)
@@ -722,13 +726,20 @@ class Evaluator:
         self.n_steps = n
         return n
 
-    def _prep(self, slot: _Slot) -> None:
-        ws = slot.ws
+    def _hops(self, slot: _Slot) -> None:
+        """Plan cursor -> the slot's descriptor -> MFG hops (the fused last hop is left
+        to _fill)."""
         st = torch.cuda.current_stream()
         L = _lib.lib()
         _lib.check(L.sal_plan_next(self.desc_all.data_ptr(), self.n_steps, self.cursor.data_ptr(),
                                    slot.desc.data_ptr(), _lib.stream_ptr(st)), "plan_next")
-        ws.run(self.dg, self.seeds_all, slot.desc, self.global_seed, self.policy, st)
+        slot.ws.run(self.dg, self.seeds_all, slot.desc, self.global_seed, self.policy, st)
+
+    def _fill(self, slot: _Slot) -> None:
+        """The layer-0 input (fused last hop, or the destination rows) and the labels."""
+        ws = slot.ws
+        st = torch.cuda.current_stream()
+        L = _lib.lib()
         nh = self.nh
         f, fx = self.model.dims[0], self.x_table.shape[1]
         if slot.fused:
@@ -767,13 +778,31 @@ class Evaluator:
             self.counts.data_ptr(), None, _lib.stream_ptr()), "argmax_correct")
 
     def _pair(self, k: int) -> None:
+        """{hops(k+2) || fill(k+1) || forward(k)} (begin() primed hops/fill of k, hops
+        of k+1)."""
+        D = self.D
         cs = torch.cuda.current_stream()
-        ps = self.prep_stream
-        ps.wait_stream(cs)
-        with torch.cuda.stream(ps):
-            self._prep(self.slots[(k + 1) % 2])
-        self._forward(self.slots[k % 2])
-        cs.wait_stream(ps)
+        hs, fs = self.hop_stream, self.fill_stream
+        hs.wait_stream(cs)
+        fs.wait_stream(cs)
+        with torch.cuda.stream(hs):
+            self._hops(self.slots[(k + 2) % D])
+        with torch.cuda.stream(fs):
+            self._fill(self.slots[(k + 1) % D])
+        self._forward(self.slots[k % D])
+        cs.wait_stream(hs)
+        cs.wait_stream(fs)
+
+    def _prime(self) -> None:
+        """Step 0's hops and fill, step 1's hops (eager, current stream).  A slot's hops
+        rely on the fill of its previous batch to have reset its id table; a capture's
+        warm-up leaves hops without their fill, so every table is reset here."""
+        for s in self.slots:
+            if s.ws.plan.reset_in_aggregate:
+                s.ws.reset_tables()
+        self._hops(self.slots[0])
+        self._fill(self.slots[0])
+        self._hops(self.slots[1 % self.D])
 
     def _capture(self, parity: int):
         torch.cuda.synchronize()
@@ -781,9 +810,11 @@ class Evaluator:
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            self._prep(self.slots[parity])  # the warm-up forward reads a prepared slot
-            for _ in range(2):
-                self._pair(parity)
+            # warm-up along a valid pipeline progression: each pair reads slots the
+            # previous ones prepared
+            self._prime()
+            for k in range(parity + 1):
+                self._pair(k)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -797,19 +828,27 @@ class Evaluator:
         self.graphs[parity] = g
         return g
 
+    def capture_all(self) -> None:
+        """Capture every slot parity's graph (before begin(): capturing replays steps)."""
+        if self.use_graphs:
+            for p in range(min(self.D, max(self.n_steps, 1))):
+                if p not in self.graphs:
+                    self._capture(p)
+
     def begin(self) -> None:
-        """Reset the cursor and counters and prepare step 0 into slot 0."""
+        """Reset the cursor and counters and prime the pipeline for step 0."""
         self.cursor.zero_()
         self.counts.zero_()
-        self._prep(self.slots[0])
+        self._prime()
 
     def steps(self, start: int, count: int) -> None:
         """Enqueue steps [start, start+count) (begin() primed step `start`)."""
+        D = self.D
         for k in range(start, start + count):
             if self.use_graphs:
-                g = self.graphs.get(k % 2) or self._capture(k % 2)
+                g = self.graphs.get(k % D) or self._capture(k % D)
                 g.replay()
-                self.kernel_launches += self.graph_kernels[k % 2]
+                self.kernel_launches += self.graph_kernels[k % D]
             else:
                 n0 = _lib.lib().sal_launch_count()
                 self._pair(k)
@@ -817,10 +856,7 @@ class Evaluator:
 
     def run(self, ids: np.ndarray) -> tuple[int, int]:
         n = self.set_ids(ids)
-        if self.use_graphs:  # capture before the pass so it does not disturb the cursor
-            for p in range(min(2, n)):
-                if p not in self.graphs:
-                    self._capture(p)
+        self.capture_all()   # before the pass: capturing replays steps
         self.begin()
         self.steps(0, n)
         if self.world > 1:
