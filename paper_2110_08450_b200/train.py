@@ -233,7 +233,9 @@ class Trainer:
             torch.distributed.broadcast(self.model.flat, src=0)
             self.model.refresh_shadow()
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
-        # pipeline depth: batches in flight (one trained, one prepared)
+        # pipeline depth: batches in flight (one trained, one prepared).  Three slots with
+        # {hops(k+2) || fused fill(k+1) || train(k)} trained the same batches and measured
+        # 171 against 148 us per step (the fill then contends with the forward): not kept
         self.depth = 2
         self.slots = [_Slot(dg, cfg, self.device) for _ in range(self.depth)]
         self.ring = 2 * self.depth   # pinned staging buffers of the end-to-end path
@@ -311,6 +313,14 @@ class Trainer:
     def _prep(self, slot: _Slot, stage: "_Staging | None", late: bool = False) -> None:
         """Enqueue one batch preparation on the current stream (capturable): seeds ->
         MFG -> layer-0 feature rows, plus (late=True) what _prep_late builds."""
+        self._hops(slot, stage)
+        self._fill(slot)
+        if late:
+            self._prep_late(slot, stage)
+
+    def _hops(self, slot: _Slot, stage: "_Staging | None") -> None:
+        """Plan cursor (or the staged H2D inputs) -> the slot's MFG (a fused last hop
+        is left to _fill)."""
         ws = slot.ws
         st = torch.cuda.current_stream()
         L = _lib.lib()
@@ -323,6 +333,12 @@ class Trainer:
             desc, seeds_base = slot.desc, self.seeds_all
         ws.run(self.dg, seeds_base, desc, self.sample_seed, self.policy, st)
         slot.desc_used = desc
+
+    def _fill(self, slot: _Slot) -> None:
+        """The slot's layer-0 input: the fused last hop, or the destination rows."""
+        ws = slot.ws
+        st = torch.cuda.current_stream()
+        desc = slot.desc_used
         nh = self.nh
         f, fx = self.model.dims[0], self.x_table.shape[1]
         if slot.fused:
@@ -334,8 +350,6 @@ class Trainer:
             n_dev = ws.sizes[nh:nh + 1] if not self.cfg.gather_free else ws.sizes[nh - 1:nh]
             gather_rows(self.x_table, ws.globals, slot.feats[:, f:f + fx], n=rows, n_dev=n_dev,
                         stream=st)
-        if late:
-            self._prep_late(slot, stage)
 
     def _prep_late(self, slot: _Slot, stage: "_Staging | None", zero_grads: bool = False) -> None:
         """The inputs only the loss / backward read: labels and the reverse adjacency
@@ -456,7 +470,7 @@ class Trainer:
                 # step's Adam has read them): no memset node in the training chain
                 self._prep_late(self.slots[k % D], stg(k), zero_grads=True)
         with torch.cuda.stream(ps):
-            self._prep(self.slots[(k + 1) % 2], stg(k + 1), late=not split)
+            self._prep(self.slots[(k + 1) % D], stg(k + 1), late=not split)
         self._train(self.slots[k % D], part, late=ls)
         cs.wait_stream(ps)
 
@@ -501,6 +515,9 @@ class Trainer:
                 torch.cuda.current_stream().wait_event(stage.copied)
             stages.append(stage)
         # with the late split, pair 0 builds slot 0's labels / reverse adjacency
+        for sl in self.slots:   # a capture's warm-up may have left hops without their fill
+            if sl.ws.plan.reset_in_aggregate:
+                sl.ws.reset_tables()
         self._prep(self.slots[0], stages[0], late=late)
 
     def run_steps(self, start: int, count: int, host_inputs: bool = False,
