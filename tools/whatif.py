@@ -21,10 +21,15 @@ def ig(self, i, dA, saved, transposes):
     rec = saved[i]
     return torch.empty((rec["a"].shape[0], self.dims[i]), dtype=self.act, device=dA.device)
 
+def no_agg(self, *a, **k):
+    self.reset_tables()   # called on the stream aggregate() would have run on
+
+
 modes = {
     "base": lambda: None,
     "no_hops": lambda: patch(sampler.MfgWorkspace, "run", lambda self, *a, **k: None),
-    "no_agg": lambda: patch(sampler.MfgWorkspace, "aggregate", lambda self, *a, **k: None),
+    # the fused kernel also resets the id table for the next batch: keep that (two memsets)
+    "no_agg": lambda: patch(sampler.MfgWorkspace, "aggregate", no_agg),
     "no_prep": lambda: (patch(sampler.MfgWorkspace, "run", lambda self, *a, **k: None),
                         patch(sampler.MfgWorkspace, "aggregate", lambda self, *a, **k: None)),
     "no_mbt": lambda: patch(model.FusedSAGE, "_input_grad", ig),
