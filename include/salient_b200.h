@@ -83,7 +83,10 @@ typedef struct {
   int64_t edge_cap[SAL_MAX_HOPS];       /* max edges emitted by hop h     */
   int64_t table_cap;
   int32_t flags;                        /* SAL_MFG_* plan flags            */
-  int32_t reserved;
+  /* SAL_MFG_LAST_HOP_FUSED plans: hop L-2's relabel second pass (its src_local) runs
+   * inside sal_sample_aggregate's kernel instead of at the end of sal_sample_mfg, so
+   * the fused kernel starts one launch earlier; read the MFG after the aggregate */
+  int32_t resolve_in_aggregate;
   /* sampler launch shape (sal_hop_sample_tuned; 0 = default), set by the
    * caller after sal_mfg_plan_init; the caller may also raise table_cap (a
    * power of two) before sal_mfg_layout_init to lower the id-table load */

@@ -50,7 +50,7 @@ class SalIdMap(ctypes.Structure):
 class SalMfgPlan(ctypes.Structure):
     _fields_ = [("num_hops", i32), ("fanout", i32 * SAL_MAX_HOPS), ("max_seeds", i64),
                 ("node_cap", i64 * (SAL_MAX_HOPS + 1)), ("edge_cap", i64 * SAL_MAX_HOPS),
-                ("table_cap", i64), ("flags", i32), ("reserved", i32), ("sample_lanes", i32),
+                ("table_cap", i64), ("flags", i32), ("resolve_in_aggregate", i32), ("sample_lanes", i32),
                 ("sample_blocks_per_sm", i32), ("aggregate_blocks_per_sm", i32),
                 ("reset_in_aggregate", i32)]
 

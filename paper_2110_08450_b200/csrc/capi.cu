@@ -284,11 +284,14 @@ static int sample_mfg_hops(const sal_graph* g, const sal_mfg_plan* plan, const s
       nc.e_total = etot + h + 1;
       nc.scan_ws = scan_ws(h + 1, 0);
     }
+    // resolve_in_aggregate: a fused plan's last sampled hop resolves inside
+    // sal_sample_aggregate's kernel (off the chain that kernel waits for)
+    const bool defer = plan->resolve_in_aggregate && last < plan->num_hops && h == last - 1;
     e = sal::launch_hop_relabel(m, etot + h, plan->edge_cap[h], sizes + h, sizes + h + 1,
                                 src_glob, slot, rank, src_local, scan_ws(h, 1), st,
-                                /*ws_zeroed=*/true, has_next ? &nc : nullptr);
+                                /*ws_zeroed=*/true, has_next ? &nc : nullptr, defer);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop relabel");
-    kernels += 3;
+    kernels += defer ? 2 : 3;
   }
   return counted(SAL_OK, kernels);
 }
@@ -335,6 +338,14 @@ int sal_sample_aggregate(const sal_graph* g, const sal_mfg_plan* plan, const sal
   hk.hop = (uint32_t)h;
   hk.batch = 0;
   hk.derive = 1;
+  sal::ResolveJob rj{};
+  if (h >= 1 && plan->resolve_in_aggregate) {   // hop L-2's deferred resolve (sample_mfg_hops)
+    rj.words = (const int32_t*)(base + L->slot);
+    rj.e_total = (const int64_t*)(base + L->etot) + (h - 1);
+    rj.size_old = sizes + (h - 1);
+    rj.rank_of = (const int32_t*)(base + L->rank);
+    rj.src_local = (int32_t*)(base + L->src_local[h - 1]);
+  }
   return counted(
       cuda_status(sal::launch_sample_mean(to_dev(g), (const int32_t*)(base + L->globals),
                                           sizes + h, plan->node_cap[h], plan->fanout[h], hk, desc,
@@ -343,7 +354,7 @@ int sal_sample_aggregate(const sal_graph* g, const sal_mfg_plan* plan, const sal
                                           plan->aggregate_blocks_per_sm,
                                           plan->reset_in_aggregate
                                               ? (unsigned long long*)(base + L->table) : nullptr,
-                                          plan->table_cap, base + L->scan, L->scan_bytes,
+                                          plan->table_cap, base + L->scan, L->scan_bytes, rj,
                                           (cudaStream_t)stream),
                   "sample_aggregate"),
       1);

@@ -9,6 +9,7 @@
 //
 // fp16 -> fp32 is exact; NaNs are canonicalised to 0x7FC00000 exactly as the
 // reference's scalar _half_to_f32 does (_kernels.py:240-242: np.float32(nan)).
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -198,7 +199,9 @@ static cudaError_t gather_dispatch(const void* x, int32_t cols, int64_t x_stride
     // whole rows per warp: the fast path for 16 B-aligned rows (f = 128 fp16 -> 16 lanes)
     const int64_t warps = (n + (32 / cpr) * kRowUnroll - 1) / ((32 / cpr) * kRowUnroll);
     int64_t wgrid = (warps + 7) / 8;
-    const int64_t wcap = (int64_t)num_sms() * 8;
+    static const int bps = [] { const char* v = getenv("SAL_GATHER_BPS");
+                                return v && atoi(v) > 0 ? atoi(v) : 8; }();
+    const int64_t wcap = (int64_t)num_sms() * bps;
     if (wgrid > wcap) wgrid = wcap;
     if (wgrid < 1) wgrid = 1;
 #define SAL_GW_CASE(L)                                                                       \

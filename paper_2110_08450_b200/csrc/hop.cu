@@ -21,7 +21,6 @@
 namespace sal {
 
 constexpr uint64_t kEmpty = ~0ull;
-constexpr uint32_t kNewFlag = 0x80000000u;
 
 SAL_DEVINL uint32_t table_hash(uint32_t key, int log2cap) {
   return (uint32_t)(((uint64_t)key * kGolden) >> (64 - log2cap));
@@ -263,7 +262,8 @@ __global__ void __launch_bounds__(kScanThreads)
 flag_scan_kernel(const unsigned long long* __restrict__ table, const int32_t* __restrict__ slot,
                  const int32_t* __restrict__ src_glob, const int64_t* __restrict__ e_total,
                  const int64_t* __restrict__ size_old_ptr, int64_t* __restrict__ size_new_ptr,
-                 int32_t* __restrict__ rank_of, int32_t* __restrict__ globals, ScanWs ws) {
+                 int32_t* __restrict__ rank_of, int32_t* __restrict__ globals, ScanWs ws,
+                 int32_t* __restrict__ word_out) {
   __shared__ uint64_t sh_scan[kScanThreads / kWarp + 1];
   __shared__ uint64_t sh_prefix;
   __shared__ int sh_tile;
@@ -281,6 +281,9 @@ flag_scan_kernel(const unsigned long long* __restrict__ table, const int32_t* __
     if (e < n) {
       const unsigned long long w = table[slot[e]];
       const uint32_t lo = (uint32_t)w;
+      // deferred resolve: keep the edge's final table word (resolve_words, run later
+      // without the table)
+      if (word_out != nullptr) word_out[e] = (int32_t)lo;
       if ((lo & kNewFlag) && (lo & ~kNewFlag) == (uint32_t)e) {
         flags |= 1u << k;
         ++local;
@@ -481,7 +484,7 @@ cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_
                                const int64_t* size_old, int64_t* size_new,
                                const int32_t* src_glob, const int32_t* slot, int32_t* rank_of,
                                int32_t* src_local, void* scan_ws, cudaStream_t st,
-                               bool ws_zeroed, const NextCount* next) {
+                               bool ws_zeroed, const NextCount* next, bool defer_resolve) {
   ScanWs ws = carve_scan_ws(scan_ws, max_edges);
   cudaError_t err;
   if (!ws_zeroed) {
@@ -489,9 +492,10 @@ cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_
     if (err != cudaSuccess) return err;
   }
   flag_scan_kernel<<<scan_grid(max_edges), kScanThreads, 0, st>>>(
-      m.table, slot, src_glob, e_total, size_old, size_new, rank_of, m.globals, ws);
+      m.table, slot, src_glob, e_total, size_old, size_new, rank_of, m.globals, ws,
+      defer_resolve ? const_cast<int32_t*>(slot) : nullptr);
   err = cudaGetLastError();
-  if (err != cudaSuccess) return err;
+  if (err != cudaSuccess || defer_resolve) return err;
   int64_t grid = (max_edges + 255) / 256;
   if (grid < 1) grid = 1;
   if (grid > num_sms() * 16) grid = num_sms() * 16;

@@ -58,6 +58,14 @@ cudaError_t launch_rehash(const IdMapDev& m, int64_t n, cudaStream_t st);
 cudaError_t launch_keys_insert(const int64_t* keys, int64_t n, const IdMapDev& m,
                                int32_t* src_glob, int32_t* slot, int64_t* e_total,
                                cudaStream_t st);
+// a hop's deferred resolve (flag_scan kept each edge's table word in `words`)
+struct ResolveJob {
+  const int32_t* words;
+  const int64_t* e_total;
+  const int64_t* size_old;
+  const int32_t* rank_of;
+  int32_t* src_local;   // null: no job
+};
 // the next hop's count + scan, fused into the resolve launch of this hop
 struct NextCount {
   GraphDev g;
@@ -71,7 +79,8 @@ cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_
                                const int64_t* size_old, int64_t* size_new,
                                const int32_t* src_glob, const int32_t* slot, int32_t* rank_of,
                                int32_t* src_local, void* scan_ws, cudaStream_t st,
-                               bool ws_zeroed = false, const NextCount* next = nullptr);
+                               bool ws_zeroed = false, const NextCount* next = nullptr,
+                               bool defer_resolve = false);
 
 cudaError_t launch_sample_mean(const GraphDev& g, const int32_t* globals, const int64_t* n_dst,
                                int64_t max_dst, int32_t fanout, HopKey hk, const BatchDesc* desc,
@@ -79,7 +88,7 @@ cudaError_t launch_sample_mean(const GraphDev& g, const int32_t* globals, const 
                                void* out, int32_t out_dtype, int64_t out_stride, int64_t self_off,
                                int64_t* size_unknown, int bps_cap, unsigned long long* reset_table,
                                int64_t table_words, void* reset_scan, int64_t scan_bytes,
-                               cudaStream_t st);
+                               const ResolveJob& resolve, cudaStream_t st);
 cudaError_t launch_gather_rows(const void* x, int64_t x_rows, int32_t cols, int64_t x_stride,
                                int32_t in_dtype, const void* ids, int32_t id_bytes,
                                const int64_t* n_dev, int64_t n, void* out, int64_t out_stride,

@@ -167,8 +167,12 @@ sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
                    const TIn* __restrict__ table, int64_t t_stride, int vpr,
                    TOut* __restrict__ out, int64_t out_stride, int64_t self_off,
                    int64_t* __restrict__ size_unknown, ulonglong2* __restrict__ reset_table,
-                   int64_t table_pairs, uint4* __restrict__ reset_scan, int64_t scan_vecs) {
+                   int64_t table_pairs, uint4* __restrict__ reset_scan, int64_t scan_vecs,
+                   ResolveJob resolve) {
   extern __shared__ __align__(16) unsigned char sm_stage[];
+  if (resolve.src_local != nullptr)   // hop L-2's local ids (sal_sample_aggregate)
+    resolve_words(resolve, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                  (int64_t)gridDim.x * blockDim.x);
   if (reset_table != nullptr) {
     // the id table and scan workspace of hops 0..L-2 are no longer read: leave them
     // reset for this workspace's next batch (sal_mfg_plan.reset_in_aggregate)
@@ -343,7 +347,8 @@ static cudaError_t launch_sm(const GraphDev& g, const int32_t* globals, const in
                              const void* table, int64_t t_stride, int vpr, void* out,
                              int64_t out_stride, int64_t self_off, int64_t* size_unknown,
                              int bps_cap, unsigned long long* reset_table, int64_t table_words,
-                             void* reset_scan, int64_t scan_bytes, cudaStream_t st) {
+                             void* reset_scan, int64_t scan_bytes, const ResolveJob& resolve,
+                             cudaStream_t st) {
   const int smem = (kSmThreads / 32) * 2 * stage_bytes<kRows>();
   auto k = vpr == 16 ? sample_mean_kernel<kPolicy, __half, TO, kRows, true>
                      : sample_mean_kernel<kPolicy, __half, TO, kRows, false>;
@@ -369,7 +374,8 @@ static cudaError_t launch_sm(const GraphDev& g, const int32_t* globals, const in
                                          (const __half*)table, t_stride, vpr, (TO*)out,
                                          out_stride, self_off, size_unknown,
                                          (ulonglong2*)reset_table, table_words / 2,
-                                         (uint4*)reset_scan, reset_table ? scan_bytes / 16 : 0);
+                                         (uint4*)reset_scan, reset_table ? scan_bytes / 16 : 0,
+                                         resolve);
   return cudaGetLastError();
 }
 
@@ -379,12 +385,12 @@ cudaError_t launch_sample_mean(const GraphDev& g, const int32_t* globals, const 
                                void* out, int32_t out_dtype, int64_t out_stride, int64_t self_off,
                                int64_t* size_unknown, int bps_cap, unsigned long long* reset_table,
                                int64_t table_words, void* reset_scan, int64_t scan_bytes,
-                               cudaStream_t st) {
+                               const ResolveJob& resolve, cudaStream_t st) {
   const int vpr = cols * 2 / 16;
 #define SAL_SM(P, TO, R)                                                                   \
   return launch_sm<P, TO, R>(g, globals, n_dst, max_dst, fanout, hk, desc, table, t_stride, \
                              vpr, out, out_stride, self_off, size_unknown, bps_cap, reset_table, \
-                             table_words, reset_scan, scan_bytes, st)
+                             table_words, reset_scan, scan_bytes, resolve, st)
 // stage rows: the smallest of 16 / 20 / 32 that holds the fanout (shared memory per
 // warp bounds the resident warps, and with them the rows in flight per SM)
 #define SAL_SM_R(P, TO)                 \

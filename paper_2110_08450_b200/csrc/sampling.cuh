@@ -58,4 +58,21 @@ SAL_DEVINL uint32_t draw_position(uint64_t key, uint2 pkey, uint32_t ctr, uint32
   }
 }
 
+// id-table word of a new key: {key:32 | kNewFlag | first_edge:31} (hop.cu)
+constexpr uint32_t kNewFlag = 0x80000000u;
+
+// Deferred relabel pass 2 of the last sampled hop of a fused plan, run by the fused
+// last hop's kernel: every edge resolves its local id from the table word flag_scan
+// kept for it (no table access; first occurrences need no finalising, the table is
+// not read again for this batch)
+SAL_DEVINL void resolve_words(const ResolveJob& j, int64_t first, int64_t stride) {
+  const int64_t n = *j.e_total;
+  const int64_t size_old = *j.size_old;
+  for (int64_t e = first; e < n; e += stride) {
+    const uint32_t lo = (uint32_t)j.words[e];
+    j.src_local[e] = (lo & kNewFlag) ? (int32_t)(size_old + j.rank_of[lo & ~kNewFlag])
+                                     : (int32_t)lo;
+  }
+}
+
 }  // namespace sal

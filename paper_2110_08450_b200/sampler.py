@@ -351,7 +351,8 @@ class MfgWorkspace:
     def __init__(self, num_nodes: int, fanouts: FanoutSpec, max_seeds: int, device=None,
                  last_hop_edges: bool = False, sample_lanes: int = 0, sample_bps: int = 0,
                  table_factor: int = 1, last_hop_fused: bool = False,
-                 aggregate_bps: int = 0, reset_in_aggregate: bool = False):
+                 aggregate_bps: int = 0, reset_in_aggregate: bool = False,
+                 resolve_in_aggregate: bool = False):
         """last_hop_edges: SAL_MFG_LAST_HOP_EDGES — the last hop only emits global
         source ids (src_glob); its relabel is skipped (training with the
         layer-0 mean read straight from the feature table).
@@ -359,7 +360,10 @@ class MfgWorkspace:
         aggregate() samples the last hop straight into the layer-0 mean.
         aggregate_bps: resident blocks per SM of aggregate() (0 = as many as fit).
         reset_in_aggregate: (fused plans) run() skips the table/scan resets and
-        aggregate() leaves them reset for the next batch; reset once here."""
+        aggregate() leaves them reset for the next batch; reset once here.
+        resolve_in_aggregate: (fused plans) hop L-2's src_local is written by
+        aggregate(), whose kernel runs that hop's relabel second pass (the fused
+        kernel starts one launch earlier); read the MFG after aggregate()."""
         _lib.require_cuda()
         L = _lib.lib()
         self.device = torch.device(device or "cuda")
@@ -380,6 +384,7 @@ class MfgWorkspace:
             raise ValueError("table_factor must be a power of two")
         self.plan.aggregate_blocks_per_sm = int(aggregate_bps)
         self.plan.reset_in_aggregate = 1 if (reset_in_aggregate and self.last_hop_fused) else 0
+        self.plan.resolve_in_aggregate = 1 if (resolve_in_aggregate and self.last_hop_fused) else 0
         self.plan.sample_lanes = int(sample_lanes)
         self.plan.sample_blocks_per_sm = int(sample_bps)
         self.plan.table_cap = int(self.plan.table_cap) * int(table_factor)

@@ -169,3 +169,39 @@ def test_reset_in_aggregate_reuses_the_workspace(g128):
         assert int(ws.sizes[h].item()) == n
         assert torch.equal(out[:n].view(torch.int16), want[:n].view(torch.int16)), b
         assert bool((ws.table == -1).all())          # left reset for the next batch
+
+
+@pytest.mark.parametrize("fan", [(15, 10, 5), (20, 20, 20), (3, 4), (2, 3, 4, 5)])
+def test_resolve_in_aggregate_gives_the_same_mfg(g128, fan):
+    """sal_mfg_plan.resolve_in_aggregate: hop L-2's relabel second pass runs inside the
+    fused kernel (from the table words flag_scan kept).  After aggregate() the MFG of
+    hops 0..L-2 (sizes, indptr, local ids, globals) and the [mean | self] buffer equal
+    the in-chain resolve's, batch after batch on one workspace."""
+    fan = FanoutSpec(fan)
+    kw = dict(device="cuda", last_hop_fused=True, reset_in_aggregate=True)
+    ref = MfgWorkspace(g128.num_nodes, fan, 1024, **kw)
+    ws = MfgWorkspace(g128.num_nodes, fan, 1024, resolve_in_aggregate=True, **kw)
+    assert ws.plan.resolve_in_aggregate == 1 and ref.plan.resolve_in_aggregate == 0
+    h = ws.num_hops - 1
+    rng = np.random.default_rng(len(fan) + 31)
+    for b in range(3):
+        seeds = torch.from_numpy(rng.choice(g128.num_nodes, 1024, replace=False)).cuda()
+        desc = torch.tensor([b, 0, 1024], dtype=torch.int64, device="cuda")
+        outs = []
+        for w in (ref, ws):
+            w.src_local[h - 1].fill_(-7)
+            w.run(g128, seeds, desc, 5, 0)
+            out = torch.zeros((w.node_cap[h], 256), dtype=torch.bfloat16, device="cuda")
+            w.aggregate(g128, g128.features, out, 128, desc, 5, 0)
+            outs.append(out)
+        assert torch.equal(ref.sizes[:h + 1], ws.sizes[:h + 1])
+        n = int(ws.sizes[h].item())
+        assert torch.equal(ref.globals[:n], ws.globals[:n])
+        for k in range(h):
+            e = int(ws.etot[k].item())
+            assert torch.equal(ref.dst_indptr[k][:int(ws.sizes[k].item()) + 1],
+                               ws.dst_indptr[k][:int(ws.sizes[k].item()) + 1]), (b, k)
+            assert torch.equal(ref.src_local[k][:e], ws.src_local[k][:e]), (b, k)
+            assert int(ws.src_local[k][:e].min()) >= 0
+        assert torch.equal(outs[0][:n].view(torch.int16), outs[1][:n].view(torch.int16))
+        assert bool((ws.table == -1).all())

@@ -2,7 +2,7 @@
 f32 features, labels) at P = 1, 2, 4, 8 concurrent batches on the papers shape, with
 the host time split into launch / wait / finish per batch.
 
-python tools/prep_scaling.py [batches]   (under gpurun)
+python tools/prep_scaling.py [batches] [P,P,...]   (under gpurun)
 """
 import sys
 import time
@@ -38,9 +38,11 @@ def finish(*a, **k):
 
 
 P._prep_one, P._finish_slot = prep_one, finish
-for p in (1, 2, 4, 8):
+ps = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 2, 4, 8]
+for p in ps:
     for delivery in ("in_order", "completion_order"):
-        cfg = PrepConfig(num_workers=p, fanouts=FanoutSpec((15, 10, 5)), delivery=delivery)
+        cfg = PrepConfig(num_workers=p, fanouts=FanoutSpec((15, 10, 5)), delivery=delivery,
+                         feature_dtype="f32")
         for _ in run_epoch_prep(dg, x, dg.labels, P.EpochPlan(batches=plan.batches[:2 * p],
                                                               batch_size=1024, shuffle_seed=0),
                                 cfg, 1):
