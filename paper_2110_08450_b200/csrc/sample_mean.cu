@@ -122,7 +122,15 @@ SAL_DEVINL int sample_dst(const int32_t* __restrict__ indices, int d, int64_t lo
 // 16 bytes global -> shared, L2 policy evict_first: every feature row is read once per
 // batch, so it should not push the step's reused tensors (the layer-0 input this
 // kernel writes, the backward's gradients) out of L2
+// pred false: the 16 bytes are zero-filled (src-size 0, nothing is read), so the
+// consumer adds +0 for rows past the count without selecting
 SAL_DEVINL void cp_async16(uint32_t smem, const void* gmem, bool pred, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(smem),
+               "l"(gmem), "r"(pred ? 16 : 0), "l"(policy)
+               : "memory");
+}
+// pred false: no copy at all (the self row's slot is shared by both lane groups)
+SAL_DEVINL void cp_async16_if(uint32_t smem, const void* gmem, bool pred, uint64_t policy) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
       "@q cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %3;\n\t}" ::"r"(smem),
@@ -220,7 +228,7 @@ sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
       const int id = __shfl_sync(0xffffffffu, sid, e);
       cp_async16(sb + e * 256, tbase + (int64_t)id * tbytes, e < cnt && vlane, pol);
     }
-    cp_async16(sb + kRows * 256, tbase + (int64_t)v * tbytes, do_self, pol);
+    cp_async16_if(sb + kRows * 256, tbase + (int64_t)v * tbytes, do_self, pol);
     cp_async_commit();
   };
   auto recip_of = [&](int64_t lo, int64_t hi) -> uint64_t {
@@ -282,19 +290,11 @@ sample_mean_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
     float acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-    // branch-free: rows past the count add +0 (acc starts at +0 and so is never -0,
-    // which makes the add exact no-op)
+    // branch-free: rows past the count were zero-filled and add +0 (acc starts at +0
+    // and so is never -0, which makes the add an exact no-op)
 #pragma unroll
-    for (int u = 0; u < kRows / 2; ++u) {
-      const int e = u * 2 + grp;
-      uint4 v = *reinterpret_cast<const uint4*>(ls + e * 256);
-      const bool on = e < cnt && vlane;
-      v.x = on ? v.x : 0u;
-      v.y = on ? v.y : 0u;
-      v.z = on ? v.z : 0u;
-      v.w = on ? v.w : 0u;
-      acc8<TIn>(acc, v);
-    }
+    for (int u = 0; u < kRows / 2; ++u)
+      acc8<TIn>(acc, *reinterpret_cast<const uint4*>(ls + (u * 2 + grp) * 256));
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
     if (cnt > 0) {
