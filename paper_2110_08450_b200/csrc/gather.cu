@@ -199,9 +199,7 @@ static cudaError_t gather_dispatch(const void* x, int32_t cols, int64_t x_stride
     // whole rows per warp: the fast path for 16 B-aligned rows (f = 128 fp16 -> 16 lanes)
     const int64_t warps = (n + (32 / cpr) * kRowUnroll - 1) / ((32 / cpr) * kRowUnroll);
     int64_t wgrid = (warps + 7) / 8;
-    static const int bps = [] { const char* v = getenv("SAL_GATHER_BPS");
-                                return v && atoi(v) > 0 ? atoi(v) : 8; }();
-    const int64_t wcap = (int64_t)num_sms() * bps;
+    const int64_t wcap = (int64_t)num_sms() * 8;
     if (wgrid > wcap) wgrid = wcap;
     if (wgrid < 1) wgrid = 1;
 #define SAL_GW_CASE(L)                                                                       \
