@@ -73,6 +73,8 @@ class TrainConfig:
     # resident blocks per SM of the fused last hop in training: three 4-warp blocks leave
     # room for a 3-stage tcgen05 weight-gradient CTA beside them (164 -> 161 us per step)
     fused_bps: int = 3
+    # hop L-2's resolve inside the fused kernel (sal_mfg_plan.resolve_in_aggregate)
+    fused_resolve: bool = True
 
 
 def shard_plan(plan, batch_size: int, rank: int, world: int):
@@ -157,9 +159,8 @@ class _Slot:
                                aggregate_bps=cfg.fused_bps if backward else 0,
                                reset_in_aggregate=True,
                                # hop L-2's resolve inside the fused kernel: sampled inference
-                               # 0.0543 -> 0.0528 s; the training step 149.9 -> 151.2 us (the
-                               # fused kernel then starts on top of the layer-0 forward)
-                               resolve_in_aggregate=not backward)
+                               # 0.0543 -> 0.0528 s, the training step 147.5 -> 146.0 us
+                               resolve_in_aggregate=(not backward) or cfg.fused_resolve)
         ws = self.ws
         nh = ws.num_hops
         rows = ws.node_cap[-1] if not cfg.gather_free else ws.node_cap[-2]
