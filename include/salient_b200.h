@@ -155,6 +155,16 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
                    void* ws_dev, const int64_t* seeds_base_dev, const sal_batch_desc* desc_dev,
                    uint64_t global_seed, int32_t rng_policy, void* stream);
 
+/* sal_plan_next + sal_sample_mfg in one: *desc_out = desc_all[*cursor] (an empty
+ * batch past n_steps), ++*cursor, then the sample of that batch — the cursor step
+ * rides in the seed-insertion kernel, so a captured per-step graph starts its
+ * batch preparation one launch earlier. */
+int sal_sample_mfg_next(const sal_graph* g, const sal_mfg_plan* plan,
+                        const sal_mfg_layout* layout, void* ws_dev,
+                        const int64_t* seeds_base_dev, const int64_t* desc_all_dev,
+                        int64_t n_steps, int64_t* cursor_dev, sal_batch_desc* desc_out_dev,
+                        uint64_t global_seed, int32_t rng_policy, void* stream);
+
 /* Fused last hop (plan flag SAL_MFG_LAST_HOP_FUSED), after sal_sample_mfg on the
  * same stream: for each destination d < sizes[L-1] of hop L-1, draw its fanout
  * sample exactly as sal_sample_mfg would (hop_kernel + _sample_positions,

@@ -108,6 +108,8 @@ SIGNATURES = {
     "sal_segment_mean_bwd": (ctypes.c_int, [vp, vp, vp, i64, vp, i32, i64, i32, vp, i64, vp]),
     "sal_segment_mean_fwd_global": (ctypes.c_int, [vp, vp, vp, vp, i64, vp, i32, i64, i32, vp,
                                                    i32, i64, vp]),
+    "sal_sample_mfg_next": (ctypes.c_int, [P(SalGraph), P(SalMfgPlan), P(SalMfgLayout), vp, vp, vp,
+                                           i64, vp, vp, u64, i32, vp]),
     "sal_plan_next": (ctypes.c_int, [vp, i64, vp, vp, vp]),
     "sal_relu_dropout_fwd": (ctypes.c_int, [vp, i64, vp, i64, i64, i32, i32, vp, ctypes.c_float,
                                             u64, vp, vp]),

@@ -200,7 +200,8 @@ int sal_mfg_layout_init(const sal_mfg_plan* plan, sal_mfg_layout* L) {
 static int sample_mfg_hops(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
                            void* ws, const int64_t* seeds_base, const sal_batch_desc* desc,
                            uint64_t global_seed, int32_t rng_policy, int32_t hop_begin,
-                           int32_t hop_end, void* stream) {
+                           int32_t hop_end, void* stream,
+                           const sal::PlanCursor* next = nullptr) {
   if (g == nullptr || plan == nullptr || L == nullptr || ws == nullptr || seeds_base == nullptr ||
       desc == nullptr)
     return fail(SAL_EINVAL, "sample_mfg: null argument");
@@ -239,7 +240,10 @@ static int sample_mfg_hops(const sal_graph* g, const sal_mfg_plan* plan, const s
       if (e == cudaSuccess) e = cudaMemsetAsync(scan, 0, L->scan_bytes, st);
       if (e != cudaSuccess) return cuda_status(e, "sample_mfg: table reset");
     }
-    e = sal::launch_seed_insert(seeds_base, desc, m, plan->max_seeds, st);
+    if (next != nullptr)   // *desc = the plan's next step, then its seeds
+      e = sal::launch_seed_insert_next(seeds_base, *next, (sal::BatchDesc*)desc, m, st);
+    else
+      e = sal::launch_seed_insert(seeds_base, desc, m, plan->max_seeds, st);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: seed insert");
     e = sal::launch_hop_count(gd, m.globals, sizes, plan->node_cap[0], plan->fanout[0],
                               (int32_t*)(base + L->dst_indptr[0]), etot, scan_ws(0, 0), st,
@@ -302,6 +306,18 @@ int sal_sample_mfg(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_l
   if (plan == nullptr) return fail(SAL_EINVAL, "sample_mfg: null argument");
   return sample_mfg_hops(g, plan, L, ws, seeds_base, desc, global_seed, rng_policy, 0,
                          plan->num_hops, stream);
+}
+
+int sal_sample_mfg_next(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,
+                        void* ws, const int64_t* seeds_base, const int64_t* desc_all,
+                        int64_t n_steps, int64_t* cursor, sal_batch_desc* desc_out,
+                        uint64_t global_seed, int32_t rng_policy, void* stream) {
+  if (plan == nullptr || desc_all == nullptr || cursor == nullptr || desc_out == nullptr)
+    return fail(SAL_EINVAL, "sample_mfg_next: null argument");
+  if (n_steps < 0) return fail(SAL_EINVAL, "sample_mfg_next: n_steps %lld < 0", (long long)n_steps);
+  const sal::PlanCursor pc{desc_all, n_steps, cursor};
+  return sample_mfg_hops(g, plan, L, ws, seeds_base, desc_out, global_seed, rng_policy, 0,
+                         plan->num_hops, stream, &pc);
 }
 
 int sal_sample_aggregate(const sal_graph* g, const sal_mfg_plan* plan, const sal_mfg_layout* L,

@@ -79,6 +79,38 @@ __global__ void seed_insert_kernel(const int64_t* __restrict__ seeds_base,
   }
 }
 
+// seed insertion that first takes the next batch off a device epoch plan (what
+// sal_plan_next does, folded in: one launch fewer at the head of the chain).  One
+// block, so thread 0 alone reads and advances the cursor.
+__global__ void __launch_bounds__(1024)
+seed_insert_next_kernel(const int64_t* __restrict__ seeds_base,
+                        const int64_t* __restrict__ desc_all, int64_t n_steps,
+                        int64_t* __restrict__ cursor, BatchDesc* __restrict__ desc_out,
+                        unsigned long long* table, int log2cap, int32_t* __restrict__ globals,
+                        int64_t* __restrict__ size0) {
+  __shared__ int64_t sh[3];
+  if (threadIdx.x == 0) {
+    const int64_t c = *cursor;
+    const bool live = c < n_steps;
+    sh[0] = live ? desc_all[3 * c + 0] : -1;
+    sh[1] = live ? desc_all[3 * c + 1] : 0;
+    sh[2] = live ? desc_all[3 * c + 2] : 0;
+    desc_out->batch_id = sh[0];
+    desc_out->seed_offset = sh[1];
+    desc_out->n_seeds = sh[2];
+    *cursor = c + 1;
+    *size0 = sh[2];
+  }
+  __syncthreads();
+  const int64_t n = sh[2];
+  const int64_t* seeds = seeds_base + sh[1];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t key = (uint32_t)seeds[i];
+    globals[i] = (int32_t)key;
+    table_insert_assigned(table, log2cap, key, (uint32_t)i);
+  }
+}
+
 // re-insert locals 0..n-1 into a fresh table (sampler.py:131-145 ensure_capacity)
 __global__ void rehash_kernel(const int32_t* __restrict__ globals, int64_t n,
                               unsigned long long* table, int log2cap) {
@@ -410,6 +442,14 @@ cudaError_t launch_seed_insert(const int64_t* seeds_base, const BatchDesc* desc,
   if (grid < 1) grid = 1;
   seed_insert_kernel<<<grid, 256, 0, st>>>(seeds_base, desc, m.table, m.log2cap, m.globals,
                                            m.size_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seed_insert_next(const int64_t* seeds_base, const PlanCursor& pc,
+                                    BatchDesc* desc_out, const IdMapDev& m, cudaStream_t st) {
+  seed_insert_next_kernel<<<1, 1024, 0, st>>>(seeds_base, pc.desc_all, pc.n_steps, pc.cursor,
+                                              desc_out, m.table, m.log2cap, m.globals,
+                                              m.size_out);
   return cudaGetLastError();
 }
 

@@ -43,6 +43,14 @@ void count_launch(int kernels);
 int log2_exact(int64_t cap);
 size_t scan_ws_bytes(int64_t max_items);
 
+// a device epoch plan: desc_all[3 * step] rows, the next step at *cursor
+struct PlanCursor {
+  const int64_t* desc_all;
+  int64_t n_steps;
+  int64_t* cursor;
+};
+cudaError_t launch_seed_insert_next(const int64_t* seeds_base, const PlanCursor& pc,
+                                    BatchDesc* desc_out, const IdMapDev& m, cudaStream_t st);
 cudaError_t launch_seed_insert(const int64_t* seeds_base, const BatchDesc* desc,
                                const IdMapDev& m, int64_t max_seeds, cudaStream_t st);
 cudaError_t launch_hop_count(const GraphDev& g, const int32_t* globals, const int64_t* n_dst,

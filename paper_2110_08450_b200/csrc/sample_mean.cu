@@ -391,10 +391,12 @@ cudaError_t launch_sample_mean(const GraphDev& g, const int32_t* globals, const 
   return launch_sm<P, TO, R>(g, globals, n_dst, max_dst, fanout, hk, desc, table, t_stride, \
                              vpr, out, out_stride, self_off, size_unknown, bps_cap, reset_table, \
                              table_words, reset_scan, scan_bytes, resolve, st)
-// stage rows: the smallest of 16 / 20 / 32 that holds the fanout (shared memory per
+// stage rows: the smallest of 8 / 16 / 20 / 32 that holds the fanout (shared memory per
 // warp bounds the resident warps, and with them the rows in flight per SM)
 #define SAL_SM_R(P, TO)                 \
-  if (fanout <= 16) {                   \
+  if (fanout <= 8) {                    \
+    SAL_SM(P, TO, 8);                   \
+  } else if (fanout <= 16) {            \
     SAL_SM(P, TO, 16);                  \
   } else if (fanout <= 20) {            \
     SAL_SM(P, TO, 20);                  \

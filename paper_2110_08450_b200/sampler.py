@@ -432,6 +432,21 @@ class MfgWorkspace:
                                     int(global_seed) & MASK64, int(rng_policy),
                                     _lib.stream_ptr(stream)), "sample_mfg")
 
+    def run_next(self, g: DeviceGraph, seeds_base: torch.Tensor, desc_all: torch.Tensor,
+                 n_steps: int, cursor: torch.Tensor, desc_out: torch.Tensor, global_seed: int,
+                 rng_policy: int = _lib.SAL_RNG_SPLITMIX, stream=None) -> None:
+        """run() on the next step of a device epoch plan: desc_out = desc_all[cursor]
+        (an empty batch past n_steps), cursor += 1, then the sample — the cursor step
+        rides in the seed-insertion kernel (sal_sample_mfg_next)."""
+        L = _lib.lib()
+        gc = g.cstruct
+        _lib.check(L.sal_sample_mfg_next(ctypes.byref(gc), ctypes.byref(self.plan),
+                                         ctypes.byref(self.layout), self.buf.data_ptr(),
+                                         seeds_base.data_ptr(), desc_all.data_ptr(), int(n_steps),
+                                         cursor.data_ptr(), desc_out.data_ptr(),
+                                         int(global_seed) & MASK64, int(rng_policy),
+                                         _lib.stream_ptr(stream)), "sample_mfg_next")
+
     def aggregate(self, g: DeviceGraph, table: torch.Tensor, out: torch.Tensor,
                   self_offset: int, desc: torch.Tensor, global_seed: int,
                   rng_policy: int = _lib.SAL_RNG_SPLITMIX, stream=None) -> None:

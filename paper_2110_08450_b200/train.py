@@ -328,15 +328,13 @@ class Trainer:
         is left to _fill)."""
         ws = slot.ws
         st = torch.cuda.current_stream()
-        L = _lib.lib()
         if stage is not None:  # this step's inputs, already copied H2D (run_steps)
             desc, seeds_base = stage.ddesc, stage.dseeds
-        else:
-            _lib.check(L.sal_plan_next(self.desc_all.data_ptr(), self.n_steps_dev,
-                                       self.cursor.data_ptr(), slot.desc.data_ptr(),
-                                       _lib.stream_ptr(st)), "plan_next")
-            desc, seeds_base = slot.desc, self.seeds_all
-        ws.run(self.dg, seeds_base, desc, self.sample_seed, self.policy, st)
+            ws.run(self.dg, seeds_base, desc, self.sample_seed, self.policy, st)
+        else:  # the plan cursor's next step, advanced inside the first sampling kernel
+            desc = slot.desc
+            ws.run_next(self.dg, self.seeds_all, self.desc_all, self.n_steps_dev, self.cursor,
+                        desc, self.sample_seed, self.policy, st)
         slot.desc_used = desc
 
     def _fill(self, slot: _Slot) -> None:

@@ -347,3 +347,43 @@ def test_pairwise_inclusion_by_degree(policy):
         assert obs.sum() == per * f * (f - 1) // 2
         assert stats.chisquare(obs).pvalue > 1e-4, (d, obs)
         assert stats.chisquare(single).pvalue > 1e-4, (d, single)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_sample_mfg_next_equals_plan_next_then_sample(fused):
+    """sal_sample_mfg_next (the plan cursor folded into the seed-insertion kernel) gives
+    the descriptor, cursor and MFG of sal_plan_next followed by sal_sample_mfg, step
+    after step, including the empty batch past the end of the plan."""
+    from paper_2110_08450_b200 import _lib
+    from paper_2110_08450_b200.graph import synth_graph_device
+    from paper_2110_08450_b200.sampler import MfgWorkspace
+    g = synth_graph_device(50_000, 12.0, 3.0, seed=3, num_features=16, num_classes=4,
+                           feature_seed=3, label_seed=3)
+    rng = np.random.default_rng(5)
+    perm = torch.from_numpy(rng.permutation(g.num_nodes)[:3000].astype(np.int64)).cuda()
+    desc_all = torch.tensor([[7, 0, 1024], [3, 1024, 1024], [9, 2048, 952]],
+                            dtype=torch.int64, device="cuda")
+    fan = FanoutSpec((15, 10, 5))
+    kw = dict(device="cuda", last_hop_fused=fused)
+    a, b = MfgWorkspace(g.num_nodes, fan, 1024, **kw), MfgWorkspace(g.num_nodes, fan, 1024, **kw)
+    ca = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    da = torch.zeros(3, dtype=torch.int64, device="cuda")
+    db = torch.zeros(3, dtype=torch.int64, device="cuda")
+    L = _lib.lib()
+    for step in range(4):
+        _lib.check(L.sal_plan_next(desc_all.data_ptr(), 3, ca.data_ptr(), da.data_ptr(),
+                                   _lib.stream_ptr()), "plan_next")
+        a.run(g, perm, da, 11, 0)
+        b.run_next(g, perm, desc_all, 3, cb, db, 11, 0)
+        assert torch.equal(da, db) and int(cb.item()) == step + 1 == int(ca.item())
+        assert torch.equal(a.sizes, b.sizes) and torch.equal(a.etot, b.etot)
+        h = a.num_hops - (1 if fused else 0)
+        for k in range(h):
+            n, e = int(a.sizes[k].item()), int(a.etot[k].item())
+            assert torch.equal(a.dst_indptr[k][:n + 1], b.dst_indptr[k][:n + 1])
+            if not (fused and k == h - 1):   # hops 0..L-2 relabelled in the chain
+                assert torch.equal(a.src_local[k][:e], b.src_local[k][:e])
+        n = int(a.sizes[h].item())
+        assert torch.equal(a.globals[:n], b.globals[:n])
+    assert db.tolist() == [-1, 0, 0] and int(b.sizes[0].item()) == 0

@@ -14,6 +14,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
+from paper_2110_08450_b200.sampler import FanoutSpec  # noqa: E402
 from paper_2110_08450_b200.train import TrainConfig, Trainer  # noqa: E402
 
 
@@ -37,6 +38,7 @@ def main():
     ap.add_argument("--steps", type=int, default=0)
     ap.add_argument("--shape", default="papers")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--fanouts", default="15,10,5")
     ap.add_argument("variants", nargs="*")
     a = ap.parse_args()
     variants = [("base", {})] + [parse_variant(v) for v in a.variants]
@@ -44,8 +46,9 @@ def main():
     res = {n: [] for n, _ in variants}
     for rep in range(a.reps):
         for name, kw in variants:
-            tr = Trainer(dg, train, TrainConfig(gather_free=True, **{k: v for k, v in kw.items()
-                                                                    if not k.startswith("m.")}))
+            tr = Trainer(dg, train, TrainConfig(gather_free=True, fanouts=FanoutSpec.parse(a.fanouts),
+                                                **{k: v for k, v in kw.items()
+                                                   if not k.startswith("m.")}))
             for k, v in kw.items():
                 if k.startswith("m."):
                     setattr(tr.model, k[2:], v)
