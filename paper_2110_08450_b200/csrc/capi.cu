@@ -295,7 +295,7 @@ static int sample_mfg_hops(const sal_graph* g, const sal_mfg_plan* plan, const s
                                 src_glob, slot, rank, src_local, scan_ws(h, 1), st,
                                 /*ws_zeroed=*/true, has_next ? &nc : nullptr, defer);
     if (e != cudaSuccess) return cuda_status(e, "sample_mfg: hop relabel");
-    kernels += defer ? 2 : 3;
+    kernels += (defer || !has_next) ? 2 : 3;   // the last relabel resolves in its scan launch
   }
   return counted(SAL_OK, kernels);
 }
@@ -416,7 +416,7 @@ int sal_idmap_insert(const sal_idmap* m, const int64_t* keys, int64_t n,
   if (e != cudaSuccess) return cuda_status(e, "idmap_insert");
   e = sal::launch_hop_relabel(d, n_dev_scratch, n, size_old, size_new, scratch_glob, scratch_slot,
                               scratch_rank, local_out, scan_ws, st);
-  return counted(cuda_status(e, "idmap_insert: relabel"), 3);
+  return counted(cuda_status(e, "idmap_insert: relabel"), 2);
 }
 
 int sal_hop_count(const sal_graph* g, const int32_t* globals, const int64_t* n_dst_dev,
@@ -485,7 +485,7 @@ int sal_hop_relabel(const sal_idmap* m, const int64_t* e_total, int64_t max_edge
   return counted(cuda_status(sal::launch_hop_relabel(d, e_total, max_edges, size_old, size_new, src_glob,
                                              slot, rank, src_local, scan_ws,
                                              (cudaStream_t)stream),
-                     "hop_relabel"), 2);
+                     "hop_relabel"), 1);
 }
 
 // ---------------------------------------------------------------------------

@@ -141,7 +141,8 @@ SAL_DEVINL T block_exclusive_scan(T v, T* smem, T* total) {
 // ---------------------------------------------------------------------------
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagInc = 2ull << 62;
-constexpr uint64_t kValMask = (1ull << 62) - 1;
+constexpr uint64_t kFlagRanks = 1ull << 61;  // flag_scan_kernel<true>: the tile's ranks are written
+constexpr uint64_t kValMask = (1ull << 61) - 1;
 
 struct ScanWs {
   unsigned long long* status;  // [max_tiles]

@@ -290,12 +290,20 @@ __global__ void keys_insert_kernel(const int64_t* __restrict__ keys, int64_t n,
 // ---------------------------------------------------------------------------
 // relabel pass 1: first-occurrence flags -> scan -> new locals appended
 // ---------------------------------------------------------------------------
+// kResolve: the chain's last relabel (no next-hop count rides with its resolve)
+// also runs pass 2 in the same launch.  Every edge already holds its table word;
+// a first occurrence at edge `first` <= e lives in this tile or an earlier one,
+// and tiles are taken in order (grab_tile), so an edge waits only for a tile that
+// is already running: that tile sets kFlagRanks in its scan status once its
+// rank_of entries are written.  A word read after the first's tile finalized its
+// slot carries the local itself, so either reading resolves to the same local.
+template <bool kResolve>
 __global__ void __launch_bounds__(kScanThreads)
-flag_scan_kernel(const unsigned long long* __restrict__ table, const int32_t* __restrict__ slot,
+flag_scan_kernel(unsigned long long* table, const int32_t* __restrict__ slot,
                  const int32_t* __restrict__ src_glob, const int64_t* __restrict__ e_total,
                  const int64_t* __restrict__ size_old_ptr, int64_t* __restrict__ size_new_ptr,
-                 int32_t* __restrict__ rank_of, int32_t* __restrict__ globals, ScanWs ws,
-                 int32_t* __restrict__ word_out) {
+                 int32_t* rank_of, int32_t* __restrict__ globals, ScanWs ws,
+                 int32_t* __restrict__ word_out, int32_t* __restrict__ src_local) {
   __shared__ uint64_t sh_scan[kScanThreads / kWarp + 1];
   __shared__ uint64_t sh_prefix;
   __shared__ int sh_tile;
@@ -307,11 +315,18 @@ flag_scan_kernel(const unsigned long long* __restrict__ table, const int32_t* __
   const int64_t base = (int64_t)tile * kScanTile + threadIdx.x * kScanItems;
   uint32_t flags = 0;
   uint64_t local = 0;
+  unsigned long long words[kScanItems];
+  int32_t slots[kScanItems];
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     const int64_t e = base + k;
+    words[k] = 0;
+    slots[k] = 0;
     if (e < n) {
-      const unsigned long long w = table[slot[e]];
+      slots[k] = slot[e];
+      const unsigned long long w = kResolve ? *((volatile unsigned long long*)&table[slots[k]])
+                                            : table[slots[k]];
+      words[k] = w;
       const uint32_t lo = (uint32_t)w;
       // deferred resolve: keep the edge's final table word (resolve_words, run later
       // without the table)
@@ -337,6 +352,32 @@ flag_scan_kernel(const unsigned long long* __restrict__ table, const int32_t* __
   }
   if (tile == ntiles - 1 && threadIdx.x == kScanThreads - 1)
     *size_new_ptr = size_old + (int64_t)(prefix + tile_total);
+  if (!kResolve) return;
+  __syncthreads();  // this tile's ranks, for the block
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicOr(&ws.status[tile], (unsigned long long)kFlagRanks);
+  }
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t e = base + k;
+    if (e >= n) continue;
+    const unsigned long long w = words[k];
+    const uint32_t lo = (uint32_t)w;
+    uint32_t loc = lo;
+    if (lo & kNewFlag) {
+      const uint32_t first = lo & ~kNewFlag;
+      const int ft = (int)(first / kScanTile);
+      if (ft != tile) {
+        while ((*((volatile unsigned long long*)&ws.status[ft]) & kFlagRanks) == 0) {
+        }
+        __threadfence();
+      }
+      loc = (uint32_t)(size_old + *((volatile int32_t*)&rank_of[first]));
+      if (first == (uint32_t)e) table[slots[k]] = (w & 0xFFFFFFFF00000000ull) | loc;
+    }
+    if (src_local != nullptr) src_local[e] = (int32_t)loc;
+  }
 }
 
 // relabel pass 2: every edge resolves its local id; first occurrences
@@ -362,15 +403,6 @@ SAL_DEVINL void resolve_range(unsigned long long* table, const int32_t* __restri
     }
     if (src_local != nullptr) src_local[e] = (int32_t)local;
   }
-}
-
-__global__ void resolve_kernel(unsigned long long* table, const int32_t* __restrict__ slot,
-                               const int64_t* __restrict__ e_total,
-                               const int64_t* __restrict__ size_old_ptr,
-                               const int32_t* __restrict__ rank_of,
-                               int32_t* __restrict__ src_local) {
-  resolve_range(table, slot, e_total, size_old_ptr, rank_of, src_local,
-                blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
 // resolve of hop h and the count + scan of hop h+1 in one launch: both read only
@@ -531,19 +563,20 @@ cudaError_t launch_hop_relabel(const IdMapDev& m, const int64_t* e_total, int64_
     err = cudaMemsetAsync(scan_ws, 0, scan_ws_bytes(max_edges), st);
     if (err != cudaSuccess) return err;
   }
-  flag_scan_kernel<<<scan_grid(max_edges), kScanThreads, 0, st>>>(
+  if (next == nullptr && !defer_resolve) {  // both passes in one launch
+    flag_scan_kernel<true><<<scan_grid(max_edges), kScanThreads, 0, st>>>(
+        m.table, slot, src_glob, e_total, size_old, size_new, rank_of, m.globals, ws, nullptr,
+        src_local);
+    return cudaGetLastError();
+  }
+  flag_scan_kernel<false><<<scan_grid(max_edges), kScanThreads, 0, st>>>(
       m.table, slot, src_glob, e_total, size_old, size_new, rank_of, m.globals, ws,
-      defer_resolve ? const_cast<int32_t*>(slot) : nullptr);
+      defer_resolve ? const_cast<int32_t*>(slot) : nullptr, nullptr);
   err = cudaGetLastError();
   if (err != cudaSuccess || defer_resolve) return err;
   int64_t grid = (max_edges + 255) / 256;
   if (grid < 1) grid = 1;
   if (grid > num_sms() * 16) grid = num_sms() * 16;
-  if (next == nullptr) {
-    resolve_kernel<<<(int)grid, 256, 0, st>>>(m.table, slot, e_total, size_old, rank_of,
-                                              src_local);
-    return cudaGetLastError();
-  }
   // the next hop's count + scan rides in the same launch (its workspace is zeroed)
   CountJob cj;
   cj.indptr = next->g.indptr;
