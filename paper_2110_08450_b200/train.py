@@ -100,6 +100,27 @@ def shard_plan(plan, batch_size: int, rank: int, world: int):
     return descs, host
 
 
+def chunk_descs(ids: np.ndarray, batch_size: int, rank: int, world: int) -> np.ndarray:
+    """shard_plan of `ids` chunked in order (batch_id = chunk index), without building
+    a SeedBatch per chunk: the same descriptors, and the same distinct-seeds check
+    (SeedBatch, sampler.py) done for all chunks in one sort."""
+    n = len(ids)
+    nb = -(-n // batch_size) if n else 0
+    nf = n // batch_size
+    full = np.sort(ids[:nf * batch_size].reshape(nf, batch_size), axis=1)
+    tail = np.sort(ids[nf * batch_size:])
+    if (full[:, 1:] == full[:, :-1]).any() or (tail[1:] == tail[:-1]).any():
+        raise ValueError("seed IDs must be distinct")
+    steps = -(-nb // world) if nb else 0
+    b = np.arange(steps, dtype=np.int64) * world + rank
+    live = b < nb
+    descs = np.zeros((steps, 3), dtype=np.int64)
+    descs[:, 0] = np.where(live, b, -1)
+    descs[:, 1] = np.where(live, b * batch_size, 0)
+    descs[:, 2] = np.where(live, np.minimum(batch_size, n - b * batch_size), 0)
+    return descs
+
+
 def allreduce_mean(t: torch.Tensor, world: int) -> None:
     """In-place mean over ranks: NCCL AVG (NVLink/NVLS), SUM / world elsewhere."""
     if world <= 1:
@@ -726,13 +747,9 @@ class Evaluator:
 
     def set_ids(self, ids: np.ndarray) -> int:
         """Chunk and shard `ids`, upload seeds + descriptors; returns this rank's steps."""
-        from .prep import EpochPlan
-        from .sampler import SeedBatch
-        ids = np.asarray(ids, dtype=np.int64)
+        ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int64).reshape(-1))
         bs = self.batch_size
-        batches = tuple(SeedBatch(i, ids[s:s + bs]) for i, s in enumerate(range(0, len(ids), bs)))
-        plan = EpochPlan(batches=batches, batch_size=bs, shuffle_seed=0)
-        descs, _ = shard_plan(plan, bs, self.rank, self.world)
+        descs = chunk_descs(ids, bs, self.rank, self.world)
         n = len(descs)
         if self.seeds_all.numel() < max(1, len(ids)):
             self.seeds_all = torch.zeros(len(ids), dtype=torch.int64, device=self.device)

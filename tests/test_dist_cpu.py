@@ -80,3 +80,31 @@ def test_shard_plan_single_rank_is_identity():
     descs, host = shard_plan(plan, 128, 0, 1)
     assert [d[0] for d in descs.tolist()] == list(range(len(plan)))
     assert descs[-1, 2] == 1000 - 128 * 7
+
+
+@pytest.mark.parametrize("n", [0, 1, 1023, 1024, 1025, 5000])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_chunk_descs_equals_shard_plan_of_chunked_ids(n, world):
+    """Evaluator.set_ids builds its descriptors with chunk_descs (one sort, no
+    SeedBatch per chunk): the same table shard_plan gives for the in-order chunks."""
+    from paper_2110_08450_b200.prep import EpochPlan
+    from paper_2110_08450_b200.sampler import SeedBatch
+    from paper_2110_08450_b200.train import chunk_descs
+    ids = np.random.default_rng(n).choice(10**7, n, replace=False).astype(np.int64)
+    bs = 1024
+    batches = tuple(SeedBatch(i, ids[s:s + bs]) for i, s in enumerate(range(0, n, bs)))
+    plan = EpochPlan(batches=batches, batch_size=bs, shuffle_seed=0)
+    for rank in range(world):
+        want, _ = shard_plan(plan, bs, rank, world)
+        got = chunk_descs(ids, bs, rank, world)
+        assert got.shape == want.shape and (got == want).all()
+
+
+def test_chunk_descs_rejects_duplicate_seeds_within_a_chunk():
+    from paper_2110_08450_b200.train import chunk_descs
+    ids = np.arange(3000)
+    ids[10] = ids[1500]          # different chunks: allowed, as with SeedBatch
+    chunk_descs(ids, 1024, 0, 1)
+    ids[2500] = ids[2100]        # same (last, partial) chunk
+    with pytest.raises(ValueError, match="seed IDs must be distinct"):
+        chunk_descs(ids, 1024, 0, 1)
