@@ -111,6 +111,29 @@ def test_idmap_growth_rehash():
     assert idm.size == 3000
 
 
+def test_idmap_insert_many_tiles_of_duplicates():
+    """One insert spanning hundreds of scan tiles whose first occurrences sit in earlier
+    tiles (the chain's last relabel resolves in its scan launch, waiting on the tile that
+    holds each first occurrence): new locals in first-occurrence order, and the slots
+    finalized for the next insert."""
+    rng = np.random.default_rng(3)
+    idm = IdMap(SamplerVariant())
+    pre = rng.permutation(20000)[:700]
+    idm.insert(pre)
+    keys = rng.integers(0, 20000, 300_000)
+    keys[:50] = keys[-50:]             # the last tile's keys first seen in tile 0
+    idm.insert(keys)
+    _, first = np.unique(keys, return_index=True)
+    order = keys[np.sort(first)]
+    want = np.concatenate([pre, order[~np.isin(order, pre)]])
+    got = idm.global_ids.cpu().numpy()
+    assert got.tolist() == want.tolist()
+    for k in (int(keys[-1]), int(keys[150_000]), int(pre[3])):
+        assert idm.local_of(k) == int(np.flatnonzero(want == k)[0])
+    idm.insert(keys[::-3])
+    assert idm.size == len(want)
+
+
 def test_injected_positions_reproduce_hop(dg_small, mfg_small):
     """Sampling driven by the reference's own pos_all (hop_kernel two-pass)."""
     z = mfg_small
