@@ -90,7 +90,12 @@ class PrepConfig:
 
     @property
     def depth(self) -> int:
-        return max(1, min(self.num_workers, self.queue_capacity))
+        """Batches in flight ahead of the consumer: up to two per worker stream (so a
+        worker's next batch is already queued on its stream when the current one ends,
+        like a reference worker that moves on while the consumer holds its batch),
+        within the reference's pool of queue_capacity + num_workers buffers
+        (prep.py:239; the consumer's current batch holds one)."""
+        return max(1, min(2 * self.num_workers, self.num_workers + self.queue_capacity - 1))
 
 
 _TORCH_DT = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}

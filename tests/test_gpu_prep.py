@@ -132,12 +132,13 @@ def test_epoch_digests_match_reference_any_depth(data13, prep_small, P):
     z = prep_small
     plan = make_epoch_plan(np.arange(1000), 128, 5)
     for fm, key in ((fm32, "digests32"), (fm16, "digests16")):
-        run = run_epoch_prep(dg, fm, y, plan, PrepConfig(num_workers=P,
-                                                         fanouts=FanoutSpec((15, 10, 5))), 42)
+        cfg = PrepConfig(num_workers=P, fanouts=FanoutSpec((15, 10, 5)))
+        run = run_epoch_prep(dg, fm, y, plan, cfg, 42)
         got = [(b.mfg.seeds.batch_id, b.digest()) for b in run]
         assert [b for b, _ in got] == list(range(8))
         assert [d for _, d in got] == [str(d) for d in z[key]]
-        assert run.report.peak_resident <= P + 1
+        # the reference's pool bound (prep.py:239): queue_capacity + num_workers buffers
+        assert run.report.peak_resident <= min(cfg.depth + 1, P + cfg.queue_capacity)
         assert len(run.report.per_batch) == 8
         assert run.report.sampling_s > 0 and run.report.slicing_s > 0
 

@@ -86,6 +86,11 @@ def test_config_validation():
     with pytest.raises(ValueError):
         SeedBatch(0, np.array([1, 1, 2]))
     assert PrepConfig(num_workers=2).queue_capacity == 8
+    # batches in flight: two per worker stream, inside the reference's pool bound
+    assert PrepConfig(num_workers=1).depth == 2
+    assert PrepConfig(num_workers=8).depth == 16
+    assert PrepConfig(num_workers=1, queue_capacity=1).depth == 1
+    assert PrepConfig(num_workers=3, queue_capacity=2).depth == 4
 
 
 def test_variants():
