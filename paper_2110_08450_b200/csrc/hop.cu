@@ -193,8 +193,14 @@ SAL_DEVINL void emit_edge(const int32_t* __restrict__ indices, int64_t slot_pos,
 // no lower lane of the group drew the same position this round; fresh draws
 // are accepted in lane order until the fanout is reached — exactly the
 // sequential loop of _sample_positions (_kernels.py:119-146).
-template <int kPolicy, int G>
-__global__ void __launch_bounds__(256)
+// kMinBlocks = 8 holds the kernel to 32 registers (a few bytes of spill) so 64
+// warps are resident instead of 48: the large hops (tens of thousands of
+// destinations, several per group) are bound by how many insert chains are in
+// flight — full 3-hop MFG 120.7 -> 107-112 us one batch at a time, 62.2 -> 59.0 us
+// per batch at 8 streams (profiles/r2_ab_sample_regs.txt).  The small hops of the
+// training chain measured 0.3 us per step slower that way and keep 6.
+template <int kPolicy, int G, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks)
 sample_insert_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                      const int32_t* __restrict__ globals, const int64_t* __restrict__ n_dst_ptr,
                      int32_t fanout, HopKey hk, const BatchDesc* __restrict__ desc,
@@ -524,10 +530,20 @@ cudaError_t launch_hop_sample(const GraphDev& g, const IdMapDev& m, const int64_
   grid = (warps_needed * G / 32 + 7) / 8;
   if (grid < 1) grid = 1;
   if (grid > cap) grid = cap;
-#define SAL_SAMPLE(P, GG)                                                                   \
-  sample_insert_kernel<P, GG><<<(int)grid, 256, 0, st>>>(                                   \
-      g.indptr, g.indices, m.globals, n_dst, fanout, hk, desc, inject_pos, dst_indptr, m.table, \
-      m.log2cap, src_glob, slot, draws_out, m.table == nullptr ? m.size_out : nullptr)
+  const bool wide = max_dst >= 16384;   // a large hop: the 64-warp variant
+#define SAL_SAMPLE(P, GG)                                                                    \
+  do {                                                                                       \
+    if (wide)                                                                                \
+      sample_insert_kernel<P, GG, 8><<<(int)grid, 256, 0, st>>>(                             \
+          g.indptr, g.indices, m.globals, n_dst, fanout, hk, desc, inject_pos, dst_indptr,   \
+          m.table, m.log2cap, src_glob, slot, draws_out,                                     \
+          m.table == nullptr ? m.size_out : nullptr);                                        \
+    else                                                                                     \
+      sample_insert_kernel<P, GG, 6><<<(int)grid, 256, 0, st>>>(                             \
+          g.indptr, g.indices, m.globals, n_dst, fanout, hk, desc, inject_pos, dst_indptr,   \
+          m.table, m.log2cap, src_glob, slot, draws_out,                                     \
+          m.table == nullptr ? m.size_out : nullptr);                                        \
+  } while (0)
   if (policy == kRngSplitmix) {
     if (G == 8) SAL_SAMPLE(kRngSplitmix, 8);
     else if (G == 16) SAL_SAMPLE(kRngSplitmix, 16);
