@@ -100,17 +100,26 @@ def shard_plan(plan, batch_size: int, rank: int, world: int):
     return descs, host
 
 
-def chunk_descs(ids: np.ndarray, batch_size: int, rank: int, world: int) -> np.ndarray:
-    """shard_plan of `ids` chunked in order (batch_id = chunk index), without building
-    a SeedBatch per chunk: the same descriptors, and the same distinct-seeds check
-    (SeedBatch, sampler.py) done for all chunks in one sort."""
+def check_chunks_distinct(ids: np.ndarray, batch_size: int) -> None:
+    """The distinct-seeds check of a SeedBatch (sampler.py) for every in-order chunk of
+    `ids`, in one sort."""
     n = len(ids)
-    nb = -(-n // batch_size) if n else 0
     nf = n // batch_size
     full = np.sort(ids[:nf * batch_size].reshape(nf, batch_size), axis=1)
     tail = np.sort(ids[nf * batch_size:])
     if (full[:, 1:] == full[:, :-1]).any() or (tail[1:] == tail[:-1]).any():
         raise ValueError("seed IDs must be distinct")
+
+
+def chunk_descs(ids: np.ndarray, batch_size: int, rank: int, world: int,
+                check: bool = True) -> np.ndarray:
+    """shard_plan of `ids` chunked in order (batch_id = chunk index), without building
+    a SeedBatch per chunk: the same descriptors (and, with `check`, the same
+    distinct-seeds check)."""
+    n = len(ids)
+    nb = -(-n // batch_size) if n else 0
+    if check:
+        check_chunks_distinct(ids, batch_size)
     steps = -(-nb // world) if nb else 0
     b = np.arange(steps, dtype=np.int64) * world + rank
     live = b < nb
@@ -745,11 +754,14 @@ class Evaluator:
         self.graph_kernels = {}
         self.kernel_launches = 0
 
-    def set_ids(self, ids: np.ndarray) -> int:
-        """Chunk and shard `ids`, upload seeds + descriptors; returns this rank's steps."""
+    def set_ids(self, ids: np.ndarray, check: bool = True) -> int:
+        """Chunk and shard `ids`, upload seeds + descriptors; returns this rank's steps.
+        check=False leaves the distinct-seeds check to the caller (run() does it on the
+        host while the pass runs)."""
         ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int64).reshape(-1))
+        self._ids = ids
         bs = self.batch_size
-        descs = chunk_descs(ids, bs, self.rank, self.world)
+        descs = chunk_descs(ids, bs, self.rank, self.world, check=check)
         n = len(descs)
         if self.seeds_all.numel() < max(1, len(ids)):
             self.seeds_all = torch.zeros(len(ids), dtype=torch.int64, device=self.device)
@@ -895,10 +907,13 @@ class Evaluator:
                 self.kernel_launches += _lib.lib().sal_launch_count() - n0
 
     def run(self, ids: np.ndarray) -> tuple[int, int]:
-        n = self.set_ids(ids)
+        n = self.set_ids(ids, check=False)
         self.capture_all()   # before the pass: capturing replays steps
         self.begin()
         self.steps(0, n)
+        # the seeds' distinct check runs on the host under the device pass; a failure
+        # raises before any result is read (every rank checks every chunk alike)
+        check_chunks_distinct(self._ids, self.batch_size)
         if self.world > 1:
             torch.distributed.all_reduce(self.counts)
         c, t = self.counts.tolist()

@@ -77,6 +77,21 @@ def test_evaluator_inference_fanout_all_ids_three_layers():
     assert te == 20000 and abs(c - ce) <= 0.003 * 20000
 
 
+def test_evaluate_rejects_duplicate_seeds_in_a_chunk():
+    """SeedBatch's distinct-seeds error (sampler.py) from the device pass, whose check
+    runs on the host under the pass; a clean call afterwards still counts right."""
+    g, fm, y, dg = _planted(n=3000, f=128, classes=16, seed=5)
+    cfg = TrainConfig(fanouts=FanoutSpec((15, 10, 5)), batch_size=1024, hidden=256,
+                      gather_free=True)
+    tr = Trainer(dg, np.arange(3000), cfg)
+    ids = np.arange(3000)
+    ids[2100] = ids[2500]
+    with pytest.raises(ValueError, match="seed IDs must be distinct"):
+        tr.evaluate(ids)
+    c, t = tr.evaluate(np.arange(3000))
+    assert t == 3000 and 0 <= c <= 3000
+
+
 def _reference_accuracy(dg, fm, y, train, test, fused, cfg, epochs):
     """fp32 torch-autograd GraphSAGE (model.GraphSAGE) on the same batches:
     make_epoch_plan(train, bs, shuffle_seed + e) -> multihop_mfg(global_seed)
