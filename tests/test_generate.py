@@ -110,7 +110,7 @@ def test_pairing_uniform_between_degree_classes(g200k):
 
 def test_features_uniform_fp16(g200k):
     x = g200k["features"]
-    assert x.shape == (200_000, 104) and x.dtype == np.float16
+    assert x.shape == (200_000, 104) and x.dtype == np.float16   # host default stride
     assert not np.any(x[:, 100:])                     # padding columns stay zero
     v = x[:, :100].astype(np.float32)
     assert v.min() >= -1.0 and v.max() <= 1.0
