@@ -146,8 +146,8 @@ def _model_width(dg: DeviceGraph) -> int:
     """Feature width the model consumes: at least the table's padded row (16-byte
     multiple), so every layer-0 row is whole 16-byte vectors for the fast kernels,
     and 128 for 16-bit tables between 64 and 128 columns, so layer 0 runs on the
-    tcgen05 kernels (K = 2 x 128).  Products' 100 fp16 columns: table 104, model
-    128.  The padding columns are zero and their weights get zero gradient, so
+    tcgen05 kernels (K = 2 x 128).  Products' 100 fp16 columns: the table is stored at
+    128 already (graph._pad_cols), so is the model.  The padding columns are zero and their weights get zero gradient, so
     the model is the unpadded one."""
     fp = dg.features.shape[1]
     if dg.features.element_size() == 2 and 64 < fp < 128:
